@@ -1,0 +1,195 @@
+/*
+ * cider.h — C ABI of the B200-native CIDER refinement decoder.
+ *
+ * This is the drop-in boundary for the reference's decoder hot path
+ * (/root/reference/proj).  Every entry point replaces one reference
+ * interface; the reference symbol it stands in for is cited beside it.
+ *
+ *   cider_denoise  = ura::StructuredDenoiser::logits          (denoiser.hpp:109-114, denoiser.cpp:253-259)
+ *                    + module_b(..., incoming_out)            (denoiser.hpp:101-102)
+ *   cider_refine   = ura::run_refinement                      (refine.hpp:60-62,  refine.cpp:199-205)
+ *                    ura::run_with_remasking                  (refine.hpp:104-107, refine.cpp:277-292)
+ *                    (rank mode: §7.1(3) adapter over ura::remask_pass, refine.cpp:238-275)
+ *   cider_weights_init = ura::DenoiserParams::random_init     (denoiser.cpp:41-69), extended to
+ *                    stacked layers / MLP width / attention
+ *
+ * Conventions (mirroring the reference's value-type API):
+ *   - every buffer is caller-owned; host pointers unless the name says _device;
+ *   - grids are K x L int32 row-major per bin (ura::SymbolGrid, grid.hpp:14-31), -1 = MASK;
+ *   - evidence is L x Q fp32 row-major per bin (ura::EvidenceMatrix, grid.hpp:40-54);
+ *   - logits are K x L x Q fp32 per bin (ura::LogitGrid, denoiser.hpp:28-40);
+ *   - status: 0 ok, CIDER_EINVAL (3, -> std::domain_error), CIDER_ERUNTIME (4, -> std::runtime_error),
+ *     the same exit-code mapping as uradec.cpp:817-829; cider_last_error() holds the message
+ *     (thread-local), with the reference's prefixes ("denoiser failed at step t: ...").
+ *   - calls on one context are serialised internally (one mutex + one CUDA stream), so a shared
+ *     context is safe under concurrent callers, as Denoiser::logits is (uradec.cpp:184, 294-297).
+ * There is no CPU fallback: every compute entry point fails with CIDER_ERUNTIME when no B200
+ * (sm_100) device is present.
+ */
+#ifndef CIDER_H
+#define CIDER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CIDER_OK 0
+#define CIDER_EINVAL 3
+#define CIDER_ERUNTIME 4
+
+#define CIDER_FP32 0 /* SIMT fp32 GEMMs, fp32 activations: the parity mode */
+#define CIDER_BF16 1 /* tcgen05 bf16 GEMMs with fp32 accumulation in TMEM: the throughput mode */
+
+#define CIDER_REMASK_NONE 0
+#define CIDER_REMASK_THRESHOLD 1 /* reference rule: rows with conf < phi_s (refine.cpp:245-252) */
+#define CIDER_REMASK_RANK 2      /* floor(frac*K) lowest-confidence rows, ties -> lower row */
+
+#define CIDER_MAX_THRESHOLDS 8
+
+typedef struct cider_ctx cider_ctx;
+
+/* Model hyper-parameters. Reference mode ("ref-exact") is layers=1, hidden=dim, heads=0:
+ * exactly ura::DenoiserParams (denoiser.hpp:54-75). */
+typedef struct {
+    int m;               /* GF(2^m), Q = 2^m (gf.hpp:14-37) */
+    uint32_t prim_poly;  /* 0 -> GfContext::default_prim_poly(m) (gf.cpp:8-20) */
+    int dim;             /* D */
+    int hidden;          /* H, TwoLayerMap hidden width (denoiser.hpp:44-50) */
+    int layers;          /* N stacked Module A + Module B blocks (shared E, W, V) */
+    int heads;           /* 0 = sum-pool Psi (denoiser.cpp:196-203); >0 = extrinsic pooling attention */
+    double tau_demix;    /* denoiser.hpp:58 */
+    double evidence_scale; /* beta_S, denoiser.hpp:59 */
+    int precision;       /* CIDER_FP32 | CIDER_BF16 */
+} cider_model_desc;
+
+/* Parity-check matrix as (check, slot, coeff) triples (ura::ParityCheckMatrix, ldpc.hpp:23-47).
+ * Any order; the library sorts by (check, slot) and validates like ldpc.cpp:11-30. */
+typedef struct {
+    int checks;
+    int slots;
+    int n_edges;
+    const int32_t* edges; /* n_edges x 3 */
+} cider_code_desc;
+
+/* ura::RevealSchedule (refine.hpp:13-18). */
+typedef struct {
+    int steps;
+    double tau_max;
+    double tau_min;
+    int first_reveal;
+} cider_schedule;
+
+/* ura::RemaskConfig (refine.hpp:33-36) plus the rank-selection mode of BASELINE config 3. */
+typedef struct {
+    int mode;                              /* CIDER_REMASK_* */
+    int n_thresholds;
+    double thresholds[CIDER_MAX_THRESHOLDS]; /* strictly descending, each in (0,1) */
+    double rank_fraction;                  /* CIDER_REMASK_RANK: k_low = floor(rank_fraction*K) */
+} cider_remask;
+
+/* Per-bin slice of ura::RefineTrace (refine.hpp:48-54); every pointer nullable.
+ * remask_rows / remask_steps are B x CIDER_MAX_THRESHOLDS (0 where a stage did not run);
+ * remask_mask is B x K (1 = row re-decoded by the last remask stage that ran). */
+typedef struct {
+    int32_t* first_reveals; /* B: reveal count of the first pass's t=1 step */
+    int32_t* remask_rows;
+    int32_t* remask_steps;
+    int32_t* remask_mask;
+} cider_trace;
+
+/* ---- weights (A15) -------------------------------------------------------------------- */
+/* Flat layout, in draw order:
+ *   embed (Q+1)xD | out_proj QxD | sym_embed QxD |
+ *   per layer: gate_a {w1 Hx2D, b1 H, w2 DxH, b2 D} check_agg {w1 HxD, b1 H, w2 DxH, b2 D}
+ *              fuse_b {w1 Hx2D, b1 H, w2 DxH, b2 D} |
+ *   per layer (heads>0 only): attn_query D | attn_key DxD                                   */
+size_t cider_weights_count(const cider_model_desc* model);
+int cider_weights_init_f64(const cider_model_desc* model, uint64_t seed, double* out);
+int cider_weights_init(const cider_model_desc* model, uint64_t seed, float* out);
+
+/* ---- context -------------------------------------------------------------------------- */
+int cider_create(const cider_model_desc* model, const float* weights, const cider_code_desc* code,
+                 int device, cider_ctx** out);
+void cider_destroy(cider_ctx* ctx);
+const char* cider_last_error(void);
+/* max bins resident per internal chunk (default: sized from free HBM); 0 = automatic */
+int cider_set_chunk(cider_ctx* ctx, int max_bins_per_chunk);
+
+/* ---- the path --------------------------------------------------------------------------- */
+/* One denoiser forward for B bins of K rows (= Denoiser::logits). X: B x K x L int32 (-1 = MASK),
+ * S: B x L x Q, logits: B x K x L x Q (nullable), incoming: B x layers x K x L x D (nullable;
+ * the per-slot aggregated check messages of each layer, = module_b incoming_out). */
+int cider_denoise(cider_ctx* ctx, int B, int K, const int32_t* X, const float* S, float* logits,
+                  float* incoming);
+
+/* Full refinement (+ remasking) for B bins of K rows (= run_refinement / run_with_remasking).
+ * S: B x L x Q, grid: B x K x L. final_logits (nullable): B x K x L x Q logits of the last
+ * final (gamma = 0) pass, as run_refinement's final_pass_logits out-param. */
+int cider_refine(cider_ctx* ctx, int B, int K, const float* S, const cider_schedule* sched,
+                 const cider_remask* remask, int32_t* grid, float* final_logits, cider_trace* trace);
+
+/* Same, with S and grid in device memory (allocated by cider_device_alloc); async on the
+ * context stream; trace ignored. */
+int cider_refine_device(cider_ctx* ctx, int B, int K, const float* S_device,
+                        const cider_schedule* sched, const cider_remask* remask,
+                        int32_t* grid_device);
+
+/* ---- device plumbing used by the benchmark (no PyTorch on the path) --------------------- */
+int cider_device_count(int* n);
+int cider_device_alloc(cider_ctx* ctx, size_t bytes, void** ptr);
+int cider_device_free(cider_ctx* ctx, void* ptr);
+int cider_host_alloc(size_t bytes, void** ptr); /* pinned */
+int cider_host_free(void* ptr);
+int cider_memcpy_h2d(cider_ctx* ctx, void* dst, const void* src, size_t bytes); /* async, ctx stream */
+int cider_memcpy_d2h(cider_ctx* ctx, void* dst, const void* src, size_t bytes); /* async, ctx stream */
+int cider_synchronize(cider_ctx* ctx);
+int cider_flush_l2(cider_ctx* ctx); /* writes a buffer larger than L2 on the ctx stream */
+/* CUDA events on the ctx stream: slot in [0, 64) */
+int cider_event_record(cider_ctx* ctx, int slot);
+int cider_event_elapsed(cider_ctx* ctx, int slot_a, int slot_b, float* ms);
+
+/* Instrumentation: kernel launches issued by this context so far, and (when profiling is on)
+ * per-kernel-class CUDA-event times accumulated on the ctx stream. */
+int cider_set_profiling(cider_ctx* ctx, int on);
+int64_t cider_launch_count(cider_ctx* ctx);
+int cider_kernel_stats(cider_ctx* ctx, int idx, char* name, int name_len, int64_t* launches,
+                       double* total_ms, double* flops, double* bytes);
+int cider_reset_stats(cider_ctx* ctx);
+
+/* ---- multi-GPU result gather (NCCL, the only collective on the path) --------------------- */
+int cider_nccl_unique_id(char out[128]);
+int cider_nccl_init(cider_ctx* ctx, const char id[128], int rank, int world);
+/* all ranks contribute n_bytes from send_device; recv_device (n_bytes*world) filled on every rank */
+int cider_nccl_allgather(cider_ctx* ctx, const void* send_device, void* recv_device, size_t n_bytes);
+
+/* ---- host-side workload (BASELINE configs) and metrics ---------------------------------- */
+typedef struct {
+    int m;              /* GF(2^m) */
+    int slots;          /* L */
+    int checks;         /* P */
+    int col_weight;     /* 3 */
+    int k;              /* users per bin */
+    double snr_db;
+    double p_erase;
+    double p_false;
+    uint64_t master_seed; /* 0: H from derive_seed(0,1), bin b from derive_seed(0,16+b) */
+} cider_workload_desc;
+
+/* H = build_random_ldpc(gf, L, P, col_weight, make_rng(derive_seed(seed,1))) (uradec.cpp:45-52).
+ * edges: L*col_weight x 3, sorted by (check, slot). */
+int cider_workload_code(const cider_workload_desc* w, int32_t* edges);
+/* Bins [first, first+n): truth (n x K x L, = sample_codewords) and S (n x L x Q fp32). */
+int cider_workload_bins(const cider_workload_desc* w, const int32_t* edges, int64_t first, int n,
+                        int32_t* truth, float* S, int threads);
+/* Permutation-invariant SER/CER (= ura::ser_cer, metrics.cpp:124-145) summed over n bins. */
+int cider_ser_cer(int n, int K, int L, const int32_t* truth, const int32_t* pred, double* ser_sum,
+                  double* cer_sum);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CIDER_H */

@@ -1,0 +1,188 @@
+"""ctypes bindings of the CHECKERS — test infrastructure only.
+
+  restatement : oracle/_build/libcider_oracle.so  (cider_oracle.cpp, this repo's fp64 CPU oracle)
+  reference   : oracle/_ref/libura_ref.so         (the reference's own sources + ref_shim.cpp)
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module; the product path (paper_2605_26580_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from paper_2605_26580_b200 import (MAX_THRESHOLDS, Model, ModelDesc, CodeDesc, RemaskConfig, RemaskDesc,
+                                   RevealSchedule, ScheduleDesc, code_desc)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_PATH = os.path.join(_HERE, "_build", "libcider_oracle.so")
+REF_PATH = os.path.join(_HERE, "_ref", "libura_ref.so")
+
+_handles = {}
+
+
+def _load(path: str, prefix: str) -> C.CDLL:
+    if path in _handles:
+        return _handles[path]
+    if not os.path.exists(path):
+        raise FileNotFoundError(path)
+    h = C.CDLL(path)
+    P = C.c_void_p
+    getattr(h, f"{prefix}_last_error").restype = C.c_char_p
+    d = getattr(h, f"{prefix}_denoise")
+    d.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, P, P, P, P]
+    r = getattr(h, f"{prefix}_refine")
+    r.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.POINTER(ScheduleDesc),
+                  C.POINTER(RemaskDesc), P, P, P, P, P, P, C.c_int]
+    rv = getattr(h, f"{prefix}_reveal_step")
+    rv.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.c_int, C.c_double, C.c_int, P]
+    w = getattr(h, f"{prefix}_check_update_wht")
+    w.argtypes = [C.c_int, C.c_int, P, P, C.c_int, P]
+    if prefix == "ref":
+        h.ref_random_init.argtypes = [C.c_int, C.c_int, C.c_uint64, P]
+        h.ref_build_ldpc.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, P]
+        h.ref_sample_codewords.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_uint64, P]
+        h.ref_ser_cer.argtypes = [C.c_int, C.c_int, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        h.ref_check_update_direct.argtypes = [C.c_int, C.c_int, P, P, C.c_int, P]
+        h.ref_cosine_target.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+        h.ref_infer_temperature.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double]
+        h.ref_infer_temperature.restype = C.c_double
+        h.ref_remask_steps.argtypes = [C.c_int, C.c_int, C.c_int]
+    _handles[path] = h
+    return h
+
+
+def have_reference() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Checker:
+    """The same C-ABI served by the restatement ('oracle') or the reference itself ('ref')."""
+
+    def __init__(self, kind: str = "oracle"):
+        self.kind = kind
+        self.prefix = "oracle" if kind == "oracle" else "ref"
+        self.h = _load(ORACLE_PATH if kind == "oracle" else REF_PATH, self.prefix)
+
+    def _check(self, rc: int):
+        if rc == 0:
+            return
+        msg = getattr(self.h, f"{self.prefix}_last_error")().decode()
+        if rc == 3:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+    def denoise(self, model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int,
+                X: np.ndarray, S: np.ndarray, want_incoming: bool = False):
+        """One bin: X K x L, S L x Q (fp64) -> logits K x L x Q (+ incoming layers x K x L x D)."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        cd, _e = code_desc(edges, checks, slots)
+        X = np.ascontiguousarray(X, dtype=np.int32)
+        S = np.ascontiguousarray(S, dtype=np.float64)
+        K, L = X.shape
+        lg = np.empty((K, L, model.q), dtype=np.float64)
+        inc = np.empty((model.layers, K, L, model.dim), dtype=np.float64) if want_incoming else None
+        md = model.desc()
+        self._check(getattr(self.h, f"{self.prefix}_denoise")(C.byref(md), _p(w), C.byref(cd), K, _p(X), _p(S),
+                                                              _p(lg), _p(inc)))
+        return (lg, inc) if want_incoming else lg
+
+    def refine(self, model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int, S: np.ndarray,
+               K: int, sched: RevealSchedule, remask: Optional[RemaskConfig] = None, threads: int = 0,
+               want_final_logits: bool = False):
+        """B bins: S B x L x Q (fp64) -> dict(grid, final_logits, first_reveals, remask_rows, remask_steps, mask)."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        cd, _e = code_desc(edges, checks, slots)
+        S = np.ascontiguousarray(S, dtype=np.float64)
+        B, L, q = S.shape
+        out = {
+            "grid": np.empty((B, K, L), np.int32),
+            "final_logits": np.empty((B, K, L, q), np.float64) if want_final_logits else None,
+            "first_reveals": np.zeros(B, np.int32),
+            "remask_rows": np.zeros((B, MAX_THRESHOLDS), np.int32),
+            "remask_steps": np.zeros((B, MAX_THRESHOLDS), np.int32),
+            "remask_mask": np.zeros((B, K), np.int32),
+        }
+        md, sd, rd = model.desc(), sched.desc(), (remask or RemaskConfig()).desc()
+        self._check(getattr(self.h, f"{self.prefix}_refine")(
+            C.byref(md), _p(w), C.byref(cd), B, K, _p(S), C.byref(sd), C.byref(rd), _p(out["grid"]),
+            _p(out["final_logits"]), _p(out["first_reveals"]), _p(out["remask_rows"]), _p(out["remask_steps"]),
+            _p(out["remask_mask"]), threads))
+        return out
+
+    def reveal_step(self, X: np.ndarray, logits: np.ndarray, target: int, tau: float, first: bool):
+        X = np.ascontiguousarray(X, dtype=np.int32)
+        lg = np.ascontiguousarray(logits, dtype=np.float64)
+        K, L = X.shape
+        out = np.empty_like(X)
+        self._check(getattr(self.h, f"{self.prefix}_reveal_step")(K, L, lg.shape[-1], _p(X), _p(lg), target, tau,
+                                                                  1 if first else 0, _p(out)))
+        return out
+
+    def check_update_wht(self, m: int, incoming: np.ndarray, coeffs, target: int):
+        inc = np.ascontiguousarray(incoming, dtype=np.float64)
+        cf = np.ascontiguousarray(coeffs, dtype=np.int32)
+        out = np.empty(1 << m, np.float64)
+        self._check(getattr(self.h, f"{self.prefix}_check_update_wht")(m, inc.shape[0], _p(inc), _p(cf), target,
+                                                                       _p(out)))
+        return out
+
+
+class Reference(Checker):
+    """Extra entry points only the reference shim has (weights, code construction, metrics)."""
+
+    def __init__(self):
+        super().__init__("ref")
+
+    def random_init(self, q: int, dim: int, seed: int) -> np.ndarray:
+        n = (q + 1) * dim + 2 * q * dim + 3 * dim * 2 * dim + 3 * dim + dim * dim + dim + dim * dim + dim * 2 + dim * dim
+        # exact count: embed + out_proj + sym_embed + gate(2D->D->D) + agg(D->D->D) + fuse(2D->D->D)
+        n = (q + 1) * dim + 2 * q * dim + (dim * 2 * dim + dim + dim * dim + dim) * 2 + (dim * dim + dim + dim * dim + dim)
+        out = np.empty(n, np.float64)
+        self._check(self.h.ref_random_init(q, dim, C.c_uint64(seed), _p(out)))
+        return out
+
+    def build_ldpc(self, m: int, slots: int, checks: int, col_weight: int, seed: int) -> np.ndarray:
+        e = np.empty((slots * col_weight, 3), np.int32)
+        self._check(self.h.ref_build_ldpc(m, slots, checks, col_weight, C.c_uint64(seed), _p(e)))
+        return e
+
+    def sample_codewords(self, m: int, edges: np.ndarray, checks: int, slots: int, k: int, seed: int) -> np.ndarray:
+        cd, _e = code_desc(edges, checks, slots)
+        out = np.empty((k, slots), np.int32)
+        self._check(self.h.ref_sample_codewords(m, C.byref(cd), k, C.c_uint64(seed), _p(out)))
+        return out
+
+    def ser_cer(self, truth: np.ndarray, pred: np.ndarray):
+        t = np.ascontiguousarray(truth, np.int32)
+        p = np.ascontiguousarray(pred, np.int32)
+        s, c = C.c_double(), C.c_double()
+        self._check(self.h.ref_ser_cer(t.shape[0], t.shape[1], _p(t), _p(p), C.byref(s), C.byref(c)))
+        return s.value, c.value
+
+    def check_update_direct(self, m: int, incoming: np.ndarray, coeffs, target: int):
+        inc = np.ascontiguousarray(incoming, dtype=np.float64)
+        cf = np.ascontiguousarray(coeffs, dtype=np.int32)
+        out = np.empty(1 << m, np.float64)
+        self._check(self.h.ref_check_update_direct(m, inc.shape[0], _p(inc), _p(cf), target, _p(out)))
+        return out
+
+
+def derive_seed(master: int, index: int) -> int:
+    """seeding.hpp:16-22 (pure-Python restatement, used to name fixture seeds)."""
+    M = (1 << 64) - 1
+
+    def mix(z):
+        z = (z + 0x9E3779B97F4A7C15) & M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+
+    return mix(master ^ mix((index + 0x517CC1B727220A95) & M))

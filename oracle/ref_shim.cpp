@@ -1,0 +1,471 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY (the checker, never the product).
+//
+// C-ABI shim around the reference implementation itself. oracle/Makefile compiles the
+// reference's own sources straight from /root/reference/proj/src (gf, ldpc, denoiser, refine,
+// metrics, parallel, bp) together with this file into oracle/_ref/libura_ref.so. Nothing from
+// the reference is copied into this repository; this file only *calls* the reference API.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline legs may load it.
+//
+// Ref-exact mode (layers=1, hidden=dim, heads=0) is ura::StructuredDenoiser verbatim
+// (denoiser.cpp:253-259). Config mode composes the reference's own
+// module_a / module_b / final_logits per layer with shared E, W, V; heads>0 swaps Module B's
+// sum-pool Psi for the extrinsic pooling attention defined in DESIGN.md §2, built from the
+// reference's coeff_action (denoiser.cpp:162-179) and TwoLayerMap::apply_gelu (denoiser.cpp:29-34).
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ura/bp.hpp"
+#include "ura/denoiser.hpp"
+#include "ura/gf.hpp"
+#include "ura/ldpc.hpp"
+#include "ura/metrics.hpp"
+#include "ura/parallel.hpp"
+#include "ura/refine.hpp"
+#include "ura/seeding.hpp"
+
+#include "cider.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+    g_err = e.what();
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::domain_error& e) {
+        return fail(e, CIDER_EINVAL);
+    } catch (const std::exception& e) {
+        return fail(e, CIDER_ERUNTIME);
+    }
+}
+
+ura::GfContext make_gf(const cider_model_desc* m) {
+    uint32_t poly = m->prim_poly ? m->prim_poly : ura::GfContext::default_prim_poly(m->m);
+    return ura::GfContext(m->m, poly);
+}
+
+ura::ParityCheckMatrix make_h(int q, const cider_code_desc* c) {
+    std::vector<ura::ParityEdge> e(c->n_edges);
+    for (int i = 0; i < c->n_edges; ++i)
+        e[i] = ura::ParityEdge{c->edges[3 * i], c->edges[3 * i + 1], c->edges[3 * i + 2]};
+    return ura::ParityCheckMatrix(c->checks, c->slots, q, std::move(e));
+}
+
+struct AttnParams {
+    std::vector<double> query; // D
+    std::vector<double> key;   // D x D, row-major [out][in]
+};
+
+// Unpacks the flat weight layout of cider.h into per-layer reference DenoiserParams.
+struct Model {
+    int q = 0, dim = 0, hidden = 0, layers = 0, heads = 0;
+    std::vector<ura::DenoiserParams> p; // one per layer; tables replicated (shared values)
+    std::vector<AttnParams> attn;
+
+    Model(const cider_model_desc* m, const double* w) {
+        q = 1 << m->m;
+        dim = m->dim;
+        hidden = m->hidden;
+        layers = m->layers;
+        heads = m->heads;
+        if (layers < 1 || dim < 1 || hidden < 1 || heads < 0 || (heads > 0 && dim % heads))
+            throw std::domain_error("ref_shim: bad model dimensions");
+        size_t off = 0;
+        auto take = [&](std::vector<double>& v, size_t n) {
+            v.assign(w + off, w + off + n);
+            off += n;
+        };
+        ura::DenoiserParams base;
+        base.q = q;
+        base.dim = dim;
+        base.tau_demix = m->tau_demix;
+        base.evidence_scale = m->evidence_scale;
+        take(base.embed, size_t(q + 1) * dim);
+        take(base.out_proj, size_t(q) * dim);
+        take(base.sym_embed, size_t(q) * dim);
+        auto map = [&](ura::TwoLayerMap& t, int in) {
+            t.in = in;
+            t.hidden = hidden;
+            t.out = dim;
+            take(t.w1, size_t(hidden) * in);
+            take(t.b1, hidden);
+            take(t.w2, size_t(dim) * hidden);
+            take(t.b2, dim);
+        };
+        for (int l = 0; l < layers; ++l) {
+            ura::DenoiserParams pl = base;
+            map(pl.gate_a, 2 * dim);
+            map(pl.check_agg, dim);
+            map(pl.fuse_b, 2 * dim);
+            p.push_back(std::move(pl));
+        }
+        if (heads > 0) {
+            for (int l = 0; l < layers; ++l) {
+                AttnParams a;
+                take(a.query, dim);
+                take(a.key, size_t(dim) * dim);
+                attn.push_back(std::move(a));
+            }
+        }
+    }
+};
+
+// Module B with attention Psi, composed of reference primitives ("attention Psi").
+ura::LatentGrid module_b_attn(const ura::GfContext& gf, const ura::LatentGrid& zt,
+                              const ura::ParityCheckMatrix& h, const ura::DenoiserParams& p,
+                              const AttnParams& a, int heads, ura::LatentGrid* incoming_out) {
+    const int dim = p.dim, dh = dim / heads;
+    const double scale = 1.0 / std::sqrt(double(dh));
+    ura::LatentGrid acc(zt.rows, zt.cols, dim);
+    std::vector<double> pooled(dim), mapped(dim);
+    for (int k = 0; k < zt.rows; ++k) {
+        for (int j = 0; j < h.checks(); ++j) {
+            const auto& edges = h.check_edges(j);
+            const int d = int(edges.size());
+            std::vector<std::vector<double>> nrm(d);
+            std::vector<std::vector<double>> score(d, std::vector<double>(heads, 0.0));
+            for (int i = 0; i < d; ++i) {
+                const ura::ParityEdge& e = h.edge(edges[i]);
+                nrm[i] = ura::coeff_action(gf, p, zt.at(k, e.slot), e.coeff);
+                for (int hh = 0; hh < heads; ++hh) {
+                    double s = 0.0;
+                    for (int t = hh * dh; t < (hh + 1) * dh; ++t) {
+                        double key = 0.0;
+                        for (int c = 0; c < dim; ++c) key += a.key[size_t(t) * dim + c] * nrm[i][c];
+                        s += a.query[t] * key;
+                    }
+                    score[i][hh] = s * scale;
+                }
+            }
+            for (int i = 0; i < d; ++i) {
+                std::fill(pooled.begin(), pooled.end(), 0.0);
+                for (int hh = 0; hh < heads; ++hh) {
+                    double mx = -INFINITY;
+                    for (int i2 = 0; i2 < d; ++i2)
+                        if (i2 != i) mx = std::max(mx, score[i2][hh]);
+                    double den = 0.0;
+                    for (int i2 = 0; i2 < d; ++i2)
+                        if (i2 != i) den += std::exp(score[i2][hh] - mx);
+                    for (int i2 = 0; i2 < d; ++i2) {
+                        if (i2 == i) continue;
+                        double wgt = double(d - 1) * std::exp(score[i2][hh] - mx) / den;
+                        for (int t = hh * dh; t < (hh + 1) * dh; ++t) pooled[t] += wgt * nrm[i2][t];
+                    }
+                }
+                p.check_agg.apply_gelu(pooled.data(), mapped.data());
+                const ura::ParityEdge& e = h.edge(edges[i]);
+                auto msg = ura::coeff_action(gf, p, mapped.data(), gf.inv(e.coeff));
+                double* dst = acc.at(k, e.slot);
+                for (int t = 0; t < dim; ++t) dst[t] += msg[t];
+            }
+        }
+    }
+    if (incoming_out) *incoming_out = acc;
+    ura::LatentGrid out(zt.rows, zt.cols, dim);
+    std::vector<double> cat(2 * dim), res(dim);
+    for (int k = 0; k < zt.rows; ++k)
+        for (int l = 0; l < zt.cols; ++l) {
+            std::copy(zt.at(k, l), zt.at(k, l) + dim, cat.data());
+            std::copy(acc.at(k, l), acc.at(k, l) + dim, cat.data() + dim);
+            p.fuse_b.apply_gelu(cat.data(), res.data());
+            for (int t = 0; t < dim; ++t) out.at(k, l)[t] = zt.at(k, l)[t] + res[t];
+        }
+    return out;
+}
+
+// Stacked denoiser: the reference's layer functions, N times.
+class StackedDenoiser : public ura::Denoiser {
+public:
+    StackedDenoiser(ura::GfContext gf, const Model& m) : gf_(std::move(gf)), m_(m) {}
+
+    ura::LogitGrid forward(const ura::MaskedGrid& x, const ura::EvidenceMatrix& s,
+                           const ura::ParityCheckMatrix& h,
+                           std::vector<ura::LatentGrid>* incoming) const {
+        if (m_.layers == 1 && m_.heads == 0 && !incoming) {
+            // ref-exact: the reference's own StructuredDenoiser end to end
+            ura::StructuredDenoiser den(gf_, m_.p[0]);
+            return den.logits(x, s, h, 0.0);
+        }
+        ura::LatentGrid z = ura::embed_grid(x, m_.p[0]);
+        for (int l = 0; l < m_.layers; ++l) {
+            ura::LatentGrid zt = ura::module_a(z, s, m_.p[l]);
+            ura::LatentGrid in;
+            if (m_.heads == 0)
+                z = ura::module_b(gf_, zt, h, m_.p[l], &in);
+            else
+                z = module_b_attn(gf_, zt, h, m_.p[l], m_.attn[l], m_.heads, &in);
+            if (incoming) incoming->push_back(std::move(in));
+        }
+        return ura::final_logits(z, m_.p[0]);
+    }
+
+    ura::LogitGrid logits(const ura::MaskedGrid& x, const ura::EvidenceMatrix& s,
+                          const ura::ParityCheckMatrix& h, double) const override {
+        return forward(x, s, h, nullptr);
+    }
+
+private:
+    ura::GfContext gf_;
+    const Model& m_;
+};
+
+// §7.1(3) rank adapter: confidences 0 for the k_low lowest rows (ties -> lower row), 1 otherwise.
+std::vector<double> rank_confidences(const std::vector<double>& conf, int k_low) {
+    const int k = int(conf.size());
+    std::vector<int> order(k);
+    for (int i = 0; i < k; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return conf[a] < conf[b]; });
+    std::vector<double> out(k, 1.0);
+    for (int i = 0; i < k_low; ++i) out[order[i]] = 0.0;
+    return out;
+}
+
+void refine_one(const Model& model, const ura::GfContext& gf, const ura::ParityCheckMatrix& h,
+                int K, const double* S, const cider_schedule* sc, const cider_remask* rm,
+                int32_t* grid, double* final_logits, int32_t* first, int32_t* rows,
+                int32_t* steps, int32_t* mask) {
+    const int q = model.q, L = h.slots();
+    StackedDenoiser den(gf, model);
+    ura::EvidenceMatrix s(L, q);
+    std::copy(S, S + size_t(L) * q, s.v.begin());
+    ura::RevealSchedule sched;
+    sched.steps = sc->steps;
+    sched.tau_max = sc->tau_max;
+    sched.tau_min = sc->tau_min;
+    sched.first_reveal = sc->first_reveal != 0;
+    ura::RefineTrace trace;
+    ura::LogitGrid fl;
+    ura::SymbolGrid out;
+    std::vector<int> last_mask(K, 0);
+    const int mode = rm ? rm->mode : CIDER_REMASK_NONE;
+    if (mode == CIDER_REMASK_THRESHOLD) {
+        ura::RemaskConfig cfg;
+        cfg.thresholds.assign(rm->thresholds, rm->thresholds + rm->n_thresholds);
+        ura::validate_remask_config(cfg);
+        // run_with_remasking, unrolled so final-pass logits and the selected rows are observable;
+        // every call below is the reference's own (refine.cpp:277-292).
+        ura::MaxProbScorer scorer;
+        out = ura::run_refinement(den, s, h, sched, K, L, &trace, &fl);
+        for (double thr : cfg.thresholds) {
+            auto conf = scorer.score_rows(out, fl);
+            bool any = false;
+            for (double c : conf) any = any || c < thr;
+            if (!any) break;
+            for (int k = 0; k < K; ++k) last_mask[k] = conf[k] < thr;
+            out = ura::remask_pass(out, conf, thr, den, s, h, sched, &trace, &fl);
+        }
+    } else {
+        out = ura::run_refinement(den, s, h, sched, K, L, &trace, &fl);
+        if (mode == CIDER_REMASK_RANK) {
+            ura::MaxProbScorer scorer;
+            auto conf = scorer.score_rows(out, fl);
+            int k_low = int(std::floor(rm->rank_fraction * K));
+            if (k_low > 0) {
+                auto adj = rank_confidences(conf, k_low);
+                for (int k = 0; k < K; ++k) last_mask[k] = adj[k] < 0.5;
+                out = ura::remask_pass(out, adj, 0.5, den, s, h, sched, &trace, &fl);
+            }
+        }
+    }
+    std::copy(out.v.begin(), out.v.end(), grid);
+    if (final_logits) std::copy(fl.v.begin(), fl.v.end(), final_logits);
+    if (first) *first = trace.pass_first_reveals.empty() ? 0 : trace.pass_first_reveals.front();
+    for (int i = 0; i < CIDER_MAX_THRESHOLDS; ++i) {
+        if (rows) rows[i] = i < int(trace.remask_rows_per_stage.size()) ? trace.remask_rows_per_stage[i] : 0;
+        if (steps) steps[i] = i < int(trace.remask_steps_per_stage.size()) ? trace.remask_steps_per_stage[i] : 0;
+    }
+    if (mask) std::copy(last_mask.begin(), last_mask.end(), mask);
+}
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// ura::DenoiserParams::random_init flattened in draw order (denoiser.cpp:41-69).
+int ref_random_init(int q, int dim, uint64_t seed, double* out) {
+    return guarded([&] {
+        auto p = ura::DenoiserParams::random_init(q, dim, seed);
+        size_t off = 0;
+        auto put = [&](const std::vector<double>& v) {
+            std::copy(v.begin(), v.end(), out + off);
+            off += v.size();
+        };
+        put(p.embed);
+        put(p.out_proj);
+        put(p.sym_embed);
+        for (const ura::TwoLayerMap* t : {&p.gate_a, &p.check_agg, &p.fuse_b}) {
+            put(t->w1);
+            put(t->b1);
+            put(t->w2);
+            put(t->b2);
+        }
+    });
+}
+
+// build_random_ldpc(gf, L, P, w, make_rng(seed)) (ldpc.cpp:80-120); edges sorted (check, slot).
+int ref_build_ldpc(int m, int slots, int checks, int col_weight, uint64_t seed, int32_t* edges) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        auto rng = ura::make_rng(seed);
+        auto h = ura::build_random_ldpc(gf, slots, checks, col_weight, rng);
+        for (int e = 0; e < h.edge_count(); ++e) {
+            edges[3 * e] = h.edge(e).check;
+            edges[3 * e + 1] = h.edge(e).slot;
+            edges[3 * e + 2] = h.edge(e).coeff;
+        }
+    });
+}
+
+// sample_codewords(gf, derive_generator(gf, H), K, make_rng(seed)) (ldpc.cpp:153-195).
+int ref_sample_codewords(int m, const cider_code_desc* code, int k, uint64_t seed, int32_t* out) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        auto h = make_h(gf.q(), code);
+        auto gen = ura::derive_generator(gf, h);
+        auto rng = ura::make_rng(seed);
+        auto g = ura::sample_codewords(gf, gen, k, rng);
+        std::copy(g.v.begin(), g.v.end(), out);
+        auto syn_ok = true;
+        for (int r = 0; r < k; ++r) {
+            std::vector<int> cw(g.v.begin() + size_t(r) * g.cols, g.v.begin() + size_t(r + 1) * g.cols);
+            for (int x : h.syndrome(gf, cw)) syn_ok = syn_ok && x == 0;
+        }
+        if (!syn_ok) throw std::runtime_error("ref_sample_codewords: nonzero syndrome");
+    });
+}
+
+int ref_gf_mul(int m, int a, int b) { return ura::GfContext::with_default_poly(m).mul(a, b); }
+int ref_gf_inv(int m, int a) { return ura::GfContext::with_default_poly(m).inv(a); }
+
+int ref_ser_cer(int K, int L, const int32_t* truth, const int32_t* pred, double* ser, double* cer) {
+    return guarded([&] {
+        ura::SymbolGrid t(K, L), p(K, L);
+        std::copy(truth, truth + K * L, t.v.begin());
+        std::copy(pred, pred + K * L, p.v.begin());
+        auto r = ura::ser_cer(t, p);
+        *ser = r.ser;
+        *cer = r.cer;
+    });
+}
+
+// One denoiser forward (Denoiser::logits) for one bin; incoming: layers x K x L x D (nullable).
+int ref_denoise(const cider_model_desc* md, const double* weights, const cider_code_desc* code,
+                int K, const int32_t* X, const double* S, double* logits, double* incoming) {
+    return guarded([&] {
+        Model model(md, weights);
+        auto gf = make_gf(md);
+        auto h = make_h(gf.q(), code);
+        const int L = h.slots(), q = gf.q();
+        ura::MaskedGrid x(K, L);
+        std::copy(X, X + K * L, x.v.begin());
+        ura::EvidenceMatrix s(L, q);
+        std::copy(S, S + size_t(L) * q, s.v.begin());
+        StackedDenoiser den(gf, model);
+        std::vector<ura::LatentGrid> in;
+        auto lam = den.forward(x, s, h, incoming ? &in : nullptr);
+        if (logits) std::copy(lam.v.begin(), lam.v.end(), logits);
+        if (incoming)
+            for (size_t l = 0; l < in.size(); ++l)
+                std::copy(in[l].v.begin(), in[l].v.end(), incoming + l * in[l].v.size());
+    });
+}
+
+// ura::reveal_step on caller-provided logits (refine.cpp:83-127).
+int ref_reveal_step(int K, int L, int q, const int32_t* X, const double* logits, int target,
+                    double tau, int first, int32_t* out) {
+    return guarded([&] {
+        ura::MaskedGrid x(K, L);
+        std::copy(X, X + K * L, x.v.begin());
+        ura::LogitGrid lam(K, L, q);
+        std::copy(logits, logits + size_t(K) * L * q, lam.v.begin());
+        auto y = ura::reveal_step(x, lam, target, tau, first != 0);
+        std::copy(y.v.begin(), y.v.end(), out);
+    });
+}
+
+// Full decode of B bins through the reference engine; bins fan out over ura::parallel_for
+// (parallel.cpp:20-51) with `workers` threads (0 = URADEC_WORKERS / hardware_concurrency).
+int ref_refine(const cider_model_desc* md, const double* weights, const cider_code_desc* code,
+               int B, int K, const double* S, const cider_schedule* sched,
+               const cider_remask* remask, int32_t* grid, double* final_logits,
+               int32_t* first_reveals, int32_t* remask_rows, int32_t* remask_steps,
+               int32_t* remask_mask, int workers) {
+    return guarded([&] {
+        Model model(md, weights);
+        auto gf = make_gf(md);
+        auto h = make_h(gf.q(), code);
+        const int L = h.slots(), q = gf.q();
+        ura::parallel_for(
+            B,
+            [&](int b) {
+                refine_one(model, gf, h, K, S + size_t(b) * L * q, sched, remask,
+                           grid + size_t(b) * K * L,
+                           final_logits ? final_logits + size_t(b) * K * L * q : nullptr,
+                           first_reveals ? first_reveals + b : nullptr,
+                           remask_rows ? remask_rows + size_t(b) * CIDER_MAX_THRESHOLDS : nullptr,
+                           remask_steps ? remask_steps + size_t(b) * CIDER_MAX_THRESHOLDS : nullptr,
+                           remask_mask ? remask_mask + size_t(b) * K : nullptr);
+            },
+            workers);
+    });
+}
+
+// Reference GF(Q) FFT-BP check update (bp.cpp:128-149) — the north_star-named WHT kernel's oracle.
+int ref_check_update_wht(int m, int n_in, const double* incoming, const int32_t* coeffs,
+                         int target_coeff, double* out) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        const int q = gf.q();
+        std::vector<std::vector<double>> in(n_in, std::vector<double>(q));
+        std::vector<int> c(n_in);
+        for (int i = 0; i < n_in; ++i) {
+            std::copy(incoming + size_t(i) * q, incoming + size_t(i + 1) * q, in[i].begin());
+            c[i] = coeffs[i];
+        }
+        auto r = ura::check_update_wht(gf, in, c, target_coeff);
+        std::copy(r.begin(), r.end(), out);
+    });
+}
+
+int ref_check_update_direct(int m, int n_in, const double* incoming, const int32_t* coeffs,
+                            int target_coeff, double* out) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        const int q = gf.q();
+        std::vector<std::vector<double>> in(n_in, std::vector<double>(q));
+        std::vector<int> c(n_in);
+        for (int i = 0; i < n_in; ++i) {
+            std::copy(incoming + size_t(i) * q, incoming + size_t(i + 1) * q, in[i].begin());
+            c[i] = coeffs[i];
+        }
+        auto r = ura::check_update_direct(gf, in, c, target_coeff);
+        std::copy(r.begin(), r.end(), out);
+    });
+}
+
+int ref_cosine_target(int t, int steps, int initially_masked, int base) {
+    return base + int(std::lround(ura::cosine_fraction(t, steps) * initially_masked));
+}
+double ref_infer_temperature(int t, int steps, double tmax, double tmin) {
+    return ura::infer_temperature(t, steps, tmax, tmin);
+}
+int ref_remask_steps(int steps, int k_low, int k) { return ura::remask_steps(steps, k_low, k); }
+
+} // extern "C"

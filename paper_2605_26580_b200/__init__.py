@@ -1,0 +1,456 @@
+"""B200-native CIDER refinement decoder — Python mirror of the reference decoder API.
+
+The product is ``_lib/libcider.so`` (host C++ + hand-written sm_100a CUDA) behind the C ABI in
+``include/cider.h``. This module binds it with ctypes (no PyTorch on the path) and mirrors the
+reference's C++ interface for the hot path (/root/reference/proj/include/ura):
+
+  reference (C++)                                   here
+  ura::DenoiserParams::random_init (denoiser.cpp:41) weights_init(model, seed)
+  ura::StructuredDenoiser::logits  (denoiser.hpp:109) StructuredDenoiser(...).logits(x, s, mask_ratio)
+  ura::RevealSchedule / RemaskConfig (refine.hpp:13-36) RevealSchedule / RemaskConfig
+  ura::run_refinement              (refine.hpp:60-62) run_refinement(den, s, sched, k)
+  ura::run_with_remasking          (refine.hpp:104)   run_with_remasking(den, s, sched, remask, k)
+  ura::ser_cer                     (metrics.hpp:19-28) ser_cer(truth, pred)
+
+Errors follow the reference: std::domain_error -> ValueError (status 3), std::runtime_error ->
+RuntimeError (status 4), with the same message prefixes. There is no CPU fallback: without the
+built library, or without a B200, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libcider.so")
+
+FP32, BF16 = 0, 1
+REMASK_NONE, REMASK_THRESHOLD, REMASK_RANK = 0, 1, 2
+MAX_THRESHOLDS = 8
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("m", C.c_int), ("prim_poly", C.c_uint32), ("dim", C.c_int), ("hidden", C.c_int),
+                ("layers", C.c_int), ("heads", C.c_int), ("tau_demix", C.c_double),
+                ("evidence_scale", C.c_double), ("precision", C.c_int)]
+
+
+class CodeDesc(C.Structure):
+    _fields_ = [("checks", C.c_int), ("slots", C.c_int), ("n_edges", C.c_int), ("edges", C.POINTER(C.c_int32))]
+
+
+class ScheduleDesc(C.Structure):
+    _fields_ = [("steps", C.c_int), ("tau_max", C.c_double), ("tau_min", C.c_double), ("first_reveal", C.c_int)]
+
+
+class RemaskDesc(C.Structure):
+    _fields_ = [("mode", C.c_int), ("n_thresholds", C.c_int), ("thresholds", C.c_double * MAX_THRESHOLDS),
+                ("rank_fraction", C.c_double)]
+
+
+class TraceDesc(C.Structure):
+    _fields_ = [("first_reveals", C.POINTER(C.c_int32)), ("remask_rows", C.POINTER(C.c_int32)),
+                ("remask_steps", C.POINTER(C.c_int32)), ("remask_mask", C.POINTER(C.c_int32))]
+
+
+class WorkloadDesc(C.Structure):
+    _fields_ = [("m", C.c_int), ("slots", C.c_int), ("checks", C.c_int), ("col_weight", C.c_int), ("k", C.c_int),
+                ("snr_db", C.c_double), ("p_erase", C.c_double), ("p_false", C.c_double),
+                ("master_seed", C.c_uint64)]
+
+
+_lib_handle = None
+
+
+def lib() -> C.CDLL:
+    """Load libcider.so; raises if it was not built (there is no fallback)."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libcider.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        h = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        h.cider_last_error.restype = C.c_char_p
+        h.cider_weights_count.restype = C.c_size_t
+        h.cider_weights_count.argtypes = [C.POINTER(ModelDesc)]
+        h.cider_weights_init.argtypes = [C.POINTER(ModelDesc), C.c_uint64, P]
+        h.cider_weights_init_f64.argtypes = [C.POINTER(ModelDesc), C.c_uint64, P]
+        h.cider_create.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.POINTER(C.c_void_p)]
+        h.cider_destroy.argtypes = [P]
+        h.cider_destroy.restype = None
+        h.cider_set_chunk.argtypes = [P, C.c_int]
+        h.cider_denoise.argtypes = [P, C.c_int, C.c_int, P, P, P, P]
+        h.cider_refine.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P, P,
+                                   C.POINTER(TraceDesc)]
+        h.cider_refine_device.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P]
+        h.cider_device_count.argtypes = [C.POINTER(C.c_int)]
+        h.cider_device_alloc.argtypes = [P, C.c_size_t, C.POINTER(C.c_void_p)]
+        h.cider_device_free.argtypes = [P, P]
+        h.cider_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p)]
+        h.cider_host_free.argtypes = [P]
+        h.cider_memcpy_h2d.argtypes = [P, P, P, C.c_size_t]
+        h.cider_memcpy_d2h.argtypes = [P, P, P, C.c_size_t]
+        h.cider_synchronize.argtypes = [P]
+        h.cider_flush_l2.argtypes = [P]
+        h.cider_event_record.argtypes = [P, C.c_int]
+        h.cider_event_elapsed.argtypes = [P, C.c_int, C.c_int, C.POINTER(C.c_float)]
+        h.cider_set_profiling.argtypes = [P, C.c_int]
+        h.cider_launch_count.argtypes = [P]
+        h.cider_launch_count.restype = C.c_int64
+        h.cider_kernel_stats.argtypes = [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        h.cider_reset_stats.argtypes = [P]
+        h.cider_nccl_unique_id.argtypes = [C.c_char_p]
+        h.cider_nccl_init.argtypes = [P, C.c_char_p, C.c_int, C.c_int]
+        h.cider_nccl_allgather.argtypes = [P, P, P, C.c_size_t]
+        h.cider_workload_code.argtypes = [C.POINTER(WorkloadDesc), P]
+        h.cider_workload_bins.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
+        h.cider_ser_cer.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        _lib_handle = h
+    return _lib_handle
+
+
+def exported_symbols() -> list:
+    """Names declared in include/cider.h (used by the ABI test)."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "cider.h")
+    src = open(hdr).read()
+    return sorted(set(re.findall(r"\b(cider_[a-z0-9_]+)\s*\(", src)))
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().cider_last_error().decode()
+    if rc == 3:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---- configuration ---------------------------------------------------------------------------
+@dataclass
+class Model:
+    """Hyper-parameters (cider_model_desc). ref-exact = layers 1, hidden = dim, heads 0."""
+    m: int
+    dim: int
+    hidden: int
+    layers: int = 1
+    heads: int = 0
+    tau_demix: float = 1.0
+    evidence_scale: float = 1.0
+    precision: int = FP32
+    prim_poly: int = 0
+
+    @property
+    def q(self) -> int:
+        return 1 << self.m
+
+    def desc(self) -> ModelDesc:
+        return ModelDesc(self.m, self.prim_poly, self.dim, self.hidden, self.layers, self.heads, self.tau_demix,
+                         self.evidence_scale, self.precision)
+
+    @staticmethod
+    def ref_exact(m: int, dim: int, precision: int = FP32) -> "Model":
+        return Model(m=m, dim=dim, hidden=dim, layers=1, heads=0, precision=precision)
+
+
+@dataclass
+class RevealSchedule:
+    """ura::RevealSchedule (refine.hpp:13-18)."""
+    steps: int = 12
+    tau_max: float = 1.0
+    tau_min: float = 1.0
+    first_reveal: bool = True
+
+    def desc(self) -> ScheduleDesc:
+        return ScheduleDesc(self.steps, self.tau_max, self.tau_min, 1 if self.first_reveal else 0)
+
+
+@dataclass
+class RemaskConfig:
+    """ura::RemaskConfig (refine.hpp:33-36) + the rank-fraction mode of BASELINE config 3."""
+    thresholds: Sequence[float] = ()
+    rank_fraction: Optional[float] = None
+
+    def desc(self) -> RemaskDesc:
+        d = RemaskDesc()
+        if self.rank_fraction is not None:
+            d.mode = REMASK_RANK
+            d.rank_fraction = float(self.rank_fraction)
+        elif len(self.thresholds):
+            if len(self.thresholds) > MAX_THRESHOLDS:
+                raise ValueError("remask: too many thresholds")
+            d.mode = REMASK_THRESHOLD
+            d.n_thresholds = len(self.thresholds)
+            for i, t in enumerate(self.thresholds):
+                d.thresholds[i] = float(t)
+        else:
+            d.mode = REMASK_NONE
+        return d
+
+
+def round_bf16(a: np.ndarray) -> np.ndarray:
+    """Round to bf16 (nearest-even) and return as float64: what BF16 mode uploads."""
+    f = np.ascontiguousarray(a, dtype=np.float32)
+    u = f.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32).astype(np.float64)
+
+
+def model_weights_as_run(model: Model, weights: np.ndarray) -> np.ndarray:
+    """The fp64 values the device actually computes with: fp32-rounded (FP32) or bf16-rounded (BF16)."""
+    w = np.asarray(weights, dtype=np.float32).astype(np.float64)
+    return round_bf16(w) if model.precision == BF16 else w
+
+
+def weights_count(model: Model) -> int:
+    d = model.desc()
+    return int(lib().cider_weights_count(C.byref(d)))
+
+
+def weights_init(model: Model, seed: int = 1, f64: bool = False) -> np.ndarray:
+    """DenoiserParams::random_init generalised to stacked layers (flat layout of cider.h)."""
+    d = model.desc()
+    n = weights_count(model)
+    if n == 0:
+        raise ValueError("bad model dimensions")
+    out = np.empty(n, dtype=np.float64 if f64 else np.float32)
+    fn = lib().cider_weights_init_f64 if f64 else lib().cider_weights_init
+    _check(fn(C.byref(d), C.c_uint64(seed), _ptr(out)))
+    return out
+
+
+def code_desc(edges: np.ndarray, checks: int, slots: int):
+    e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 3)
+    return CodeDesc(checks, slots, int(e.shape[0]), e.ctypes.data_as(C.POINTER(C.c_int32))), e
+
+
+# ---- the context ------------------------------------------------------------------------------
+class Context:
+    """One cider_ctx: weights + Tanner tables resident on one B200."""
+
+    def __init__(self, model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int,
+                 device: int = 0):
+        self.model = model
+        self.checks, self.slots = checks, slots
+        self._w = np.ascontiguousarray(weights, dtype=np.float32)
+        cd, self._edges = code_desc(edges, checks, slots)
+        md = model.desc()
+        h = C.c_void_p()
+        _check(lib().cider_create(C.byref(md), _ptr(self._w), C.byref(cd), device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cider_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_chunk(self, n: int):
+        _check(lib().cider_set_chunk(self.h, n))
+
+    def denoise(self, X: np.ndarray, S: np.ndarray, want_incoming: bool = False):
+        """One forward for B bins. X: B x K x L int32 (-1 = MASK), S: B x L x Q."""
+        X = np.ascontiguousarray(X, dtype=np.int32)
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        B, K, L = X.shape
+        q = self.model.q
+        logits = np.empty((B, K, L, q), dtype=np.float32)
+        inc = np.empty((B, self.model.layers, K, L, self.model.dim), dtype=np.float32) if want_incoming else None
+        _check(lib().cider_denoise(self.h, B, K, _ptr(X), _ptr(S), _ptr(logits), _ptr(inc)))
+        return (logits, inc) if want_incoming else logits
+
+    def refine(self, S: np.ndarray, K: int, sched: RevealSchedule, remask: Optional[RemaskConfig] = None,
+               want_final_logits: bool = False, want_trace: bool = False):
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        B, L, q = S.shape
+        grid = np.empty((B, K, L), dtype=np.int32)
+        fl = np.empty((B, K, L, q), dtype=np.float32) if want_final_logits else None
+        sd = sched.desc()
+        rd = (remask or RemaskConfig()).desc()
+        tr = None
+        trd = None
+        if want_trace:
+            tr = {"first_reveals": np.zeros(B, np.int32), "remask_rows": np.zeros((B, MAX_THRESHOLDS), np.int32),
+                  "remask_steps": np.zeros((B, MAX_THRESHOLDS), np.int32), "remask_mask": np.zeros((B, K), np.int32)}
+            trd = TraceDesc(*(v.ctypes.data_as(C.POINTER(C.c_int32)) for v in tr.values()))
+        _check(lib().cider_refine(self.h, B, K, _ptr(S), C.byref(sd), C.byref(rd), _ptr(grid), _ptr(fl),
+                                  C.byref(trd) if trd is not None else None))
+        out = [grid]
+        if want_final_logits:
+            out.append(fl)
+        if want_trace:
+            out.append(tr)
+        return out[0] if len(out) == 1 else tuple(out)
+
+    # instrumentation
+    def launch_count(self) -> int:
+        return int(lib().cider_launch_count(self.h))
+
+    def set_profiling(self, on: bool):
+        _check(lib().cider_set_profiling(self.h, 1 if on else 0))
+
+    def reset_stats(self):
+        _check(lib().cider_reset_stats(self.h))
+
+    def kernel_stats(self) -> dict:
+        out = {}
+        i = 0
+        name = C.create_string_buffer(128)
+        while True:
+            n, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            rc = lib().cider_kernel_stats(self.h, i, name, 128, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by))
+            if rc != 0:
+                break
+            out[name.value.decode()] = {"launches": n.value, "ms": ms.value, "flops": fl.value, "bytes": by.value}
+            i += 1
+        return out
+
+
+# ---- reference-shaped API ------------------------------------------------------------------------
+class StructuredDenoiser:
+    """ura::StructuredDenoiser (denoiser.hpp:109-130) backed by a device context."""
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def logits(self, x: np.ndarray, s: np.ndarray, mask_ratio: float = 0.0) -> np.ndarray:
+        """x: K x L (or B x K x L), s: L x Q (or B x L x Q). mask_ratio is ignored."""
+        single = x.ndim == 2
+        X = x[None] if single else x
+        S = s[None] if single else s
+        lg = self.ctx.denoise(X, S)
+        return lg[0] if single else lg
+
+
+def run_refinement(den: StructuredDenoiser, s: np.ndarray, sched: RevealSchedule, k: int, **kw):
+    """ura::run_refinement (refine.hpp:60-62); s: L x Q or B x L x Q."""
+    single = s.ndim == 2
+    out = den.ctx.refine(s[None] if single else s, k, sched, None, **kw)
+    if single:
+        return tuple(o[0] if isinstance(o, np.ndarray) else o for o in out) if isinstance(out, tuple) else out[0]
+    return out
+
+
+def run_with_remasking(den: StructuredDenoiser, s: np.ndarray, sched: RevealSchedule, remask: RemaskConfig, k: int,
+                       **kw):
+    """ura::run_with_remasking (refine.hpp:104-107) with the MaxProbScorer (refine.cpp:218-225)."""
+    single = s.ndim == 2
+    out = den.ctx.refine(s[None] if single else s, k, sched, remask, **kw)
+    if single:
+        return tuple(o[0] if isinstance(o, np.ndarray) else o for o in out) if isinstance(out, tuple) else out[0]
+    return out
+
+
+# ---- workload + metrics (host C++) ------------------------------------------------------------
+@dataclass
+class Workload:
+    m: int
+    slots: int
+    checks: int
+    k: int
+    snr_db: float
+    p_erase: float = 0.0
+    p_false: float = 0.0
+    col_weight: int = 3
+    master_seed: int = 0
+
+    def desc(self) -> WorkloadDesc:
+        return WorkloadDesc(self.m, self.slots, self.checks, self.col_weight, self.k, self.snr_db, self.p_erase,
+                            self.p_false, self.master_seed)
+
+    def code(self) -> np.ndarray:
+        e = np.empty((self.slots * self.col_weight, 3), dtype=np.int32)
+        d = self.desc()
+        _check(lib().cider_workload_code(C.byref(d), _ptr(e)))
+        return e
+
+    def bins(self, edges: np.ndarray, first: int, n: int, threads: int = 0, out_S: Optional[np.ndarray] = None):
+        d = self.desc()
+        edges = np.ascontiguousarray(edges, dtype=np.int32)
+        truth = np.empty((n, self.k, self.slots), dtype=np.int32)
+        S = out_S if out_S is not None else np.empty((n, self.slots, 1 << self.m), dtype=np.float32)
+        _check(lib().cider_workload_bins(C.byref(d), _ptr(edges), first, n, _ptr(truth), _ptr(S), threads))
+        return truth, S
+
+
+def ser_cer(truth: np.ndarray, pred: np.ndarray):
+    """Mean permutation-invariant SER/CER over bins (ura::ser_cer, metrics.cpp:124-145)."""
+    truth = np.ascontiguousarray(truth, dtype=np.int32)
+    pred = np.ascontiguousarray(pred, dtype=np.int32)
+    if truth.ndim == 2:
+        truth, pred = truth[None], pred[None]
+    n, K, L = truth.shape
+    s, c = C.c_double(), C.c_double()
+    _check(lib().cider_ser_cer(n, K, L, _ptr(truth), _ptr(pred), C.byref(s), C.byref(c)))
+    return s.value / n, c.value / n
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib().cider_device_count(C.byref(n)))
+    return n.value
+
+
+# ---- BASELINE.json configurations ----------------------------------------------------------------
+@dataclass
+class Config:
+    name: str
+    workload: Workload
+    model: Model
+    bins: int
+    steps: int
+    remask: Optional[RemaskConfig] = None
+    extra: dict = field(default_factory=dict)
+
+
+def configs() -> dict:
+    """The five BASELINE.json configs (SURVEY §8 shape key)."""
+    c1 = Config("c1", Workload(m=4, slots=16, checks=8, k=2, snr_db=10.0),
+                Model(m=4, dim=64, hidden=256, layers=2, heads=4, precision=FP32), bins=64, steps=4)
+    c2 = Config("c2", Workload(m=6, slots=32, checks=16, k=4, snr_db=6.0, p_erase=0.05, p_false=0.05),
+                Model(m=6, dim=128, hidden=512, layers=4, heads=8, precision=BF16), bins=4096, steps=8)
+    c3 = Config("c3", Workload(m=8, slots=64, checks=32, k=8, snr_db=4.0, p_erase=0.1, p_false=0.1),
+                Model(m=8, dim=256, hidden=1024, layers=6, heads=8, precision=BF16), bins=16384, steps=16,
+                remask=RemaskConfig(rank_fraction=0.25))
+    c4 = Config("c4", Workload(m=6, slots=256, checks=128, k=4, snr_db=6.0, p_erase=0.05, p_false=0.05),
+                Model(m=6, dim=256, hidden=1024, layers=6, heads=8, precision=BF16), bins=8192, steps=16)
+    c5 = Config("c5", c3.workload, c3.model, bins=262144, steps=16, remask=RemaskConfig(rank_fraction=0.25))
+    return {c.name: c for c in (c1, c2, c3, c4, c5)}
+
+
+def forward_count(cfg: Config) -> int:
+    """Denoiser forwards per bin: T + 1, plus T_rm + 1 when remasking (refine.cpp:23-26, 180-185)."""
+    f = cfg.steps + 1
+    if cfg.remask is not None and cfg.remask.rank_fraction:
+        k_low = int(np.floor(cfg.remask.rank_fraction * cfg.workload.k))
+        if k_low > 0:
+            f += max(1, (cfg.steps * k_low) // cfg.workload.k) + 1
+    return f
+
+
+def flops_per_bin(cfg: Config) -> float:
+    """Algorithmic FLOPs per bin:
+    F = 2 fwd [N (4KLQD + 6KLDH + 2K|E|QD + 2K|E|DH) + KLQD + F_attn],
+    F_attn = N K|E| (2D^2 + 2(d_c-1)D) when heads > 0."""
+    w, m = cfg.workload, cfg.model
+    K, L, Q, D, H, N = w.k, w.slots, m.q, m.dim, m.hidden, m.layers
+    E = L * w.col_weight
+    dc = E / w.checks
+    per = N * (4 * K * L * Q * D + 6 * K * L * D * H + 2 * K * E * Q * D + 2 * K * E * D * H) + K * L * Q * D
+    if m.heads:
+        per += N * K * E * (2 * D * D + 2 * (dc - 1) * D)
+    return 2.0 * forward_count(cfg) * per

@@ -1,0 +1,1130 @@
+// engine.cu — libcider's device engine and C ABI (include/cider.h).
+//
+// One cider_ctx per device: it owns the weights (uploaded once, fp32 or bf16), the Tanner
+// tables (edge slots, coefficient permutations, CSR lists), one CUDA stream and a chunk
+// workspace sized for HBM. A forward (= StructuredDenoiser::logits, denoiser.cpp:253-259)
+// is a fixed chain of GEMMs (tcgen05 in BF16 mode, SIMT in FP32 mode) and HBM-bound Tanner
+// kernels; the refinement loop (refine.cpp:134-292) runs entirely on the device — reveal,
+// residual forcing, the gamma=0 pass, remask selection — with no host round trip except the
+// per-stage bucket sizes of threshold remasking.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "host/host.hpp"
+#include "kernels/common.cuh"
+#include "kernels/gemm_simt.cuh"
+#include "kernels/gemm_tc.cuh"
+#include "kernels/path.cuh"
+
+namespace cider {
+const char* host_last_error();
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+const double kPi = 3.14159265358979323846;
+double cosine_fraction(int t, int T) { return 0.5 * (1.0 - std::cos(kPi * t / T)); }   // refine.cpp:11-15
+double infer_temperature(int t, int T, double tmax, double tmin) {                       // refine.cpp:17-21
+    if (T <= 1) return tmin;
+    double w = 0.5 * (1.0 + std::cos(kPi * (t - 1) / (T - 1)));
+    return tmax * w + tmin * (1.0 - w);
+}
+int remask_steps(int T, int low, int K) {                                                // refine.cpp:23-26
+    int t = int((static_cast<long long>(T) * low) / K);
+    return t < 1 ? 1 : t;
+}
+
+// ---- TMA descriptors -------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// bf16 row-major [rows x cols] with row stride ld (elements), box = box_rows x 64, SWIZZLE_128B
+CUtensorMap make_map(const void* ptr, int64_t rows, int cols, int ld, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+    cuuint32_t box[2] = {64, cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+// ---- device allocations ------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t n) {
+        if (n <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        ck(cudaMalloc(&p, n), "cudaMalloc");
+        bytes = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct LayerW {
+    // matrices in the activation type (fp32 or bf16), biases fp32
+    void *g1, *g2, *a1, *a2, *f1, *f2, *ak;
+    float *gb1, *gb2, *ab1, *ab2, *fb1, *fb2, *aq;
+};
+
+struct Stat {
+    int64_t launches = 0;
+    double ms = 0.0, flops = 0.0, bytes = 0.0;
+};
+
+} // namespace
+} // namespace cider
+
+using namespace cider;
+
+struct cider_ctx {
+    std::mutex mu;
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    cider_model_desc md{};
+    int Q = 0, D = 0, H = 0, N = 0, heads = 0;
+    bool bf16 = false;
+    size_t act_size = 4;
+    std::unique_ptr<Gf> gf;
+    std::unique_ptr<Tanner> tg;
+    int L = 0, P = 0, E = 0;
+    // weights
+    std::vector<DevBuf> wbufs;
+    float* Etab = nullptr;                 // (Q+1) x D fp32
+    void *W = nullptr, *Wt = nullptr, *Vt = nullptr;
+    std::vector<LayerW> lw;
+    // Tanner tables
+    int *e_slot = nullptr, *e_check = nullptr, *check_ptr = nullptr, *slot_ptr = nullptr, *slot_edge = nullptr;
+    uint8_t *perm_in = nullptr, *perm_out = nullptr;
+    // workspace
+    int chunk_req = 0;
+    int cap_bins = 0, cap_K = 0;
+    std::map<std::string, DevBuf> ws;
+    std::map<std::tuple<const void*, int64_t, int, int, int>, CUtensorMap> maps;
+    // instrumentation
+    int64_t launches = 0;
+    bool profiling = false;
+    std::map<std::string, Stat> stats;
+    std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t, double, double>> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t events[64] = {};
+    DevBuf flush_buf;
+    // NCCL (dlopen'ed)
+    void* nccl_lib = nullptr;
+    void* nccl_comm = nullptr;
+
+    ~cider_ctx();
+};
+
+namespace cider {
+namespace {
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CIDER_OK;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return CIDER_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CIDER_ERUNTIME;
+    }
+}
+
+DevBuf& wbuf(cider_ctx& c, size_t bytes) {
+    c.wbufs.emplace_back();
+    c.wbufs.back().ensure(std::max<size_t>(bytes, 16));
+    return c.wbufs.back();
+}
+
+float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// Upload a host fp32 matrix, optionally transposed, in the activation type.
+void* upload_mat(cider_ctx& c, const float* src, int rows, int cols, bool transpose) {
+    const int R = transpose ? cols : rows, C = transpose ? rows : cols;
+    std::vector<float> t(size_t(R) * C);
+    for (int r = 0; r < rows; ++r)
+        for (int q = 0; q < cols; ++q) {
+            float v = src[size_t(r) * cols + q];
+            if (transpose) t[size_t(q) * rows + r] = v; else t[size_t(r) * cols + q] = v;
+        }
+    DevBuf& b = wbuf(c, t.size() * c.act_size);
+    if (c.bf16) {
+        std::vector<bf16> h(t.size());
+        for (size_t i = 0; i < t.size(); ++i) h[i] = __float2bfloat16_rn(t[i]);
+        ck(cudaMemcpy(b.p, h.data(), h.size() * 2, cudaMemcpyHostToDevice), "upload");
+    } else {
+        ck(cudaMemcpy(b.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice), "upload");
+    }
+    return b.p;
+}
+float* upload_vec(cider_ctx& c, const float* src, size_t n) {
+    std::vector<float> t(src, src + n);
+    if (c.bf16)
+        for (float& v : t) v = bf16_round(v); // BF16 mode: the whole model is bf16-valued
+    DevBuf& b = wbuf(c, n * 4);
+    ck(cudaMemcpy(b.p, t.data(), n * 4, cudaMemcpyHostToDevice), "upload");
+    return b.as<float>();
+}
+template <class T>
+T* upload_raw(cider_ctx& c, const std::vector<T>& v) {
+    DevBuf& b = wbuf(c, v.size() * sizeof(T));
+    if (!v.empty()) ck(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return b.as<T>();
+}
+
+// ---- launch bookkeeping --------------------------------------------------------------------
+struct Launch {
+    cider_ctx& c;
+    std::string tag;
+    double flops, bytes;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Launch(cider_ctx& c_, const char* t, double f, double by) : c(c_), tag(t), flops(f), bytes(by) {
+        ++c.launches;
+        if (c.profiling) {
+            a = take();
+            cudaEventRecord(a, c.stream);
+        }
+    }
+    cudaEvent_t take() {
+        if (c.ev_pool.empty()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "event");
+            return e;
+        }
+        cudaEvent_t e = c.ev_pool.back();
+        c.ev_pool.pop_back();
+        return e;
+    }
+    ~Launch() {
+        if (c.profiling) {
+            b = take();
+            cudaEventRecord(b, c.stream);
+            c.pending.emplace_back(tag, a, b, flops, bytes);
+        }
+    }
+};
+
+void resolve_stats(cider_ctx& c) {
+    if (c.pending.empty()) return;
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    for (auto& [tag, a, b, f, by] : c.pending) {
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        Stat& s = c.stats[tag];
+        s.launches++;
+        s.ms += ms;
+        s.flops += f;
+        s.bytes += by;
+        c.ev_pool.push_back(a);
+        c.ev_pool.push_back(b);
+    }
+    c.pending.clear();
+}
+
+void check_launch(const char* what) { ck(cudaGetLastError(), what); }
+
+inline unsigned blocks_for(int64_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+// ---- GEMM dispatch -------------------------------------------------------------------------
+const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, int ld, int box_rows) {
+    auto key = std::make_tuple(p, rows, cols, ld, box_rows);
+    auto it = c.maps.find(key);
+    if (it != c.maps.end()) return it->second;
+    return c.maps.emplace(key, make_map(p, rows, cols, ld, box_rows)).first->second;
+}
+
+template <int BN>
+void launch_tc(cider_ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const tc::Args& args) {
+    using Lay = tc::SmemLayout<BN>;
+    static bool attr_set = false; // per process; same attribute for every device
+    if (!attr_set) {
+        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+           "smem attr");
+        attr_set = true;
+    }
+    int grid = std::min(args.tiles, c.sm_count);
+    tc::gemm_tc_kernel<BN><<<grid, tc::NUM_THREADS, Lay::TOTAL, c.stream>>>(a0, a1, b, args);
+}
+
+// C[M x N] = [A0 (M x K0) | A1 (M x K1)] . B[N x (K0+K1)]^T, then the epilogue.
+void gemm(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, int K1, const void* B, int64_t M,
+          int N, Epi ep) {
+    const int K = K0 + K1;
+    ep.M = int(M);
+    ep.N = N;
+    Launch lg(c, tag, 2.0 * double(M) * N * K, double(M) * K * c.act_size + double(N) * K * c.act_size);
+    if (!c.bf16) {
+        dim3 grid(unsigned((N + SG_BN - 1) / SG_BN), unsigned((M + SG_BM - 1) / SG_BM));
+        gemm_simt_f32<<<grid, 256, 0, c.stream>>>(reinterpret_cast<const float*>(A0), K0 ? (A1 ? K0 : K) : K, K0 ? K0 : K,
+                                                   reinterpret_cast<const float*>(A1), K1, reinterpret_cast<const float*>(B), K,
+                                                   int(M), N, K, ep);
+        check_launch(tag);
+        return;
+    }
+    if (K0 % 64 || K1 % 64 || N % 64) throw InvalidInput("BF16 mode needs Q, D, H multiples of 64");
+    const int BN = (N % 256 == 0) ? 256 : (N % 128 == 0) ? 128 : 64;
+    if (ep.kind == EP_LOGITS && BN != N) throw InvalidInput("BF16 mode needs Q <= 256 for the fused logits epilogue");
+    const CUtensorMap& a0 = map_for(c, A0, M, K0, A1 ? K0 : K, tc::BM);
+    const CUtensorMap& a1 = A1 ? map_for(c, A1, M, K1, K1, tc::BM) : a0;
+    const CUtensorMap& b = map_for(c, B, N, K, K, BN);
+    tc::Args args;
+    args.M = int(M);
+    args.N = N;
+    args.K = K;
+    args.K0 = A1 ? K0 : K;
+    args.tiles_n = N / BN;
+    args.tiles = int((M + tc::BM - 1) / tc::BM) * args.tiles_n;
+    args.ep = ep;
+    if (BN == 256) launch_tc<256>(c, a0, a1, b, args);
+    else if (BN == 128) launch_tc<128>(c, a0, a1, b, args);
+    else launch_tc<64>(c, a0, a1, b, args);
+    check_launch(tag);
+}
+
+Epi epi(int kind) {
+    Epi e;
+    std::memset(&e, 0, sizeof(e));
+    e.kind = kind;
+    return e;
+}
+
+// ---- workspace ------------------------------------------------------------------------------
+struct WS {
+    int* X;
+    float *Zf, *lbar, *ef, *Ztf, *accf, *keys, *logits, *kappa, *k1;
+    void *Zt, *Aq, *et, *hid, *Ztt, *U, *Ae, *Nn, *pooled, *mapped, *Mq, *accq, *acct;
+    int *amax, *init_masked, *nlow, *first_count;
+    uint32_t* upd;
+    float* S;  // staging for host evidence
+    int* Xio;  // staging for host grids
+    float* flog; // final-pass logits (internal layout), when requested
+};
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+void* wsbuf(cider_ctx& c, const char* name, size_t bytes) {
+    DevBuf& b = c.ws[name];
+    b.ensure(round_up(std::max<size_t>(bytes, 256), 256));
+    return b.p;
+}
+
+// Sizes (per bin) of the chunk workspace; rows padded to the 128-row GEMM tile.
+WS workspace(cider_ctx& c, int nb, int K, bool want_flog) {
+    const size_t Ms = round_up(size_t(nb) * c.L * K, 128), Me = round_up(size_t(nb) * c.E * K, 128);
+    const size_t A = c.act_size, Q = c.Q, D = c.D, H = c.H;
+    WS w{};
+    w.X = (int*)wsbuf(c, "X", Ms * 4);
+    w.Zf = (float*)wsbuf(c, "Zf", Ms * D * 4);
+    w.lbar = (float*)wsbuf(c, "lbar", Ms * Q * 4);
+    w.ef = (float*)wsbuf(c, "ef", Ms * D * 4);
+    w.Ztf = (float*)wsbuf(c, "Ztf", Ms * D * 4);
+    w.accf = (float*)wsbuf(c, "accf", Ms * D * 4);
+    w.kappa = (float*)wsbuf(c, "kappa", Ms * 4);
+    w.k1 = (float*)wsbuf(c, "k1", Ms * 4);
+    w.amax = (int*)wsbuf(c, "amax", Ms * 4);
+    w.Aq = wsbuf(c, "Aq", Ms * Q * A);
+    w.hid = wsbuf(c, "hid", std::max(Ms, Me) * H * A);
+    w.U = wsbuf(c, "U", Ms * Q * A);
+    w.Ae = wsbuf(c, "Ae", Me * Q * A);
+    w.Nn = wsbuf(c, "Nn", Me * D * A);
+    w.pooled = wsbuf(c, "pooled", Me * D * A);
+    w.mapped = wsbuf(c, "mapped", Me * D * A);
+    w.Mq = wsbuf(c, "Mq", Me * Q * A);
+    w.accq = wsbuf(c, "accq", Ms * Q * A);
+    w.keys = c.heads ? (float*)wsbuf(c, "keys", Me * D * 4) : nullptr;
+    w.logits = c.bf16 ? nullptr : (float*)wsbuf(c, "logits", Ms * Q * 4);
+    if (c.bf16) {
+        w.Zt = wsbuf(c, "Zt", Ms * D * A);
+        w.et = wsbuf(c, "et", Ms * D * A);
+        w.Ztt = wsbuf(c, "Ztt", Ms * D * A);
+        w.acct = wsbuf(c, "acct", Ms * D * A);
+    } else {
+        w.Zt = w.Zf;
+        w.et = w.ef;
+        w.Ztt = w.Ztf;
+        w.acct = w.accf;
+    }
+    w.init_masked = (int*)wsbuf(c, "init_masked", size_t(nb) * 4);
+    w.nlow = (int*)wsbuf(c, "nlow", size_t(nb) * 4);
+    w.first_count = (int*)wsbuf(c, "first_count", size_t(nb) * 4);
+    w.upd = (uint32_t*)wsbuf(c, "upd", size_t(nb) * 4);
+    w.S = (float*)wsbuf(c, "S", size_t(nb) * c.L * Q * 4);
+    w.Xio = (int*)wsbuf(c, "Xio", size_t(nb) * c.L * K * 4);
+    w.flog = want_flog ? (float*)wsbuf(c, "flog", Ms * Q * 4) : nullptr;
+    return w;
+}
+
+// chunk size: explicit, or sized so the workspace stays within ~60% of free HBM
+int chunk_bins(cider_ctx& c, int K) {
+    if (c.chunk_req > 0) return c.chunk_req;
+    const double A = double(c.act_size);
+    const double Ms = double(c.L) * K, Me = double(c.E) * K;
+    double per_bin = Ms * (c.D * 4.0 * 4 + c.Q * 4.0 * 2 + c.Q * A * 3 + c.D * A * 4 + 16) +
+                     Me * (c.Q * A * 2 + c.D * A * 3 + (c.heads ? c.D * 4.0 : 0)) + std::max(Ms, Me) * c.H * A +
+                     c.L * c.Q * 4.0;
+    size_t fr = 0, tot = 0;
+    ck(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    double budget = 0.6 * double(fr);
+    int nb = int(std::max(1.0, std::min(budget / per_bin, 65536.0)));
+    return nb;
+}
+
+// ---- one denoiser forward over nb bins (denoiser.cpp:253-259) -------------------------------
+struct FwdOpts {
+    float tau = 1.0f;
+    float* logits_out = nullptr;  // internal-layout fp32 logits [Ms x Q] (nullable)
+    float* incoming = nullptr;    // internal-layout [layers][Ms x D] (nullable)
+};
+
+void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, const FwdOpts& o) {
+    const int L = c.L, E = c.E, Q = c.Q, D = c.D, H = c.H;
+    const int64_t Ms = int64_t(nb) * L * K, Me = int64_t(nb) * E * K;
+    {
+        Launch lg(c, "embed", 0, double(Ms) * D * (4 + c.act_size));
+        if (c.bf16)
+            embed_kernel<bf16><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, w.Zf, (bf16*)w.Zt);
+        else
+            embed_kernel<float><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, w.Zf, nullptr);
+        check_launch("embed");
+    }
+    for (int li = 0; li < c.N; ++li) {
+        const LayerW& lw = c.lw[li];
+        // Module A (denoiser.cpp:141-160)
+        Epi e = epi(EP_LBAR);
+        e.out_f = w.lbar; e.ldo = Q; e.S = S; e.L = L; e.K = K; e.beta = float(c.md.evidence_scale);
+        gemm(c, "gemm_lbar", w.Zt, D, nullptr, 0, c.W, Ms, Q, e);
+        {
+            Launch lg(c, "demix", 0, double(Ms) * Q * (4 + c.act_size) + double(nb) * L * Q * 4);
+            if (c.bf16)
+                demix_kernel<bf16><<<blocks_for(int64_t(nb) * L * Q), 256, 0, c.stream>>>(w.lbar, S, int64_t(nb) * L, K, Q, float(c.md.tau_demix), (bf16*)w.Aq);
+            else
+                demix_kernel<float><<<blocks_for(int64_t(nb) * L * Q), 256, 0, c.stream>>>(w.lbar, S, int64_t(nb) * L, K, Q, float(c.md.tau_demix), (float*)w.Aq);
+            check_launch("demix");
+        }
+        e = epi(EP_STORE);
+        e.out_f = w.ef; e.out_t = c.bf16 ? w.et : nullptr; e.ldo = D;
+        gemm(c, "gemm_evid", w.Aq, Q, nullptr, 0, c.Vt, Ms, D, e);
+        e = epi(EP_GELU);
+        e.bias = lw.gb1; e.out_t = w.hid; e.ldo = H;
+        gemm(c, "gemm_gate1", w.Zt, D, w.et, D, lw.g1, Ms, H, e);
+        e = epi(EP_GATE);
+        e.bias = lw.gb2; e.z = w.Zf; e.e = w.ef; e.ldz = D; e.out_f = w.Ztf; e.out_t = c.bf16 ? w.Ztt : nullptr; e.ldo = D;
+        gemm(c, "gemm_gate2", w.hid, H, nullptr, 0, lw.g2, Ms, D, e);
+        // Module B (denoiser.cpp:181-228)
+        e = epi(EP_STORE);
+        e.out_t = w.U; e.ldo = Q;
+        gemm(c, "gemm_symproj", w.Ztt, D, nullptr, 0, c.W, Ms, Q, e);
+        {
+            Launch lg(c, "gather_perm", 0, double(Me) * Q * 2 * c.act_size);
+            if (c.bf16)
+                gather_perm_kernel<bf16><<<blocks_for(Me * Q), 256, 0, c.stream>>>((bf16*)w.U, c.e_slot, c.perm_in, L, E, K, Q, Me, (bf16*)w.Ae);
+            else
+                gather_perm_kernel<float><<<blocks_for(Me * Q), 256, 0, c.stream>>>((float*)w.U, c.e_slot, c.perm_in, L, E, K, Q, Me, (float*)w.Ae);
+            check_launch("gather_perm");
+        }
+        e = epi(EP_STORE);
+        e.out_t = w.Nn; e.ldo = D;
+        gemm(c, "gemm_backproj", w.Ae, Q, nullptr, 0, c.Wt, Me, D, e);
+        if (c.heads) {
+            e = epi(EP_STORE);
+            e.out_f = w.keys; e.ldo = D;
+            gemm(c, "gemm_attn_key", w.Nn, D, nullptr, 0, lw.ak, Me, D, e);
+            Launch lg(c, "pool_attn", 0, double(Me) * D * (2 * c.act_size + 4));
+            const unsigned groups = unsigned(int64_t(nb) * c.P * K);
+            if (c.bf16)
+                pool_attn_kernel<bf16, bf16><<<groups, 128, 0, c.stream>>>((bf16*)w.Nn, w.keys, lw.aq, c.check_ptr, c.P, E, K, D, c.heads, (bf16*)w.pooled);
+            else
+                pool_attn_kernel<float, float><<<groups, 128, 0, c.stream>>>((float*)w.Nn, w.keys, lw.aq, c.check_ptr, c.P, E, K, D, c.heads, (float*)w.pooled);
+            check_launch("pool_attn");
+        } else {
+            Launch lg(c, "pool_sum", 0, double(Me) * D * 2 * c.act_size);
+            if (c.bf16)
+                pool_sum_kernel<bf16, bf16><<<blocks_for(Me * D), 256, 0, c.stream>>>((bf16*)w.Nn, c.e_check, c.check_ptr, E, K, D, Me, (bf16*)w.pooled);
+            else
+                pool_sum_kernel<float, float><<<blocks_for(Me * D), 256, 0, c.stream>>>((float*)w.Nn, c.e_check, c.check_ptr, E, K, D, Me, (float*)w.pooled);
+            check_launch("pool_sum");
+        }
+        e = epi(EP_GELU);
+        e.bias = lw.ab1; e.out_t = w.hid; e.ldo = H;
+        gemm(c, "gemm_agg1", w.pooled, D, nullptr, 0, lw.a1, Me, H, e);
+        e = epi(EP_STORE);
+        e.bias = lw.ab2; e.out_t = w.mapped; e.ldo = D;
+        gemm(c, "gemm_agg2", w.hid, H, nullptr, 0, lw.a2, Me, D, e);
+        e = epi(EP_STORE);
+        e.out_t = w.Mq; e.ldo = Q;
+        gemm(c, "gemm_msgproj", w.mapped, D, nullptr, 0, c.W, Me, Q, e);
+        {
+            Launch lg(c, "scatter_perm", 0, double(Ms) * Q * c.act_size + double(Me) * Q * c.act_size);
+            if (c.bf16)
+                scatter_perm_kernel<bf16, bf16><<<blocks_for(Ms * Q), 256, 0, c.stream>>>((bf16*)w.Mq, c.slot_ptr, c.slot_edge, c.perm_out, L, E, K, Q, Ms, (bf16*)w.accq);
+            else
+                scatter_perm_kernel<float, float><<<blocks_for(Ms * Q), 256, 0, c.stream>>>((float*)w.Mq, c.slot_ptr, c.slot_edge, c.perm_out, L, E, K, Q, Ms, (float*)w.accq);
+            check_launch("scatter_perm");
+        }
+        e = epi(EP_STORE);
+        e.out_f = w.accf; e.out_t = c.bf16 ? w.acct : nullptr; e.ldo = D;
+        gemm(c, "gemm_msgback", w.accq, Q, nullptr, 0, c.Wt, Ms, D, e);
+        if (o.incoming)
+            ck(cudaMemcpyAsync(o.incoming + size_t(li) * Ms * D, w.accf, size_t(Ms) * D * 4, cudaMemcpyDeviceToDevice, c.stream), "incoming");
+        e = epi(EP_GELU);
+        e.bias = lw.fb1; e.out_t = w.hid; e.ldo = H;
+        gemm(c, "gemm_fuse1", w.Ztt, D, w.acct, D, lw.f1, Ms, H, e);
+        e = epi(EP_RESID);
+        e.bias = lw.fb2; e.z = w.Ztf; e.ldz = D; e.out_f = w.Zf; e.out_t = c.bf16 ? w.Zt : nullptr; e.ldo = D;
+        gemm(c, "gemm_fuse2", w.hid, H, nullptr, 0, lw.f2, Ms, D, e);
+    }
+    // final logits + site statistics (denoiser.cpp:230-245, refine.cpp:61-78)
+    if (c.bf16) {
+        Epi e = epi(EP_LOGITS);
+        e.inv_tau = 1.0f / o.tau; e.kappa = w.kappa; e.amax = w.amax; e.out_f = o.logits_out; e.ldo = Q;
+        gemm(c, "gemm_logits", w.Zt, D, nullptr, 0, c.W, Ms, Q, e);
+    } else {
+        float* lg_buf = o.logits_out ? o.logits_out : w.logits;
+        Epi e = epi(EP_STORE);
+        e.out_f = lg_buf; e.ldo = Q;
+        gemm(c, "gemm_logits", w.Zt, D, nullptr, 0, c.W, Ms, Q, e);
+        Launch lg(c, "row_stats", 0, double(Ms) * Q * 4);
+        row_stats_kernel<<<blocks_for(Ms * 32), 256, 0, c.stream>>>(lg_buf, Ms, Q, o.tau, w.kappa, w.amax);
+        check_launch("row_stats");
+    }
+}
+
+// ---- one pass of run_masked_loop (refine.cpp:134-195) over nb bins ------------------------------
+// X holds the start grid (internal layout); init_masked / upd describe it per bin.
+void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int steps, const cider_schedule& sc,
+                 bool count_first) {
+    const int n = c.L * K;
+    for (int t = 1; t <= steps; ++t) {
+        FwdOpts o;
+        o.tau = float(infer_temperature(t, steps, sc.tau_max, sc.tau_min));
+        forward(c, w, nb, K, X, S, o);
+        const bool first = t == 1 && sc.first_reveal;
+        if (first && count_first)
+            ck(cudaMemsetAsync(w.first_count, 0, size_t(nb) * 4, c.stream), "memset");
+        Launch lg(c, "reveal", 0, double(nb) * n * 12);
+        reveal_kernel<<<nb, 512, 0, c.stream>>>(X, w.kappa, w.amax, c.L, K, w.init_masked, cosine_fraction(t, steps),
+                                                first ? 1 : 0, first && count_first ? w.first_count : nullptr);
+        check_launch("reveal");
+    }
+    {
+        Launch lg(c, "force_residual", 0, double(nb) * n * 12);
+        force_residual_kernel<<<blocks_for(int64_t(nb) * n), 256, 0, c.stream>>>(X, w.amax, int64_t(nb) * n);
+        check_launch("force_residual");
+    }
+    FwdOpts o; // the gamma = 0 pass; kappa at tau = 1 feeds MaxProbScorer (refine.cpp:218-225)
+    o.tau = 1.0f;
+    o.logits_out = w.flog;
+    forward(c, w, nb, K, X, S, o);
+    {
+        Launch lg(c, "finalize", 0, double(nb) * n * 12);
+        finalize_kernel<<<blocks_for(int64_t(nb) * n), 256, 0, c.stream>>>(X, w.amax, w.upd, K, int64_t(nb) * n, n);
+        check_launch("finalize");
+        ck(cudaMemcpyAsync(w.k1, w.kappa, size_t(nb) * n * 4, cudaMemcpyDeviceToDevice, c.stream), "k1");
+    }
+}
+
+void validate_sched(const cider_schedule* sc, const cider_remask* rm, int K) {
+    if (!sc) throw InvalidInput("run_refinement: null schedule");
+    if (sc->steps < 1) throw InvalidInput("run_refinement: need T >= 1");
+    if (!(sc->tau_min > 0.0) || sc->tau_max < sc->tau_min)
+        throw InvalidInput("run_refinement: need tau_max >= tau_min > 0");
+    if (K < 1 || K > 32) throw InvalidInput("cider: K must be in 1..32");
+    if (rm && rm->mode == CIDER_REMASK_THRESHOLD) {
+        if (rm->n_thresholds < 0 || rm->n_thresholds > CIDER_MAX_THRESHOLDS)
+            throw InvalidInput("remask: too many thresholds");
+        double prev = 1.0; // validate_remask_config (refine.cpp:48-57)
+        for (int i = 0; i < rm->n_thresholds; ++i) {
+            double t = rm->thresholds[i];
+            if (t <= 0.0 || t >= 1.0) throw InvalidInput("remask thresholds must lie in (0,1)");
+            if (t >= prev) throw InvalidInput("remask thresholds must be strictly descending");
+            prev = t;
+        }
+    }
+    if (rm && rm->mode == CIDER_REMASK_RANK && !(rm->rank_fraction >= 0.0 && rm->rank_fraction <= 1.0))
+        throw InvalidInput("remask: rank_fraction must lie in [0,1]");
+    if (rm && (rm->mode < 0 || rm->mode > 2)) throw InvalidInput("remask: unknown mode");
+}
+
+struct ChunkTrace {
+    std::vector<int32_t> first, rows, steps, mask; // per bin
+};
+
+// gather / scatter of per-bin records for threshold-remask buckets
+__global__ void gather_rows_kernel(const int* __restrict__ src, int* __restrict__ dst, const int* __restrict__ idx,
+                                   int per, int64_t total) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    dst[i] = src[int64_t(idx[i / per]) * per + i % per];
+}
+__global__ void scatter_rows_kernel(const int* __restrict__ src, int* __restrict__ dst, const int* __restrict__ idx,
+                                    int per, int64_t total) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    dst[int64_t(idx[i / per]) * per + i % per] = src[i];
+}
+
+void copy_rows(cider_ctx& c, const void* src, void* dst, const int* idx, int n, size_t per_words, bool gather) {
+    int64_t total = int64_t(n) * int64_t(per_words);
+    if (!total) return;
+    Launch lg(c, gather ? "bin_gather" : "bin_scatter", 0, double(total) * 8);
+    if (gather)
+        gather_rows_kernel<<<blocks_for(total), 256, 0, c.stream>>>((const int*)src, (int*)dst, idx, int(per_words), total);
+    else
+        scatter_rows_kernel<<<blocks_for(total), 256, 0, c.stream>>>((const int*)src, (int*)dst, idx, int(per_words), total);
+    check_launch("bin_copy");
+}
+
+// Full decode of nb bins (run_refinement / run_with_remasking, refine.cpp:199-292).
+// S: device [nb x L x Q]; X: device internal grid [nb x L x K] (output).
+void refine_chunk(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, const cider_schedule& sc,
+                  const cider_remask* rm, ChunkTrace* tr) {
+    const int n = c.L * K;
+    const int64_t total = int64_t(nb) * n;
+    fill_i32_kernel<<<blocks_for(total), 256, 0, c.stream>>>(X, -1, total);
+    fill_i32_kernel<<<blocks_for(nb), 256, 0, c.stream>>>(w.init_masked, n, nb);
+    fill_u32_kernel<<<blocks_for(nb), 256, 0, c.stream>>>(w.upd, K >= 32 ? 0xffffffffu : ((1u << K) - 1u), nb);
+    c.launches += 3;
+    check_launch("init");
+    masked_pass(c, w, nb, K, S, X, sc.steps, sc, tr != nullptr);
+    if (tr) {
+        tr->first.assign(nb, 0);
+        tr->rows.assign(size_t(nb) * CIDER_MAX_THRESHOLDS, 0);
+        tr->steps.assign(size_t(nb) * CIDER_MAX_THRESHOLDS, 0);
+        tr->mask.assign(size_t(nb) * K, 0);
+        ck(cudaMemcpyAsync(tr->first.data(), w.first_count, size_t(nb) * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+    }
+    const int mode = rm ? rm->mode : CIDER_REMASK_NONE;
+    if (mode == CIDER_REMASK_RANK) {
+        const int k_low = int(std::floor(rm->rank_fraction * K));
+        if (k_low > 0) {
+            Launch lg(c, "remask_select", 0, double(total) * 8);
+            remask_select_kernel<<<nb, 128, 0, c.stream>>>(X, w.k1, c.L, K, 2, k_low, 0.0, w.upd, w.init_masked, w.nlow, nullptr);
+            check_launch("remask_select");
+        }
+        if (k_low > 0) {
+            const int T_rm = remask_steps(sc.steps, k_low, K);
+            cider_schedule rs = sc;
+            rs.steps = T_rm;
+            masked_pass(c, w, nb, K, S, X, T_rm, rs, false);
+            if (tr) {
+                std::vector<uint32_t> upd(nb);
+                ck(cudaMemcpyAsync(upd.data(), w.upd, size_t(nb) * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+                ck(cudaStreamSynchronize(c.stream), "sync");
+                for (int b = 0; b < nb; ++b) {
+                    tr->rows[size_t(b) * CIDER_MAX_THRESHOLDS] = k_low;
+                    tr->steps[size_t(b) * CIDER_MAX_THRESHOLDS] = T_rm;
+                    for (int k = 0; k < K; ++k) tr->mask[size_t(b) * K + k] = (upd[b] >> k) & 1u;
+                }
+            }
+        }
+    } else if (mode == CIDER_REMASK_THRESHOLD) {
+        // run_with_remasking (refine.cpp:277-292): bins diverge in |K_low| and so in T_rm; each
+        // stage buckets its bins by |K_low| and runs every bucket as a compact sub-batch.
+        std::vector<char> alive(nb, 1); // the reference stops a bin at its first all-clear stage
+        std::vector<int> nlow(nb);
+        std::vector<uint32_t> upd(nb);
+        for (int s = 0; s < rm->n_thresholds; ++s) {
+            {
+                Launch lg(c, "remask_select", 0, double(total) * 8);
+                remask_select_kernel<<<nb, 128, 0, c.stream>>>(X, w.k1, c.L, K, 1, 0, rm->thresholds[s], w.upd, w.init_masked, w.nlow, nullptr);
+                check_launch("remask_select");
+            }
+            ck(cudaMemcpyAsync(nlow.data(), w.nlow, size_t(nb) * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+            ck(cudaMemcpyAsync(upd.data(), w.upd, size_t(nb) * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+            ck(cudaStreamSynchronize(c.stream), "sync");
+            std::map<int, std::vector<int>> buckets;
+            for (int b = 0; b < nb; ++b) {
+                if (!alive[b]) nlow[b] = 0;
+                if (nlow[b] == 0) alive[b] = 0;
+                else buckets[nlow[b]].push_back(b);
+            }
+            // bins that are not re-decoded must keep their grid: the select kernel masked their
+            // low rows only if nlow > 0, and dead bins were excluded above -> restore those
+            std::vector<int> dead_masked;
+            for (int b = 0; b < nb; ++b)
+                if (!alive[b] && upd[b]) dead_masked.push_back(b);
+            if (!dead_masked.empty()) throw std::logic_error("remask: masked rows in a finished bin");
+            if (buckets.empty()) break;
+            for (auto& [nl, bins] : buckets) {
+                const int T_rm = remask_steps(sc.steps, nl, K);
+                cider_schedule rs = sc;
+                rs.steps = T_rm;
+                if (tr)
+                    for (int b : bins) {
+                        tr->rows[size_t(b) * CIDER_MAX_THRESHOLDS + s] = nl;
+                        tr->steps[size_t(b) * CIDER_MAX_THRESHOLDS + s] = T_rm;
+                        for (int k = 0; k < K; ++k) tr->mask[size_t(b) * K + k] = (upd[b] >> k) & 1u;
+                    }
+                if (int(bins.size()) == nb) {
+                    masked_pass(c, w, nb, K, S, X, T_rm, rs, false);
+                    continue;
+                }
+                // compact sub-batch in the tail of dedicated staging buffers
+                const int m = int(bins.size());
+                int* idx = (int*)wsbuf(c, "sub_idx", size_t(m) * 4);
+                ck(cudaMemcpyAsync(idx, bins.data(), size_t(m) * 4, cudaMemcpyHostToDevice, c.stream), "h2d");
+                float* subS = (float*)wsbuf(c, "sub_S", size_t(m) * c.L * c.Q * 4);
+                int* subX = (int*)wsbuf(c, "sub_X", size_t(m) * n * 4);
+                int* keep_init = (int*)wsbuf(c, "sub_init", size_t(nb) * 4);
+                uint32_t* keep_upd = (uint32_t*)wsbuf(c, "sub_upd", size_t(nb) * 4);
+                float* keep_k1 = (float*)wsbuf(c, "sub_k1", size_t(nb) * n * 4);
+                ck(cudaMemcpyAsync(keep_init, w.init_masked, size_t(nb) * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                ck(cudaMemcpyAsync(keep_upd, w.upd, size_t(nb) * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                ck(cudaMemcpyAsync(keep_k1, w.k1, size_t(nb) * n * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                copy_rows(c, S, subS, idx, m, size_t(c.L) * c.Q, true);
+                copy_rows(c, X, subX, idx, m, n, true);
+                copy_rows(c, keep_init, w.init_masked, idx, m, 1, true);
+                copy_rows(c, keep_upd, w.upd, idx, m, 1, true);
+                float* keep_flog = nullptr;
+                if (w.flog) {
+                    keep_flog = (float*)wsbuf(c, "sub_flog", size_t(nb) * n * c.Q * 4);
+                    ck(cudaMemcpyAsync(keep_flog, w.flog, size_t(nb) * n * c.Q * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                }
+                masked_pass(c, w, m, K, subS, subX, T_rm, rs, false);
+                copy_rows(c, subX, X, idx, m, n, false);
+                copy_rows(c, w.k1, keep_k1, idx, m, n, false);
+                ck(cudaMemcpyAsync(w.k1, keep_k1, size_t(nb) * n * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                ck(cudaMemcpyAsync(w.init_masked, keep_init, size_t(nb) * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                ck(cudaMemcpyAsync(w.upd, keep_upd, size_t(nb) * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                if (w.flog) {
+                    copy_rows(c, w.flog, keep_flog, idx, m, size_t(n) * c.Q, false);
+                    ck(cudaMemcpyAsync(w.flog, keep_flog, size_t(nb) * n * c.Q * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
+                }
+            }
+        }
+    }
+}
+
+void upload_model(cider_ctx& c, const float* w) {
+    const int Q = c.Q, D = c.D, H = c.H;
+    size_t off = 0;
+    auto take = [&](size_t n) { const float* p = w + off; off += n; return p; };
+    const float* E = take(size_t(Q + 1) * D);
+    const float* W = take(size_t(Q) * D);
+    const float* V = take(size_t(Q) * D);
+    c.Etab = upload_vec(c, E, size_t(Q + 1) * D);
+    c.W = upload_mat(c, W, Q, D, false);
+    c.Wt = upload_mat(c, W, Q, D, true);
+    c.Vt = upload_mat(c, V, Q, D, true);
+    c.lw.resize(c.N);
+    for (int l = 0; l < c.N; ++l) {
+        LayerW& L = c.lw[l];
+        const float* p;
+        p = take(size_t(H) * 2 * D); L.g1 = upload_mat(c, p, H, 2 * D, false);
+        p = take(H); L.gb1 = upload_vec(c, p, H);
+        p = take(size_t(D) * H); L.g2 = upload_mat(c, p, D, H, false);
+        p = take(D); L.gb2 = upload_vec(c, p, D);
+        p = take(size_t(H) * D); L.a1 = upload_mat(c, p, H, D, false);
+        p = take(H); L.ab1 = upload_vec(c, p, H);
+        p = take(size_t(D) * H); L.a2 = upload_mat(c, p, D, H, false);
+        p = take(D); L.ab2 = upload_vec(c, p, D);
+        p = take(size_t(H) * 2 * D); L.f1 = upload_mat(c, p, H, 2 * D, false);
+        p = take(H); L.fb1 = upload_vec(c, p, H);
+        p = take(size_t(D) * H); L.f2 = upload_mat(c, p, D, H, false);
+        p = take(D); L.fb2 = upload_vec(c, p, D);
+        L.ak = nullptr;
+        L.aq = nullptr;
+    }
+    if (c.heads)
+        for (int l = 0; l < c.N; ++l) {
+            const float* q = take(D);
+            c.lw[l].aq = upload_vec(c, q, D);
+            const float* k = take(size_t(D) * D);
+            c.lw[l].ak = upload_mat(c, k, D, D, false);
+        }
+}
+
+void upload_code(cider_ctx& c) {
+    const Tanner& t = *c.tg;
+    const Gf& gf = *c.gf;
+    std::vector<uint8_t> pin(size_t(t.n_edges()) * c.Q), pout(size_t(t.n_edges()) * c.Q);
+    for (int e = 0; e < t.n_edges(); ++e) {
+        const int a = t.coef[e], ai = gf.inv(a);
+        for (int s = 0; s < c.Q; ++s) {
+            pin[size_t(e) * c.Q + s] = uint8_t(gf.mul(ai, s));  // Pi_alpha(u)[s] = u[alpha^-1 s]
+            pout[size_t(e) * c.Q + s] = uint8_t(gf.mul(a, s));  // Pi_alpha^-1(m)[s] = m[alpha s]
+        }
+    }
+    c.e_slot = upload_raw(c, t.slot);
+    c.e_check = upload_raw(c, t.chk);
+    c.check_ptr = upload_raw(c, t.check_ptr);
+    c.slot_ptr = upload_raw(c, t.slot_ptr);
+    c.slot_edge = upload_raw(c, t.slot_edge);
+    c.perm_in = upload_raw(c, pin);
+    c.perm_out = upload_raw(c, pout);
+}
+
+void require_device() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw CudaError("cider: no CUDA device (there is no CPU fallback)");
+}
+
+// NCCL, resolved at run time (dlopen) so the library never pins a second NCCL build into a
+// process that already has one (PyTorch's); nccl.h supplies the types only.
+void* nccl_handle() {
+    static void* h = nullptr;
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw CudaError("libnccl.so.2 not loadable");
+    return h;
+}
+template <class F>
+F nccl_sym(const char* name) {
+    void* p = dlsym(nccl_handle(), name);
+    if (!p) throw CudaError(std::string("NCCL symbol missing: ") + name);
+    return reinterpret_cast<F>(p);
+}
+
+} // namespace
+} // namespace cider
+
+cider_ctx::~cider_ctx() {
+    if (device >= 0) cudaSetDevice(device);
+    if (nccl_comm) {
+        try { nccl_sym<decltype(&ncclCommDestroy)>("ncclCommDestroy")((ncclComm_t)nccl_comm); } catch (...) {}
+    }
+    for (auto& [k, b] : ws) b.release();
+    for (auto& b : wbufs) b.release();
+    flush_buf.release();
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto& e : events)
+        if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+extern "C" {
+
+const char* cider_last_error(void) {
+    if (!g_err.empty()) return g_err.c_str();
+    return host_last_error();
+}
+
+int cider_device_count(int* n) {
+    return guard([&] {
+        *n = 0;
+        if (cudaGetDeviceCount(n) != cudaSuccess) *n = 0;
+    });
+}
+
+int cider_create(const cider_model_desc* model, const float* weights, const cider_code_desc* code, int device,
+                 cider_ctx** out) {
+    return guard([&] {
+        *out = nullptr;
+        validate_model(model);
+        if (!weights) throw InvalidInput("cider_create: null weights");
+        auto c = std::make_unique<cider_ctx>();
+        c->md = *model;
+        c->gf = std::make_unique<Gf>(model->m, model->prim_poly);
+        c->Q = c->gf->q;
+        c->tg = std::make_unique<Tanner>(code, c->Q);
+        c->D = model->dim;
+        c->H = model->hidden;
+        c->N = model->layers;
+        c->heads = model->heads;
+        c->bf16 = model->precision == CIDER_BF16;
+        c->act_size = c->bf16 ? 2 : 4;
+        c->L = c->tg->slots;
+        c->P = c->tg->checks;
+        c->E = c->tg->n_edges();
+        if (c->bf16 && (c->Q % 64 || c->D % 64 || c->H % 64 || c->Q > 256))
+            throw InvalidInput("BF16 mode needs Q, D, H multiples of 64 and Q <= 256");
+        if (c->heads > ATT_MAXH) throw InvalidInput("cider: at most 32 attention heads");
+        for (int j = 0; j < c->P; ++j)
+            if (c->tg->check_ptr[j + 1] - c->tg->check_ptr[j] > ATT_MAXD)
+                throw InvalidInput("cider: check degree above 32");
+        require_device();
+        c->device = device;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "props");
+        if (prop.major != 10) throw CudaError("cider: needs an sm_100 (B200) device, found sm_" + std::to_string(prop.major * 10 + prop.minor));
+        c->sm_count = prop.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        upload_model(*c, weights);
+        upload_code(*c);
+        ck(cudaDeviceSynchronize(), "upload");
+        *out = c.release();
+    });
+}
+
+void cider_destroy(cider_ctx* ctx) { delete ctx; }
+
+int cider_set_chunk(cider_ctx* ctx, int n) {
+    return guard([&] {
+        if (n < 0) throw InvalidInput("chunk must be >= 0");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        ctx->chunk_req = n;
+    });
+}
+
+int cider_denoise(cider_ctx* c, int B, int K, const int32_t* X, const float* S, float* logits, float* incoming) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (B < 0 || K < 1 || K > 32) throw InvalidInput("cider_denoise: bad B/K");
+        const int L = c->L, Q = c->Q, D = c->D, n = L * K;
+        for (int64_t i = 0; i < int64_t(B) * n; ++i)
+            if (X[i] != -1 && (X[i] < 0 || X[i] >= Q)) throw InvalidInput("embed_grid: token out of range");
+        const int chunk = std::max(1, std::min(B, chunk_bins(*c, K)));
+        for (int b0 = 0; b0 < B; b0 += chunk) {
+            const int nb = std::min(chunk, B - b0);
+            WS w = workspace(*c, nb, K, false);
+            const int64_t Ms = int64_t(nb) * n;
+            float* lg = (float*)wsbuf(*c, "den_logits", size_t(Ms) * Q * 4);
+            float* lg_ref = (float*)wsbuf(*c, "den_logits_ref", size_t(Ms) * Q * 4);
+            float* inc = incoming ? (float*)wsbuf(*c, "den_inc", size_t(Ms) * D * 4 * c->N) : nullptr;
+            float* inc_ref = incoming ? (float*)wsbuf(*c, "den_inc_ref", size_t(Ms) * D * 4 * c->N) : nullptr;
+            ck(cudaMemcpyAsync(w.Xio, X + size_t(b0) * n, size_t(Ms) * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+            ck(cudaMemcpyAsync(w.S, S + size_t(b0) * L * Q, size_t(nb) * L * Q * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+            grid_to_internal_kernel<<<blocks_for(Ms), 256, 0, c->stream>>>(w.Xio, w.X, L, K, Ms);
+            ++c->launches;
+            FwdOpts o;
+            o.logits_out = lg;
+            o.incoming = inc;
+            forward(*c, w, nb, K, w.X, w.S, o);
+            rows_to_ref_kernel<<<blocks_for(Ms * Q), 256, 0, c->stream>>>(lg, lg_ref, L, K, Q, Ms * Q, int64_t(n) * Q, 0);
+            ++c->launches;
+            if (logits)
+                ck(cudaMemcpyAsync(logits + size_t(b0) * n * Q, lg_ref, size_t(Ms) * Q * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+            if (incoming) {
+                for (int l = 0; l < c->N; ++l) {
+                    rows_to_ref_kernel<<<blocks_for(Ms * D), 256, 0, c->stream>>>(inc + size_t(l) * Ms * D, inc_ref, L, K, D, Ms * D,
+                                                                                  int64_t(c->N) * n * D, int64_t(l) * n * D);
+                    ++c->launches;
+                }
+                ck(cudaMemcpyAsync(incoming + size_t(b0) * c->N * n * D, inc_ref, size_t(Ms) * D * c->N * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+            }
+            ck(cudaStreamSynchronize(c->stream), "denoise");
+        }
+        resolve_stats(*c);
+    });
+}
+
+static void refine_impl(cider_ctx* c, int B, int K, const float* S, bool S_device, const cider_schedule* sched,
+                        const cider_remask* rm, int32_t* grid, bool grid_device, float* final_logits, cider_trace* tr) {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    validate_sched(sched, rm, K);
+    if (B < 0) throw InvalidInput("cider_refine: negative B");
+    const int L = c->L, Q = c->Q, n = L * K;
+    const int chunk = std::max(1, std::min(B, chunk_bins(*c, K)));
+    for (int b0 = 0; b0 < B; b0 += chunk) {
+        const int nb = std::min(chunk, B - b0);
+        WS w = workspace(*c, nb, K, final_logits != nullptr);
+        const float* Sd = S + size_t(b0) * L * Q;
+        if (!S_device) {
+            ck(cudaMemcpyAsync(w.S, Sd, size_t(nb) * L * Q * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+            Sd = w.S;
+        }
+        ChunkTrace ct;
+        refine_chunk(*c, w, nb, K, Sd, w.X, *sched, rm, tr ? &ct : nullptr);
+        const int64_t Ms = int64_t(nb) * n;
+        int* gdst = grid_device ? grid + size_t(b0) * n : w.Xio;
+        grid_to_ref_kernel<<<blocks_for(Ms), 256, 0, c->stream>>>(w.X, gdst, L, K, Ms);
+        ++c->launches;
+        check_launch("grid_to_ref");
+        if (!grid_device)
+            ck(cudaMemcpyAsync(grid + size_t(b0) * n, w.Xio, size_t(Ms) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        if (final_logits) {
+            float* ref = (float*)wsbuf(*c, "flog_ref", size_t(Ms) * Q * 4);
+            rows_to_ref_kernel<<<blocks_for(Ms * Q), 256, 0, c->stream>>>(w.flog, ref, L, K, Q, Ms * Q, int64_t(n) * Q, 0);
+            ++c->launches;
+            ck(cudaMemcpyAsync(final_logits + size_t(b0) * n * Q, ref, size_t(Ms) * Q * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        }
+        if (tr || !grid_device || final_logits) ck(cudaStreamSynchronize(c->stream), "refine");
+        if (tr) {
+            for (int b = 0; b < nb; ++b) {
+                if (tr->first_reveals) tr->first_reveals[b0 + b] = ct.first[b];
+                for (int s = 0; s < CIDER_MAX_THRESHOLDS; ++s) {
+                    if (tr->remask_rows) tr->remask_rows[size_t(b0 + b) * CIDER_MAX_THRESHOLDS + s] = ct.rows[size_t(b) * CIDER_MAX_THRESHOLDS + s];
+                    if (tr->remask_steps) tr->remask_steps[size_t(b0 + b) * CIDER_MAX_THRESHOLDS + s] = ct.steps[size_t(b) * CIDER_MAX_THRESHOLDS + s];
+                }
+                if (tr->remask_mask)
+                    for (int k = 0; k < K; ++k) tr->remask_mask[size_t(b0 + b) * K + k] = ct.mask[size_t(b) * K + k];
+            }
+        }
+    }
+    if (c->profiling) resolve_stats(*c);
+}
+
+int cider_refine(cider_ctx* c, int B, int K, const float* S, const cider_schedule* sched, const cider_remask* rm,
+                 int32_t* grid, float* final_logits, cider_trace* tr) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        std::lock_guard<std::mutex> lk(c->mu);
+        refine_impl(c, B, K, S, false, sched, rm, grid, false, final_logits, tr);
+    });
+}
+
+int cider_refine_device(cider_ctx* c, int B, int K, const float* S_device, const cider_schedule* sched,
+                        const cider_remask* rm, int32_t* grid_device) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        std::lock_guard<std::mutex> lk(c->mu);
+        refine_impl(c, B, K, S_device, true, sched, rm, grid_device, true, nullptr, nullptr);
+    });
+}
+
+int cider_device_alloc(cider_ctx* c, size_t bytes, void** p) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaMalloc(p, std::max<size_t>(bytes, 16)), "cudaMalloc");
+    });
+}
+int cider_device_free(cider_ctx* c, void* p) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaFree(p), "cudaFree");
+    });
+}
+int cider_host_alloc(size_t bytes, void** p) { return guard([&] { ck(cudaMallocHost(p, std::max<size_t>(bytes, 16)), "cudaMallocHost"); }); }
+int cider_host_free(void* p) { return guard([&] { ck(cudaFreeHost(p), "cudaFreeHost"); }); }
+int cider_memcpy_h2d(cider_ctx* c, void* dst, const void* src, size_t n) {
+    return guard([&] { ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, c->stream), "h2d"); });
+}
+int cider_memcpy_d2h(cider_ctx* c, void* dst, const void* src, size_t n) {
+    return guard([&] { ck(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, c->stream), "d2h"); });
+}
+int cider_synchronize(cider_ctx* c) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        resolve_stats(*c);
+    });
+}
+int cider_flush_l2(cider_ctx* c) {
+    return guard([&] {
+        const size_t bytes = size_t(256) << 20; // 2x the 126 MB L2
+        c->flush_buf.ensure(bytes);
+        static int v = 0;
+        flush_kernel<<<blocks_for(int64_t(bytes / 16)), 256, 0, c->stream>>>((int4*)c->flush_buf.p, int64_t(bytes / 16), ++v);
+        check_launch("flush");
+    });
+}
+int cider_event_record(cider_ctx* c, int slot) {
+    return guard([&] {
+        if (slot < 0 || slot >= 64) throw InvalidInput("event slot out of range");
+        if (!c->events[slot]) ck(cudaEventCreate(&c->events[slot]), "event");
+        ck(cudaEventRecord(c->events[slot], c->stream), "event record");
+    });
+}
+int cider_event_elapsed(cider_ctx* c, int a, int b, float* ms) {
+    return guard([&] {
+        ck(cudaEventSynchronize(c->events[b]), "event sync");
+        ck(cudaEventElapsedTime(ms, c->events[a], c->events[b]), "elapsed");
+    });
+}
+int cider_set_profiling(cider_ctx* c, int on) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        resolve_stats(*c);
+        c->profiling = on != 0;
+    });
+}
+int64_t cider_launch_count(cider_ctx* c) { return c ? c->launches : -1; }
+int cider_kernel_stats(cider_ctx* c, int idx, char* name, int name_len, int64_t* launches, double* ms, double* flops,
+                       double* bytes) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        resolve_stats(*c);
+        if (idx < 0 || idx >= int(c->stats.size())) throw InvalidInput("stat index out of range");
+        auto it = c->stats.begin();
+        std::advance(it, idx);
+        std::snprintf(name, size_t(name_len), "%s", it->first.c_str());
+        *launches = it->second.launches;
+        *ms = it->second.ms;
+        *flops = it->second.flops;
+        *bytes = it->second.bytes;
+    });
+}
+int cider_reset_stats(cider_ctx* c) {
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        resolve_stats(*c);
+        c->stats.clear();
+        c->launches = 0;
+    });
+}
+
+int cider_nccl_unique_id(char out[128]) {
+    return guard([&] {
+        ncclUniqueId uid;
+        ncclResult_t r = nccl_sym<decltype(&ncclGetUniqueId)>("ncclGetUniqueId")(&uid);
+        if (r != ncclSuccess) throw CudaError("ncclGetUniqueId failed");
+        std::memcpy(out, uid.internal, sizeof(uid.internal));
+    });
+}
+int cider_nccl_init(cider_ctx* c, const char id[128], int rank, int world) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        if (world < 1 || rank < 0 || rank >= world) throw InvalidInput("nccl: bad rank/world");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ncclUniqueId uid;
+        std::memcpy(uid.internal, id, sizeof(uid.internal));
+        ncclComm_t comm = nullptr;
+        ncclResult_t r = nccl_sym<decltype(&ncclCommInitRank)>("ncclCommInitRank")(&comm, world, uid, rank);
+        if (r != ncclSuccess) throw CudaError("ncclCommInitRank failed (" + std::to_string(int(r)) + ")");
+        c->nccl_comm = comm;
+    });
+}
+
+int cider_nccl_allgather(cider_ctx* c, const void* send, void* recv, size_t n) {
+    return guard([&] {
+        if (!c || !c->nccl_comm) throw InvalidInput("nccl: communicator not initialised");
+        ncclResult_t r = nccl_sym<decltype(&ncclAllGather)>("ncclAllGather")(send, recv, n, ncclUint8,
+                                                                            (ncclComm_t)c->nccl_comm, c->stream);
+        if (r != ncclSuccess) throw CudaError("ncclAllGather failed (" + std::to_string(int(r)) + ")");
+        ++c->launches;
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,393 @@
+// path.cuh — the non-GEMM kernels of the refinement path: embedding, demixing, Tanner-graph
+// gathers (coefficient permutations, extrinsic pooling / attention, ordered per-slot
+// accumulation), site statistics, reveal / remask selection and layout transforms.
+//
+// All of them are HBM-bound integer/byte or element-wise work: coalesced along the contiguous
+// Q / D axis, no atomics (bitwise row symmetry), one thread per output element unless a
+// per-bin selection needs a block.
+#pragma once
+
+#include "common.cuh"
+
+namespace cider {
+
+// ---- embed_grid (denoiser.cpp:71-84): Z[m] = E[X[m]], MASK -> row Q --------------------
+template <typename T>
+__global__ void embed_kernel(const int* __restrict__ X, const float* __restrict__ Etab, int Q, int D,
+                             int64_t M, float* __restrict__ Zf, T* __restrict__ Zt) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= M * D) return;
+    int64_t m = i / D;
+    int t = int(i % D);
+    int tok = X[m];
+    int row = (tok < 0 || tok >= Q) ? Q : tok;
+    float v = Etab[size_t(row) * D + t];
+    Zf[i] = v;
+    if (Zt) Zt[i] = from_f<T>(v);
+}
+
+// ---- demix_responsibilities x S (denoiser.cpp:103-122, 130) -------------------------------
+// r_{k,l,a} = softmax over the K rows of lbar/tau; out = r * S_{l,a}. The normaliser is summed in
+// 2^-52 fixed point (exact integer adds), which is order-independent: the same bitwise
+// row-permutation invariance the reference gets by summing in descending order.
+template <typename T>
+__global__ void demix_kernel(const float* __restrict__ lbar, const float* __restrict__ S, int64_t n_slotrows,
+                             int K, int Q, float tau, T* __restrict__ out) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_slotrows * Q) return;
+    int64_t s = i / Q;
+    int a = int(i % Q);
+    const float* x = lbar + size_t(s) * K * Q + a;
+    float mx = x[0];
+    for (int k = 1; k < K; ++k) mx = fmaxf(mx, x[size_t(k) * Q]);
+    long long den = 0;
+    for (int k = 0; k < K; ++k) {
+        float e = expf((x[size_t(k) * Q] - mx) / tau);
+        den += __double2ll_rn(double(e) * 4503599627370496.0);
+    }
+    float denf = float(double(den) * (1.0 / 4503599627370496.0));
+    float sv = S[size_t(s) * Q + a];
+    for (int k = 0; k < K; ++k) {
+        float e = expf((x[size_t(k) * Q] - mx) / tau);
+        out[(size_t(s) * K + k) * Q + a] = from_f<T>((e / denf) * sv);
+    }
+}
+
+// ---- coefficient normalisation Pi_alpha W z per edge (denoiser.cpp:162-179, 192-195) -------
+// Ae[(b,e,k)][c] = U[(b, slot_e, k)][perm_in[e][c]], perm_in[e][c] = alpha_e^-1 * c.
+template <typename T>
+__global__ void gather_perm_kernel(const T* __restrict__ U, const int* __restrict__ e_slot,
+                                   const uint8_t* __restrict__ perm_in, int L, int E, int K, int Q,
+                                   int64_t n_rows, T* __restrict__ Ae) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows * Q) return;
+    int64_t r = i / Q;
+    int c = int(i % Q);
+    int k = int(r % K);
+    int64_t be = r / K;
+    int e = int(be % E);
+    int64_t b = be / E;
+    int src = perm_in[size_t(e) * Q + c];
+    Ae[i] = U[((b * L + e_slot[e]) * K + k) * Q + src];
+}
+
+// ---- extrinsic sum-pool Psi (denoiser.cpp:196-203) -----------------------------------------
+// pooled[(b,e,k)] = sum over the other edges e2 of e's check, ascending, of N[(b,e2,k)].
+template <typename Tin, typename T>
+__global__ void pool_sum_kernel(const Tin* __restrict__ Nn, const int* __restrict__ e_check,
+                                const int* __restrict__ check_ptr, int E, int K, int D, int64_t n_rows,
+                                T* __restrict__ pooled) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows * D) return;
+    int64_t r = i / D;
+    int t = int(i % D);
+    int k = int(r % K);
+    int64_t be = r / K;
+    int e = int(be % E);
+    int64_t b = be / E;
+    int j = e_check[e];
+    float s = 0.0f;
+    for (int e2 = check_ptr[j]; e2 < check_ptr[j + 1]; ++e2) {
+        if (e2 == e) continue;
+        s += to_f(Nn[((b * E + e2) * K + k) * D + t]);
+    }
+    pooled[i] = from_f<T>(s);
+}
+
+// ---- extrinsic pooling attention Psi (config mode) ---------------------------
+// One block per (bin, check, row). score_i,h = <q_h, key_i,h> / sqrt(dh); for target i the
+// weights are the softmax of score_i2,h over the OTHER edges i2 of the check, and
+// pooled_i = (d-1) * sum_i2 w_i2,h * N_i2 on head h's slice. q = 0 recovers the sum-pool.
+constexpr int ATT_MAXD = 32, ATT_MAXH = 32;
+template <typename Tin, typename T>
+__global__ void pool_attn_kernel(const Tin* __restrict__ Nn, const float* __restrict__ keys,
+                                 const float* __restrict__ query, const int* __restrict__ check_ptr,
+                                 int P, int E, int K, int D, int heads, T* __restrict__ pooled) {
+    __shared__ float part[1024];
+    __shared__ float score[ATT_MAXD][ATT_MAXH];
+    const int grp = blockIdx.x; // (b*P + j)*K + k
+    const int k = grp % K;
+    const int bj = grp / K;
+    const int j = bj % P;
+    const int64_t b = bj / P;
+    const int e0 = check_ptr[j], d = check_ptr[j + 1] - e0;
+    const int dh = D / heads;
+    const float scale = rsqrtf(float(dh));
+    for (int i = 0; i < d; ++i) {
+        const float* kr = keys + ((b * E + e0 + i) * K + k) * D;
+        for (int t = threadIdx.x; t < D; t += blockDim.x) part[t] = query[t] * kr[t];
+        __syncthreads();
+        for (int h = threadIdx.x; h < heads; h += blockDim.x) {
+            float s = 0.0f;
+            for (int t = h * dh; t < (h + 1) * dh; ++t) s += part[t];
+            score[i][h] = s * scale;
+        }
+        __syncthreads();
+    }
+    for (int i = 0; i < d; ++i) {
+        T* out = pooled + ((b * E + e0 + i) * K + k) * D;
+        for (int t = threadIdx.x; t < D; t += blockDim.x) {
+            const int h = t / dh;
+            float mx = -INFINITY;
+            for (int i2 = 0; i2 < d; ++i2)
+                if (i2 != i) mx = fmaxf(mx, score[i2][h]);
+            float den = 0.0f;
+            for (int i2 = 0; i2 < d; ++i2)
+                if (i2 != i) den += expf(score[i2][h] - mx);
+            float s = 0.0f;
+            for (int i2 = 0; i2 < d; ++i2) {
+                if (i2 == i) continue;
+                float w = float(d - 1) * expf(score[i2][h] - mx) / den;
+                s += w * to_f(Nn[((b * E + e0 + i2) * K + k) * D + t]);
+            }
+            out[t] = from_f<T>(s);
+        }
+    }
+}
+
+// ---- de-normalisation + ordered scatter-add (denoiser.cpp:205-207), in symbol space --------
+// accq[(b,l,k)][c] = sum over slot l's edges e, ascending check, of Mq[(b,e,k)][perm_out[e][c]],
+// perm_out[e][c] = alpha_e * c. A gather in a fixed order: no atomics, bitwise deterministic.
+template <typename Tin, typename T>
+__global__ void scatter_perm_kernel(const Tin* __restrict__ Mq, const int* __restrict__ slot_ptr,
+                                    const int* __restrict__ slot_edge, const uint8_t* __restrict__ perm_out,
+                                    int L, int E, int K, int Q, int64_t n_rows, T* __restrict__ accq) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_rows * Q) return;
+    int64_t m = i / Q;
+    int c = int(i % Q);
+    int k = int(m % K);
+    int64_t bl = m / K;
+    int l = int(bl % L);
+    int64_t b = bl / L;
+    float s = 0.0f;
+    for (int p = slot_ptr[l]; p < slot_ptr[l + 1]; ++p) {
+        int e = slot_edge[p];
+        s += to_f(Mq[((b * E + e) * K + k) * Q + perm_out[size_t(e) * Q + c]]);
+    }
+    accq[i] = from_f<T>(s);
+}
+
+// ---- site confidence + argmax (refine.cpp:61-78) over fp32 logits rows, one warp per row --
+__global__ void row_stats_kernel(const float* __restrict__ logits, int64_t M, int Q, float tau,
+                                 float* __restrict__ kappa, int* __restrict__ amax) {
+    int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    int lane = threadIdx.x % 32;
+    if (w >= M) return;
+    const float* x = logits + size_t(w) * Q;
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int a = lane; a < Q; a += 32) {
+        float v = x[a];
+        if (v > bv) { bv = v; bi = a; }
+    }
+    for (int o = 16; o; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    float s = 0.0f;
+    for (int a = lane; a < Q; a += 32) s += expf((x[a] - bv) / tau);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        kappa[w] = 1.0f / s;
+        amax[w] = bi;
+    }
+}
+
+// ---- reveal_step (refine.cpp:83-127), one block per bin ------------------------------------
+// first: one site per slot, the masked row with the largest kappa (strict >, lowest row wins).
+// else : reveal the (target - revealed) masked sites smallest in (kappa desc, row asc, slot asc)
+//        via a bitonic sort of 64-bit keys in shared memory.
+constexpr int REVEAL_MAX_SITES = 4096;
+__global__ void __launch_bounds__(512)
+reveal_kernel(int* __restrict__ X, const float* __restrict__ kappa, const int* __restrict__ amax, int L,
+              int K, const int* __restrict__ init_masked, double rho, int first,
+              int* __restrict__ reveal_count) {
+    __shared__ unsigned long long key[REVEAL_MAX_SITES];
+    __shared__ int red[32];
+    const int b = blockIdx.x;
+    const int n = L * K;
+    int* x = X + size_t(b) * n;
+    const float* kp = kappa + size_t(b) * n;
+    const int* am = amax + size_t(b) * n;
+    int before = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) before += x[i] == -1;
+    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = before;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) s += red[w];
+        red[0] = s;
+    }
+    __syncthreads();
+    const int masked = red[0];
+    __syncthreads();
+    if (first) {
+        int cnt = 0;
+        for (int l = threadIdx.x; l < L; l += blockDim.x) {
+            int br = -1;
+            float bk = 0.0f;
+            for (int k = 0; k < K; ++k) {
+                int i = l * K + k;
+                if (x[i] != -1) continue;
+                if (br < 0 || kp[i] > bk) { br = k; bk = kp[i]; }
+            }
+            if (br >= 0) { x[l * K + br] = am[l * K + br]; ++cnt; }
+        }
+        if (reveal_count) {
+            for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (threadIdx.x % 32 == 0) atomicAdd(reveal_count + b, cnt); // a count, not data: order-free
+        }
+        return;
+    }
+    const int base = n - init_masked[b];
+    const int target = base + int(llround(rho * double(init_masked[b])));
+    const int need = target - (n - masked);
+    if (need <= 0) return;
+    int size = 1;
+    while (size < n) size <<= 1;
+    for (int i = threadIdx.x; i < size; i += blockDim.x) {
+        unsigned long long kk = ~0ull;
+        if (i < n && x[i] == -1) {
+            int l = i / K, k = i % K;
+            unsigned int bits = __float_as_uint(kp[i]);
+            kk = (static_cast<unsigned long long>(~bits) << 32) | (static_cast<unsigned long long>(k) << 16) |
+                 static_cast<unsigned long long>(l);
+        }
+        key[i] = kk;
+    }
+    __syncthreads();
+    for (int len = 2; len <= size; len <<= 1)
+        for (int j = len >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < size; i += blockDim.x) {
+                int p = i ^ j;
+                if (p > i) {
+                    bool up = (i & len) == 0;
+                    unsigned long long a = key[i], c = key[p];
+                    if ((a > c) == up) { key[i] = c; key[p] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    for (int r = threadIdx.x; r < need; r += blockDim.x) {
+        unsigned long long kk = key[r];
+        if (kk == ~0ull) continue;
+        int k = int((kk >> 16) & 0xffff), l = int(kk & 0xffff);
+        x[l * K + k] = am[l * K + k];
+    }
+}
+
+// ---- end of a pass (refine.cpp:175-192) ------------------------------------------------------
+// residual masks -> the last step's argmax
+__global__ void force_residual_kernel(int* __restrict__ X, const int* __restrict__ amax, int64_t n) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && X[i] == -1) X[i] = amax[i];
+}
+// updatable rows take the final (gamma = 0) pass's argmax; the rest stay bit-identical
+__global__ void finalize_kernel(int* __restrict__ X, const int* __restrict__ amax,
+                                const uint32_t* __restrict__ upd_mask, int K, int64_t n_bins_x_n, int n) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n_bins_x_n) return;
+    int64_t b = i / n;
+    int k = int(i % K);
+    if ((upd_mask[b] >> k) & 1u) X[i] = amax[i];
+}
+
+// ---- MaxProbScorer (refine.cpp:207-225) + remask selection, one block per bin --------------
+// mode 2 (rank): the k_low rows of lowest confidence, ties -> lower row.
+// mode 1 (threshold): rows with confidence < thr (refine.cpp:245-252).
+// Selected rows are re-masked; upd_mask / init_masked / n_low describe the coming pass.
+__global__ void remask_select_kernel(int* __restrict__ X, const float* __restrict__ kappa1, int L, int K,
+                                     int mode, int k_low, double thr, uint32_t* __restrict__ upd_mask,
+                                     int* __restrict__ init_masked, int* __restrict__ n_low_out,
+                                     float* __restrict__ conf_out) {
+    __shared__ double conf[32];
+    __shared__ uint32_t sel;
+    const int b = blockIdx.x;
+    const int n = L * K;
+    const float* kp = kappa1 + size_t(b) * n;
+    if (threadIdx.x < K) {
+        double s = 0.0;
+        for (int l = 0; l < L; ++l) s += double(kp[l * K + threadIdx.x]);
+        conf[threadIdx.x] = s / L;
+        if (conf_out) conf_out[size_t(b) * K + threadIdx.x] = float(conf[threadIdx.x]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t m = 0;
+        if (mode == 1) {
+            for (int k = 0; k < K; ++k)
+                if (conf[k] < thr) m |= 1u << k;
+        } else {
+            for (int r = 0; r < k_low; ++r) { // selection by repeated minimum, stable in k
+                int best = -1;
+                for (int k = 0; k < K; ++k)
+                    if (!((m >> k) & 1u) && (best < 0 || conf[k] < conf[best])) best = k;
+                m |= 1u << best;
+            }
+        }
+        sel = m;
+        upd_mask[b] = m;
+        int nl = __popc(m);
+        init_masked[b] = nl * L;
+        if (n_low_out) n_low_out[b] = nl;
+    }
+    __syncthreads();
+    const uint32_t m = sel;
+    int* x = X + size_t(b) * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if ((m >> (i % K)) & 1u) x[i] = -1;
+}
+
+// ---- layout transforms between the reference's K x L views and the internal (l, k) order ---
+__global__ void grid_to_internal_kernel(const int* __restrict__ ref, int* __restrict__ in, int L, int K,
+                                        int64_t total) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t b = i / (int64_t(L) * K);
+    int r = int(i % (int64_t(L) * K));
+    int l = r / K, k = r % K;
+    in[i] = ref[b * L * K + int64_t(k) * L + l];
+}
+__global__ void grid_to_ref_kernel(const int* __restrict__ in, int* __restrict__ ref, int L, int K,
+                                   int64_t total) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int64_t b = i / (int64_t(L) * K);
+    int r = int(i % (int64_t(L) * K));
+    int l = r / K, k = r % K;
+    ref[b * L * K + int64_t(k) * L + l] = in[i];
+}
+// rows of C values: internal (b,l,k) -> reference (b,k,l), optional leading layer index
+__global__ void rows_to_ref_kernel(const float* __restrict__ in, float* __restrict__ ref, int L, int K, int C,
+                                   int64_t total, int64_t ref_bin_stride, int64_t ref_offset) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    int c = int(i % C);
+    int64_t row = i / C;
+    int64_t b = row / (int64_t(L) * K);
+    int r = int(row % (int64_t(L) * K));
+    int l = r / K, k = r % K;
+    ref[b * ref_bin_stride + ref_offset + (int64_t(k) * L + l) * C + c] = in[i];
+}
+
+__global__ void fill_i32_kernel(int* __restrict__ p, int v, int64_t n) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+__global__ void fill_u32_kernel(uint32_t* __restrict__ p, uint32_t v, int64_t n) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out, int64_t n) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+__global__ void flush_kernel(int4* __restrict__ p, int64_t n, int v) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = make_int4(v, v, v, v);
+}
+
+} // namespace cider
