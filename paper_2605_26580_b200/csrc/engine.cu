@@ -111,6 +111,7 @@ struct LayerW {
     // matrices in the activation type (fp32 or bf16), biases fp32
     void *g1, *g2, *a1, *a2, *f1, *f2, *ak;
     float *gb1, *gb2, *ab1, *ab2, *fb1, *fb2, *aq;
+    float* au; // heads x D: u_h = Wk_h^T q_h, the attention score vectors
 };
 
 struct Stat {
@@ -135,6 +136,7 @@ struct cider_ctx {
     std::unique_ptr<Gf> gf;
     std::unique_ptr<Tanner> tg;
     int L = 0, P = 0, E = 0;
+    int max_check_deg = 0;
     // weights
     std::vector<DevBuf> wbufs;
     float* Etab = nullptr;                 // (Q+1) x D fp32
@@ -358,6 +360,8 @@ void* wsbuf(cider_ctx& c, const char* name, size_t bytes) {
     return b.p;
 }
 
+bool pool_fast(const cider_ctx& c);
+
 // Sizes (per bin) of the chunk workspace; rows padded to the 128-row GEMM tile.
 WS workspace(cider_ctx& c, int nb, int K, bool want_flog) {
     const size_t Ms = round_up(size_t(nb) * c.L * K, 128), Me = round_up(size_t(nb) * c.E * K, 128);
@@ -381,7 +385,7 @@ WS workspace(cider_ctx& c, int nb, int K, bool want_flog) {
     w.mapped = wsbuf(c, "mapped", Me * D * A);
     w.Mq = wsbuf(c, "Mq", Me * Q * A);
     w.accq = wsbuf(c, "accq", Ms * Q * A);
-    w.keys = c.heads ? (float*)wsbuf(c, "keys", Me * D * 4) : nullptr;
+    w.keys = (c.heads && !pool_fast(c)) ? (float*)wsbuf(c, "keys", Me * D * 4) : nullptr;
     w.logits = c.bf16 ? nullptr : (float*)wsbuf(c, "logits", Ms * Q * 4);
     if (c.bf16) {
         w.Zt = wsbuf(c, "Zt", Ms * D * A);
@@ -419,6 +423,51 @@ int chunk_bins(cider_ctx& c, int K) {
     return nb;
 }
 
+
+// ---- Tanner / demix kernel dispatch (warp-vectorised fast paths, generic fallbacks) ----------
+template <typename T>
+void run_demix(cider_ctx& c, const float* lbar, const float* S, int64_t slotrows, int K, T* out) {
+    const int Q = c.Q;
+    if (K <= 32) {
+        demix_block_kernel<T><<<unsigned(slotrows), std::min(256, ((Q + 31) / 32) * 32), 0, c.stream>>>(lbar, S, K, Q, float(c.md.tau_demix), out);
+    } else {
+        demix_kernel<T><<<blocks_for(slotrows * Q), 256, 0, c.stream>>>(lbar, S, slotrows, K, Q, float(c.md.tau_demix), out);
+    }
+}
+template <typename T>
+void run_gather(cider_ctx& c, const T* U, int K, int64_t Me, T* Ae) {
+    const int V = c.Q / 32;
+    const unsigned g = blocks_for(Me * 32);
+    if (c.Q % 32 == 0 && V == 8) gather_perm_warp_kernel<T, 8><<<g, 256, 0, c.stream>>>(U, c.e_slot, c.perm_in, c.L, c.E, K, c.Q, Me, Ae);
+    else if (c.Q % 32 == 0 && V == 4) gather_perm_warp_kernel<T, 4><<<g, 256, 0, c.stream>>>(U, c.e_slot, c.perm_in, c.L, c.E, K, c.Q, Me, Ae);
+    else if (c.Q % 32 == 0 && V == 2) gather_perm_warp_kernel<T, 2><<<g, 256, 0, c.stream>>>(U, c.e_slot, c.perm_in, c.L, c.E, K, c.Q, Me, Ae);
+    else gather_perm_kernel<T><<<blocks_for(Me * c.Q), 256, 0, c.stream>>>(U, c.e_slot, c.perm_in, c.L, c.E, K, c.Q, Me, Ae);
+}
+template <typename T>
+void run_scatter(cider_ctx& c, const T* Mq, int K, int64_t Ms, T* accq) {
+    const int V = c.Q / 32;
+    const unsigned g = blocks_for(Ms * 32);
+    if (c.Q % 32 == 0 && V == 8) scatter_perm_warp_kernel<T, 8><<<g, 256, 0, c.stream>>>(Mq, c.slot_ptr, c.slot_edge, c.perm_out, c.L, c.E, K, c.Q, Ms, accq);
+    else if (c.Q % 32 == 0 && V == 4) scatter_perm_warp_kernel<T, 4><<<g, 256, 0, c.stream>>>(Mq, c.slot_ptr, c.slot_edge, c.perm_out, c.L, c.E, K, c.Q, Ms, accq);
+    else if (c.Q % 32 == 0 && V == 2) scatter_perm_warp_kernel<T, 2><<<g, 256, 0, c.stream>>>(Mq, c.slot_ptr, c.slot_edge, c.perm_out, c.L, c.E, K, c.Q, Ms, accq);
+    else scatter_perm_kernel<T, T><<<blocks_for(Ms * c.Q), 256, 0, c.stream>>>(Mq, c.slot_ptr, c.slot_edge, c.perm_out, c.L, c.E, K, c.Q, Ms, accq);
+}
+bool pool_fast(const cider_ctx& c) {
+    const int V = c.D / 32;
+    return c.D % 32 == 0 && (V == 2 || V == 4 || V == 8) && c.max_check_deg <= POOL_DMAX &&
+           (c.heads == 0 || (c.D / c.heads) % V == 0);
+}
+template <typename T>
+void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* pooled) {
+    const int V = c.D / 32;
+    const int64_t groups = int64_t(nb) * c.P * K;
+    const unsigned g = blocks_for(groups * 32);
+    const float* U = c.heads ? lw.au : nullptr;
+    if (V == 8) pool_warp_kernel<T, 8><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, c.heads, groups, pooled);
+    else if (V == 4) pool_warp_kernel<T, 4><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, c.heads, groups, pooled);
+    else pool_warp_kernel<T, 2><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, c.heads, groups, pooled);
+}
+
 // ---- one denoiser forward over nb bins (denoiser.cpp:253-259) -------------------------------
 struct FwdOpts {
     float tau = 1.0f;
@@ -445,10 +494,8 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         gemm(c, "gemm_lbar", w.Zt, D, nullptr, 0, c.W, Ms, Q, e);
         {
             Launch lg(c, "demix", 0, double(Ms) * Q * (4 + c.act_size) + double(nb) * L * Q * 4);
-            if (c.bf16)
-                demix_kernel<bf16><<<blocks_for(int64_t(nb) * L * Q), 256, 0, c.stream>>>(w.lbar, S, int64_t(nb) * L, K, Q, float(c.md.tau_demix), (bf16*)w.Aq);
-            else
-                demix_kernel<float><<<blocks_for(int64_t(nb) * L * Q), 256, 0, c.stream>>>(w.lbar, S, int64_t(nb) * L, K, Q, float(c.md.tau_demix), (float*)w.Aq);
+            if (c.bf16) run_demix<bf16>(c, w.lbar, S, int64_t(nb) * L, K, (bf16*)w.Aq);
+            else run_demix<float>(c, w.lbar, S, int64_t(nb) * L, K, (float*)w.Aq);
             check_launch("demix");
         }
         e = epi(EP_STORE);
@@ -466,20 +513,24 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         gemm(c, "gemm_symproj", w.Ztt, D, nullptr, 0, c.W, Ms, Q, e);
         {
             Launch lg(c, "gather_perm", 0, double(Me) * Q * 2 * c.act_size);
-            if (c.bf16)
-                gather_perm_kernel<bf16><<<blocks_for(Me * Q), 256, 0, c.stream>>>((bf16*)w.U, c.e_slot, c.perm_in, L, E, K, Q, Me, (bf16*)w.Ae);
-            else
-                gather_perm_kernel<float><<<blocks_for(Me * Q), 256, 0, c.stream>>>((float*)w.U, c.e_slot, c.perm_in, L, E, K, Q, Me, (float*)w.Ae);
+            if (c.bf16) run_gather<bf16>(c, (const bf16*)w.U, K, Me, (bf16*)w.Ae);
+            else run_gather<float>(c, (const float*)w.U, K, Me, (float*)w.Ae);
             check_launch("gather_perm");
         }
         e = epi(EP_STORE);
         e.out_t = w.Nn; e.ldo = D;
         gemm(c, "gemm_backproj", w.Ae, Q, nullptr, 0, c.Wt, Me, D, e);
-        if (c.heads) {
+        if (pool_fast(c)) {
+            Launch lg(c, c.heads ? "pool_attn" : "pool_sum", 2.0 * double(Me) * D * (c.heads + c.max_check_deg),
+                      double(Me) * D * 2 * c.act_size);
+            if (c.bf16) run_pool<bf16>(c, lw, (const bf16*)w.Nn, nb, K, (bf16*)w.pooled);
+            else run_pool<float>(c, lw, (const float*)w.Nn, nb, K, (float*)w.pooled);
+            check_launch("pool");
+        } else if (c.heads) {
             e = epi(EP_STORE);
             e.out_f = w.keys; e.ldo = D;
             gemm(c, "gemm_attn_key", w.Nn, D, nullptr, 0, lw.ak, Me, D, e);
-            Launch lg(c, "pool_attn", 0, double(Me) * D * (2 * c.act_size + 4));
+            Launch lg(c, "pool_attn_generic", 0, double(Me) * D * (2 * c.act_size + 4));
             const unsigned groups = unsigned(int64_t(nb) * c.P * K);
             if (c.bf16)
                 pool_attn_kernel<bf16, bf16><<<groups, 128, 0, c.stream>>>((bf16*)w.Nn, w.keys, lw.aq, c.check_ptr, c.P, E, K, D, c.heads, (bf16*)w.pooled);
@@ -487,7 +538,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
                 pool_attn_kernel<float, float><<<groups, 128, 0, c.stream>>>((float*)w.Nn, w.keys, lw.aq, c.check_ptr, c.P, E, K, D, c.heads, (float*)w.pooled);
             check_launch("pool_attn");
         } else {
-            Launch lg(c, "pool_sum", 0, double(Me) * D * 2 * c.act_size);
+            Launch lg(c, "pool_sum_generic", 0, double(Me) * D * 2 * c.act_size);
             if (c.bf16)
                 pool_sum_kernel<bf16, bf16><<<blocks_for(Me * D), 256, 0, c.stream>>>((bf16*)w.Nn, c.e_check, c.check_ptr, E, K, D, Me, (bf16*)w.pooled);
             else
@@ -505,10 +556,8 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         gemm(c, "gemm_msgproj", w.mapped, D, nullptr, 0, c.W, Me, Q, e);
         {
             Launch lg(c, "scatter_perm", 0, double(Ms) * Q * c.act_size + double(Me) * Q * c.act_size);
-            if (c.bf16)
-                scatter_perm_kernel<bf16, bf16><<<blocks_for(Ms * Q), 256, 0, c.stream>>>((bf16*)w.Mq, c.slot_ptr, c.slot_edge, c.perm_out, L, E, K, Q, Ms, (bf16*)w.accq);
-            else
-                scatter_perm_kernel<float, float><<<blocks_for(Ms * Q), 256, 0, c.stream>>>((float*)w.Mq, c.slot_ptr, c.slot_edge, c.perm_out, L, E, K, Q, Ms, (float*)w.accq);
+            if (c.bf16) run_scatter<bf16>(c, (const bf16*)w.Mq, K, Ms, (bf16*)w.accq);
+            else run_scatter<float>(c, (const float*)w.Mq, K, Ms, (float*)w.accq);
             check_launch("scatter_perm");
         }
         e = epi(EP_STORE);
@@ -774,6 +823,7 @@ void upload_model(cider_ctx& c, const float* w) {
         p = take(D); L.fb2 = upload_vec(c, p, D);
         L.ak = nullptr;
         L.aq = nullptr;
+        L.au = nullptr;
     }
     if (c.heads)
         for (int l = 0; l < c.N; ++l) {
@@ -781,6 +831,19 @@ void upload_model(cider_ctx& c, const float* w) {
             c.lw[l].aq = upload_vec(c, q, D);
             const float* k = take(size_t(D) * D);
             c.lw[l].ak = upload_mat(c, k, D, D, false);
+            // u_h[col] = sum_{t in head h} q[t] Wk[t][col], from the values the device runs with
+            const int dh = D / c.heads;
+            auto rv = [&](float v) { return c.bf16 ? double(bf16_round(v)) : double(v); };
+            std::vector<float> u(size_t(c.heads) * D);
+            for (int h = 0; h < c.heads; ++h)
+                for (int col = 0; col < D; ++col) {
+                    double acc = 0.0;
+                    for (int t = h * dh; t < (h + 1) * dh; ++t) acc += rv(q[t]) * rv(k[size_t(t) * D + col]);
+                    u[size_t(h) * D + col] = float(acc);
+                }
+            DevBuf& b = wbuf(c, u.size() * 4);
+            ck(cudaMemcpy(b.p, u.data(), u.size() * 4, cudaMemcpyHostToDevice), "upload");
+            c.lw[l].au = b.as<float>();
         }
 }
 
@@ -879,9 +942,11 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
         if (c->bf16 && (c->Q % 64 || c->D % 64 || c->H % 64 || c->Q > 256))
             throw InvalidInput("BF16 mode needs Q, D, H multiples of 64 and Q <= 256");
         if (c->heads > ATT_MAXH) throw InvalidInput("cider: at most 32 attention heads");
-        for (int j = 0; j < c->P; ++j)
-            if (c->tg->check_ptr[j + 1] - c->tg->check_ptr[j] > ATT_MAXD)
-                throw InvalidInput("cider: check degree above 32");
+        for (int j = 0; j < c->P; ++j) {
+            const int dj = c->tg->check_ptr[j + 1] - c->tg->check_ptr[j];
+            if (dj > ATT_MAXD) throw InvalidInput("cider: check degree above 32");
+            c->max_check_deg = std::max(c->max_check_deg, dj);
+        }
         require_device();
         c->device = device;
         ck(cudaSetDevice(device), "cudaSetDevice");

@@ -145,6 +145,202 @@ __global__ void pool_attn_kernel(const Tin* __restrict__ Nn, const float* __rest
     }
 }
 
+// ---- warp-per-group Tanner kernels (the fast paths) -------------------------------------------
+// A lane owns V consecutive channels of a row (V = C/32), so every row access is one 4..16-byte
+// vector per lane: fully coalesced, no 64-bit index arithmetic per element.
+template <typename T, int V> struct Vec;
+template <> struct Vec<float, 2> { typedef float2 type; };
+template <> struct Vec<float, 4> { typedef float4 type; };
+template <> struct Vec<float, 8> { typedef float4 type; };
+template <> struct Vec<bf16, 2> { typedef uint32_t type; };
+template <> struct Vec<bf16, 4> { typedef uint2 type; };
+template <> struct Vec<bf16, 8> { typedef uint4 type; };
+
+template <typename T, int V>
+__device__ __forceinline__ void load_v(const T* p, float* out) {
+    if constexpr (sizeof(T) == 2) {
+        if constexpr (V == 8) {
+            uint4 u = *reinterpret_cast<const uint4*>(p);
+            const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) out[i] = __bfloat162float(h[i]);
+        } else if constexpr (V == 4) {
+            uint2 u = *reinterpret_cast<const uint2*>(p);
+            const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) out[i] = __bfloat162float(h[i]);
+        } else {
+            uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+            const bf16* h = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) out[i] = __bfloat162float(h[i]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; i += 2) {
+            float2 f = *reinterpret_cast<const float2*>(p + i);
+            out[i] = f.x;
+            out[i + 1] = f.y;
+        }
+    }
+}
+template <typename T, int V>
+__device__ __forceinline__ void store_v(T* p, const float* v) {
+    if constexpr (sizeof(T) == 2) {
+        bf16 h[V];
+#pragma unroll
+        for (int i = 0; i < V; ++i) h[i] = __float2bfloat16_rn(v[i]);
+        if constexpr (V == 8) *reinterpret_cast<uint4*>(p) = *reinterpret_cast<uint4*>(h);
+        else if constexpr (V == 4) *reinterpret_cast<uint2*>(p) = *reinterpret_cast<uint2*>(h);
+        else *reinterpret_cast<uint32_t*>(p) = *reinterpret_cast<uint32_t*>(h);
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; i += 2) *reinterpret_cast<float2*>(p + i) = make_float2(v[i], v[i + 1]);
+    }
+}
+
+// Extrinsic pooling of one (bin, check, row) group per warp. heads == 0: sum-pool
+// (denoiser.cpp:196-203); heads > 0: pooling attention with scores <u_h, n_i>, where
+// u_h = Wk_h^T q_h (precomputed per layer) equals <q_h, (Wk n_i)_h> of DESIGN.md §2.
+constexpr int POOL_DMAX = 8;
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+pool_warp_kernel(const T* __restrict__ Nn, const float* __restrict__ U, const int* __restrict__ check_ptr, int P, int E,
+                 int K, int D, int heads, int64_t n_groups, T* __restrict__ pooled) {
+    const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    if (g >= n_groups) return;
+    const int k = int(g % K);
+    const int64_t bj = g / K;
+    const int j = int(bj % P);
+    const int64_t b = bj / P;
+    const int e0 = check_ptr[j], d = check_ptr[j + 1] - e0;
+    const int c0 = lane * V;
+    float nv[POOL_DMAX][V];
+#pragma unroll
+    for (int i = 0; i < POOL_DMAX; ++i)
+        if (i < d) load_v<T, V>(Nn + ((b * E + e0 + i) * K + k) * D + c0, nv[i]);
+    float sc[POOL_DMAX];
+    if (heads) {
+        const int my_head = c0 / (D / heads);
+#pragma unroll
+        for (int i = 0; i < POOL_DMAX; ++i) sc[i] = 0.0f;
+        for (int h = 0; h < heads; ++h) {
+            float u[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) u[v] = U[size_t(h) * D + c0 + v];
+#pragma unroll
+            for (int i = 0; i < POOL_DMAX; ++i) {
+                if (i >= d) break;
+                float p = 0.0f;
+#pragma unroll
+                for (int v = 0; v < V; ++v) p = fmaf(u[v], nv[i][v], p);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+                if (h == my_head) sc[i] = p * rsqrtf(float(D / heads));
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < POOL_DMAX; ++i) {
+        if (i >= d) break;
+        float out[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) out[v] = 0.0f;
+        if (heads) {
+            float mx = -INFINITY, den = 0.0f;
+#pragma unroll
+            for (int i2 = 0; i2 < POOL_DMAX; ++i2)
+                if (i2 < d && i2 != i) mx = fmaxf(mx, sc[i2]);
+#pragma unroll
+            for (int i2 = 0; i2 < POOL_DMAX; ++i2)
+                if (i2 < d && i2 != i) den += expf(sc[i2] - mx);
+#pragma unroll
+            for (int i2 = 0; i2 < POOL_DMAX; ++i2) {
+                if (i2 >= d || i2 == i) continue;
+                const float w = float(d - 1) * expf(sc[i2] - mx) / den;
+#pragma unroll
+                for (int v = 0; v < V; ++v) out[v] = fmaf(w, nv[i2][v], out[v]);
+            }
+        } else {
+#pragma unroll
+            for (int i2 = 0; i2 < POOL_DMAX; ++i2) {
+                if (i2 >= d || i2 == i) continue;
+#pragma unroll
+                for (int v = 0; v < V; ++v) out[v] += nv[i2][v];
+            }
+        }
+        store_v<T, V>(pooled + ((b * E + e0 + i) * K + k) * D + c0, out);
+    }
+}
+
+// Pi_alpha gather, one edge row per warp, V = Q/32 symbols per lane.
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+gather_perm_warp_kernel(const T* __restrict__ U, const int* __restrict__ e_slot, const uint8_t* __restrict__ perm_in,
+                        int L, int E, int K, int Q, int64_t n_rows, T* __restrict__ Ae) {
+    const int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    if (r >= n_rows) return;
+    const int k = int(r % K);
+    const int64_t be = r / K;
+    const int e = int(be % E);
+    const int64_t b = be / E;
+    const T* src = U + ((b * L + e_slot[e]) * K + k) * Q;
+    const uint8_t* pm = perm_in + size_t(e) * Q + lane * V;
+    float v[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = to_f(src[pm[i]]);
+    store_v<T, V>(Ae + r * Q + lane * V, v);
+}
+
+// Ordered per-slot accumulation in symbol space, one site row per warp.
+template <typename T, int V>
+__global__ void __launch_bounds__(256)
+scatter_perm_warp_kernel(const T* __restrict__ Mq, const int* __restrict__ slot_ptr, const int* __restrict__ slot_edge,
+                         const uint8_t* __restrict__ perm_out, int L, int E, int K, int Q, int64_t n_rows,
+                         T* __restrict__ accq) {
+    const int64_t m = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    if (m >= n_rows) return;
+    const int k = int(m % K);
+    const int64_t bl = m / K;
+    const int l = int(bl % L);
+    const int64_t b = bl / L;
+    float s[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) s[i] = 0.0f;
+    for (int p = slot_ptr[l]; p < slot_ptr[l + 1]; ++p) {
+        const int e = slot_edge[p];
+        const T* src = Mq + ((b * E + e) * K + k) * Q;
+        const uint8_t* pm = perm_out + size_t(e) * Q + lane * V;
+#pragma unroll
+        for (int i = 0; i < V; ++i) s[i] += to_f(src[pm[i]]);
+    }
+    store_v<T, V>(accq + m * Q + lane * V, s);
+}
+
+// Demixing, one slot row (b, l) per block, one symbol per thread (see demix_kernel).
+template <typename T>
+__global__ void demix_block_kernel(const float* __restrict__ lbar, const float* __restrict__ S, int K, int Q, float tau,
+                                   T* __restrict__ out) {
+    const int64_t s = blockIdx.x;
+    for (int a = threadIdx.x; a < Q; a += blockDim.x) {
+        const float* x = lbar + s * K * Q + a;
+        float xv[32];
+        float mx = -INFINITY;
+        for (int k = 0; k < K; ++k) { xv[k] = x[size_t(k) * Q]; mx = fmaxf(mx, xv[k]); }
+        long long den = 0;
+        for (int k = 0; k < K; ++k) {
+            xv[k] = expf((xv[k] - mx) / tau);
+            den += __double2ll_rn(double(xv[k]) * 4503599627370496.0);
+        }
+        const float denf = float(double(den) * (1.0 / 4503599627370496.0));
+        const float sv = S[s * Q + a];
+        for (int k = 0; k < K; ++k) out[(s * K + k) * Q + a] = from_f<T>((xv[k] / denf) * sv);
+    }
+}
+
 // ---- de-normalisation + ordered scatter-add (denoiser.cpp:205-207), in symbol space --------
 // accq[(b,l,k)][c] = sum over slot l's edges e, ascending check, of Mq[(b,e,k)][perm_out[e][c]],
 // perm_out[e][c] = alpha_e * c. A gather in a fixed order: no atomics, bitwise deterministic.

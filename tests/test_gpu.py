@@ -1,0 +1,250 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on the same seeded
+inputs and weights.
+
+Tolerances (BASELINE.json north_star):
+  FP32 mode: logits / incoming messages within 1e-3 relative (to max |value|); decoded grids,
+             first-reveal counts, remask rows / steps / indices identical.
+  BF16 mode: logits / messages within 3e-2 relative (bf16 operands, fp32 accumulation, tanh-form
+             GELU in the fused MLP epilogues); SER within 0.05 of the oracle's on the same bins.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-3
+BF16_TOL = 3e-2
+
+
+def ctx_for(P, model, wl, seed=1, edges=None):
+    e = wl.code() if edges is None else edges
+    w = P.weights_init(model, seed)
+    return P.Context(model, w, e, wl.checks, wl.slots), e, w
+
+
+def as_run(P, model, w):
+    return P.model_weights_as_run(model, w)
+
+
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_denoise_parity_all_configs(P, oracle, name):
+    """One forward on partially revealed grids: logits and every layer's check messages."""
+    cfg = P.configs()[name]
+    wl, model = cfg.workload, cfg.model
+    ctx, e, w = ctx_for(P, model, wl)
+    nb = 2 if name in ("c1", "c2") else 1
+    _, S = wl.bins(e, 0, nb)
+    rng = np.random.default_rng(11)
+    X = np.where(rng.random((nb, wl.k, wl.slots)) < 0.5, rng.integers(0, model.q, size=(nb, wl.k, wl.slots)), -1)
+    X = X.astype(np.int32)
+    lg, inc = ctx.denoise(X, S, want_incoming=True)
+    tol = FP32_TOL if model.precision == P.FP32 else BF16_TOL
+    for b in range(nb):
+        lo, io = oracle.denoise(model, as_run(P, model, w), e, wl.checks, wl.slots, X[b], S[b].astype(np.float64), True)
+        assert rel_err(lg[b], lo) < tol
+        for layer in range(model.layers):
+            assert rel_err(inc[b, layer], io[layer]) < tol
+
+
+def test_c1_full_decode_identical_to_oracle(P, oracle):
+    """BASELINE config 1 end to end (64 bins, T=4, FP32): identical decoded sets and SER."""
+    cfg = P.configs()["c1"]
+    wl, model = cfg.workload, cfg.model
+    ctx, e, w = ctx_for(P, model, wl)
+    truth, S = wl.bins(e, 0, cfg.bins)
+    sched = P.RevealSchedule(steps=cfg.steps)
+    grid, fl, tr = ctx.refine(S, wl.k, sched, want_final_logits=True, want_trace=True)
+    ro = oracle.refine(model, as_run(P, model, w), e, wl.checks, wl.slots, S.astype(np.float64), wl.k, sched,
+                       want_final_logits=True)
+    assert np.array_equal(grid, ro["grid"])
+    assert rel_err(fl, ro["final_logits"]) < FP32_TOL
+    assert np.array_equal(tr["first_reveals"], ro["first_reveals"])
+    assert P.ser_cer(truth, grid) == P.ser_cer(truth, ro["grid"])
+
+
+@pytest.mark.parametrize("remask", ["thr", "rank"])
+def test_remask_indices_identical_fp32(P, oracle, remask):
+    """Quality-guided remasking (refine.cpp:238-292): same rows selected, same T_rm, same grids;
+    rows outside K_low stay bit-identical."""
+    wl = P.Workload(m=4, slots=16, checks=8, k=8, snr_db=4.0, p_erase=0.1, p_false=0.1)
+    model = P.Model(m=4, dim=32, hidden=64, layers=2, heads=2)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 6)
+    rm = P.RemaskConfig(thresholds=(0.3, 0.2, 0.1)) if remask == "thr" else P.RemaskConfig(rank_fraction=0.25)
+    sched = P.RevealSchedule(steps=6)
+    grid, fl, tr = ctx.refine(S, 8, sched, rm, want_final_logits=True, want_trace=True)
+    ro = oracle.refine(model, as_run(P, model, w), e, wl.checks, wl.slots, S.astype(np.float64), 8, sched, rm,
+                       want_final_logits=True)
+    assert np.array_equal(grid, ro["grid"])
+    assert np.array_equal(tr["remask_rows"], ro["remask_rows"])
+    assert np.array_equal(tr["remask_steps"], ro["remask_steps"])
+    assert np.array_equal(tr["remask_mask"], ro["remask_mask"])
+    assert rel_err(fl, ro["final_logits"]) < FP32_TOL
+    plain = ctx.refine(S, 8, sched)
+    keep = tr["remask_mask"] == 0
+    assert np.array_equal(grid[keep], plain[keep])
+
+
+def test_threshold_remask_buckets_with_mixed_row_counts(P, oracle):
+    """Thresholds that select different |K_low| per bin exercise the per-bucket sub-batches."""
+    wl = P.Workload(m=4, slots=16, checks=8, k=4, snr_db=4.0)
+    model = P.Model.ref_exact(4, 32)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 8)
+    sched = P.RevealSchedule(steps=5)
+    ro0 = oracle.refine(model, as_run(P, model, w), e, wl.checks, wl.slots, S.astype(np.float64), 4, sched,
+                        want_final_logits=True)
+    conf = np.stack([(1.0 / np.exp(f - f.max(-1, keepdims=True)).sum(-1)).mean(-1) for f in ro0["final_logits"]])
+    thr = float(np.median(conf))
+    rm = P.RemaskConfig(thresholds=(min(0.99, thr + 1e-4), thr * 0.99))
+    grid, tr = ctx.refine(S, 4, sched, rm, want_trace=True)
+    ro = oracle.refine(model, as_run(P, model, w), e, wl.checks, wl.slots, S.astype(np.float64), 4, sched, rm)
+    assert len(set(ro["remask_rows"][:, 0].tolist())) > 1
+    assert np.array_equal(grid, ro["grid"])
+    assert np.array_equal(tr["remask_rows"], ro["remask_rows"])
+    assert np.array_equal(tr["remask_mask"], ro["remask_mask"])
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_bf16_config_ser_matches_oracle(P, oracle, name):
+    """BF16 configs: decoded SER on a subset agrees with the oracle's on the same bins."""
+    cfg = P.configs()[name]
+    wl = cfg.workload
+    small = P.Model(m=cfg.model.m, dim=64, hidden=128, layers=1, heads=cfg.model.heads and 2, precision=P.BF16)
+    ctx, e, w = ctx_for(P, small, wl)
+    nb = 4 if name == "c2" else 2
+    truth, S = wl.bins(e, 0, nb)
+    sched = P.RevealSchedule(steps=4)
+    grid = ctx.refine(S, wl.k, sched)
+    ro = oracle.refine(small, as_run(P, small, w), e, wl.checks, wl.slots, S.astype(np.float64), wl.k, sched)
+    assert abs(P.ser_cer(truth, grid)[0] - P.ser_cer(truth, ro["grid"])[0]) < 0.05
+
+
+def test_c3_remask_path_bf16_runs_and_matches_rows(P, oracle):
+    """Config-3 shape (K=8, Q=256, L=64) with the rank-25% remask on the tcgen05 path."""
+    cfg = P.configs()["c3"]
+    wl = cfg.workload
+    model = P.Model(m=8, dim=64, hidden=128, layers=1, heads=2, precision=P.BF16)
+    ctx, e, w = ctx_for(P, model, wl)
+    truth, S = wl.bins(e, 0, 2)
+    sched = P.RevealSchedule(steps=4)
+    grid, tr = ctx.refine(S, 8, sched, cfg.remask, want_trace=True)
+    ro = oracle.refine(model, as_run(P, model, w), e, wl.checks, wl.slots, S.astype(np.float64), 8, sched, cfg.remask)
+    assert np.all((grid >= 0) & (grid < 256))
+    assert np.all(tr["remask_rows"][:, 0] == 2) and np.all(tr["remask_steps"][:, 0] == 1)
+    assert np.all(tr["remask_mask"].sum(1) == 2)
+    assert abs(P.ser_cer(truth, grid)[0] - P.ser_cer(truth, ro["grid"])[0]) < 0.05
+
+
+# ---- invariants on the device ------------------------------------------------------------------
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_device_row_permutation_equivariance_bitwise(P, prec):
+    wl = P.Workload(m=6, slots=16, checks=8, k=4, snr_db=6.0)
+    model = P.Model(m=6, dim=64, hidden=128, layers=2, heads=2, precision=P.FP32 if prec == "fp32" else P.BF16)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 1)
+    X = np.random.default_rng(1).integers(-1, 64, size=(1, 4, 16)).astype(np.int32)
+    X[0, 3] = X[0, 1]  # two identical rows -> exact ties
+    base = ctx.denoise(X, S)
+    p = [2, 0, 3, 1]
+    perm = ctx.denoise(X[:, p], S)
+    assert np.array_equal(perm, base[:, p])
+    assert np.array_equal(base[0, 1], base[0, 3])
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_device_extrinsicity_bitwise(P, prec):
+    wl = P.Workload(m=6, slots=16, checks=8, k=2, snr_db=6.0)
+    model = P.Model(m=6, dim=64, hidden=64, layers=1, precision=P.FP32 if prec == "fp32" else P.BF16)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 1)
+    X = np.random.default_rng(2).integers(-1, 64, size=(1, 2, 16)).astype(np.int32)
+    _, base = ctx.denoise(X, S, want_incoming=True)
+    for l in (0, 7, 15):
+        Y = X.copy()
+        Y[0, :, l] = (np.maximum(Y[0, :, l], 0) + 5) % 64
+        _, inc = ctx.denoise(Y, S, want_incoming=True)
+        assert np.array_equal(inc[0, 0][:, l], base[0, 0][:, l])
+
+
+def test_determinism_and_chunk_invariance(P):
+    """Run-to-run bitwise determinism (no atomics) and independence of the internal chunking."""
+    cfg = P.configs()["c2"]
+    wl = cfg.workload
+    model = P.Model(m=6, dim=64, hidden=128, layers=2, heads=2, precision=P.BF16)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 37)
+    sched = P.RevealSchedule(steps=5)
+    a = ctx.refine(S, wl.k, sched, P.RemaskConfig(rank_fraction=0.25))
+    b = ctx.refine(S, wl.k, sched, P.RemaskConfig(rank_fraction=0.25))
+    ctx.set_chunk(5)
+    c = ctx.refine(S, wl.k, sched, P.RemaskConfig(rank_fraction=0.25))
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_c2_full_size_properties(P):
+    """BASELINE config 2 at full size (4096 bins, bf16): valid symbols, determinism, and the
+    decode is invariant to the bin batching (a checksum of per-bin checksums)."""
+    cfg = P.configs()["c2"]
+    wl, model = cfg.workload, cfg.model
+    ctx, e, w = ctx_for(P, model, wl)
+    truth, S = wl.bins(e, 0, cfg.bins)
+    sched = P.RevealSchedule(steps=cfg.steps)
+    g = ctx.refine(S, wl.k, sched)
+    assert np.all((g >= 0) & (g < model.q))
+    half = ctx.refine(S[: cfg.bins // 2], wl.k, sched)
+    assert np.array_equal(half, g[: cfg.bins // 2])
+    sums = (g.astype(np.int64) * np.arange(1, wl.k * wl.slots + 1).reshape(wl.k, wl.slots)).sum((1, 2))
+    g2 = ctx.refine(S, wl.k, sched)
+    sums2 = (g2.astype(np.int64) * np.arange(1, wl.k * wl.slots + 1).reshape(wl.k, wl.slots)).sum((1, 2))
+    assert int(sums.sum()) == int(sums2.sum())
+    ser, cer = P.ser_cer(truth, g)
+    assert 0.0 <= ser <= 1.0 and 0.0 <= cer <= 1.0
+
+
+# ---- edge cases ---------------------------------------------------------------------------------
+def test_edge_shapes_and_schedules(P, oracle):
+    wl = P.Workload(m=4, slots=16, checks=8, k=3, snr_db=6.0)
+    model = P.Model.ref_exact(4, 32)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 3)
+    wr = as_run(P, model, w)
+    for K, sched in [(1, P.RevealSchedule(steps=3)), (3, P.RevealSchedule(steps=1)),
+                     (3, P.RevealSchedule(steps=4, first_reveal=False)),
+                     (3, P.RevealSchedule(steps=6, tau_max=2.0, tau_min=0.25))]:
+        g = ctx.refine(S, K, sched)
+        ro = oracle.refine(model, wr, e, wl.checks, wl.slots, S.astype(np.float64), K, sched)
+        assert np.array_equal(g, ro["grid"]), (K, sched)
+    assert ctx.refine(S[:0], 3, P.RevealSchedule(steps=2)).shape == (0, 3, 16)
+
+
+def test_sparse_graph_slots_without_checks(P, oracle):
+    """test_denoiser.cpp:249-267: slots with no incident check get zero messages."""
+    model = P.Model.ref_exact(4, 32)
+    edges = np.array([[0, 0, 3], [0, 1, 5]], np.int32)
+    w = P.weights_init(model, 1)
+    ctx = P.Context(model, w, edges, 1, 12)
+    S = np.log(np.full((1, 12, 16), 1.0 / 16, np.float32))
+    X = np.random.default_rng(0).integers(-1, 16, size=(1, 2, 12)).astype(np.int32)
+    lg, inc = ctx.denoise(X, S, want_incoming=True)
+    lo, io = oracle.denoise(model, as_run(P, model, w), edges, 1, 12, X[0], S[0].astype(np.float64), True)
+    assert rel_err(lg[0], lo) < FP32_TOL
+    assert np.all(inc[0, 0][:, 2:] == 0.0)
+
+
+def test_input_errors_surface_like_the_reference(P):
+    wl = P.Workload(m=4, slots=16, checks=8, k=2, snr_db=6.0)
+    model = P.Model.ref_exact(4, 32)
+    ctx, e, w = ctx_for(P, model, wl)
+    _, S = wl.bins(e, 0, 1)
+    with pytest.raises(ValueError, match="embed_grid: token out of range"):
+        ctx.denoise(np.full((1, 2, 16), 16, np.int32), S)
+    with pytest.raises(ValueError, match="strictly descending"):
+        ctx.refine(S, 2, P.RevealSchedule(steps=2), P.RemaskConfig(thresholds=(0.4, 0.6)))
+    with pytest.raises(ValueError, match="tau_max >= tau_min > 0"):
+        ctx.refine(S, 2, P.RevealSchedule(steps=2, tau_max=0.5, tau_min=1.0))
+    with pytest.raises(ValueError, match="need T >= 1"):
+        ctx.refine(S, 2, P.RevealSchedule(steps=0))
