@@ -26,6 +26,7 @@
 #include "kernels/common.cuh"
 #include "kernels/gemm_simt.cuh"
 #include "kernels/gemm_tc.cuh"
+#include "kernels/mlp_tc.cuh"
 #include "kernels/path.cuh"
 
 namespace cider {
@@ -340,6 +341,57 @@ Epi epi(int kind) {
     return e;
 }
 
+// ---- fused two-layer maps (BF16 mode) -----------------------------------------------------------
+template <int KIN, int D>
+void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
+                const CUtensorMap& w2, const tc::MlpArgs& a) {
+    using Lay = tc::MlpLayout<KIN, D>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        ck(cudaFuncSetAttribute(tc::mlp_tc_kernel<KIN, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+           "smem attr");
+        attr_set = true;
+    }
+    const int grid = std::min(a.tiles, c.sm_count);
+    tc::mlp_tc_kernel<KIN, D><<<grid, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
+}
+
+bool mlp_fusable(const cider_ctx& c, int Kin) {
+    return c.bf16 && c.H % tc::MLP_HC == 0 && (c.D == 64 || c.D == 128 || c.D == 256) && (Kin == c.D || Kin == 2 * c.D);
+}
+
+// Y = ep(GELU([A0|A1] W1^T + b1) W2^T + b2); falls back to two GEMMs through the `hid` buffer.
+void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, int K1, const void* W1,
+         const float* b1, const void* W2, int64_t M, Epi ep, void* hid) {
+    const int Kin = K0 + K1, D = c.D, H = c.H;
+    if (!mlp_fusable(c, Kin)) {
+        std::string t1 = std::string(tag) + "_1", t2 = std::string(tag) + "_2";
+        Epi e1 = epi(EP_GELU);
+        e1.bias = b1; e1.out_t = hid; e1.ldo = H;
+        gemm(c, t1.c_str(), A0, K0, A1, K1, W1, M, H, e1);
+        gemm(c, t2.c_str(), hid, H, nullptr, 0, W2, M, D, ep);
+        return;
+    }
+    ep.M = int(M);
+    ep.N = D;
+    Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
+    const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
+    const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;
+    const CUtensorMap& w1 = map_for(c, W1, H, Kin, Kin, tc::MLP_HC);
+    const CUtensorMap& w2 = map_for(c, W2, D, H, H, D);
+    tc::MlpArgs a;
+    a.M = int(M);
+    a.K0 = A1 ? K0 : Kin;
+    a.H = H;
+    a.tiles = int((M + 127) / 128);
+    a.b1 = b1;
+    a.ep = ep;
+    if (D == 256) { if (Kin == 512) launch_mlp<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp<256, 256>(c, x0, x1, w1, w2, a); }
+    else if (D == 128) { if (Kin == 256) launch_mlp<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp<128, 128>(c, x0, x1, w1, w2, a); }
+    else { if (Kin == 128) launch_mlp<128, 64>(c, x0, x1, w1, w2, a); else launch_mlp<64, 64>(c, x0, x1, w1, w2, a); }
+    check_launch(tag);
+}
+
 // ---- workspace ------------------------------------------------------------------------------
 struct WS {
     int* X;
@@ -368,10 +420,11 @@ WS workspace(cider_ctx& c, int nb, int K, bool want_flog) {
     const size_t A = c.act_size, Q = c.Q, D = c.D, H = c.H;
     WS w{};
     w.X = (int*)wsbuf(c, "X", Ms * 4);
-    w.Zf = (float*)wsbuf(c, "Zf", Ms * D * 4);
+    // the fp32 residual stream exists only in FP32 mode; BF16 mode keeps it in bf16
+    w.Zf = c.bf16 ? nullptr : (float*)wsbuf(c, "Zf", Ms * D * 4);
     w.lbar = (float*)wsbuf(c, "lbar", Ms * Q * 4);
-    w.ef = (float*)wsbuf(c, "ef", Ms * D * 4);
-    w.Ztf = (float*)wsbuf(c, "Ztf", Ms * D * 4);
+    w.ef = c.bf16 ? nullptr : (float*)wsbuf(c, "ef", Ms * D * 4);
+    w.Ztf = c.bf16 ? nullptr : (float*)wsbuf(c, "Ztf", Ms * D * 4);
     w.accf = (float*)wsbuf(c, "accf", Ms * D * 4);
     w.kappa = (float*)wsbuf(c, "kappa", Ms * 4);
     w.k1 = (float*)wsbuf(c, "k1", Ms * 4);
@@ -454,20 +507,35 @@ void run_scatter(cider_ctx& c, const T* Mq, int K, int64_t Ms, T* accq) {
 }
 bool pool_fast(const cider_ctx& c) {
     const int V = c.D / 32;
-    return c.D % 32 == 0 && (V == 2 || V == 4 || V == 8) && c.max_check_deg <= POOL_DMAX &&
-           (c.heads == 0 || (c.D / c.heads) % V == 0);
+    const bool heads_ok = c.heads == 0 || ((c.heads == 2 || c.heads == 4 || c.heads == 8 || c.heads == 16) &&
+                                           (c.D / c.heads) % V == 0);
+    return c.D % 32 == 0 && (V == 2 || V == 4 || V == 8) && c.max_check_deg <= POOL_DMAX && heads_ok;
+}
+template <typename T, int V, int DM>
+void run_pool_d(cider_ctx& c, const LayerW& lw, const T* Nn, int K, int64_t groups, T* pooled) {
+    const unsigned g = blocks_for(groups * 32);
+    const float* U = lw.au;
+    switch (c.heads) {
+        case 0: pool_warp_kernel<T, V, 0, DM><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 2: pool_warp_kernel<T, V, 2, DM><<<g, 256, size_t(2) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 4: pool_warp_kernel<T, V, 4, DM><<<g, 256, size_t(4) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 8: pool_warp_kernel<T, V, 8, DM><<<g, 256, size_t(8) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        default: pool_warp_kernel<T, V, 16, DM><<<g, 256, size_t(16) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+    }
+}
+template <typename T, int V>
+void run_pool_v(cider_ctx& c, const LayerW& lw, const T* Nn, int K, int64_t groups, T* pooled) {
+    if (c.max_check_deg <= 6) run_pool_d<T, V, 6>(c, lw, Nn, K, groups, pooled);
+    else run_pool_d<T, V, 8>(c, lw, Nn, K, groups, pooled);
 }
 template <typename T>
 void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* pooled) {
     const int V = c.D / 32;
     const int64_t groups = int64_t(nb) * c.P * K;
-    const unsigned g = blocks_for(groups * 32);
-    const float* U = c.heads ? lw.au : nullptr;
-    if (V == 8) pool_warp_kernel<T, 8><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, c.heads, groups, pooled);
-    else if (V == 4) pool_warp_kernel<T, 4><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, c.heads, groups, pooled);
-    else pool_warp_kernel<T, 2><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, c.heads, groups, pooled);
+    if (V == 8) run_pool_v<T, 8>(c, lw, Nn, K, groups, pooled);
+    else if (V == 4) run_pool_v<T, 4>(c, lw, Nn, K, groups, pooled);
+    else run_pool_v<T, 2>(c, lw, Nn, K, groups, pooled);
 }
-
 // ---- one denoiser forward over nb bins (denoiser.cpp:253-259) -------------------------------
 struct FwdOpts {
     float tau = 1.0f;
@@ -481,7 +549,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
     {
         Launch lg(c, "embed", 0, double(Ms) * D * (4 + c.act_size));
         if (c.bf16)
-            embed_kernel<bf16><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, w.Zf, (bf16*)w.Zt);
+            embed_kernel<bf16><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, nullptr, (bf16*)w.Zt);
         else
             embed_kernel<float><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, w.Zf, nullptr);
         check_launch("embed");
@@ -499,14 +567,12 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             check_launch("demix");
         }
         e = epi(EP_STORE);
-        e.out_f = w.ef; e.out_t = c.bf16 ? w.et : nullptr; e.ldo = D;
+        e.out_f = w.ef; e.out_t = c.bf16 ? w.et : nullptr; e.ldo = D; // (ef is null in BF16 mode)
         gemm(c, "gemm_evid", w.Aq, Q, nullptr, 0, c.Vt, Ms, D, e);
-        e = epi(EP_GELU);
-        e.bias = lw.gb1; e.out_t = w.hid; e.ldo = H;
-        gemm(c, "gemm_gate1", w.Zt, D, w.et, D, lw.g1, Ms, H, e);
         e = epi(EP_GATE);
-        e.bias = lw.gb2; e.z = w.Zf; e.e = w.ef; e.ldz = D; e.out_f = w.Ztf; e.out_t = c.bf16 ? w.Ztt : nullptr; e.ldo = D;
-        gemm(c, "gemm_gate2", w.hid, H, nullptr, 0, lw.g2, Ms, D, e);
+        e.bias = lw.gb2; e.z = w.Zf; e.e = w.ef; e.zb = (const bf16*)w.Zt; e.eb = (const bf16*)w.et; e.ldz = D;
+        e.out_f = w.Ztf; e.out_t = c.bf16 ? w.Ztt : nullptr; e.ldo = D;
+        mlp(c, "mlp_gate", w.Zt, D, w.et, D, lw.g1, lw.gb1, lw.g2, Ms, e, w.hid);
         // Module B (denoiser.cpp:181-228)
         e = epi(EP_STORE);
         e.out_t = w.U; e.ldo = Q;
@@ -545,12 +611,9 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
                 pool_sum_kernel<float, float><<<blocks_for(Me * D), 256, 0, c.stream>>>((float*)w.Nn, c.e_check, c.check_ptr, E, K, D, Me, (float*)w.pooled);
             check_launch("pool_sum");
         }
-        e = epi(EP_GELU);
-        e.bias = lw.ab1; e.out_t = w.hid; e.ldo = H;
-        gemm(c, "gemm_agg1", w.pooled, D, nullptr, 0, lw.a1, Me, H, e);
         e = epi(EP_STORE);
         e.bias = lw.ab2; e.out_t = w.mapped; e.ldo = D;
-        gemm(c, "gemm_agg2", w.hid, H, nullptr, 0, lw.a2, Me, D, e);
+        mlp(c, "mlp_agg", w.pooled, D, nullptr, 0, lw.a1, lw.ab1, lw.a2, Me, e, w.hid);
         e = epi(EP_STORE);
         e.out_t = w.Mq; e.ldo = Q;
         gemm(c, "gemm_msgproj", w.mapped, D, nullptr, 0, c.W, Me, Q, e);
@@ -561,16 +624,13 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             check_launch("scatter_perm");
         }
         e = epi(EP_STORE);
-        e.out_f = w.accf; e.out_t = c.bf16 ? w.acct : nullptr; e.ldo = D;
+        e.out_f = (c.bf16 && !o.incoming) ? nullptr : w.accf; e.out_t = c.bf16 ? w.acct : nullptr; e.ldo = D;
         gemm(c, "gemm_msgback", w.accq, Q, nullptr, 0, c.Wt, Ms, D, e);
         if (o.incoming)
             ck(cudaMemcpyAsync(o.incoming + size_t(li) * Ms * D, w.accf, size_t(Ms) * D * 4, cudaMemcpyDeviceToDevice, c.stream), "incoming");
-        e = epi(EP_GELU);
-        e.bias = lw.fb1; e.out_t = w.hid; e.ldo = H;
-        gemm(c, "gemm_fuse1", w.Ztt, D, w.acct, D, lw.f1, Ms, H, e);
         e = epi(EP_RESID);
-        e.bias = lw.fb2; e.z = w.Ztf; e.ldz = D; e.out_f = w.Zf; e.out_t = c.bf16 ? w.Zt : nullptr; e.ldo = D;
-        gemm(c, "gemm_fuse2", w.hid, H, nullptr, 0, lw.f2, Ms, D, e);
+        e.bias = lw.fb2; e.z = w.Ztf; e.zb = (const bf16*)w.Ztt; e.ldz = D; e.out_f = w.Zf; e.out_t = c.bf16 ? w.Zt : nullptr; e.ldo = D;
+        mlp(c, "mlp_fuse", w.Ztt, D, w.acct, D, lw.f1, lw.fb1, lw.f2, Ms, e, w.hid);
     }
     // final logits + site statistics (denoiser.cpp:230-245, refine.cpp:61-78)
     if (c.bf16) {

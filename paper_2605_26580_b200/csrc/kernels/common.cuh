@@ -44,6 +44,8 @@ struct Epi {
     const float* z;      // fp32 [M x ldz]: gate's z, residual's z
     const float* e;      // fp32 [M x ldz]: gate's e
     int ldz;
+    const bf16* zb;      // BF16 mode: bf16 z / e [M x ldz] (fused-MLP final epilogue)
+    const bf16* eb;
     const float* S;      // evidence [bins x L x Q]
     int L, K;
     float beta;

@@ -132,26 +132,39 @@ __device__ __forceinline__ void epi_row32(const Epi& ep, int m, int n0, float* v
     if (ep.kind == EP_GELU) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
-    } else if (ep.kind == EP_GATE) {
-        const float* zr = ep.z + size_t(m) * ep.ldz + n0;
-        const float* er = ep.e + size_t(m) * ep.ldz + n0;
+    } else if (ep.kind == EP_GATE || ep.kind == EP_RESID) {
+        // z / e from the fp32 stream when present, else from the bf16 stream (BF16 mode)
+        float zz[32], ee[32];
+        if (ep.z) {
+            const float* zr = ep.z + size_t(m) * ep.ldz + n0;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-            float4 z4 = *reinterpret_cast<const float4*>(zr + i);
-            float4 e4 = *reinterpret_cast<const float4*>(er + i);
-            float zz[4] = {z4.x, z4.y, z4.z, z4.w}, ee[4] = {e4.x, e4.y, e4.z, e4.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float g = sigmoid_f(v[i + j]);
-                v[i + j] = g * zz[j] + (1.0f - g) * ee[j];
+            for (int i = 0; i < 32; i += 4) {
+                float4 z4 = *reinterpret_cast<const float4*>(zr + i);
+                zz[i] = z4.x; zz[i + 1] = z4.y; zz[i + 2] = z4.z; zz[i + 3] = z4.w;
             }
-        }
-    } else if (ep.kind == EP_RESID) {
-        const float* zr = ep.z + size_t(m) * ep.ldz + n0;
+        } else {
+            const bf16* zr = ep.zb + size_t(m) * ep.ldz + n0;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4) {
-            float4 z4 = *reinterpret_cast<const float4*>(zr + i);
-            v[i] += z4.x; v[i + 1] += z4.y; v[i + 2] += z4.z; v[i + 3] += z4.w;
+            for (int i = 0; i < 32; ++i) zz[i] = __bfloat162float(zr[i]);
+        }
+        if (ep.kind == EP_GATE) {
+            if (ep.e) {
+                const float* er = ep.e + size_t(m) * ep.ldz + n0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) ee[i] = er[i];
+            } else {
+                const bf16* er = ep.eb + size_t(m) * ep.ldz + n0;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) ee[i] = __bfloat162float(er[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                float g = sigmoid_f(v[i]);
+                v[i] = g * zz[i] + (1.0f - g) * ee[i];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] += zz[i];
         }
     } else if (ep.kind == EP_LBAR) {
         const float* s = ep.S + lbar_s_index(ep, m, n0);

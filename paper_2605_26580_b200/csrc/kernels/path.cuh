@@ -22,7 +22,7 @@ __global__ void embed_kernel(const int* __restrict__ X, const float* __restrict_
     int tok = X[m];
     int row = (tok < 0 || tok >= Q) ? Q : tok;
     float v = Etab[size_t(row) * D + t];
-    Zf[i] = v;
+    if (Zf) Zf[i] = v;
     if (Zt) Zt[i] = from_f<T>(v);
 }
 
@@ -151,7 +151,7 @@ __global__ void pool_attn_kernel(const Tin* __restrict__ Nn, const float* __rest
 template <typename T, int V> struct Vec;
 template <> struct Vec<float, 2> { typedef float2 type; };
 template <> struct Vec<float, 4> { typedef float4 type; };
-template <> struct Vec<float, 8> { typedef float4 type; };
+template <> struct Vec<float, 8> { typedef struct { float4 a, b; } type; };
 template <> struct Vec<bf16, 2> { typedef uint32_t type; };
 template <> struct Vec<bf16, 4> { typedef uint2 type; };
 template <> struct Vec<bf16, 8> { typedef uint4 type; };
@@ -202,11 +202,44 @@ __device__ __forceinline__ void store_v(T* p, const float* v) {
 // Extrinsic pooling of one (bin, check, row) group per warp. heads == 0: sum-pool
 // (denoiser.cpp:196-203); heads > 0: pooling attention with scores <u_h, n_i>, where
 // u_h = Wk_h^T q_h (precomputed per layer) equals <q_h, (Wk n_i)_h> of DESIGN.md §2.
+// Lane l owns channels [lV, lV+V) — all inside head l*heads/32 — so a reduce-scatter butterfly
+// (log2(heads) halving exchanges, then a plain xor-reduce) leaves every lane holding exactly its
+// own head's score: 9 shuffles per edge for 8 heads instead of 40. The max / normaliser run over
+// the OTHER edges only, so pooled_i is bitwise independent of edge i (extrinsic).
 constexpr int POOL_DMAX = 8;
-template <typename T, int V>
-__global__ void __launch_bounds__(256)
+template <int NH>
+__device__ __forceinline__ float head_score(float* p, int lane) {
+    // p[NH] per-lane partials; returns the full sum for head (lane * NH / 32)
+    int width = NH;
+    int xo = 16;
+#pragma unroll
+    for (int step = 0; (1 << step) < NH; ++step) {
+        const int half = width / 2;
+        const bool upper = (lane & xo) != 0;
+#pragma unroll
+        for (int j = 0; j < NH / 2; ++j) {
+            if (j >= half) break;
+            const float send = upper ? p[j] : p[j + half];
+            const float keep = upper ? p[j + half] : p[j];
+            p[j] = keep + __shfl_xor_sync(0xffffffffu, send, xo);
+        }
+        width = half;
+        xo >>= 1;
+    }
+    float v = p[0];
+    for (; xo; xo >>= 1) v += __shfl_xor_sync(0xffffffffu, v, xo);
+    return v;
+}
+
+template <typename T, int V, int NH, int DMAX>
+__global__ void __launch_bounds__(256, 2)
 pool_warp_kernel(const T* __restrict__ Nn, const float* __restrict__ U, const int* __restrict__ check_ptr, int P, int E,
-                 int K, int D, int heads, int64_t n_groups, T* __restrict__ pooled) {
+                 int K, int D, int64_t n_groups, T* __restrict__ pooled) {
+    extern __shared__ float u_s[]; // NH x D score vectors
+    if constexpr (NH > 0) {
+        for (int i = threadIdx.x; i < NH * D; i += blockDim.x) u_s[i] = U[i];
+        __syncthreads();
+    }
     const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const int lane = threadIdx.x % 32;
     if (g >= n_groups) return;
@@ -216,58 +249,67 @@ pool_warp_kernel(const T* __restrict__ Nn, const float* __restrict__ U, const in
     const int64_t b = bj / P;
     const int e0 = check_ptr[j], d = check_ptr[j + 1] - e0;
     const int c0 = lane * V;
-    float nv[POOL_DMAX][V];
+    // neighbour rows kept in their storage type (bf16 rows: V/2 registers each)
+    typedef typename Vec<T, V>::type VT;
+    VT raw[DMAX];
 #pragma unroll
-    for (int i = 0; i < POOL_DMAX; ++i)
-        if (i < d) load_v<T, V>(Nn + ((b * E + e0 + i) * K + k) * D + c0, nv[i]);
-    float sc[POOL_DMAX];
-    if (heads) {
-        const int my_head = c0 / (D / heads);
+    for (int i = 0; i < DMAX; ++i)
+        if (i < d) raw[i] = *reinterpret_cast<const VT*>(Nn + ((b * E + e0 + i) * K + k) * D + c0);
+    auto unpack = [&](int i, float* f) { load_v<T, V>(reinterpret_cast<const T*>(&raw[i]), f); };
+    float sc[DMAX];
+    if constexpr (NH > 0) {
+        const float scale = rsqrtf(float(D / NH));
 #pragma unroll
-        for (int i = 0; i < POOL_DMAX; ++i) sc[i] = 0.0f;
-        for (int h = 0; h < heads; ++h) {
-            float u[V];
+        for (int i = 0; i < DMAX; ++i) {
+            if (i >= d) break;
+            float f[V];
+            unpack(i, f);
+            float p[NH];
 #pragma unroll
-            for (int v = 0; v < V; ++v) u[v] = U[size_t(h) * D + c0 + v];
+            for (int h = 0; h < NH; ++h) {
+                const float* uh = u_s + h * D + c0;
+                float a = 0.0f;
 #pragma unroll
-            for (int i = 0; i < POOL_DMAX; ++i) {
-                if (i >= d) break;
-                float p = 0.0f;
-#pragma unroll
-                for (int v = 0; v < V; ++v) p = fmaf(u[v], nv[i][v], p);
-#pragma unroll
-                for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-                if (h == my_head) sc[i] = p * rsqrtf(float(D / heads));
+                for (int v = 0; v < V; ++v) a = fmaf(uh[v], f[v], a);
+                p[h] = a;
             }
+            sc[i] = head_score<NH>(p, lane) * scale;
         }
     }
-#pragma unroll
-    for (int i = 0; i < POOL_DMAX; ++i) {
-        if (i >= d) break;
+#pragma unroll 1
+    for (int i = 0; i < d; ++i) {
         float out[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) out[v] = 0.0f;
-        if (heads) {
+        if constexpr (NH > 0) {
             float mx = -INFINITY, den = 0.0f;
 #pragma unroll
-            for (int i2 = 0; i2 < POOL_DMAX; ++i2)
+            for (int i2 = 0; i2 < DMAX; ++i2)
                 if (i2 < d && i2 != i) mx = fmaxf(mx, sc[i2]);
+            float ex[DMAX];
 #pragma unroll
-            for (int i2 = 0; i2 < POOL_DMAX; ++i2)
-                if (i2 < d && i2 != i) den += expf(sc[i2] - mx);
+            for (int i2 = 0; i2 < DMAX; ++i2) {
+                ex[i2] = (i2 < d && i2 != i) ? __expf(sc[i2] - mx) : 0.0f;
+                den += ex[i2];
+            }
+            const float fct = float(d - 1) / den;
 #pragma unroll
-            for (int i2 = 0; i2 < POOL_DMAX; ++i2) {
+            for (int i2 = 0; i2 < DMAX; ++i2) {
                 if (i2 >= d || i2 == i) continue;
-                const float w = float(d - 1) * expf(sc[i2] - mx) / den;
+                const float w = ex[i2] * fct;
+                float f[V];
+                unpack(i2, f);
 #pragma unroll
-                for (int v = 0; v < V; ++v) out[v] = fmaf(w, nv[i2][v], out[v]);
+                for (int v = 0; v < V; ++v) out[v] = fmaf(w, f[v], out[v]);
             }
         } else {
 #pragma unroll
-            for (int i2 = 0; i2 < POOL_DMAX; ++i2) {
+            for (int i2 = 0; i2 < DMAX; ++i2) {
                 if (i2 >= d || i2 == i) continue;
+                float f[V];
+                unpack(i2, f);
 #pragma unroll
-                for (int v = 0; v < V; ++v) out[v] += nv[i2][v];
+                for (int v = 0; v < V; ++v) out[v] += f[v];
             }
         }
         store_v<T, V>(pooled + ((b * E + e0 + i) * K + k) * D + c0, out);
