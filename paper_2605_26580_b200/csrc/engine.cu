@@ -378,7 +378,7 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
     const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;
     const CUtensorMap& w1 = map_for(c, W1, H, Kin, Kin, tc::MLP_HC);
-    const CUtensorMap& w2 = map_for(c, W2, D, H, H, D);
+    const CUtensorMap& w2 = map_for(c, W2, D, H, H, D > 128 ? 128 : D);
     tc::MlpArgs a;
     a.M = int(M);
     a.K0 = A1 ? K0 : Kin;

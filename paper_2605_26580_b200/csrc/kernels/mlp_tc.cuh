@@ -36,20 +36,23 @@ __device__ __forceinline__ float gelu_fast(float x) {
 }
 
 constexpr int MLP_HC = 128;
-constexpr int MLP_THREADS = 192;
+constexpr int MLP_THREADS = 320; // producer, MMA, 8 epilogue warps (two per TMEM lane quarter)
+constexpr int MLP_EPI = 256;
 constexpr int SMEM_LIMIT = 232448; // 227 KB opt-in per block
 
 template <int KIN, int D>
 struct MlpLayout {
     static constexpr int KB1 = KIN / 64;                     // k-blocks of the first MMA
     static constexpr int KB2 = MLP_HC / 64;                  // k-blocks of the second MMA
+    static constexpr int NB2 = D > 128 ? D / 128 : 1;        // N halves of the second MMA (N <= 128 each)
+    static constexpr int N2 = D > 128 ? 128 : D;
     static constexpr int X_BYTES = KB1 * 128 * 64 * 2;       // resident row tile
     static constexpr int H_BYTES = KB2 * 128 * 64 * 2;       // one hidden chunk (32 KB)
-    static constexpr int SLOT = (D * 64 * 2 > MLP_HC * 64 * 2) ? D * 64 * 2 : MLP_HC * 64 * 2;
+    static constexpr int SLOT = 16384;                       // ring slot: one 128x64 bf16 k-block
     static constexpr int FIXED = 1024 + 512;                 // alignment slack + barriers
-    static constexpr int NHB = (X_BYTES + 2 * H_BYTES + 2 * SLOT + FIXED <= SMEM_LIMIT) ? 2 : 1;
+    static constexpr int NHB = (X_BYTES + 2 * H_BYTES + 4 * SLOT + FIXED <= SMEM_LIMIT) ? 2 : 1;
     static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - X_BYTES - NHB * H_BYTES) / SLOT;
-    static constexpr int NS = NS_RAW > 8 ? 8 : NS_RAW;
+    static constexpr int NS = NS_RAW > 12 ? 12 : NS_RAW;
     static constexpr int H_OFF = X_BYTES;
     static constexpr int R_OFF = H_OFF + NHB * H_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
@@ -95,10 +98,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
         mbar_init(x_full, 1);
         mbar_init(x_empty, 1);
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&a1_full[b], 1); mbar_init(&a1_empty[b], 128); }
-        for (int b = 0; b < NHB; ++b) { mbar_init(&h_full[b], 128); mbar_init(&h_empty[b], 1); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&a1_full[b], 1); mbar_init(&a1_empty[b], MLP_EPI); }
+        for (int b = 0; b < NHB; ++b) { mbar_init(&h_full[b], MLP_EPI); mbar_init(&h_empty[b], 1); }
         mbar_init(a2_full, 1);
-        mbar_init(a2_empty, 128);
+        mbar_init(a2_empty, MLP_EPI);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW1)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW2)) : "memory");
@@ -126,7 +129,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                 for (int kb = 0; kb < KB1; ++kb) load_w(&tmW1, kb * 64, c * MLP_HC, MLP_HC * 64 * 2);
             };
             auto load_w2 = [&](int c) {
-                for (int kb = 0; kb < KB2; ++kb) load_w(&tmW2, c * MLP_HC + kb * 64, 0, D * 64 * 2);
+                for (int kb = 0; kb < KB2; ++kb)
+                    for (int nh = 0; nh < Lay::NB2; ++nh) load_w(&tmW2, c * MLP_HC + kb * 64, nh * 128, Lay::N2 * 64 * 2);
             };
             for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x) {
                 mbar_wait(x_empty, xph ^ 1);
@@ -147,7 +151,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t id1 = idesc_bf16(128, MLP_HC);
-            constexpr uint32_t id2 = idesc_bf16(128, D);
+            constexpr uint32_t id2 = idesc_bf16(128, Lay::N2);
             int slot = 0;
             uint32_t rph = 0, xph = 0, a2ph = 0;
             uint32_t a1ph[2] = {0, 0}, hph[NHB];
@@ -190,14 +194,17 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                         fence_after();
                     }
                     for (int kb = 0; kb < KB2; ++kb) {
-                        mbar_wait(&r_full[slot], rph);
-                        fence_after();
                         const uint64_t da = sw128_desc(hs + hb * Lay::H_BYTES + kb * 16384);
-                        const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
+                        for (int nh = 0; nh < Lay::NB2; ++nh) {
+                            mbar_wait(&r_full[slot], rph);
+                            fence_after();
+                            const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) mma_bf16(tmem, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
-                        mma_commit(&r_empty[slot]);
-                        if (++slot == NS) { slot = 0; rph ^= 1; }
+                            for (int kk = 0; kk < 4; ++kk)
+                                mma_bf16(tmem + nh * 128, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
+                            mma_commit(&r_empty[slot]);
+                            if (++slot == NS) { slot = 0; rph ^= 1; }
+                        }
                     }
                     mma_commit(&h_empty[hb]);
                 }
@@ -205,7 +212,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
             }
         }
     } else {
+        // 8 epilogue warps: warp w touches TMEM lane quarter (w % 4); the two warps of a quarter
+        // split every chunk's columns in halves, so each SM sub-partition runs two epilogue warps.
         const int quarter = warp % 4;
+        const int half = (warp - 2) / 4;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         uint32_t e1ph[2] = {0, 0}, ehph[NHB], e2ph = 0;
@@ -214,32 +224,33 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
         for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x) {
             for (int c = 0; c < NC; ++c) {
                 const int b = c & 1, hb = c % NHB;
+                const float* b1 = args.b1 + c * MLP_HC + half * 64;
+                float4 bias4[16]; // this warp's 64 bias values, fetched before any wait
+#pragma unroll
+                for (int q = 0; q < 16; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + q);
                 mbar_wait(&a1_full[b], e1ph[b]);
                 e1ph[b] ^= 1;
                 mbar_wait(&h_empty[hb], ehph[hb] ^ 1);
                 ehph[hb] ^= 1;
                 fence_after();
-                uint8_t* hrow = hs + hb * Lay::H_BYTES + row * 128;
-                const float* b1 = args.b1 + c * MLP_HC;
-#pragma unroll 1
-                for (int j0 = 0; j0 < MLP_HC; j0 += 32) {
+                uint8_t* hrow = hs + hb * Lay::H_BYTES + half * 16384 + row * 128; // k-block = half
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
                     float v[32];
-                    tmem_ld32(tmem + lane_off + 256 + b * MLP_HC + j0, v);
+                    tmem_ld32(tmem + lane_off + 256 + b * MLP_HC + half * 64 + g * 32, v);
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {
-                        const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + j0 + i));
+                        const float4 bb = bias4[g * 8 + i / 4];
                         __nv_bfloat162 p0 = __floats2bfloat162_rn(gelu_fast(v[i] + bb.x), gelu_fast(v[i + 1] + bb.y));
                         __nv_bfloat162 p1 = __floats2bfloat162_rn(gelu_fast(v[i + 2] + bb.z), gelu_fast(v[i + 3] + bb.w));
                         pk[i / 2] = *reinterpret_cast<uint32_t*>(&p0);
                         pk[i / 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
                     }
-                    const int kb = j0 / 64;
-                    uint8_t* blk = hrow + kb * 16384;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const int chunk = ((j0 % 64) / 8 + q) ^ (row & 7);
-                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(blk + chunk * 16)),
+                        const int chunk = (g * 4 + q) ^ (row & 7);
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(hrow + chunk * 16)),
                                      "r"(pk[4 * q]), "r"(pk[4 * q + 1]), "r"(pk[4 * q + 2]), "r"(pk[4 * q + 3])
                                      : "memory");
                     }
@@ -249,52 +260,65 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&h_full[hb]);
             }
-            mbar_wait(a2_full, e2ph);
-            e2ph ^= 1;
-            fence_after();
             // Final epilogue, transposed through the (now idle) hidden buffer so that global
             // traffic is lane-contiguous: 64-column fp32 slabs, row-per-thread in (from TMEM),
             // row-per-warp out (z / e reads and the output writes coalesce).
             float* slab = reinterpret_cast<float*>(hs);
             const int m0 = tile * 128;
+            const int wq = warp - 2; // rows [16 wq, 16 wq + 16) of every slab
+            mbar_wait(a2_full, e2ph);
+            e2ph ^= 1;
+            fence_after();
 #pragma unroll 1
             for (int n0 = 0; n0 < D; n0 += 64) {
-                float v[32];
+                uint32_t zr[16], er[16];
+                if (ep.kind == EP_GATE || ep.kind == EP_RESID) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    tmem_ld32(tmem + lane_off + n0 + h * 32, v);
-                    if (h == 1 && n0 + 64 >= D) {
+                    for (int rr = 0; rr < 16; ++rr) {
+                        const int m = m0 + wq * 16 + rr;
+                        const size_t off = size_t(m < ep.M ? m : 0) * ep.ldz + n0 + 2 * lane;
+                        zr[rr] = __ldg(reinterpret_cast<const unsigned int*>(ep.zb + off));
+                        er[rr] = ep.kind == EP_GATE ? __ldg(reinterpret_cast<const unsigned int*>(ep.eb + off)) : 0u;
+                    }
+                }
+                float4 bias4[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    bias4[q] = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + half * 32) + q)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                {
+                    float v[32];
+                    tmem_ld32(tmem + lane_off + n0 + half * 32, v);
+                    if (n0 + 64 >= D) {
                         fence_before();
                         mbar_arrive(a2_empty); // accumulator drained: next tile's MMA2 may start
                     }
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {
-                        const int c = (h * 32 + i) / 4; // 16-byte chunk 0..15 of the 256-byte row
-                        float4 bb = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + h * 32 + i))
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const int cidx = (half * 32 + i) / 4; // 16-byte chunk 0..15 of the 256-byte row
+                        const float4 bb = bias4[i / 4];
                         float4 q = make_float4(v[i] + bb.x, v[i + 1] + bb.y, v[i + 2] + bb.z, v[i + 3] + bb.w);
-                        *reinterpret_cast<float4*>(slab + row * 64 + ((c ^ (row & 15)) * 4)) = q;
+                        *reinterpret_cast<float4*>(slab + row * 64 + ((cidx ^ (row & 15)) * 4)) = q;
                     }
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                const int wq = warp - 2; // epilogue warp 0..3 -> rows [32 wq, 32 wq + 32)
-#pragma unroll 4
-                for (int rr = 0; rr < 32; ++rr) {
-                    const int r = wq * 32 + rr;
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+                for (int rr = 0; rr < 16; ++rr) {
+                    const int r = wq * 16 + rr;
                     const int m = m0 + r;
                     if (m >= ep.M) break;
-                    const int c = lane / 2;
-                    const float2 a = *reinterpret_cast<const float2*>(slab + r * 64 + ((c ^ (r & 15)) * 4) + (lane & 1) * 2);
+                    const int cidx = lane / 2;
+                    const float2 a = *reinterpret_cast<const float2*>(slab + r * 64 + ((cidx ^ (r & 15)) * 4) + (lane & 1) * 2);
                     const int n = n0 + 2 * lane;
                     float o0 = a.x, o1 = a.y;
                     if (ep.kind == EP_GATE) {
-                        const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(ep.zb + size_t(m) * ep.ldz + n));
-                        const float2 e = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(ep.eb + size_t(m) * ep.ldz + n));
+                        const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zr[rr]));
+                        const float2 e = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&er[rr]));
                         const float g0 = sigmoid_f(o0), g1 = sigmoid_f(o1);
                         o0 = g0 * z.x + (1.0f - g0) * e.x;
                         o1 = g1 * z.y + (1.0f - g1) * e.y;
                     } else if (ep.kind == EP_RESID) {
-                        const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(ep.zb + size_t(m) * ep.ldz + n));
+                        const float2 z = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zr[rr]));
                         o0 += z.x;
                         o1 += z.y;
                     }
@@ -303,7 +327,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                         *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<bf16*>(ep.out_t) + size_t(m) * ep.ldo + n) =
                             __floats2bfloat162_rn(o0, o1);
                 }
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, 256;" ::: "memory");
             }
         }
     }
