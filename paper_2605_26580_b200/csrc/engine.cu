@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -27,6 +29,7 @@
 #include "kernels/gemm_simt.cuh"
 #include "kernels/gemm_tc.cuh"
 #include "kernels/mlp_tc.cuh"
+#include "kernels/mlp_tc2.cuh"
 #include "kernels/path.cuh"
 
 namespace cider {
@@ -85,6 +88,20 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int cols, int ld, int box_ro
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+// W1 of the 2-SM MLP as {64 cols, rows, k-blocks}: one box = box_rows rows x 2 k-blocks (16 KB)
+CUtensorMap make_map_w1_3d(const void* ptr, int64_t rows, int cols, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {64, cuuint64_t(rows), cuuint64_t(cols / 64)};
+    cuuint64_t strides[2] = {cuuint64_t(cols) * 2, 128};
+    cuuint32_t box[3] = {64, cuuint32_t(box_rows), 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (3d) failed (" + std::to_string(int(r)) + ")");
     return m;
 }
 
@@ -341,6 +358,8 @@ Epi epi(int kind) {
     return e;
 }
 
+void* wsbuf(cider_ctx& c, const char* name, size_t bytes);
+
 // ---- fused two-layer maps (BF16 mode) -----------------------------------------------------------
 template <int KIN, int D>
 void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
@@ -354,6 +373,20 @@ void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, cons
     }
     const int grid = std::min(a.tiles, c.sm_count);
     tc::mlp_tc_kernel<KIN, D><<<grid, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
+}
+
+template <int KIN, int D>
+void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
+                 const CUtensorMap& w2, const tc::MlpArgs& a) {
+    using Lay = tc::Mlp2Layout<KIN, D>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+           "smem attr");
+        attr_set = true;
+    }
+    const int pairs = std::min(a.tiles, c.sm_count / 2);
+    tc::mlp_tc2_kernel<KIN, D><<<2 * pairs, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
 }
 
 bool mlp_fusable(const cider_ctx& c, int Kin) {
@@ -374,22 +407,55 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     }
     ep.M = int(M);
     ep.N = D;
+    static const bool one_sm = std::getenv("CIDER_MLP_1SM") != nullptr;
+    const bool pair = !one_sm && Kin % 128 == 0 && (D == 128 || D == 256);
     Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
     const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;
-    const CUtensorMap& w1 = map_for(c, W1, H, Kin, Kin, tc::MLP_HC);
-    const CUtensorMap& w2 = map_for(c, W2, D, H, H, D > 128 ? 128 : D);
+    CUtensorMap w1_3d;
+    if (pair) w1_3d = make_map_w1_3d(W1, H, Kin, tc::MLP_HC / 2);
+    const CUtensorMap& w1 = pair ? w1_3d : map_for(c, W1, H, Kin, Kin, tc::MLP_HC);
+    const CUtensorMap& w2 = map_for(c, W2, D, H, H, pair ? D / 2 : (D > 128 ? 128 : D));
     tc::MlpArgs a;
     a.M = int(M);
     a.K0 = A1 ? K0 : Kin;
     a.H = H;
-    a.tiles = int((M + 127) / 128);
+    a.tiles = int((M + (pair ? 255 : 127)) / (pair ? 256 : 128));
     a.b1 = b1;
     a.ep = ep;
-    if (D == 256) { if (Kin == 512) launch_mlp<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp<256, 256>(c, x0, x1, w1, w2, a); }
+    a.trace = nullptr;
+    static const int dbg = std::getenv("CIDER_MLP_DBG") ? std::atoi(std::getenv("CIDER_MLP_DBG")) : 0;
+    a.dbg = dbg;
+    static const bool trace_on = std::getenv("CIDER_TRACE_MLP") != nullptr;
+    long long* tbuf = nullptr;
+    if (trace_on) {
+        tbuf = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
+        cudaMemsetAsync(tbuf, 0, 8 * 1024, c.stream);
+        a.trace = tbuf;
+    }
+    if (pair) {
+        if (D == 256) { if (Kin == 512) launch_mlp2<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp2<256, 256>(c, x0, x1, w1, w2, a); }
+        else { if (Kin == 256) launch_mlp2<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp2<128, 128>(c, x0, x1, w1, w2, a); }
+    } else if (D == 256) { if (Kin == 512) launch_mlp<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp<256, 256>(c, x0, x1, w1, w2, a); }
     else if (D == 128) { if (Kin == 256) launch_mlp<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp<128, 128>(c, x0, x1, w1, w2, a); }
     else { if (Kin == 128) launch_mlp<128, 64>(c, x0, x1, w1, w2, a); else launch_mlp<64, 64>(c, x0, x1, w1, w2, a); }
     check_launch(tag);
+    if (tbuf) {
+        long long h[1024];
+        cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, c.stream);
+        cudaStreamSynchronize(c.stream);
+        const long long t0 = h[2];
+        std::fprintf(stderr, "[mlp trace %s M=%lld pair=%d] chunk: mma_wait_h  mma_got_h  mma_issued | epi_wait_a1  epi_got_a1  epi_done\n", tag, (long long)M, int(pair));
+        for (int ch = 0; ch < H / tc::MLP_HC; ++ch)
+            std::fprintf(stderr, "  %2d: %8lld %8lld %8lld | %8lld %8lld %8lld\n", ch, h[ch * 8] - t0, h[ch * 8 + 1] - t0, h[ch * 8 + 5] - t0,
+                         h[ch * 8 + 2] - t0, h[ch * 8 + 3] - t0, h[ch * 8 + 4] - t0);
+        std::fprintf(stderr, "  slot n: prod_wait_empty prod_tma_issued | mma_wait_full mma_got_full mma_issued | tma_latency(got-issued)\n");
+        for (int n = 0; n < 40; ++n)
+            if (h[512 + n * 4 + 1])
+                std::fprintf(stderr, "   %2d: %8lld %8lld | %8lld %8lld %8lld | %6lld\n", n, h[512 + n * 4] - t0, h[512 + n * 4 + 3] - t0,
+                             h[768 + n * 4] - t0, h[768 + n * 4 + 1] - t0, h[768 + n * 4 + 2] - t0,
+                             h[768 + n * 4 + 1] - h[512 + n * 4 + 3]);
+    }
 }
 
 // ---- workspace ------------------------------------------------------------------------------

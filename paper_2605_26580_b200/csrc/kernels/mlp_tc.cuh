@@ -64,6 +64,8 @@ struct MlpLayout {
 struct MlpArgs {
     int M, K0, H, tiles;
     const float* b1;
+    long long* trace; // debug (CIDER_TRACE_MLP): per-chunk clock64 stamps of CTA 0, else null
+    int dbg;          // debug ablations (CIDER_MLP_DBG): 1 = skip GELU work, 2 = skip final epilogue
     Epi ep; // final epilogue (bias = b2)
 };
 
@@ -185,9 +187,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                         if (c + 1 == NC - 1) mma_commit(x_empty); // row tile no longer read
                     }
                     const int hb = c % NHB;
+                    if (args.trace && blockIdx.x == 0 && tile == 0) args.trace[c * 8 + 0] = clock64();
                     mbar_wait(&h_full[hb], hph[hb]);
                     hph[hb] ^= 1;
                     fence_after();
+                    if (args.trace && blockIdx.x == 0 && tile == 0) args.trace[c * 8 + 1] = clock64();
                     if (c == 0) {
                         mbar_wait(a2_empty, a2ph ^ 1);
                         a2ph ^= 1;
@@ -228,8 +232,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                 float4 bias4[16]; // this warp's 64 bias values, fetched before any wait
 #pragma unroll
                 for (int q = 0; q < 16; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + q);
+                const bool tr = args.trace && blockIdx.x == 0 && tile == 0 && warp == 2 && lane == 0;
+                if (tr) args.trace[c * 8 + 2] = clock64();
                 mbar_wait(&a1_full[b], e1ph[b]);
                 e1ph[b] ^= 1;
+                if (tr) args.trace[c * 8 + 3] = clock64();
                 mbar_wait(&h_empty[hb], ehph[hb] ^ 1);
                 ehph[hb] ^= 1;
                 fence_after();
@@ -259,6 +266,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
                 mbar_arrive(&a1_empty[b]);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&h_full[hb]);
+                if (tr) args.trace[c * 8 + 4] = clock64();
             }
             // Final epilogue, transposed through the (now idle) hidden buffer so that global
             // traffic is lane-contiguous: 64-column fp32 slabs, row-per-thread in (from TMEM),
