@@ -408,7 +408,9 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     ep.M = int(M);
     ep.N = D;
     static const bool one_sm = std::getenv("CIDER_MLP_1SM") != nullptr;
-    const bool pair = !one_sm && Kin % 128 == 0 && (D == 128 || D == 256);
+    // 2-SM kernel for the plain-epilogue map (check aggregator); the gate / fusion maps keep the
+    // 1-SM kernel, whose SMEM-staged final epilogue reads the residual operands coalesced.
+    const bool pair = !one_sm && ep.kind == EP_STORE && Kin % 128 == 0 && (D == 128 || D == 256);
     Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
     const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;
