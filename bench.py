@@ -244,7 +244,7 @@ def main():
     s_bytes, g_bytes = B * L * Q * 4, B * K * L * 4
     hostS, devS, devG, truths = [], [], [], []
     for i in range(n_batch):
-        first = (i * world + rank) * B
+        first, _ = P.shard(0, B, rank, world, step=i)
         hp = C.c_void_p()
         P._check(lib.cider_host_alloc(s_bytes, C.byref(hp)))
         arr = np.ctypeslib.as_array((C.c_float * (B * L * Q)).from_address(hp.value)).reshape(B, L, Q)
@@ -377,7 +377,8 @@ def main():
                        "bins_per_gpu_per_step": B, "global_batch": B * world,
                        "parallelism": f"bin-sharded x{world} (no per-step collective)",
                        "l2": "inputs+working set per step >> 126 MB L2 (no flush needed)",
-                       "forwards_per_bin": P.forward_count(cfg), "gflop_per_bin": round(fpb / 1e9, 2)},
+                       "forwards_per_bin": P.forward_count(cfg), "gflop_per_bin": round(fpb / 1e9, 2),
+                       "survey_gflop_per_bin": round(P.survey_flops_per_bin(cfg) / 1e9, 2)},
             "e2e": {"value": round(e2e, 2), "unit": "bins/s", "h2d_bytes_per_step": s_bytes * world,
                     "d2h_bytes_per_step": g_bytes * world, "steps": e2e_steps},
             "gpu_launches": int(launches),

@@ -1,0 +1,186 @@
+// cider_ura.hpp — header-only C++ adapter: the B200 engine behind the reference's own decoder
+// types (/root/reference/proj/include/ura). Include it from code that already builds against the
+// reference (it needs ura/*.hpp) and link libcider.so. Nothing here does arithmetic: every call
+// goes through the C ABI of cider.h.
+//
+//   cider::GpuStructuredDenoiser : ura::Denoiser          (denoiser.hpp:109-130)
+//       drop-in for ura::StructuredDenoiser inside the reference's run_refinement /
+//       run_with_remasking / remask_pass (refine.cpp:134-292) — one forward per call.
+//   cider::GpuRefiner::run_refinement / run_with_remasking (refine.hpp:60-62, 104-107)
+//       the whole T-step loop on the device, batched over bins.
+//   cider::make_bin_decoder -> ura::BinDecoder            (protocol.hpp:32-40)
+//       for run_protocol_frame (protocol.cpp:73).
+//
+// Errors: status 3 -> std::domain_error, 4 -> std::runtime_error, with the library's message
+// (which keeps the reference's prefixes, e.g. "embed_grid: token out of range").
+#pragma once
+
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cider.h"
+#include "ura/denoiser.hpp"
+#include "ura/protocol.hpp"
+#include "ura/refine.hpp"
+
+namespace cider {
+
+inline void check(int rc) {
+    if (rc == CIDER_OK) return;
+    const std::string msg = cider_last_error();
+    if (rc == CIDER_EINVAL) throw std::domain_error(msg);
+    throw std::runtime_error(msg);
+}
+
+// ura::DenoiserParams (ref-exact: 1 block, hidden = D, sum-pool Psi) -> cider.h flat weights.
+inline std::vector<float> flatten(const ura::DenoiserParams& p) {
+    std::vector<float> w;
+    auto put = [&](const std::vector<double>& v) {
+        for (double x : v) w.push_back(float(x));
+    };
+    put(p.embed);
+    put(p.out_proj);
+    put(p.sym_embed);
+    for (const ura::TwoLayerMap* t : {&p.gate_a, &p.check_agg, &p.fuse_b}) {
+        if (t->hidden != p.gate_a.hidden) throw std::domain_error("cider: maps must share one hidden width");
+        put(t->w1);
+        put(t->b1);
+        put(t->w2);
+        put(t->b2);
+    }
+    return w;
+}
+
+inline std::vector<int32_t> edges_of(const ura::ParityCheckMatrix& h) {
+    std::vector<int32_t> e;
+    for (const ura::ParityEdge& x : h.entries()) e.insert(e.end(), {x.check, x.slot, x.coeff});
+    return e;
+}
+
+// Owns one device context (weights + Tanner tables resident on one B200).
+class Context {
+public:
+    Context(const ura::GfContext& gf, const ura::DenoiserParams& p, const ura::ParityCheckMatrix& h, int device = 0,
+            int precision = CIDER_FP32)
+        : checks_(h.checks()), slots_(h.slots()), q_(p.q), dim_(p.dim) {
+        cider_model_desc md{};
+        md.m = gf.m();
+        md.prim_poly = gf.prim_poly();
+        md.dim = p.dim;
+        md.hidden = p.gate_a.hidden;
+        md.layers = 1;
+        md.heads = 0;
+        md.tau_demix = p.tau_demix;
+        md.evidence_scale = p.evidence_scale;
+        md.precision = precision;
+        const auto w = flatten(p);
+        edges_ = edges_of(h);
+        cider_code_desc cd{h.checks(), h.slots(), int(edges_.size() / 3), edges_.data()};
+        cider_ctx* c = nullptr;
+        check(cider_create(&md, w.data(), &cd, device, &c));
+        ctx_.reset(c);
+    }
+    cider_ctx* get() const { return ctx_.get(); }
+    int q() const { return q_; }
+    int slots() const { return slots_; }
+    // the context is built for one parity-check matrix; calls must pass the same one
+    void require_same(const ura::ParityCheckMatrix& h) const {
+        if (h.checks() != checks_ || h.slots() != slots_ || edges_of(h) != edges_)
+            throw std::domain_error("cider: parity-check matrix differs from the one the context was built with");
+    }
+
+private:
+    struct Del {
+        void operator()(cider_ctx* c) const { cider_destroy(c); }
+    };
+    std::unique_ptr<cider_ctx, Del> ctx_;
+    int checks_, slots_, q_, dim_;
+    std::vector<int32_t> edges_;
+};
+
+// Per-step drop-in for ura::StructuredDenoiser (denoiser.cpp:253-259). Thread-safe like the
+// reference's const logits(): the context serialises calls internally.
+class GpuStructuredDenoiser : public ura::Denoiser {
+public:
+    explicit GpuStructuredDenoiser(std::shared_ptr<Context> ctx) : ctx_(std::move(ctx)) {}
+    ura::LogitGrid logits(const ura::MaskedGrid& x, const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
+                          double /*mask_ratio: time-homogeneous*/) const override {
+        ctx_->require_same(h);
+        if (s.slots != ctx_->slots() || s.q != ctx_->q() || x.cols != ctx_->slots())
+            throw std::domain_error("module_b: slot count mismatch");
+        std::vector<int32_t> X(x.v.begin(), x.v.end());
+        std::vector<float> S(s.v.begin(), s.v.end());
+        std::vector<float> lg(size_t(x.rows) * x.cols * s.q);
+        check(cider_denoise(ctx_->get(), 1, x.rows, X.data(), S.data(), lg.data(), nullptr));
+        ura::LogitGrid out(x.rows, x.cols, s.q);
+        for (size_t i = 0; i < lg.size(); ++i) out.v[i] = lg[i];
+        return out;
+    }
+
+private:
+    std::shared_ptr<Context> ctx_;
+};
+
+// Whole-pass drop-in (the device runs the T-step loop, reveal, gamma=0 pass and remasking).
+class GpuRefiner {
+public:
+    explicit GpuRefiner(std::shared_ptr<Context> ctx) : ctx_(std::move(ctx)) {}
+
+    // = ura::run_refinement(den, s, h, sched, k, l) for one bin
+    ura::SymbolGrid run_refinement(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
+                                   const ura::RevealSchedule& sched, int k) const {
+        return run(s, h, sched, nullptr, k);
+    }
+    // = ura::run_with_remasking(den, MaxProbScorer, s, h, sched, remask, k, l)
+    ura::SymbolGrid run_with_remasking(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
+                                       const ura::RevealSchedule& sched, const ura::RemaskConfig& remask, int k) const {
+        cider_remask rm{};
+        rm.mode = remask.thresholds.empty() ? CIDER_REMASK_NONE : CIDER_REMASK_THRESHOLD;
+        if (remask.thresholds.size() > CIDER_MAX_THRESHOLDS) throw std::domain_error("remask: too many thresholds");
+        rm.n_thresholds = int(remask.thresholds.size());
+        for (size_t i = 0; i < remask.thresholds.size(); ++i) rm.thresholds[i] = remask.thresholds[i];
+        return run(s, h, sched, &rm, k);
+    }
+    // batched: B evidence matrices -> B grids in one device call
+    std::vector<ura::SymbolGrid> run_batch(const std::vector<const ura::EvidenceMatrix*>& ss, const ura::ParityCheckMatrix& h,
+                                           const ura::RevealSchedule& sched, const cider_remask* rm, int k) const {
+        ctx_->require_same(h);
+        const int B = int(ss.size()), L = ctx_->slots(), Q = ctx_->q();
+        std::vector<float> S(size_t(B) * L * Q);
+        for (int b = 0; b < B; ++b)
+            for (size_t i = 0; i < size_t(L) * Q; ++i) S[size_t(b) * L * Q + i] = float(ss[b]->v[i]);
+        std::vector<int32_t> g(size_t(B) * k * L);
+        cider_schedule sc{sched.steps, sched.tau_max, sched.tau_min, sched.first_reveal ? 1 : 0};
+        check(cider_refine(ctx_->get(), B, k, S.data(), &sc, rm, g.data(), nullptr, nullptr));
+        std::vector<ura::SymbolGrid> out(B, ura::SymbolGrid(k, L));
+        for (int b = 0; b < B; ++b) std::copy(g.begin() + size_t(b) * k * L, g.begin() + size_t(b + 1) * k * L, out[b].v.begin());
+        return out;
+    }
+
+private:
+    ura::SymbolGrid run(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h, const ura::RevealSchedule& sched,
+                        const cider_remask* rm, int k) const {
+        return run_batch({&s}, h, sched, rm, k)[0];
+    }
+    std::shared_ptr<Context> ctx_;
+};
+
+// ura::BinDecoder (protocol.hpp:40) for run_protocol_frame (protocol.cpp:73); bins of load K
+// with the default per-load schedule (refine.cpp:28-46) unless `sched_override.steps > 0`.
+inline ura::BinDecoder make_bin_decoder(std::shared_ptr<Context> ctx, ura::RevealSchedule sched_override = {0, 1.0, 1.0, true},
+                                        bool per_load_remask = true) {
+    auto refiner = std::make_shared<GpuRefiner>(ctx);
+    return [refiner, sched_override, per_load_remask](const ura::BinTask& t) {
+        ura::RevealSchedule sched = sched_override;
+        if (sched.steps <= 0) sched.steps = ura::default_steps_for_load(t.load);
+        ura::RemaskConfig rm;
+        if (per_load_remask) rm.thresholds = ura::default_remask_thresholds(t.load);
+        return refiner->run_with_remasking(t.evidence, t.h, sched, rm, t.load);
+    };
+}
+
+} // namespace cider

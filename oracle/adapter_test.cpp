@@ -1,0 +1,93 @@
+// adapter_test.cpp — TEST PROGRAM: the reference's own engine driving the B200 denoiser.
+//
+// Built by oracle/Makefile (only where /root/reference exists) against the reference objects in
+// oracle/_ref/obj and libcider.so; the binary travels to the GPU box in oracle/_ref/ and is run by
+// tests/test_gpu.py::test_reference_engine_with_gpu_denoiser. It checks the drop-in boundary:
+//   (1) ura::run_refinement + ura::StructuredDenoiser        (the reference, CPU, fp64)
+//   (2) ura::run_refinement + cider::GpuStructuredDenoiser   (reference loop, B200 forward)
+//   (3) cider::GpuRefiner::run_refinement                    (whole loop on the B200)
+//   (4) ura::run_with_remasking vs GpuRefiner::run_with_remasking, and a BinDecoder call
+// on fp32-rounded parameters and evidence (FP32 mode), and requires identical grids.
+// Exit code = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "cider_ura.hpp"
+#include "ura/ldpc.hpp"
+#include "ura/seeding.hpp"
+
+static void round_f32(std::vector<double>& v) {
+    for (double& x : v) x = double(float(x));
+}
+
+int main() {
+    int fails = 0;
+    try {
+        auto gf = ura::GfContext::with_default_poly(6);
+        auto rng = ura::make_rng(ura::derive_seed(0, 1));
+        auto h = ura::build_random_ldpc(gf, 16, 8, 3, rng);
+        auto p = ura::DenoiserParams::random_init(64, 32, 1);
+        for (auto* v : {&p.embed, &p.out_proj, &p.sym_embed}) round_f32(*v);
+        for (auto* t : {&p.gate_a, &p.check_agg, &p.fuse_b}) {
+            round_f32(t->w1);
+            round_f32(t->b1);
+            round_f32(t->w2);
+            round_f32(t->b2);
+        }
+        auto ctx = std::make_shared<cider::Context>(gf, p, h, 0, CIDER_FP32);
+        ura::StructuredDenoiser cpu(gf, p);
+        cider::GpuStructuredDenoiser gpu(ctx);
+        cider::GpuRefiner refiner(ctx);
+        ura::RevealSchedule sched;
+        sched.steps = 5;
+        int identical = 0, identical_loop = 0, identical_rm = 0;
+        const int bins = 6;
+        for (int b = 0; b < bins; ++b) {
+            ura::EvidenceMatrix s(16, 64);
+            auto er = ura::make_rng(ura::derive_seed(7, b));
+            std::uniform_real_distribution<double> u(-8.0, 0.0);
+            for (double& x : s.v) x = double(float(u(er)));
+            const int k = 3;
+            auto a = ura::run_refinement(cpu, s, h, sched, k, 16);
+            auto g = ura::run_refinement(gpu, s, h, sched, k, 16);
+            auto d = refiner.run_refinement(s, h, sched, k);
+            identical += (a == g);
+            identical_loop += (a == d);
+            ura::RemaskConfig rm{{0.9, 0.5}};
+            ura::MaxProbScorer scorer;
+            auto ar = ura::run_with_remasking(cpu, scorer, s, h, sched, rm, k, 16);
+            auto dr = refiner.run_with_remasking(s, h, sched, rm, k);
+            identical_rm += (ar == dr);
+        }
+        std::printf("reference loop + GPU denoiser: %d/%d identical grids\n", identical, bins);
+        std::printf("GPU loop vs reference:         %d/%d identical grids\n", identical_loop, bins);
+        std::printf("GPU remasking vs reference:    %d/%d identical grids\n", identical_rm, bins);
+        fails += identical != bins;
+        fails += identical_loop != bins;
+        fails += identical_rm != bins;
+        // BinDecoder plug-in (protocol.hpp:40)
+        auto dec = cider::make_bin_decoder(ctx, sched, false);
+        ura::EvidenceMatrix s(16, 64, -1.0);
+        ura::SymbolGrid truth(2, 16);
+        ura::BinTask task{gf, h, s, truth, 2};
+        auto out = dec(task);
+        const bool shape_ok = out.rows == 2 && out.cols == 16;
+        std::printf("BinDecoder call: %s\n", shape_ok ? "ok" : "FAILED");
+        fails += !shape_ok;
+        // error contract: a different H must be rejected like a bad input
+        auto rng2 = ura::make_rng(99);
+        auto h2 = ura::build_random_ldpc(gf, 16, 8, 3, rng2);
+        try {
+            gpu.logits(ura::all_masked_grid(2, 16), s, h2, 0.0);
+            std::printf("foreign H accepted: FAILED\n");
+            ++fails;
+        } catch (const std::domain_error&) {
+            std::printf("foreign H rejected with std::domain_error: ok\n");
+        }
+    } catch (const std::exception& e) {
+        std::printf("exception: %s\n", e.what());
+        ++fails;
+    }
+    return fails;
+}

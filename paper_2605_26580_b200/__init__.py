@@ -443,14 +443,25 @@ def forward_count(cfg: Config) -> int:
 
 
 def flops_per_bin(cfg: Config) -> float:
-    """Algorithmic FLOPs per bin:
-    F = 2 fwd [N (4KLQD + 6KLDH + 2K|E|QD + 2K|E|DH) + KLQD + F_attn],
-    F_attn = N K|E| (2D^2 + 2(d_c-1)D) when heads > 0."""
+    """Executed tensor-core FLOPs per decoded bin:
+    F = 2 fwd [N (4KLQD + 6KLDH + 2K|E|QD + 2K|E|DH) + KLQD]  (SURVEY §8(d) without its attention
+    D^2 key-projection term: the device computes attention scores through u_h = Wk_h^T q_h)."""
     w, m = cfg.workload, cfg.model
     K, L, Q, D, H, N = w.k, w.slots, m.q, m.dim, m.hidden, m.layers
     E = L * w.col_weight
-    dc = E / w.checks
     per = N * (4 * K * L * Q * D + 6 * K * L * D * H + 2 * K * E * Q * D + 2 * K * E * D * H) + K * L * Q * D
-    if m.heads:
-        per += N * K * E * (2 * D * D + 2 * (dc - 1) * D)
     return 2.0 * forward_count(cfg) * per
+
+
+def survey_flops_per_bin(cfg: Config) -> float:
+    """SURVEY §8(d)'s formula including F_attn = N K|E| (2D^2 + 2(d_c-1)D) (informational)."""
+    w, m = cfg.workload, cfg.model
+    K, E, D, N = w.k, w.slots * w.col_weight, m.dim, m.layers
+    dc = E / w.checks
+    extra = N * K * E * (2 * D * D + 2 * (dc - 1) * D) if m.heads else 0.0
+    return flops_per_bin(cfg) + 2.0 * forward_count(cfg) * extra
+
+
+def shard(first_bin: int, n_bins: int, rank: int, world: int, step: int = 0):
+    """Contiguous bin shard of `rank` for `step`: [start, start + n_bins)."""
+    return first_bin + (step * world + rank) * n_bins, n_bins

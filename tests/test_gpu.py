@@ -248,3 +248,17 @@ def test_input_errors_surface_like_the_reference(P):
         ctx.refine(S, 2, P.RevealSchedule(steps=2, tau_max=0.5, tau_min=1.0))
     with pytest.raises(ValueError, match="need T >= 1"):
         ctx.refine(S, 2, P.RevealSchedule(steps=0))
+
+
+def test_reference_engine_with_gpu_denoiser():
+    """The drop-in boundary end to end: the reference's own ura::run_refinement /
+    run_with_remasking driving cider::GpuStructuredDenoiser (include/cider_ura.hpp), the device
+    loop, and a BinDecoder — identical grids to the reference (oracle/adapter_test.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "adapter_test")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_test not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
