@@ -22,6 +22,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <thread>
 #include <vector>
 
 #include "host/host.hpp"
@@ -30,6 +31,7 @@
 #include "kernels/gemm_tc.cuh"
 #include "kernels/mlp_tc.cuh"
 #include "kernels/mlp_tc2.cuh"
+#include "kernels/gemm_grp.cuh"
 #include "kernels/path.cuh"
 
 namespace cider {
@@ -105,6 +107,34 @@ CUtensorMap make_map_w1_3d(const void* ptr, int64_t rows, int cols, int box_rows
     return m;
 }
 
+// Rows of a [bins][blocks][K] x cols bf16 tensor as a 3-D map {cols, blocks*K, bins}: one box =
+// K rows of one block for bb consecutive bins (gemm_grp.cuh A operands).
+CUtensorMap make_map_rows3d(const void* ptr, int bins, int rows_per_bin, int cols, int K, int bb) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {cuuint64_t(cols), cuuint64_t(rows_per_bin), cuuint64_t(bins)};
+    cuuint64_t strides[2] = {cuuint64_t(cols) * 2, cuuint64_t(rows_per_bin) * cols * 2};
+    cuuint32_t box[3] = {64, cuuint32_t(K), cuuint32_t(bb)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (rows3d) failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+// The T table [alpha][n][k] as {k, n, alpha}, box {64, 256, 1}.
+CUtensorMap make_map_ttab(const void* ptr, int D, int Q) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(D), cuuint64_t(Q)};
+    cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(D) * D * 2};
+    cuuint32_t box[3] = {64, cuuint32_t(D), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (ttab) failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
 // ---- device allocations ------------------------------------------------------------------
 struct DevBuf {
     void* p = nullptr;
@@ -163,6 +193,13 @@ struct cider_ctx {
     // Tanner tables
     int *e_slot = nullptr, *e_check = nullptr, *check_ptr = nullptr, *slot_ptr = nullptr, *slot_edge = nullptr;
     uint8_t *perm_in = nullptr, *perm_out = nullptr;
+    // Q >= D path (gemm_grp.cuh): T_alpha = W^T Pi_alpha W table + group tables
+    bool tpath = false;
+    void* Ttab = nullptr;                          // bf16 [Q][D][D] as B tiles [alpha][n][k]
+    int *gn_count = nullptr, *gn_arow = nullptr, *gn_alpha = nullptr, *gn_out = nullptr;  // per edge
+    int *gm_count = nullptr, *gm_arow = nullptr, *gm_alpha = nullptr, *gm_out = nullptr;  // per slot
+    int gm_max_seg = 0;
+    std::vector<float> W_host; // out_proj as the device computes with it (bf16-rounded in BF16 mode)
     // workspace
     int chunk_req = 0;
     int cap_bins = 0, cap_K = 0;
@@ -604,6 +641,45 @@ void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* poo
     else if (V == 4) run_pool_v<T, 4>(c, lw, Nn, K, groups, pooled);
     else run_pool_v<T, 2>(c, lw, Nn, K, groups, pooled);
 }
+
+// ---- grouped GEMMs of the Q >= D path ----------------------------------------------------------
+void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, int nb, int K, int groups,
+              const int* cnt, const int* arow, const int* alpha, int max_seg, const int* out_row, int out_rows_per_bin,
+              void* out_t, float* out_f, int mean_seg) {
+    const int D = c.D;
+    const int bb = std::max(1, 128 / K);
+    if (K > 128) throw InvalidInput("cider: K > 128 unsupported on the grouped path");
+    tc::GrpArgs a;
+    a.groups = groups;
+    a.mtiles = (nb + bb - 1) / bb;
+    a.bins = nb;
+    a.K = K;
+    a.bb = bb;
+    a.kb_per_seg = D / 64;
+    a.max_seg = max_seg;
+    a.seg_count = cnt;
+    a.seg_arow = arow;
+    a.seg_alpha = alpha;
+    a.out_rows_per_bin = out_rows_per_bin;
+    a.out_row = out_row;
+    a.D = D;
+    a.out_t = reinterpret_cast<bf16*>(out_t);
+    a.out_f = out_f;
+    const double rows = double(nb) * K * groups;
+    Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, rows * D * 2.0 * (mean_seg + 1));
+    CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
+    CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
+    using Lay = tc::SmemLayout<256>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
+        attr_set = true;
+    }
+    const int tiles = a.groups * a.mtiles;
+    tc::gemm_grp_kernel<<<std::min(tiles, c.sm_count), tc::NUM_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
+    check_launch(tag);
+}
+
 // ---- one denoiser forward over nb bins (denoiser.cpp:253-259) -------------------------------
 struct FwdOpts {
     float tau = 1.0f;
@@ -642,18 +718,24 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         e.out_f = w.Ztf; e.out_t = c.bf16 ? w.Ztt : nullptr; e.ldo = D;
         mlp(c, "mlp_gate", w.Zt, D, w.et, D, lw.g1, lw.gb1, lw.g2, Ms, e, w.hid);
         // Module B (denoiser.cpp:181-228)
-        e = epi(EP_STORE);
-        e.out_t = w.U; e.ldo = Q;
-        gemm(c, "gemm_symproj", w.Ztt, D, nullptr, 0, c.W, Ms, Q, e);
-        {
-            Launch lg(c, "gather_perm", 0, double(Me) * Q * 2 * c.act_size);
-            if (c.bf16) run_gather<bf16>(c, (const bf16*)w.U, K, Me, (bf16*)w.Ae);
-            else run_gather<float>(c, (const float*)w.U, K, Me, (float*)w.Ae);
-            check_launch("gather_perm");
+        if (c.tpath) {
+            // N[(b,e,k)] = z~[(b,slot_e,k)] . T_{alpha_e}
+            grp_gemm(c, "grp_normalise", w.Ztt, L, nb, K, E, c.gn_count, c.gn_arow, c.gn_alpha, 1, c.gn_out, E, w.Nn,
+                     nullptr, 1);
+        } else {
+            e = epi(EP_STORE);
+            e.out_t = w.U; e.ldo = Q;
+            gemm(c, "gemm_symproj", w.Ztt, D, nullptr, 0, c.W, Ms, Q, e);
+            {
+                Launch lg(c, "gather_perm", 0, double(Me) * Q * 2 * c.act_size);
+                if (c.bf16) run_gather<bf16>(c, (const bf16*)w.U, K, Me, (bf16*)w.Ae);
+                else run_gather<float>(c, (const float*)w.U, K, Me, (float*)w.Ae);
+                check_launch("gather_perm");
+            }
+            e = epi(EP_STORE);
+            e.out_t = w.Nn; e.ldo = D;
+            gemm(c, "gemm_backproj", w.Ae, Q, nullptr, 0, c.Wt, Me, D, e);
         }
-        e = epi(EP_STORE);
-        e.out_t = w.Nn; e.ldo = D;
-        gemm(c, "gemm_backproj", w.Ae, Q, nullptr, 0, c.Wt, Me, D, e);
         if (pool_fast(c)) {
             Launch lg(c, c.heads ? "pool_attn" : "pool_sum", 2.0 * double(Me) * D * (c.heads + c.max_check_deg),
                       double(Me) * D * 2 * c.act_size);
@@ -682,18 +764,24 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         e = epi(EP_STORE);
         e.bias = lw.ab2; e.out_t = w.mapped; e.ldo = D;
         mlp(c, "mlp_agg", w.pooled, D, nullptr, 0, lw.a1, lw.ab1, lw.a2, Me, e, w.hid);
-        e = epi(EP_STORE);
-        e.out_t = w.Mq; e.ldo = Q;
-        gemm(c, "gemm_msgproj", w.mapped, D, nullptr, 0, c.W, Me, Q, e);
-        {
-            Launch lg(c, "scatter_perm", 0, double(Ms) * Q * c.act_size + double(Me) * Q * c.act_size);
-            if (c.bf16) run_scatter<bf16>(c, (const bf16*)w.Mq, K, Ms, (bf16*)w.accq);
-            else run_scatter<float>(c, (const float*)w.Mq, K, Ms, (float*)w.accq);
-            check_launch("scatter_perm");
+        if (c.tpath) {
+            // acc[(b,s,k)] = sum over slot s's edges (ascending check) of mapped[(b,e,k)] . T_{alpha_e^-1}
+            grp_gemm(c, "grp_message", w.mapped, E, nb, K, L, c.gm_count, c.gm_arow, c.gm_alpha, c.gm_max_seg, c.gm_out, L,
+                     w.acct, o.incoming ? w.accf : nullptr, std::max(1, E / std::max(1, L)));
+        } else {
+            e = epi(EP_STORE);
+            e.out_t = w.Mq; e.ldo = Q;
+            gemm(c, "gemm_msgproj", w.mapped, D, nullptr, 0, c.W, Me, Q, e);
+            {
+                Launch lg(c, "scatter_perm", 0, double(Ms) * Q * c.act_size + double(Me) * Q * c.act_size);
+                if (c.bf16) run_scatter<bf16>(c, (const bf16*)w.Mq, K, Ms, (bf16*)w.accq);
+                else run_scatter<float>(c, (const float*)w.Mq, K, Ms, (float*)w.accq);
+                check_launch("scatter_perm");
+            }
+            e = epi(EP_STORE);
+            e.out_f = (c.bf16 && !o.incoming) ? nullptr : w.accf; e.out_t = c.bf16 ? w.acct : nullptr; e.ldo = D;
+            gemm(c, "gemm_msgback", w.accq, Q, nullptr, 0, c.Wt, Ms, D, e);
         }
-        e = epi(EP_STORE);
-        e.out_f = (c.bf16 && !o.incoming) ? nullptr : w.accf; e.out_t = c.bf16 ? w.acct : nullptr; e.ldo = D;
-        gemm(c, "gemm_msgback", w.accq, Q, nullptr, 0, c.Wt, Ms, D, e);
         if (o.incoming)
             ck(cudaMemcpyAsync(o.incoming + size_t(li) * Ms * D, w.accf, size_t(Ms) * D * 4, cudaMemcpyDeviceToDevice, c.stream), "incoming");
         e = epi(EP_RESID);
@@ -930,6 +1018,9 @@ void upload_model(cider_ctx& c, const float* w) {
     const float* W = take(size_t(Q) * D);
     const float* V = take(size_t(Q) * D);
     c.Etab = upload_vec(c, E, size_t(Q + 1) * D);
+    c.W_host.assign(W, W + size_t(Q) * D);
+    if (c.bf16)
+        for (float& v : c.W_host) v = bf16_round(v);
     c.W = upload_mat(c, W, Q, D, false);
     c.Wt = upload_mat(c, W, Q, D, true);
     c.Vt = upload_mat(c, V, Q, D, true);
@@ -993,6 +1084,72 @@ void upload_code(cider_ctx& c) {
     c.slot_edge = upload_raw(c, t.slot_edge);
     c.perm_in = upload_raw(c, pin);
     c.perm_out = upload_raw(c, pout);
+}
+
+
+// T_alpha[k][n] = sum_c W[alpha^-1 c][k] W[c][n]  (= W^T P_alpha W, the coefficient action of
+// denoiser.cpp:162-179 as one D x D matrix), stored as GEMM B tiles Tt[alpha][n][k], plus the
+// group tables of the two grouped GEMMs (gemm_grp.cuh). Host fp64, threaded over alpha.
+void build_tpath(cider_ctx& c) {
+    const int Q = c.Q, D = c.D;
+    const Gf& gf = *c.gf;
+    const Tanner& t = *c.tg;
+    std::vector<bf16> T(size_t(Q) * D * D, __float2bfloat16_rn(0.0f));
+    const float* W = c.W_host.data();
+    auto work = [&](int a0, int stride) {
+        std::vector<double> acc(size_t(D) * D);
+        for (int alpha = a0; alpha < Q; alpha += stride) {
+            if (alpha == 0) continue;
+            const int ai = gf.inv(alpha);
+            std::fill(acc.begin(), acc.end(), 0.0);
+            for (int cc = 0; cc < Q; ++cc) {
+                const float* wr = W + size_t(gf.mul(ai, cc)) * D; // W[alpha^-1 c][.]
+                const float* wc = W + size_t(cc) * D;             // W[c][.]
+                for (int n = 0; n < D; ++n) {
+                    const double wn = wc[n];
+                    double* row = &acc[size_t(n) * D];
+                    for (int k = 0; k < D; ++k) row[k] += double(wr[k]) * wn;
+                }
+            }
+            bf16* dst = &T[size_t(alpha) * D * D];
+            for (size_t i = 0; i < size_t(D) * D; ++i) dst[i] = __float2bfloat16_rn(float(acc[i]));
+        }
+    };
+    const int nt = int(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    for (int i = 0; i < nt; ++i) pool.emplace_back(work, i, nt);
+    for (auto& th : pool) th.join();
+    c.Ttab = upload_raw(c, T);
+    // normalise GEMM: one group per edge
+    std::vector<int> n_count(t.n_edges(), 1), n_arow(t.n_edges()), n_alpha(t.n_edges()), n_out(t.n_edges());
+    for (int e = 0; e < t.n_edges(); ++e) {
+        n_arow[e] = t.slot[e];
+        n_alpha[e] = t.coef[e];
+        n_out[e] = e;
+    }
+    c.gn_count = upload_raw(c, n_count);
+    c.gn_arow = upload_raw(c, n_arow);
+    c.gn_alpha = upload_raw(c, n_alpha);
+    c.gn_out = upload_raw(c, n_out);
+    // message GEMM: one group per slot, its edges in ascending check order (slot_edge order)
+    int maxd = 1;
+    for (int l = 0; l < t.slots; ++l) maxd = std::max(maxd, t.slot_ptr[l + 1] - t.slot_ptr[l]);
+    std::vector<int> m_count(t.slots), m_arow(size_t(t.slots) * maxd, 0), m_alpha(size_t(t.slots) * maxd, 1), m_out(t.slots);
+    for (int l = 0; l < t.slots; ++l) {
+        m_count[l] = t.slot_ptr[l + 1] - t.slot_ptr[l];
+        m_out[l] = l;
+        for (int p = t.slot_ptr[l]; p < t.slot_ptr[l + 1]; ++p) {
+            const int e = t.slot_edge[p];
+            m_arow[size_t(l) * maxd + (p - t.slot_ptr[l])] = e;
+            m_alpha[size_t(l) * maxd + (p - t.slot_ptr[l])] = gf.inv(t.coef[e]);
+        }
+    }
+    c.gm_max_seg = maxd;
+    c.gm_count = upload_raw(c, m_count);
+    c.gm_arow = upload_raw(c, m_arow);
+    c.gm_alpha = upload_raw(c, m_alpha);
+    c.gm_out = upload_raw(c, m_out);
+    c.tpath = true;
 }
 
 void require_device() {
@@ -1085,6 +1242,12 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
         ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
         upload_model(*c, weights);
         upload_code(*c);
+        // Q >= D: Module B through precomputed coefficient actions (gemm_grp.cuh); slots with no
+        // incident check (possible in external codes) would make an empty group -> generic path
+        bool every_slot_checked = true;
+        for (int l = 0; l < c->L; ++l) every_slot_checked &= c->tg->slot_ptr[l + 1] > c->tg->slot_ptr[l];
+        if (c->bf16 && c->D == 256 && c->Q >= c->D && every_slot_checked && !std::getenv("CIDER_NO_TPATH"))
+            build_tpath(*c);
         ck(cudaDeviceSynchronize(), "upload");
         *out = c.release();
     });

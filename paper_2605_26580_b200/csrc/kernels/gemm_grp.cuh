@@ -1,0 +1,172 @@
+// gemm_grp.cuh — grouped tcgen05 GEMM for Module B's coefficient actions when Q >= D (BF16 mode).
+//
+// T_alpha(x) = W^T Pi_alpha W x (denoiser.cpp:162-179) is linear in x, so for each GF(Q)
+// coefficient the D x D matrix T_alpha = W^T P_alpha W is precomputed once and Module B's
+// projection / permutation / back-projection chains become two grouped GEMMs:
+//
+//   normalise  (group = edge e):  N[(b,e,k)] = z~[(b, slot_e, k)] . T_{alpha_e}
+//   messages   (group = slot s):  acc[(b,s,k)] = sum_{e in s, ascending check} mapped[(b,e,k)] . T_{alpha_e^-1}
+//
+// The message GEMM concatenates the slot's edges along K, so the per-slot sum happens inside the
+// tensor core in a fixed order (no atomics). A rows are gathered by 3-D TMA boxes
+// {64 cols, K rows, 128/K bins} straight out of the [bin][slot|edge][row] layouts; B tiles come
+// from a 3-D map over the T table [alpha][n][k]. Same warp roles / pipeline as gemm_tc.cuh.
+#pragma once
+
+#include "gemm_tc.cuh"
+
+namespace cider {
+namespace tc {
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+
+struct GrpArgs {
+    int groups, mtiles, bins, K, bb;  // bb = bins per 128-row tile (K * bb <= 128)
+    int kb_per_seg;                   // D / 64
+    int max_seg;                      // segments (edges) per group
+    const int* seg_count;             // [groups]
+    const int* seg_arow;              // [groups][max_seg]: A row block (slot or edge index)
+    const int* seg_alpha;             // [groups][max_seg]: T-table index
+    int out_rows_per_bin;             // L (site output) or E (edge output)
+    const int* out_row;               // [groups]: output row block (edge or slot index)
+    int D;
+    bf16* out_t;                      // bf16 output [bins * out_rows_per_bin * K x D]
+    float* out_f;                     // optional fp32 copy
+};
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
+    constexpr int BN = 256;
+    using Lay = SmemLayout<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int tiles = args.groups * args.mtiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(Lay::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int a_bytes = args.K * args.bb * 128; // the A box actually filled (<= 16 KB)
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int g = tile / args.mtiles, mt = tile % args.mtiles;
+                const int nseg = args.seg_count[g];
+                for (int sg = 0; sg < nseg; ++sg) {
+                    const int arow = args.seg_arow[g * args.max_seg + sg];
+                    const int alpha = args.seg_alpha[g * args.max_seg + sg];
+                    for (int kk = 0; kk < args.kb_per_seg; ++kk) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
+                        uint8_t* sb = sa + Lay::A_BYTES;
+                        mbar_expect_tx(&full[stage], a_bytes + Lay::B_BYTES);
+                        tma_load_3d(sa, &tmA, &full[stage], kk * 64, arow * args.K, mt * args.bb);
+                        tma_load_3d(sb, &tmT, &full[stage], kk * 64, 0, alpha);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+                const int g = tile / args.mtiles;
+                const int kblocks = args.seg_count[g] * args.kb_per_seg;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
+                    uint8_t* sb = sa + Lay::A_BYTES;
+                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
+                    mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        const int quarter = warp % 4;
+        const int row = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int g = tile / args.mtiles, mt = tile % args.mtiles;
+            mbar_wait(&tfull[acc], acc_phase);
+            fence_after();
+            const int b = mt * args.bb + row / args.K, k = row % args.K;
+            const bool live = row < args.K * args.bb && b < args.bins;
+            const size_t orow = (size_t(b) * args.out_rows_per_bin + args.out_row[g]) * args.K + k;
+            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+            for (int c0 = 0; c0 < args.D; c0 += 32) {
+                float v[32];
+                tmem_ld32(tbase + c0, v);
+                if (!live) continue;
+                if (args.out_f) {
+                    float* o = args.out_f + orow * args.D + c0;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                }
+                bf16* o = args.out_t + orow * args.D + c0;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+                    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+                    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
+                    __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+                    uint4 u;
+                    u.x = *reinterpret_cast<uint32_t*>(&p0);
+                    u.y = *reinterpret_cast<uint32_t*>(&p1);
+                    u.z = *reinterpret_cast<uint32_t*>(&p2);
+                    u.w = *reinterpret_cast<uint32_t*>(&p3);
+                    *reinterpret_cast<uint4*>(o + i) = u;
+                }
+            }
+            fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Lay::TMEM_COLS));
+    }
+}
+
+} // namespace tc
+} // namespace cider

@@ -362,24 +362,36 @@ scatter_perm_warp_kernel(const T* __restrict__ Mq, const int* __restrict__ slot_
     store_v<T, V>(accq + m * Q + lane * V, s);
 }
 
-// Demixing, one slot row (b, l) per block, one symbol per thread (see demix_kernel).
+// Demixing, one slot row (b, l) per block, one symbol per thread (see demix_kernel). The
+// normaliser is summed in 2^-26 fixed point in 32-bit integers (K <= 32 terms <= 1 each, so no
+// overflow): exact integer adds, hence order-independent — bitwise row-permutation invariant —
+// without the fp64 conversions of the generic kernel (the demix ncu profile was issue-bound).
+// BF16 mode uses the MUFU exp2; FP32 mode keeps expf.
 template <typename T>
-__global__ void demix_block_kernel(const float* __restrict__ lbar, const float* __restrict__ S, int K, int Q, float tau,
-                                   T* __restrict__ out) {
+__global__ void __launch_bounds__(256)
+demix_block_kernel(const float* __restrict__ lbar, const float* __restrict__ S, int K, int Q, float tau,
+                   T* __restrict__ out) {
     const int64_t s = blockIdx.x;
+    const float inv_tau = 1.0f / tau;
     for (int a = threadIdx.x; a < Q; a += blockDim.x) {
         const float* x = lbar + s * K * Q + a;
         float xv[32];
         float mx = -INFINITY;
-        for (int k = 0; k < K; ++k) { xv[k] = x[size_t(k) * Q]; mx = fmaxf(mx, xv[k]); }
-        long long den = 0;
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) { xv[k] = __ldg(x + size_t(k) * Q); mx = fmaxf(mx, xv[k]); }
+        uint32_t den = 0;
+#pragma unroll 8
         for (int k = 0; k < K; ++k) {
-            xv[k] = expf((xv[k] - mx) / tau);
-            den += __double2ll_rn(double(xv[k]) * 4503599627370496.0);
+            float e;
+            if constexpr (sizeof(T) == 2) e = exp2f((xv[k] - mx) * (inv_tau * 1.4426950408889634f));
+            else e = expf((xv[k] - mx) / tau);
+            xv[k] = e;
+            den += __float2uint_rn(e * 67108864.0f); // 2^26
         }
-        const float denf = float(double(den) * (1.0 / 4503599627370496.0));
-        const float sv = S[s * Q + a];
-        for (int k = 0; k < K; ++k) out[(s * K + k) * Q + a] = from_f<T>((xv[k] / denf) * sv);
+        const float rden = 1.0f / (float(den) * (1.0f / 67108864.0f));
+        const float sv = __ldg(S + s * Q + a);
+#pragma unroll 8
+        for (int k = 0; k < K; ++k) out[(s * K + k) * Q + a] = from_f<T>((xv[k] * rden) * sv);
     }
 }
 
