@@ -137,6 +137,13 @@ int cider_refine_device(cider_ctx* ctx, int B, int K, const float* S_device,
                         const cider_schedule* sched, const cider_remask* remask,
                         int32_t* grid_device);
 
+/* ---- GF(Q) check-node update in the WHT domain --------------------- */
+/* = ura::update_check_wht (bp.cpp:222-269) for n_checks checks of degree d at once: v2c and c2v are
+ * n_checks x d x Q (fp64), coeffs n_checks x d; c2v[i] is the extrinsic message to edge i
+ * (check_update_wht(gf, others, their coeffs, coeff_i), bp.cpp:128-149). Host buffers. */
+int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const int32_t* coeffs, double* c2v,
+                           int device);
+
 /* ---- device plumbing used by the benchmark (no PyTorch on the path) --------------------- */
 int cider_device_count(int* n);
 int cider_device_alloc(cider_ctx* ctx, size_t bytes, void** ptr);

@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
         h.cider_workload_code.argtypes = [C.POINTER(WorkloadDesc), P]
         h.cider_workload_bins.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
         h.cider_ser_cer.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        h.cider_check_update_wht.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, C.c_int]
         _lib_handle = h
     return _lib_handle
 
@@ -397,6 +398,17 @@ def ser_cer(truth: np.ndarray, pred: np.ndarray):
     s, c = C.c_double(), C.c_double()
     _check(lib().cider_ser_cer(n, K, L, _ptr(truth), _ptr(pred), C.byref(s), C.byref(c)))
     return s.value / n, c.value / n
+
+
+def check_update_wht(m: int, v2c: np.ndarray, coeffs: np.ndarray, device: int = 0) -> np.ndarray:
+    """All extrinsic check-to-variable messages of a batch of GF(2^m) checks, WHT domain
+    (= ura::update_check_wht, bp.cpp:222-269). v2c: n x d x Q fp64, coeffs: n x d."""
+    v = np.ascontiguousarray(v2c, dtype=np.float64)
+    cf = np.ascontiguousarray(coeffs, dtype=np.int32)
+    n, d, q = v.shape
+    out = np.empty_like(v)
+    _check(lib().cider_check_update_wht(m, n, d, _ptr(v), _ptr(cf), _ptr(out), device))
+    return out
 
 
 def device_count() -> int:

@@ -32,6 +32,7 @@
 #include "kernels/mlp_tc.cuh"
 #include "kernels/mlp_tc2.cuh"
 #include "kernels/gemm_grp.cuh"
+#include "kernels/wht.cuh"
 #include "kernels/path.cuh"
 
 namespace cider {
@@ -445,9 +446,7 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     ep.M = int(M);
     ep.N = D;
     static const bool one_sm = std::getenv("CIDER_MLP_1SM") != nullptr;
-    // 2-SM kernel for the plain-epilogue map (check aggregator); the gate / fusion maps keep the
-    // 1-SM kernel, whose SMEM-staged final epilogue reads the residual operands coalesced.
-    const bool pair = !one_sm && ep.kind == EP_STORE && Kin % 128 == 0 && (D == 128 || D == 256);
+    const bool pair = !one_sm && Kin % 128 == 0 && (D == 128 || D == 256);
     Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
     const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;
@@ -676,7 +675,7 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         attr_set = true;
     }
     const int tiles = a.groups * a.mtiles;
-    tc::gemm_grp_kernel<<<std::min(tiles, c.sm_count), tc::NUM_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
+    tc::gemm_grp_kernel<<<std::min(tiles, c.sm_count), tc::GRP_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
     check_launch(tag);
 }
 
@@ -1121,11 +1120,13 @@ void build_tpath(cider_ctx& c) {
     for (auto& th : pool) th.join();
     c.Ttab = upload_raw(c, T);
     // normalise GEMM: one group per edge
+    // groups in slot-major edge order (slot_edge), so a slot's edges are consecutive groups
     std::vector<int> n_count(t.n_edges(), 1), n_arow(t.n_edges()), n_alpha(t.n_edges()), n_out(t.n_edges());
-    for (int e = 0; e < t.n_edges(); ++e) {
-        n_arow[e] = t.slot[e];
-        n_alpha[e] = t.coef[e];
-        n_out[e] = e;
+    for (int g = 0; g < t.n_edges(); ++g) {
+        const int e = t.slot_edge[g];
+        n_arow[g] = t.slot[e];
+        n_alpha[g] = t.coef[e];
+        n_out[g] = e;
     }
     c.gn_count = upload_raw(c, n_count);
     c.gn_arow = upload_raw(c, n_arow);
@@ -1448,6 +1449,47 @@ int cider_reset_stats(cider_ctx* c) {
         resolve_stats(*c);
         c->stats.clear();
         c->launches = 0;
+    });
+}
+
+
+// Batched GF(Q) check-node update in the WHT domain (bp.cpp:128-149, 222-269):
+// for each of n_checks checks with d incident edges, all d extrinsic check-to-variable messages.
+int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const int32_t* coeffs, double* c2v,
+                           int device) {
+    return guard([&] {
+        Gf gf(m, 0);
+        const int Q = gf.q;
+        if (n_checks < 0 || d < 1 || d > WHT_MAXD) throw InvalidInput("check_update_wht: need 1 <= d <= 32");
+        for (int64_t i = 0; i < int64_t(n_checks) * d; ++i)
+            if (coeffs[i] <= 0 || coeffs[i] >= Q) throw InvalidInput("coeff_map: coefficient must be a nonzero field element");
+        if (n_checks == 0) return;
+        require_device();
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        std::vector<uint8_t> mul(size_t(Q) * Q);
+        for (int a = 0; a < Q; ++a)
+            for (int b = 0; b < Q; ++b) mul[size_t(a) * Q + b] = uint8_t(gf.mul(a, b));
+        const size_t nmsg = size_t(n_checks) * d * Q;
+        DevBuf din, dout, dcf, dmul;
+        din.ensure(nmsg * 8);
+        dout.ensure(nmsg * 8);
+        dcf.ensure(size_t(n_checks) * d * 4);
+        dmul.ensure(mul.size());
+        cudaStream_t st;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        ck(cudaMemcpyAsync(din.p, v2c, nmsg * 8, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(dcf.p, coeffs, size_t(n_checks) * d * 4, cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(dmul.p, mul.data(), mul.size(), cudaMemcpyHostToDevice, st), "h2d");
+        const size_t smem = size_t(2) * d * Q * 8;
+        if (smem > 200 * 1024) throw InvalidInput("check_update_wht: d * Q too large for one CTA");
+        ck(cudaFuncSetAttribute(wht_check_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+        wht_check_update_kernel<<<n_checks, std::min(256, std::max(32, Q)), smem, st>>>(
+            din.as<double>(), dcf.as<int>(), dmul.as<uint8_t>(), d, Q, dout.as<double>());
+        check_launch("wht_check_update");
+        ck(cudaMemcpyAsync(c2v, dout.p, nmsg * 8, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "wht");
+        cudaStreamDestroy(st);
+        din.release(); dout.release(); dcf.release(); dmul.release();
     });
 }
 

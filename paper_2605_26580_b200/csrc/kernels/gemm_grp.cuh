@@ -11,6 +11,9 @@
 // tensor core in a fixed order (no atomics). A rows are gathered by 3-D TMA boxes
 // {64 cols, K rows, 128/K bins} straight out of the [bin][slot|edge][row] layouts; B tiles come
 // from a 3-D map over the T table [alpha][n][k]. Same warp roles / pipeline as gemm_tc.cuh.
+// Tiles run m-tile-major (all groups of one 128-row block back to back, groups sorted so edges of
+// one slot are adjacent): the A rows a slot shares among its edges are L2 hits, and the <= 24 MB
+// of T matrices stay L2-resident.
 #pragma once
 
 #include "gemm_tc.cuh"
@@ -40,7 +43,9 @@ struct GrpArgs {
     float* out_f;                     // optional fp32 copy
 };
 
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+constexpr int GRP_THREADS = 320; // producer, MMA, 8 epilogue warps (two per TMEM lane quarter)
+
+__global__ void __launch_bounds__(GRP_THREADS, 1)
 gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
     constexpr int BN = 256;
     using Lay = SmemLayout<BN>;
@@ -56,7 +61,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 256); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -75,7 +80,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int g = tile / args.mtiles, mt = tile % args.mtiles;
+                const int g = tile % args.groups, mt = tile / args.groups; // m-tile major: L2 reuse of A rows
                 const int nseg = args.seg_count[g];
                 for (int sg = 0; sg < nseg; ++sg) {
                     const int arow = args.seg_arow[g * args.max_seg + sg];
@@ -98,7 +103,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int g = tile / args.mtiles;
+                const int g = tile % args.groups;
                 const int kblocks = args.seg_count[g] * args.kb_per_seg;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 fence_after();
@@ -121,18 +126,20 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     } else {
         const int quarter = warp % 4;
+        const int half = (warp - 2) / 4; // the two warps of a lane quarter split the columns
         const int row = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-            const int g = tile / args.mtiles, mt = tile % args.mtiles;
+            const int g = tile % args.groups, mt = tile / args.groups;
             mbar_wait(&tfull[acc], acc_phase);
             fence_after();
             const int b = mt * args.bb + row / args.K, k = row % args.K;
             const bool live = row < args.K * args.bb && b < args.bins;
             const size_t orow = (size_t(b) * args.out_rows_per_bin + args.out_row[g]) * args.K + k;
             const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-            for (int c0 = 0; c0 < args.D; c0 += 32) {
+            const int cw = args.D / 2;
+            for (int c0 = half * cw; c0 < (half + 1) * cw; c0 += 32) {
                 float v[32];
                 tmem_ld32(tbase + c0, v);
                 if (!live) continue;

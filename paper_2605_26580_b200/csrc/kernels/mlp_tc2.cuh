@@ -144,9 +144,12 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     const int NC = args.H / MLP_HC;
     constexpr int EPI_ARRIVALS = 2 * 8; // one elected lane per epilogue warp, both CTAs
 
+    // gate / fusion epilogues read z (and e) back from the resident row tile X, so X is released by
+    // the last MMA1's commit AND by the 8 epilogue warps once their final epilogue is done
+    const bool epi_reads_x = args.ep.kind == EP_GATE || args.ep.kind == EP_RESID;
     if (threadIdx.x == 0) {
         mbar_init(x_full, 1);
-        mbar_init(x_empty, 1);
+        mbar_init(x_empty, epi_reads_x ? 1 + 8 : 1);
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) { mbar_init(&a1_full[b], 1); mbar_init(&h_full[b], EPI_ARRIVALS); }
         mbar_init(a2_full, 1);
@@ -349,43 +352,35 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 if (tr) args.trace[c * 8 + 4] = clock64();
             }
             // final epilogue straight from TMEM: this thread's row, this warp's half of D in
-            // 32-column groups; residual / gate operands prefetched one group ahead.
+            // 32-column groups; z (and e) come from the row tile X still resident in SMEM
+            // (SWIZZLE_128B K-major: 16-byte chunk c of row r sits at chunk c ^ (r & 7)).
             const int m = tile * 256 + int(rank) * 128 + row;
             const bool live = m < ep.M;
-            const bool need_z = ep.kind == EP_GATE || ep.kind == EP_RESID;
             const int ncol = D / 2;
             const int c0 = half * ncol;
-            uint4 zq[2][4], eq[2][4];
-            auto fetch = [&](int buf, int n0) {
-                if (!need_z || !live) return;
-                const uint4* zp = reinterpret_cast<const uint4*>(ep.zb + size_t(m) * ep.ldz + n0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) zq[buf][q] = __ldg(zp + q);
-                if (ep.kind == EP_GATE) {
-                    const uint4* epp = reinterpret_cast<const uint4*>(ep.eb + size_t(m) * ep.ldz + n0);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) eq[buf][q] = __ldg(epp + q);
-                }
+            auto xrow_chunk = [&](int col) -> uint4 { // 8 bf16 at columns [col, col+8) of this row of X
+                const int kb = col / 64, ch = (col % 64) / 8;
+                return *reinterpret_cast<const uint4*>(xs + kb * 16384 + row * 128 + ((ch ^ (row & 7)) * 16));
             };
-            fetch(0, c0);
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
             fence_after();
-            if (args.dbg & 2) {
-                fence_before();
-                release(L_a2_empty);
-                continue;
-            }
 #pragma unroll 1
             for (int g = 0; g < ncol / 32; ++g) {
                 const int n0 = c0 + g * 32;
-                const int cur = g & 1;
-                if (g + 1 < ncol / 32) fetch(cur ^ 1, n0 + 32);
                 float v[32];
                 tmem_ld32(tmem + lane_off + n0, v);
                 if (g + 1 == ncol / 32) {
                     fence_before();
                     release(L_a2_empty); // accumulator drained: next tile's MMA2 may start
+                }
+                uint4 zq[4], eq[4];
+                if (epi_reads_x) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        zq[q] = xrow_chunk(n0 + q * 8);
+                        if (ep.kind == EP_GATE) eq[q] = xrow_chunk(D + n0 + q * 8);
+                    }
                 }
                 if (!live) continue;
 #pragma unroll
@@ -393,9 +388,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     const float4 bb = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
                     v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
                 }
-                if (need_z) {
-                    const bf16* zz = reinterpret_cast<const bf16*>(zq[cur]);
-                    const bf16* ee = reinterpret_cast<const bf16*>(eq[cur]);
+                if (epi_reads_x) {
+                    const bf16* zz = reinterpret_cast<const bf16*>(zq);
+                    const bf16* ee = reinterpret_cast<const bf16*>(eq);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const float z = __bfloat162float(zz[i]);
@@ -428,6 +423,10 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         *reinterpret_cast<uint4*>(o + i) = u;
                     }
                 }
+            }
+            if (epi_reads_x) { // this warp no longer reads X: the producer may load the next tile
+                __syncwarp();
+                if (lane == 0) mbar_arrive(x_empty);
             }
         }
     }

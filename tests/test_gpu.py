@@ -262,3 +262,23 @@ def test_reference_engine_with_gpu_denoiser():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("m,d", [(4, 3), (6, 5), (6, 6), (8, 6)])
+def test_wht_check_update_matches_reference_vectors(P, oracle, m, d):
+    """batched WHT-domain GF(Q) check update on the device vs the oracle's
+    restatement of check_update_wht (bp.cpp:128-149; pinned to the reference by test_oracle.py),
+    within the reference's own WHT-vs-direct tolerance (test_bp.cpp:145-168: 1e-8)."""
+    q = 1 << m
+    rng = np.random.default_rng(m * 10 + d)
+    n = 64
+    v2c = rng.random((n, d, q)) ** 3
+    v2c /= v2c.sum(-1, keepdims=True)
+    cf = rng.integers(1, q, size=(n, d)).astype(np.int32)
+    out = P.check_update_wht(m, v2c, cf)
+    for c in range(0, n, 7):
+        for i in range(d):
+            others = [j for j in range(d) if j != i]
+            ref = oracle.check_update_wht(m, v2c[c, others], cf[c, others], int(cf[c, i]))
+            assert np.abs(out[c, i] - ref).max() < 1e-8
+    assert np.allclose(out.sum(-1), 1.0)

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(320, 1) bench_kernel(int iters, unsigned long 
 
 // The MLP issue pattern: per chunk 2 "W1 slots" of 8 SS MMAs (N=128 -> acc1[c&1]) and 2 "W2 slots"
 // of 4 TS MMAs (N=256 -> acc2), each slot followed by a commit; COMMIT=0 drops the per-slot commits.
-template <int CG, int COMMIT>
+template <int CG, int COMMIT, int WAITS = 0>
 __global__ void __launch_bounds__(128, 1) pattern_kernel(int chunks, unsigned long long* out) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -146,34 +146,36 @@ __global__ void __launch_bounds__(128, 1) pattern_kernel(int chunks, unsigned lo
     const uint32_t tmem = *slot;
     if (threadIdx.x == 0 && rank == 0) {
         const uint32_t id1 = idesc_bf16(128 * CG, 128), id2 = idesc_bf16(128 * CG, 256);
+        if (WAITS) { mbar_arrive(&bar[6]); } // completes phase 0 of bar[6]
         long long t0 = clock64();
         int s = 0;
         for (int c = 0; c < chunks; ++c) {
             for (int w = 0; w < 2; ++w) { // W1 slots
+                if (WAITS) { mbar_wait(&bar[6], 0); fence_after(); }
                 const uint64_t da = sw128_desc(smem + ((c + w) % 4) * 16384), db = sw128_desc(smem + 65536 + ((c + w) % 4) * 16384);
                 for (int j = 0; j < 2; ++j)
                     for (int kk = 0; kk < 4; ++kk) {
                         if (CG == 1) mma_bf16(tmem + 256 + (c & 1) * 128, da + j * 512 + kk * 2, db + j * 512 + kk * 2, id1, 1);
                         else mma_bf16_2sm(tmem + 256 + (c & 1) * 128, da + j * 512 + kk * 2, db + j * 512 + kk * 2, id1, 1);
                     }
-                if (COMMIT) { if (CG == 1) mma_commit(&bar[s % 8]); else mma_commit_2sm(&bar[s % 8]); }
+                if (COMMIT) { if (CG == 1) mma_commit(&bar[s % 6]); else mma_commit_2sm(&bar[s % 6]); }
                 ++s;
             }
             for (int w = 0; w < 2; ++w) { // W2 slots (TS)
+                if (WAITS) { mbar_wait(&bar[6], 0); fence_after(); }
                 const uint64_t db = sw128_desc(smem + 65536 + ((c + w) % 4) * 16384);
                 for (int kk = 0; kk < 4; ++kk) {
                     if (CG == 1) mma_ts_1(tmem, tmem + 256 + ((c + 1) & 1) * 128 + w * 64 + kk * 8, db + kk * 2, id2, 1);
                     else mma_bf16_2sm_ts(tmem, tmem + 256 + ((c + 1) & 1) * 128 + w * 64 + kk * 8, db + kk * 2, id2, 1);
                 }
-                if (COMMIT) { if (CG == 1) mma_commit(&bar[s % 8]); else mma_commit_2sm(&bar[s % 8]); }
+                if (COMMIT) { if (CG == 1) mma_commit(&bar[s % 6]); else mma_commit_2sm(&bar[s % 6]); }
                 ++s;
             }
         }
         uint64_t* fin = &bar[7];
         if (CG == 1) mma_commit(fin); else mma_commit_2sm(fin);
         // wait for the final commit: phase parity = number of completed phases of bar[7] so far, mod 2
-        const int uses7 = COMMIT ? (s / 8 + ((s % 8) > 7 ? 1 : 0)) : 0;
-        mbar_wait(fin, uses7 & 1);
+        mbar_wait(fin, 0);
         long long t1 = clock64();
         if (blockIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
     }
@@ -186,12 +188,12 @@ __global__ void __launch_bounds__(128, 1) pattern_kernel(int chunks, unsigned lo
     }
 }
 
-template <int CG, int COMMIT>
+template <int CG, int COMMIT, int WAITS = 0>
 void run_pattern(int sms, const char* label) {
     unsigned long long* d;
     cudaMalloc(&d, 16);
     const int smem = 131072 + 1024 + 128;
-    auto k = pattern_kernel<CG, COMMIT>;
+    auto k = pattern_kernel<CG, COMMIT, WAITS>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int chunks = 400;
     cudaLaunchConfig_t cfg = {};
@@ -267,6 +269,6 @@ int main() {
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     run_pattern<2, 1>(sms, "MLP pattern (W1 SS N=128, W2 TS N=256)");
     run_pattern<2, 0>(sms, "MLP pattern, no per-slot commits");
-    run_pattern<1, 1>(sms, "MLP pattern 1-SM");
+    run_pattern<2, 1, 1>(sms, "MLP pattern + try_wait/fence per slot");
     return 0;
 }
