@@ -185,7 +185,7 @@ struct cider_ctx {
     std::unique_ptr<Gf> gf;
     std::unique_ptr<Tanner> tg;
     int L = 0, P = 0, E = 0;
-    int max_check_deg = 0;
+    int max_check_deg = 0, min_check_deg = 1 << 30;
     // weights
     std::vector<DevBuf> wbufs;
     float* Etab = nullptr;                 // (Q+1) x D fp32
@@ -627,9 +627,23 @@ void run_pool_d(cider_ctx& c, const LayerW& lw, const T* Nn, int K, int64_t grou
         default: pool_warp_kernel<T, V, 16, DM><<<g, 256, size_t(16) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
     }
 }
+template <typename T, int V, int DEG>
+void run_pool_fixed(cider_ctx& c, const LayerW& lw, const T* Nn, int K, int64_t groups, T* pooled) {
+    const unsigned g = blocks_for(groups * 32);
+    const float* U = lw.au;
+    switch (c.heads) {
+        case 0: pool_warp_fixed_kernel<T, V, 0, DEG><<<g, 256, 0, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 2: pool_warp_fixed_kernel<T, V, 2, DEG><<<g, 256, size_t(2) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 4: pool_warp_fixed_kernel<T, V, 4, DEG><<<g, 256, size_t(4) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 8: pool_warp_fixed_kernel<T, V, 8, DEG><<<g, 256, size_t(8) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        default: pool_warp_fixed_kernel<T, V, 16, DEG><<<g, 256, size_t(16) * c.D * 4, c.stream>>>(Nn, U, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+    }
+}
 template <typename T, int V>
 void run_pool_v(cider_ctx& c, const LayerW& lw, const T* Nn, int K, int64_t groups, T* pooled) {
-    if (c.max_check_deg <= 6) run_pool_d<T, V, 6>(c, lw, Nn, K, groups, pooled);
+    // check-regular codes of degree 6 (all BASELINE codes): the unrolled fixed-degree kernel
+    if (c.bf16 && c.max_check_deg == 6 && c.min_check_deg == 6 && V == 8) run_pool_fixed<T, V, 6>(c, lw, Nn, K, groups, pooled);
+    else if (c.max_check_deg <= 6) run_pool_d<T, V, 6>(c, lw, Nn, K, groups, pooled);
     else run_pool_d<T, V, 8>(c, lw, Nn, K, groups, pooled);
 }
 template <typename T>
@@ -1232,6 +1246,7 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
             const int dj = c->tg->check_ptr[j + 1] - c->tg->check_ptr[j];
             if (dj > ATT_MAXD) throw InvalidInput("cider: check degree above 32");
             c->max_check_deg = std::max(c->max_check_deg, dj);
+            c->min_check_deg = std::min(c->min_check_deg, dj);
         }
         require_device();
         c->device = device;

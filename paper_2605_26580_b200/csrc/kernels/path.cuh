@@ -316,6 +316,84 @@ pool_warp_kernel(const T* __restrict__ Nn, const float* __restrict__ U, const in
     }
 }
 
+
+// Fixed-degree variant for check-regular codes (every check has exactly DEG edges — all BASELINE
+// codes, degree 3L/P = 6): fully unrolled, neighbour rows unpacked once, no runtime degree tests
+// (the generic kernel spent ~70% of its instructions on them — profiles/r1/pool_ncu_full.txt).
+template <typename T, int V, int NH, int DEG>
+__global__ void __launch_bounds__(256, 2)
+pool_warp_fixed_kernel(const T* __restrict__ Nn, const float* __restrict__ U, const int* __restrict__ check_ptr, int P,
+                       int E, int K, int D, int64_t n_groups, T* __restrict__ pooled) {
+    extern __shared__ float u_s[]; // NH x D score vectors
+    if constexpr (NH > 0) {
+        for (int i = threadIdx.x; i < NH * D; i += blockDim.x) u_s[i] = U[i];
+        __syncthreads();
+    }
+    const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    if (g >= n_groups) return;
+    const int k = int(g % K);
+    const int64_t bj = g / K;
+    const int j = int(bj % P);
+    const int64_t b = bj / P;
+    const int e0 = check_ptr[j];
+    const int c0 = lane * V;
+    float f[DEG][V];
+#pragma unroll
+    for (int i = 0; i < DEG; ++i) load_v<T, V>(Nn + ((b * E + e0 + i) * K + k) * D + c0, f[i]);
+    float sc[DEG];
+    if constexpr (NH > 0) {
+        const float scale = rsqrtf(float(D / NH));
+#pragma unroll
+        for (int i = 0; i < DEG; ++i) {
+            float p[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const float* uh = u_s + h * D + c0;
+                float a = 0.0f;
+#pragma unroll
+                for (int v = 0; v < V; ++v) a = fmaf(uh[v], f[i][v], a);
+                p[h] = a;
+            }
+            sc[i] = head_score<NH>(p, lane) * scale;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < DEG; ++i) {
+        float out[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) out[v] = 0.0f;
+        if constexpr (NH > 0) {
+            float mx = -INFINITY;
+#pragma unroll
+            for (int i2 = 0; i2 < DEG; ++i2)
+                if (i2 != i) mx = fmaxf(mx, sc[i2]);
+            float ex[DEG], den = 0.0f;
+#pragma unroll
+            for (int i2 = 0; i2 < DEG; ++i2) {
+                ex[i2] = i2 != i ? __expf(sc[i2] - mx) : 0.0f;
+                den += ex[i2];
+            }
+            const float fct = float(DEG - 1) / den;
+#pragma unroll
+            for (int i2 = 0; i2 < DEG; ++i2) {
+                if (i2 == i) continue;
+                const float w = ex[i2] * fct;
+#pragma unroll
+                for (int v = 0; v < V; ++v) out[v] = fmaf(w, f[i2][v], out[v]);
+            }
+        } else {
+#pragma unroll
+            for (int i2 = 0; i2 < DEG; ++i2) {
+                if (i2 == i) continue;
+#pragma unroll
+                for (int v = 0; v < V; ++v) out[v] += f[i2][v];
+            }
+        }
+        store_v<T, V>(pooled + ((b * E + e0 + i) * K + k) * D + c0, out);
+    }
+}
+
 // Pi_alpha gather, one edge row per warp, V = Q/32 symbols per lane.
 template <typename T, int V>
 __global__ void __launch_bounds__(256)
