@@ -413,18 +413,19 @@ void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, cons
     tc::mlp_tc_kernel<KIN, D><<<grid, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
 }
 
-template <int KIN, int D>
+template <int KIN, int D, int EPK>
 void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
                  const CUtensorMap& w2, const tc::MlpArgs& a) {
     using Lay = tc::Mlp2Layout<KIN, D>;
     static bool attr_set = false;
     if (!attr_set) {
-        ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+        ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D, EPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
         attr_set = true;
     }
-    const int pairs = std::min(a.tiles, c.sm_count / 2);
-    tc::mlp_tc2_kernel<KIN, D><<<2 * pairs, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
+    static const int cap = std::getenv("CIDER_MLP_PAIRS") ? std::atoi(std::getenv("CIDER_MLP_PAIRS")) : 0;
+    const int pairs = std::min(a.tiles, cap > 0 ? cap : c.sm_count / 2);
+    tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::MLP2_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
 }
 
 bool mlp_fusable(const cider_ctx& c, int Kin) {
@@ -446,7 +447,9 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     ep.M = int(M);
     ep.N = D;
     static const bool one_sm = std::getenv("CIDER_MLP_1SM") != nullptr;
-    const bool pair = !one_sm && Kin % 128 == 0 && (D == 128 || D == 256);
+    // 2-SM kernel variants: aggregator (Kin = D, plain store), gate / fusion (Kin = 2D, z (e) epilogue)
+    const bool pair = !one_sm && (D == 128 || D == 256) &&
+                      ((Kin == D && ep.kind == EP_STORE) || (Kin == 2 * D && (ep.kind == EP_GATE || ep.kind == EP_RESID)));
     Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
     const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;
@@ -472,8 +475,15 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
         a.trace = tbuf;
     }
     if (pair) {
-        if (D == 256) { if (Kin == 512) launch_mlp2<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp2<256, 256>(c, x0, x1, w1, w2, a); }
-        else { if (Kin == 256) launch_mlp2<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp2<128, 128>(c, x0, x1, w1, w2, a); }
+        if (D == 256) {
+            if (ep.kind == EP_GATE) launch_mlp2<512, 256, EP_GATE>(c, x0, x1, w1, w2, a);
+            else if (ep.kind == EP_RESID) launch_mlp2<512, 256, EP_RESID>(c, x0, x1, w1, w2, a);
+            else launch_mlp2<256, 256, EP_STORE>(c, x0, x1, w1, w2, a);
+        } else {
+            if (ep.kind == EP_GATE) launch_mlp2<256, 128, EP_GATE>(c, x0, x1, w1, w2, a);
+            else if (ep.kind == EP_RESID) launch_mlp2<256, 128, EP_RESID>(c, x0, x1, w1, w2, a);
+            else launch_mlp2<128, 128, EP_STORE>(c, x0, x1, w1, w2, a);
+        }
     } else if (D == 256) { if (Kin == 512) launch_mlp<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp<256, 256>(c, x0, x1, w1, w2, a); }
     else if (D == 128) { if (Kin == 256) launch_mlp<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp<128, 128>(c, x0, x1, w1, w2, a); }
     else { if (Kin == 128) launch_mlp<128, 64>(c, x0, x1, w1, w2, a); else launch_mlp<64, 64>(c, x0, x1, w1, w2, a); }
@@ -483,16 +493,22 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
         cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, c.stream);
         cudaStreamSynchronize(c.stream);
         const long long t0 = h[2];
-        std::fprintf(stderr, "[mlp trace %s M=%lld pair=%d] chunk: mma_wait_h  mma_got_h  mma_issued | epi_wait_a1  epi_got_a1  epi_done\n", tag, (long long)M, int(pair));
-        for (int ch = 0; ch < H / tc::MLP_HC; ++ch)
-            std::fprintf(stderr, "  %2d: %8lld %8lld %8lld | %8lld %8lld %8lld\n", ch, h[ch * 8] - t0, h[ch * 8 + 1] - t0, h[ch * 8 + 5] - t0,
-                         h[ch * 8 + 2] - t0, h[ch * 8 + 3] - t0, h[ch * 8 + 4] - t0);
-        std::fprintf(stderr, "  slot n: prod_wait_empty prod_tma_issued | mma_wait_full mma_got_full mma_issued | tma_latency(got-issued)\n");
-        for (int n = 0; n < 40; ++n)
-            if (h[512 + n * 4 + 1])
-                std::fprintf(stderr, "   %2d: %8lld %8lld | %8lld %8lld %8lld | %6lld\n", n, h[512 + n * 4] - t0, h[512 + n * 4 + 3] - t0,
-                             h[768 + n * 4] - t0, h[768 + n * 4 + 1] - t0, h[768 + n * 4 + 2] - t0,
-                             h[768 + n * 4 + 1] - h[512 + n * 4 + 3]);
+        std::fprintf(stderr, "[mlp trace %s M=%lld pair=%d] chunk: mma1_wait_free mma1_issued | mma2_wait_h mma2_got_h mma2_issued | epi_wait_a1 epi_got_a1 epi_done\n", tag, (long long)M, int(pair));
+        for (int it = 0; it < (pair ? 4 : 1); ++it)
+            for (int ch = 0; ch < H / tc::MLP_HC; ++ch) {
+                const long long* r = h + it * 64 + ch * 8;
+                std::fprintf(stderr, "  t%d c%d: %8lld %8lld | %8lld %8lld %8lld | %8lld %8lld %8lld\n", it, ch, r[6] - t0, r[7] - t0,
+                             r[0] - t0, r[1] - t0, r[5] - t0, r[2] - t0, r[3] - t0, r[4] - t0);
+            }
+        for (int it = 0; it < (pair ? 4 : 0); ++it) {
+            std::fprintf(stderr, "  t%d mma1 got_free:", it);
+            for (int ch = 0; ch < H / tc::MLP_HC; ++ch) std::fprintf(stderr, " %lld", h[896 + it * 8 + ch] - t0);
+            std::fprintf(stderr, "\n");
+            std::fprintf(stderr, "\n");
+        }
+        for (int it = 0; it < (pair ? 4 : 0); ++it)
+            std::fprintf(stderr, "  t%d final epilogue: wait %lld got %lld done %lld\n", it, h[512 + it * 4] - t0, h[512 + it * 4 + 1] - t0,
+                         h[512 + it * 4 + 2] - t0);
     }
 }
 

@@ -88,6 +88,46 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
+__device__ __forceinline__ void ld_global_v8(const void* p, uint32_t* r) { // 32 bytes, one sector
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t* r) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]),
+                 "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+// 64 consecutive accumulator columns of this warp's lane quarter, waited in the same statement
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+    uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+        "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+        "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+          "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+          "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+          "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+          "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void mma_commit_2sm_mask(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -106,9 +146,13 @@ struct Mlp2Layout {
     static constexpr int W1_PER_SLOT = SLOT / W1_HALF;       // 2
     static constexpr int X_BYTES = KB1 * 128 * 64 * 2;
     static constexpr int FIXED = 1024 + 512;
-    static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - X_BYTES) / SLOT;
+    // output staging for coalesced stores: one 32-row x 64-column bf16 block per epilogue warp (the
+    // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
+    static constexpr int STG_BYTES = KIN == D ? 8 * 4096 : 0;
+    static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - X_BYTES - STG_BYTES) / SLOT;
     static constexpr int NS = NS_RAW > 16 ? 16 : NS_RAW;
-    static constexpr int R_OFF = X_BYTES;
+    static constexpr int STG_OFF = X_BYTES;
+    static constexpr int R_OFF = X_BYTES + STG_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
     static constexpr int TOTAL = BAR_OFF + 512 + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
@@ -116,24 +160,32 @@ struct Mlp2Layout {
     static_assert(KB1 % W1_PER_SLOT == 0, "input width must be a multiple of 128");
 };
 
-template <int KIN, int D>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP_THREADS, 1)
+constexpr int MLP2_MMA2_WARP = 10;
+constexpr int MLP2_XLOAD_WARP = 11;
+constexpr int MLP2_THREADS = 384; // ring producer, MMA1 issuer, 8 epilogue warps (2-9), MMA2 issuer, X producer
+
+// EPK: final-epilogue kind (EP_STORE, EP_GATE or EP_RESID), a template parameter so each variant
+// carries only the registers its epilogue needs.
+template <int KIN, int D, int EPK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP2_THREADS, 1)
 mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2, const MlpArgs args) {
     using Lay = Mlp2Layout<KIN, D>;
     constexpr int KB1 = Lay::KB1, KB2 = Lay::KB2, NS = Lay::NS;
+    constexpr int KBD = D / 64; // output k-blocks = final-epilogue steps (half h takes k-blocks h, h+2, ...)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* xs = smem;
     uint8_t* ring = smem + Lay::R_OFF;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
-    uint64_t* x_full = bar;
-    uint64_t* x_empty = bar + 1;
-    uint64_t* r_full = bar + 2;
+    uint64_t* x_full = bar;             // [KB1] row-tile k-block landed (leader copy counts both CTAs)
+    uint64_t* x_empty = x_full + KB1;   // [KB1] k-block free: last MMA1 read it (+ final-epilogue readers)
+    uint64_t* r_full = x_empty + KB1;
     uint64_t* r_empty = r_full + NS;
     uint64_t* a1_full = r_empty + NS;   // [2] first-layer accumulator ready
     uint64_t* h_full = a1_full + 2;     // [2] bf16 hidden packed in TMEM (leader copy counts both CTAs)
-    uint64_t* a2_full = h_full + 2;
+    uint64_t* a1_free = h_full + 2;     // [2] MMA2 done reading acc1[b] (leader only)
+    uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
 
@@ -144,14 +196,15 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     const int NC = args.H / MLP_HC;
     constexpr int EPI_ARRIVALS = 2 * 8; // one elected lane per epilogue warp, both CTAs
 
-    // gate / fusion epilogues read z (and e) back from the resident row tile X, so X is released by
-    // the last MMA1's commit AND by the 8 epilogue warps once their final epilogue is done
-    const bool epi_reads_x = args.ep.kind == EP_GATE || args.ep.kind == EP_RESID;
+    // Gate / fusion epilogues read z (and e) from global memory (L2: the same rows were just TMA'd
+    // into X), so every X k-block is free once the tile's last MMA1 has read it and the next tile's
+    // rows stream in while this tile's final epilogue runs.
+    constexpr bool reads_z = EPK == EP_GATE || EPK == EP_RESID;
+    constexpr bool reads_e = EPK == EP_GATE;
     if (threadIdx.x == 0) {
-        mbar_init(x_full, 1);
-        mbar_init(x_empty, epi_reads_x ? 1 + 8 : 1);
+        for (int kb = 0; kb < KB1; ++kb) { mbar_init(&x_full[kb], 1); mbar_init(&x_empty[kb], 1); }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&a1_full[b], 1); mbar_init(&h_full[b], EPI_ARRIVALS); }
+        for (int b = 0; b < 2; ++b) { mbar_init(&a1_full[b], 1); mbar_init(&h_full[b], EPI_ARRIVALS); mbar_init(&a1_free[b], 1); }
         mbar_init(a2_full, 1);
         mbar_init(a2_empty, EPI_ARRIVALS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -164,35 +217,32 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     cluster_sync_all(); // barriers of both CTAs initialised before any remote signal
     fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t L_x_full = mapa_u32(smem_u32(x_full), 0);
+    const uint32_t L_x_full0 = mapa_u32(smem_u32(&x_full[0]), 0);
     const uint32_t L_r_full0 = mapa_u32(smem_u32(&r_full[0]), 0);
     const uint32_t L_h_full0 = mapa_u32(smem_u32(&h_full[0]), 0);
     const uint32_t L_a2_empty = mapa_u32(smem_u32(a2_empty), 0);
 
+    // Weight-ring sequence of one tile (the producer's order): W1(0), W1(1), then W2(c), W1(c+2) ...
+    // Both MMA issuers locate their loads in it by position, so one ring serves both.
+    constexpr int S1 = KB1 / Lay::W1_PER_SLOT, S2 = KB2;
+    const int per_tile = NC * (S1 + S2);
+    auto pos_w1 = [&](int c) { return c < 2 ? c * S1 : 2 * S1 + (c - 1) * S2 + (c - 2) * S1; };
+    auto pos_w2 = [&](int c) { return 2 * S1 + c * S2 + min(c, NC - 2) * S1; };
+
     if (warp == 0) {
-        if (lane == 0) {
+        if (lane == 0) { // weight ring producer
             int slot = 0;
-            uint32_t rph = 0, xph = 0;
+            uint32_t rph = 0;
             auto next = [&] { if (++slot == NS) { slot = 0; rph ^= 1; } };
-            int nload = 0;
-            const bool trp = args.trace && blockIdx.x == 0;
             auto acquire = [&](uint32_t bytes_both) {
-                if (trp && nload < 40) args.trace[512 + nload * 4 + 0] = clock64();
                 mbar_wait(&r_empty[slot], rph ^ 1);
-                if (trp && nload < 40) args.trace[512 + nload * 4 + 1] = clock64();
                 if (leader) mbar_expect_tx(&r_full[slot], bytes_both); // the leader arms its own barrier
-                if (trp && nload < 40) args.trace[512 + nload * 4 + 2] = clock64();
-            };
-            auto issued = [&] {
-                if (trp && nload < 40) args.trace[512 + nload * 4 + 3] = clock64();
-                ++nload;
             };
             auto load_w1 = [&](int c) { // tmW1 is 3-D: {64 cols, H rows, KIN/64 k-blocks}
                 for (int kb = 0; kb < KB1; kb += Lay::W1_PER_SLOT) {
                     acquire(2 * Lay::W1_PER_SLOT * Lay::W1_HALF);
                     tma_load_3d_2sm(ring + slot * Lay::SLOT, &tmW1, L_r_full0 + slot * 8, 0,
                                     c * MLP_HC + int(rank) * (MLP_HC / 2), kb);
-                    issued();
                     next();
                 }
             };
@@ -201,21 +251,10 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     acquire(2 * Lay::W2_HALF);
                     tma_load_2d_2sm(ring + slot * Lay::SLOT, &tmW2, L_r_full0 + slot * 8, c * MLP_HC + kb * 64,
                                     int(rank) * (D / 2));
-                    issued();
                     next();
                 }
             };
             for (int tile = pair; tile < args.tiles; tile += npairs) {
-                mbar_wait(x_empty, xph ^ 1);
-                xph ^= 1;
-                if (leader) mbar_expect_tx(x_full, 2 * Lay::X_BYTES);
-                const int row0 = tile * 256 + int(rank) * 128;
-                for (int kb = 0; kb < KB1; ++kb) {
-                    const int k = kb * 64;
-                    if (k < args.K0) tma_load_2d_2sm(xs + kb * 16384, &tmX0, L_x_full, k, row0);
-                    else tma_load_2d_2sm(xs + kb * 16384, &tmX1, L_x_full, k - args.K0, row0);
-                }
-                // consumption order of the MMA warp: W1(0), W1(1), then W2(c), W1(c+2) ...
                 load_w1(0);
                 if (NC > 1) load_w1(1);
                 for (int c = 0; c < NC; ++c) {
@@ -224,110 +263,133 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
             }
         }
-    } else if (warp == 1) {
-        if (leader && lane == 0) {
-            constexpr uint32_t id1 = idesc_bf16(256, MLP_HC);
-            constexpr uint32_t id2 = idesc_bf16(256, D);
-            int slot = 0;
-            uint32_t rph = 0, xph = 0, a2ph = 0;
-            uint32_t hph[2] = {0, 0};
-            int ncons = 0;
-            const bool trm = args.trace && blockIdx.x == 0;
-            auto next = [&] {
-                if (trm && ncons < 40) args.trace[768 + ncons * 4 + 2] = clock64(); // slot's MMAs issued
-                ++ncons;
-                if (++slot == NS) { slot = 0; rph ^= 1; }
-            };
-            auto wfull = [&] {
-                if (trm && ncons < 40) args.trace[768 + ncons * 4 + 0] = clock64();
-                mbar_wait(&r_full[slot], rph);
-                if (trm && ncons < 40) args.trace[768 + ncons * 4 + 1] = clock64();
-            };
-            auto mma1 = [&](int c) { // acc1[c&1] = X . W1(c)^T   (both operands in SMEM)
-                const uint32_t d = tmem + 256 + (c & 1) * MLP_HC;
-                for (int kb = 0; kb < KB1; kb += Lay::W1_PER_SLOT) {
-                    wfull();
-                    fence_after();
-                    for (int j = 0; j < Lay::W1_PER_SLOT; ++j) {
-                        const uint64_t da = sw128_desc(xs + (kb + j) * 16384);
-                        const uint64_t db = sw128_desc(ring + slot * Lay::SLOT + j * Lay::W1_HALF);
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id1, ((kb + j) | kk) != 0);
-                    }
-                    mma_commit_2sm(&r_empty[slot]);
-                    next();
-                }
-                mma_commit_2sm(&a1_full[c & 1]);
-            };
+    } else if (warp == MLP2_XLOAD_WARP) {
+        if (lane == 0) { // row-tile producer, one k-block at a time
+            uint32_t eph = 0;
             for (int tile = pair; tile < args.tiles; tile += npairs) {
-                mbar_wait(x_full, xph);
-                xph ^= 1;
-                fence_after();
-                mma1(0);
-                if (NC > 1) mma1(1);
-                if (NC <= 2) mma_commit_2sm(x_empty);
-                for (int c = 0; c < NC; ++c) {
-                    const int b = c & 1;
-                    const bool tr = args.trace && blockIdx.x == 0 && tile == pair;
-                    if (tr) args.trace[c * 8 + 0] = clock64();
-                    mbar_wait(&h_full[b], hph[b]); // GELU(c) packed into acc1[b]
-                    hph[b] ^= 1;
-                    fence_after();
-                    if (tr) args.trace[c * 8 + 1] = clock64();
-                    if (c == 0) {
-                        mbar_wait(a2_empty, a2ph ^ 1);
-                        a2ph ^= 1;
-                        fence_after();
-                    }
-                    // acc2 += H(c) . W2(c)^T with A = bf16 hidden in TMEM: k-steps 0-3 at cols
-                    // [0,32), 4-7 at [64,96) of the chunk's buffer (see the epilogue packing)
-                    const uint32_t a_base = tmem + 256 + b * MLP_HC;
-                    for (int kb = 0; kb < KB2; ++kb) {
-                            mbar_wait(&r_full[slot], rph);
-                        fence_after();
-                        const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            mma_bf16_2sm_ts(tmem, a_base + kb * 64 + kk * 8, db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
-                        mma_commit_2sm(&r_empty[slot]);
-                        next();
-                    }
-                    if (c + 2 < NC) { // in-order tensor pipe: MMA2(c) has read acc1[b] before this overwrites it
-                        mma1(c + 2);
-                        if (c + 2 == NC - 1) mma_commit_2sm(x_empty);
-                    }
-                    if (tr) args.trace[c * 8 + 5] = clock64();
+                const int row0 = tile * 256 + int(rank) * 128;
+                for (int kb = 0; kb < KB1; ++kb) {
+                    mbar_wait(&x_empty[kb], eph ^ 1);
+                    if (leader) mbar_expect_tx(&x_full[kb], 2 * 16384);
+                    const int k = kb * 64;
+                    if (k < args.K0) tma_load_2d_2sm(xs + kb * 16384, &tmX0, L_x_full0 + kb * 8, k, row0);
+                    else tma_load_2d_2sm(xs + kb * 16384, &tmX1, L_x_full0 + kb * 8, k - args.K0, row0);
                 }
-                mma_commit_2sm(a2_full);
+                eph ^= 1;
+            }
+        }
+    } else if (warp == 1 || warp == MLP2_MMA2_WARP) {
+        // Two MMA issuers on the leader: the tensor pipe queues only ~50 cycles of work, so every
+        // barrier wait of a single issuing thread is a pipe bubble (tools/mma_bench.cu issue2_kernel:
+        // 200-cycle waits per slot cost 22% with one issuer, 11% with two). Warp 1 issues the first
+        // layer (acc1 buffers), warp 10 the second (acc2); a1_free orders MMA2(n) before MMA1(n+2).
+        if (leader && lane == 0) {
+            auto ring_slot = [&](int gpos, uint32_t& ph) { ph = uint32_t(gpos / NS) & 1u; return gpos % NS; };
+            const bool tr = args.trace && blockIdx.x == 0;
+            if (warp == 1) {
+                constexpr uint32_t id1 = idesc_bf16(256, MLP_HC);
+                uint32_t xph = 0, fph = 0; // fph bit b: phase of a1_free[b]
+                int n = 0, it = 0;
+                for (int tile = pair; tile < args.tiles; tile += npairs, ++it) {
+                    for (int c = 0; c < NC; ++c, ++n) {
+                        const int b = n & 1;
+                        if (tr && it < 4) args.trace[it * 64 + c * 8 + 6] = clock64();
+                        mbar_wait(&a1_free[b], ((fph >> b) & 1u) ^ 1u); // MMA2 of the chunk two back has read acc1[b]
+                        fph ^= 1u << b;
+                        fence_after();
+                        if (tr && it < 4) args.trace[896 + it * 8 + c] = clock64();
+                        const uint32_t d = tmem + 256 + b * MLP_HC;
+                        for (int sg = 0; sg < S1; ++sg) {
+                            uint32_t ph;
+                            const int slot = ring_slot(it * per_tile + pos_w1(c) + sg, ph);
+                            if (c == 0) // the tile's k-blocks arrive one by one
+                                for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[sg * Lay::W1_PER_SLOT + j], xph);
+                            mbar_wait(&r_full[slot], ph);
+                            fence_after();
+#pragma unroll
+                            for (int j = 0; j < Lay::W1_PER_SLOT; ++j) {
+                                const int kb = sg * Lay::W1_PER_SLOT + j;
+                                const uint64_t da = sw128_desc(xs + kb * 16384);
+                                const uint64_t db = sw128_desc(ring + slot * Lay::SLOT + j * Lay::W1_HALF);
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)
+                                    mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id1, (kb | kk) != 0);
+                            }
+                            mma_commit_2sm(&r_empty[slot]);
+                        }
+                        mma_commit_2sm(&a1_full[b]);
+                        if (c == NC - 1)
+                            for (int kb = 0; kb < KB1; ++kb) mma_commit_2sm(&x_empty[kb]);
+                        if (tr && it < 4) args.trace[it * 64 + c * 8 + 7] = clock64();
+                    }
+                    xph ^= 1;
+                }
+            } else {
+                constexpr uint32_t id2 = idesc_bf16(256, D);
+                uint32_t hph = 0, a2ph = 0; // hph bit b: phase of h_full[b]
+                int n = 0, it = 0;
+                for (int tile = pair; tile < args.tiles; tile += npairs, ++it) {
+                    for (int c = 0; c < NC; ++c, ++n) {
+                        const int b = n & 1;
+                        if (tr && it < 4) args.trace[it * 64 + c * 8 + 0] = clock64();
+                        mbar_wait(&h_full[b], (hph >> b) & 1u); // GELU(n) packed into acc1[b]
+                        hph ^= 1u << b;
+                        fence_after();
+                        if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
+                        if (c == 0) {
+                            mbar_wait(a2_empty, a2ph ^ 1);
+                            a2ph ^= 1;
+                            fence_after();
+                        }
+                        // acc2 += H(c) . W2(c)^T with A = bf16 hidden in TMEM: k-steps 0-3 at cols
+                        // [0,32), 4-7 at [64,96) of the chunk's buffer (see the epilogue packing)
+                        const uint32_t a_base = tmem + 256 + b * MLP_HC;
+                        for (int kb = 0; kb < S2; ++kb) {
+                            uint32_t ph;
+                            const int slot = ring_slot(it * per_tile + pos_w2(c) + kb, ph);
+                            mbar_wait(&r_full[slot], ph);
+                            fence_after();
+                            const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                mma_bf16_2sm_ts(tmem, a_base + kb * 64 + kk * 8, db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
+                            mma_commit_2sm(&r_empty[slot]);
+                        }
+                        mma_commit_2sm_mask(&a1_free[b], 1);
+                        if (tr && it < 4) args.trace[it * 64 + c * 8 + 5] = clock64();
+                    }
+                    mma_commit_2sm(a2_full);
+                }
             }
         }
     } else {
         // 8 epilogue warps: TMEM lane quarter = warp % 4; the two warps of a quarter own the two
-        // 64-column halves of every chunk (and of the output).
+        // 64-column halves of every hidden chunk, and alternate 64-column k-blocks of the output.
         const int quarter = warp % 4;
         const int half = (warp - 2) / 4;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-        uint32_t e1ph[2] = {0, 0}, e2ph = 0;
+        uint32_t e1ph = 0, e2ph = 0; // e1ph bit b: phase of a1_full[b]
         const Epi& ep = args.ep;
         auto release = [&](uint32_t leader_bar) { // elected remote arrive once the whole warp is done
             __syncwarp();
             if (lane == 0) mbar_arrive_cl(leader_bar);
         };
+        int n = 0; // chunk counter across tiles: acc1 buffer = n & 1
         for (int tile = pair; tile < args.tiles; tile += npairs) {
-            for (int c = 0; c < NC; ++c) {
-                const int b = c & 1;
+            const int it = (tile - pair) / npairs;
+            for (int c = 0; c < NC; ++c, ++n) {
+                const int b = n & 1;
                 const float* b1 = args.b1 + c * MLP_HC + half * 64;
                 float4 bias4[16];
 #pragma unroll
                 for (int q = 0; q < 16; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + q);
-                const bool tr = args.trace && blockIdx.x == 0 && tile == pair && warp == 2 && lane == 0;
-                if (tr) args.trace[c * 8 + 2] = clock64();
-                mbar_wait(&a1_full[b], e1ph[b]);
-                e1ph[b] ^= 1;
+                const bool tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
+                if (tr) args.trace[it * 64 + c * 8 + 2] = clock64();
+                mbar_wait(&a1_full[b], (e1ph >> b) & 1u);
+                e1ph ^= 1u << b;
                 fence_after();
-                if (tr) args.trace[c * 8 + 3] = clock64();
+                if (tr) args.trace[it * 64 + c * 8 + 3] = clock64();
                 // fp32 columns [64 half, 64 half + 64) -> GELU -> bf16 pairs packed into the first 32
                 // of those columns (32 g .. ): every column is read before it is overwritten.
                 const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 64;
@@ -349,85 +411,110 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 fence_before();
                 release(L_h_full0 + b * 8);
-                if (tr) args.trace[c * 8 + 4] = clock64();
+                if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
-            // final epilogue straight from TMEM: this thread's row, this warp's half of D in
-            // 32-column groups; z (and e) come from the row tile X still resident in SMEM
-            // (SWIZZLE_128B K-major: 16-byte chunk c of row r sits at chunk c ^ (r & 7)).
+            // final epilogue straight from TMEM: this thread's row, output k-blocks half, half + 2, ...
+            // (64 columns per TMEM load). z / e rows come from global memory with 32-byte loads issued
+            // before the accumulator is read; gate / fusion results go out with 32-byte stores, the
+            // aggregator's through a per-warp staging block (coalesced whole-row stores).
             const int m = tile * 256 + int(rank) * 128 + row;
             const bool live = m < ep.M;
-            const int ncol = D / 2;
-            const int c0 = half * ncol;
-            auto xrow_chunk = [&](int col) -> uint4 { // 8 bf16 at columns [col, col+8) of this row of X
-                const int kb = col / 64, ch = (col % 64) / 8;
-                return *reinterpret_cast<const uint4*>(xs + kb * 16384 + row * 128 + ((ch ^ (row & 7)) * 16));
-            };
+            const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
+            if (trf) args.trace[512 + it * 4 + 0] = clock64();
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
             fence_after();
+            if (trf) args.trace[512 + it * 4 + 1] = clock64();
 #pragma unroll 1
-            for (int g = 0; g < ncol / 32; ++g) {
-                const int n0 = c0 + g * 32;
-                float v[32];
-                tmem_ld32(tmem + lane_off + n0, v);
-                if (g + 1 == ncol / 32) {
-                    fence_before();
-                    release(L_a2_empty); // accumulator drained: next tile's MMA2 may start
-                }
-                uint4 zq[4], eq[4];
-                if (epi_reads_x) {
+            for (int kb = half; kb < KBD; kb += 2) {
+                const int n0 = kb * 64;
+                uint32_t zr[reads_z ? 32 : 1], er[reads_e ? 32 : 1];
+                if (reads_z && (args.dbg & 2)) { // timing experiment: no z / e loads
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        zq[q] = xrow_chunk(n0 + q * 8);
-                        if (ep.kind == EP_GATE) eq[q] = xrow_chunk(D + n0 + q * 8);
+                    for (int q = 0; q < 32; ++q) { zr[q] = 0; if (reads_e) er[q] = 0; }
+                } else if (reads_z && live) {
+                    const bf16* zp = ep.zb + size_t(m) * ep.ldz + n0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) ld_global_v8(zp + q * 16, zr + q * 8);
+                    if (reads_e) {
+                        const bf16* eptr = ep.eb + size_t(m) * ep.ldz + n0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) ld_global_v8(eptr + q * 16, er + q * 8);
                     }
                 }
-                if (!live) continue;
+                uint32_t pkl[reads_z ? 1 : 32];
+                uint32_t* pk = reads_z ? zr : pkl; // results packed over the consumed z registers
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    const float4 bb = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + i)) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
-                }
-                if (epi_reads_x) {
-                    const bf16* zz = reinterpret_cast<const bf16*>(zq);
-                    const bf16* ee = reinterpret_cast<const bf16*>(eq);
+                for (int s2 = 0; s2 < 2; ++s2) { // two 32-column halves of the k-block
+                    float v[32];
+                    tmem_ld32(tmem + lane_off + n0 + s2 * 32, v);
+                    if (s2 == 1 && kb + 2 >= KBD) {
+                        fence_before();
+                        release(L_a2_empty); // accumulator drained: next tile's MMA2 may start
+                    }
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const float z = __bfloat162float(zz[i]);
-                        if (ep.kind == EP_GATE) {
-                            const float gt = sigmoid_f(v[i]);
-                            v[i] = gt * z + (1.0f - gt) * __bfloat162float(ee[i]);
-                        } else {
-                            v[i] += z;
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 bb = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + s2 * 32 + i))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                        v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const int w = s2 * 16 + i / 2; // packed-pair index within the k-block
+                        float a0 = v[i], a1 = v[i + 1];
+                        if (reads_z) {
+                            const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zr[w]));
+                            if (reads_e) {
+                                const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&er[w]));
+                                const float g0 = sigmoid_fast(a0), g1 = sigmoid_fast(a1);
+                                a0 = fmaf(g0, z2.x - e2.x, e2.x); // g z + (1 - g) e
+                                a1 = fmaf(g1, z2.y - e2.y, e2.y);
+                            } else {
+                                a0 += z2.x;
+                                a1 += z2.y;
+                            }
                         }
+                        if (ep.out_f && live) {
+                            v[i] = a0;
+                            v[i + 1] = a1;
+                        }
+                        __nv_bfloat162 p = __floats2bfloat162_rn(a0, a1);
+                        pk[w] = *reinterpret_cast<uint32_t*>(&p);
+                    }
+                    if (ep.out_f && live) {
+                        float* o = ep.out_f + size_t(m) * ep.ldo + n0 + s2 * 32;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                     }
                 }
-                if (ep.out_f) {
-                    float* o = ep.out_f + size_t(m) * ep.ldo + n0;
+                if (ep.out_t && !(args.dbg & 4)) {
+                    bf16* ot = reinterpret_cast<bf16*>(ep.out_t);
+                    if constexpr (Lay::STG_BYTES > 0) {
+                        // this row's 128 B into the warp's staging block (chunk j of row r at j ^ (r & 7)),
+                        // then the warp copies 4 whole rows (4 x 128 B) per store instruction
+                        uint8_t* stg = smem + Lay::STG_OFF + (warp - 2) * 4096;
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                }
-                if (ep.out_t) {
-                    bf16* o = reinterpret_cast<bf16*>(ep.out_t) + size_t(m) * ep.ldo + n0;
+                        for (int j = 0; j < 8; ++j)
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + lane * 128 + ((j ^ (lane & 7)) * 16))),
+                                         "r"(pk[4 * j]), "r"(pk[4 * j + 1]), "r"(pk[4 * j + 2]), "r"(pk[4 * j + 3])
+                                         : "memory");
+                        __syncwarp();
+                        const int j = lane & 7;
 #pragma unroll
-                    for (int i = 0; i < 32; i += 8) {
-                        __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-                        __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-                        __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
-                        __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-                        uint4 u;
-                        u.x = *reinterpret_cast<uint32_t*>(&p0);
-                        u.y = *reinterpret_cast<uint32_t*>(&p1);
-                        u.z = *reinterpret_cast<uint32_t*>(&p2);
-                        u.w = *reinterpret_cast<uint32_t*>(&p3);
-                        *reinterpret_cast<uint4*>(o + i) = u;
+                        for (int i = 0; i < 8; ++i) {
+                            const int r = i * 4 + lane / 8;
+                            const uint4 u = *reinterpret_cast<const uint4*>(stg + r * 128 + ((j ^ (r & 7)) * 16));
+                            const int mr = tile * 256 + int(rank) * 128 + quarter * 32 + r;
+                            if (mr < ep.M) *reinterpret_cast<uint4*>(ot + size_t(mr) * ep.ldo + n0 + j * 8) = u;
+                        }
+                        __syncwarp();
+                    } else if (live) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) st_global_v8(ot + size_t(m) * ep.ldo + n0 + q * 16, pk + q * 8);
                     }
                 }
             }
-            if (epi_reads_x) { // this warp no longer reads X: the producer may load the next tile
-                __syncwarp();
-                if (lane == 0) mbar_arrive(x_empty);
-            }
+            if (trf) args.trace[512 + it * 4 + 2] = clock64();
         }
     }
     fence_before();

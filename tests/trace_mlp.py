@@ -4,7 +4,7 @@ os.environ["CIDER_TRACE_MLP"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2605_26580_b200 as P
-cfg = P.configs()["c3"]
+cfg = P.configs()[os.environ.get("CFG", "c3")]
 wl, m = cfg.workload, cfg.model
 m = P.Model(m=m.m, dim=m.dim, hidden=m.hidden, layers=1, heads=m.heads, precision=m.precision)
 e = wl.code()

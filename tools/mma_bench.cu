@@ -125,13 +125,20 @@ __global__ void __launch_bounds__(320, 1) bench_kernel(int iters, unsigned long 
 
 // The MLP issue pattern: per chunk 2 "W1 slots" of 8 SS MMAs (N=128 -> acc1[c&1]) and 2 "W2 slots"
 // of 4 TS MMAs (N=256 -> acc2), each slot followed by a commit; COMMIT=0 drops the per-slot commits.
-template <int CG, int COMMIT, int WAITS = 0>
+template <int CG, int COMMIT, int WAITS = 0, int RANDOM = 0>
 __global__ void __launch_bounds__(128, 1) pattern_kernel(int chunks, unsigned long long* out) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 131072);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 8);
-    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) {
+        uint32_t h = uint32_t(i) * 2654435761u ^ (blockIdx.x * 40503u);
+        h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+        // random sign / mantissa, exponent in [2^-3, 2^0]: bf16 = s eeeeeeee mmmmmmm
+        const uint32_t lo = (h & 0x807fu) | ((0x7cu + ((h >> 7) & 3u)) << 7);
+        const uint32_t hi = ((h >> 16) & 0x807fu) | ((0x7cu + ((h >> 23) & 3u)) << 7);
+        reinterpret_cast<uint32_t*>(smem)[i] = RANDOM ? (lo | (hi << 16)) : 0x3c003c00u;
+    }
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     if (threadIdx.x == 0) { for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -188,14 +195,13 @@ __global__ void __launch_bounds__(128, 1) pattern_kernel(int chunks, unsigned lo
     }
 }
 
-template <int CG, int COMMIT, int WAITS = 0>
-void run_pattern(int sms, const char* label) {
+template <int CG, int COMMIT, int WAITS = 0, int RANDOM = 0>
+void run_pattern(int sms, const char* label, int chunks = 400) {
     unsigned long long* d;
     cudaMalloc(&d, 16);
     const int smem = 131072 + 1024 + 128;
-    auto k = pattern_kernel<CG, COMMIT, WAITS>;
+    auto k = pattern_kernel<CG, COMMIT, WAITS, RANDOM>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int chunks = 400;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(sms);
     cfg.blockDim = dim3(128);
@@ -211,6 +217,87 @@ void run_pattern(int sms, const char* label) {
     const double ideal = chunks * 2048.0 * (CG == 2 ? 1.0 : 2.0); // 2-SM: 2048 clk/chunk; 1-SM: double the MMA cycles
     printf("%-40s cg=%d commit=%d: %.0f cyc/chunk (ideal %.0f) -> %.0f%%  %s\n", label, CG, COMMIT, double(cyc) / chunks,
            ideal / chunks, 100.0 * ideal / double(cyc), err == cudaSuccess ? "" : cudaGetErrorString(err));
+    cudaFree(d);
+}
+
+
+// Two issuers: thread 0 issues the W1 slots (SS N=128 -> acc1), thread 32 the W2 slots (TS N=256 ->
+// acc2); each stalls STALL cycles (spin on clock64) before every slot, as a try_wait would.
+template <int ISSUERS, int STALL>
+__global__ void __launch_bounds__(128, 1) issue2_kernel(int chunks, unsigned long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 131072);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 16);
+    for (int i = threadIdx.x; i < 131072 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+    const int warp = threadIdx.x / 32;
+    const uint32_t rank = cluster_rank();
+    if (threadIdx.x == 0) { for (int i = 0; i < 16; ++i) mbar_init(&bar[i], 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (warp == 0) { asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot))); asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;"); }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    fence_before();
+    cluster_sync_all();
+    fence_after();
+    const uint32_t tmem = *slot;
+    auto stall = [] { if (STALL) { const long long t = clock64(); while (clock64() - t < STALL) {} } };
+    const uint32_t id1 = idesc_bf16(256, 128), id2 = idesc_bf16(256, 256);
+    auto w1 = [&](int c, int w) {
+        const uint64_t da = sw128_desc(smem + ((c + w) % 4) * 16384), db = sw128_desc(smem + 65536 + ((c + w) % 4) * 16384);
+        for (int j = 0; j < 2; ++j)
+            for (int kk = 0; kk < 4; ++kk) mma_bf16_2sm(tmem + 256 + (c & 1) * 128, da + j * 512 + kk * 2, db + j * 512 + kk * 2, id1, 1);
+    };
+    auto w2 = [&](int c, int w) {
+        const uint64_t db = sw128_desc(smem + 65536 + ((c + w) % 4) * 16384);
+        for (int kk = 0; kk < 4; ++kk) mma_bf16_2sm_ts(tmem, tmem + 256 + ((c + 1) & 1) * 128 + w * 64 + kk * 8, db + kk * 2, id2, 1);
+    };
+    if (rank == 0 && (threadIdx.x == 0 || (ISSUERS == 2 && threadIdx.x == 32))) {
+        const bool first = threadIdx.x == 0;
+        long long t0 = clock64();
+        int s = first ? 0 : 8;
+        for (int c = 0; c < chunks; ++c) {
+            if (ISSUERS == 1 || first)
+                for (int w = 0; w < 2; ++w) { stall(); w1(c, w); mma_commit_2sm(&bar[s % 6]); ++s; }
+            if (ISSUERS == 1 || !first)
+                for (int w = 0; w < 2; ++w) { stall(); w2(c, w); mma_commit_2sm(&bar[(ISSUERS == 1 ? 0 : 8) + s % 6]); ++s; }
+        }
+        uint64_t* fin = &bar[first ? 7 : 15];
+        mma_commit_2sm(fin);
+        mbar_wait(fin, 0);
+        long long t1 = clock64();
+        if (blockIdx.x == 0) out[first ? 0 : 1] = (unsigned long long)(t1 - t0);
+    }
+    fence_before();
+    cluster_sync_all();
+    if (warp == 0) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <int ISSUERS, int STALL>
+void run_issue2(int sms, const char* label) {
+    unsigned long long* d;
+    cudaMalloc(&d, 16);
+    cudaMemset(d, 0, 16);
+    const int smem = 131072 + 1024 + 256;
+    auto k = issue2_kernel<ISSUERS, STALL>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int chunks = 2000;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, chunks, d);
+    cudaError_t err = cudaDeviceSynchronize();
+    unsigned long long cyc[2] = {0, 0};
+    cudaMemcpy(cyc, d, 16, cudaMemcpyDeviceToHost);
+    const unsigned long long c = cyc[0] > cyc[1] ? cyc[0] : cyc[1];
+    printf("%-44s: %.0f cyc/chunk (ideal 2048) -> %.0f%%  %s\n", label, double(c) / chunks, 100.0 * 2048.0 * chunks / double(c),
+           err == cudaSuccess ? "" : cudaGetErrorString(err));
     cudaFree(d);
 }
 
@@ -267,8 +354,12 @@ int main() {
     reinterpret_cast<EncodeFn>(p)(&h_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, mat, dims, strides, box, es,
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    run_pattern<2, 1>(sms, "MLP pattern (W1 SS N=128, W2 TS N=256)");
-    run_pattern<2, 0>(sms, "MLP pattern, no per-slot commits");
-    run_pattern<2, 1, 1>(sms, "MLP pattern + try_wait/fence per slot");
+    run<128, 2, false, 0, 2>(sms, "SS N=128 2-SM quiet");
+    run<128, 2, false, 2, 2>(sms, "SS N=128 2-SM + SMEM ld/st noise");
+    run<128, 2, false, 4, 2>(sms, "SS N=128 2-SM + TMA stream");
+    run<128, 2, false, 3, 2>(sms, "SS N=128 2-SM + TMEM ld/st noise");
+    run<256, 2, false, 2, 2>(sms, "SS N=256 2-SM + SMEM ld/st noise");
+    run<256, 2, false, 4, 2>(sms, "SS N=256 2-SM + TMA stream");
+    run<256, 2, true, 2, 2>(sms, "TS N=256 2-SM + SMEM ld/st noise");
     return 0;
 }
