@@ -36,6 +36,17 @@ __device__ __forceinline__ float gelu_fast(float x) {
     const float hx = 0.5f * x;
     return fmaf(hx, tanh_approx(inner), hx);
 }
+// Two lanes at once with the sm_100 packed fp32 ops (FFMA2/FMUL2/FADD2): same arithmetic as
+// gelu_fast(x + b) per element, half the FP32 instructions.
+__device__ __forceinline__ uint32_t gelu2_bias_bf16(float x0, float x1, float b0, float b1) {
+    const float2 x = __fadd2_rn(make_float2(x0, x1), make_float2(b0, b1));
+    const float2 p = __ffma2_rn(__fmul2_rn(x, x), make_float2(0.0356774081f, 0.0356774081f), make_float2(0.7978845608f, 0.7978845608f));
+    const float2 in = __fmul2_rn(x, p);
+    const float2 hx = __fmul2_rn(x, make_float2(0.5f, 0.5f));
+    const float2 y = __ffma2_rn(hx, make_float2(tanh_approx(in.x), tanh_approx(in.y)), hx);
+    __nv_bfloat162 r = __floats2bfloat162_rn(y.x, y.y);
+    return *reinterpret_cast<uint32_t*>(&r);
+}
 
 constexpr int MLP_HC = 128;
 constexpr int MLP_THREADS = 320; // producer, MMA, 8 epilogue warps (two per TMEM lane quarter)

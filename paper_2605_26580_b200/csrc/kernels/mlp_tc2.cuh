@@ -183,8 +183,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint64_t* r_full = x_empty + KB1;
     uint64_t* r_empty = r_full + NS;
     uint64_t* a1_full = r_empty + NS;   // [2] first-layer accumulator ready
-    uint64_t* h_full = a1_full + 2;     // [2] bf16 hidden packed in TMEM (leader copy counts both CTAs)
-    uint64_t* a1_free = h_full + 2;     // [2] MMA2 done reading acc1[b] (leader only)
+    uint64_t* h_full = a1_full + 2;     // [2][2] GELU group g of acc1[b] packed (leader copy counts both CTAs)
+    uint64_t* a1_free = h_full + 4;     // [2] MMA2 done reading acc1[b] (leader only)
     uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
@@ -204,7 +204,12 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     if (threadIdx.x == 0) {
         for (int kb = 0; kb < KB1; ++kb) { mbar_init(&x_full[kb], 1); mbar_init(&x_empty[kb], 1); }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mbar_init(&a1_full[b], 1); mbar_init(&h_full[b], EPI_ARRIVALS); mbar_init(&a1_free[b], 1); }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&a1_full[b], 1);
+            mbar_init(&h_full[2 * b], EPI_ARRIVALS);
+            mbar_init(&h_full[2 * b + 1], EPI_ARRIVALS);
+            mbar_init(&a1_free[b], 1);
+        }
         mbar_init(a2_full, 1);
         mbar_init(a2_empty, EPI_ARRIVALS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -332,29 +337,39 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     for (int c = 0; c < NC; ++c, ++n) {
                         const int b = n & 1;
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 0] = clock64();
-                        mbar_wait(&h_full[b], (hph >> b) & 1u); // GELU(n) packed into acc1[b]
-                        hph ^= 1u << b;
-                        fence_after();
-                        if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
-                        if (c == 0) {
-                            mbar_wait(a2_empty, a2ph ^ 1);
-                            a2ph ^= 1;
-                            fence_after();
-                        }
-                        // acc2 += H(c) . W2(c)^T with A = bf16 hidden in TMEM: k-steps 0-3 at cols
-                        // [0,32), 4-7 at [64,96) of the chunk's buffer (see the epilogue packing)
+                        // acc2 += H(c) . W2(c)^T with A = bf16 hidden in TMEM. Hidden columns [64 kb + 32 g,
+                        // +32) are GELU group g of warp-half kb, packed at TMEM cols 64 kb + 16 g: k-steps
+                        // 2g, 2g+1 of W2 slot kb. Group 0 of both halves is issued as soon as it lands.
                         const uint32_t a_base = tmem + 256 + b * MLP_HC;
-                        for (int kb = 0; kb < S2; ++kb) {
-                            uint32_t ph;
-                            const int slot = ring_slot(it * per_tile + pos_w2(c) + kb, ph);
-                            mbar_wait(&r_full[slot], ph);
-                            fence_after();
-                            const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
+                        int slots[S2];
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                mma_bf16_2sm_ts(tmem, a_base + kb * 64 + kk * 8, db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
-                            mma_commit_2sm(&r_empty[slot]);
+                        for (int g = 0; g < 2; ++g) {
+                            mbar_wait(&h_full[2 * b + g], (hph >> b) & 1u);
+                            fence_after();
+                            if (g == 0) {
+                                if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
+                                if (c == 0) {
+                                    mbar_wait(a2_empty, a2ph ^ 1);
+                                    a2ph ^= 1;
+                                    fence_after();
+                                }
+                            }
+#pragma unroll
+                            for (int kb = 0; kb < S2; ++kb) {
+                                if (g == 0) {
+                                    uint32_t ph;
+                                    slots[kb] = ring_slot(it * per_tile + pos_w2(c) + kb, ph);
+                                    mbar_wait(&r_full[slots[kb]], ph);
+                                    fence_after();
+                                }
+                                const uint64_t db = sw128_desc(ring + slots[kb] * Lay::SLOT);
+#pragma unroll
+                                for (int kk = 2 * g; kk < 2 * g + 2; ++kk)
+                                    mma_bf16_2sm_ts(tmem, a_base + kb * 64 + kk * 8, db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
+                                if (g == 1) mma_commit_2sm(&r_empty[slots[kb]]);
+                            }
                         }
+                        hph ^= 1u << b;
                         mma_commit_2sm_mask(&a1_free[b], 1);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 5] = clock64();
                     }
@@ -401,16 +416,19 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {
                         const float4 bb = bias4[g * 8 + i / 4];
-                        __nv_bfloat162 p0 = __floats2bfloat162_rn(gelu_fast(v[i] + bb.x), gelu_fast(v[i + 1] + bb.y));
-                        __nv_bfloat162 p1 = __floats2bfloat162_rn(gelu_fast(v[i + 2] + bb.z), gelu_fast(v[i + 3] + bb.w));
-                        pk[i / 2] = *reinterpret_cast<uint32_t*>(&p0);
-                        pk[i / 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
+                        pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
+                        pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
                     }
                     tmem_st16(base + g * 16, pk);
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    fence_before();
+                    release(L_h_full0 + (2 * b + g) * 8); // group g of both halves -> MMA2 k-steps 2g, 2g+1
                 }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                fence_before();
-                release(L_h_full0 + b * 8);
+                if (args.dbg & 1) { // timing experiment (GELU skipped): still release both groups
+                    fence_before();
+                    release(L_h_full0 + (2 * b) * 8);
+                    release(L_h_full0 + (2 * b + 1) * 8);
+                }
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
             // final epilogue straight from TMEM: this thread's row, output k-blocks half, half + 2, ...
