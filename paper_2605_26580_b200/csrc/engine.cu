@@ -161,6 +161,8 @@ struct LayerW {
     void *g1, *g2, *a1, *a2, *f1, *f2, *ak;
     float *gb1, *gb2, *ab1, *ab2, *fb1, *fb2, *aq;
     float* au; // heads x D: u_h = Wk_h^T q_h, the attention score vectors
+    void* aus; // BF16 mode, heads <= 16: 64 x D bf16 score matrix, rows h = hi(u_h / sqrt(D/heads)),
+               // rows 16 + h = the bf16 remainder (lo), zero elsewhere: scores = N . aus^T (EP_SCORES)
 };
 
 struct Stat {
@@ -341,17 +343,17 @@ const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, 
     return c.maps.emplace(key, make_map(p, rows, cols, ld, box_rows)).first->second;
 }
 
-template <int BN>
+template <int BN, int EPW = 4>
 void launch_tc(cider_ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const tc::Args& args) {
-    using Lay = tc::SmemLayout<BN>;
+    using Lay = tc::SmemLayout<BN, EPW>;
     static bool attr_set = false; // per process; same attribute for every device
     if (!attr_set) {
-        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
         attr_set = true;
     }
     int grid = std::min(args.tiles, c.sm_count);
-    tc::gemm_tc_kernel<BN><<<grid, tc::NUM_THREADS, Lay::TOTAL, c.stream>>>(a0, a1, b, args);
+    tc::gemm_tc_kernel<BN, EPW><<<grid, 64 + 32 * EPW, Lay::TOTAL, c.stream>>>(a0, a1, b, args);
 }
 
 // C[M x N] = [A0 (M x K0) | A1 (M x K1)] . B[N x (K0+K1)]^T, then the epilogue.
@@ -383,7 +385,14 @@ void gemm(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1,
     args.tiles_n = N / BN;
     args.tiles = int((M + tc::BM - 1) / tc::BM) * args.tiles_n;
     args.ep = ep;
-    if (BN == 256) launch_tc<256>(c, a0, a1, b, args);
+    static const int epw_demix = std::getenv("CIDER_EPW_DEMIX") ? std::atoi(std::getenv("CIDER_EPW_DEMIX")) : 16;
+    static const int epw_store = std::getenv("CIDER_EPW_STORE") ? std::atoi(std::getenv("CIDER_EPW_STORE")) : 4;
+    static const int epw_scores = std::getenv("CIDER_EPW_SCORES") ? std::atoi(std::getenv("CIDER_EPW_SCORES")) : 4;
+    const int epw = ep.kind == EP_DEMIX ? epw_demix : ep.kind == EP_STORE ? epw_store : ep.kind == EP_SCORES ? epw_scores : 4;
+    if (BN == 256 && epw == 16) launch_tc<256, 16>(c, a0, a1, b, args);
+    else if (BN == 256 && epw == 8) launch_tc<256, 8>(c, a0, a1, b, args);
+    else if (BN == 64 && epw == 8) launch_tc<64, 8>(c, a0, a1, b, args);
+    else if (BN == 256) launch_tc<256>(c, a0, a1, b, args);
     else if (BN == 128) launch_tc<128>(c, a0, a1, b, args);
     else launch_tc<64>(c, a0, a1, b, args);
     check_launch(tag);
@@ -671,6 +680,23 @@ void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* poo
     else run_pool_v<T, 2>(c, lw, Nn, K, groups, pooled);
 }
 
+// BF16, check-regular degree 6, D = 256, 1..16 heads dividing 32 lanes: scores from EP_SCORES
+bool pool_scored(const cider_ctx& c, const LayerW& lw) {
+    return c.bf16 && lw.aus && c.D == 256 && c.max_check_deg == 6 && c.min_check_deg == 6 && 32 % c.heads == 0 &&
+           !std::getenv("CIDER_NO_SCORE_GEMM");
+}
+void run_pool_scored(cider_ctx& c, const bf16* Nn, const float* sc, int nb, int K, bf16* pooled) {
+    const int64_t groups = int64_t(nb) * c.P * K;
+    const unsigned g = blocks_for(groups * 32);
+    switch (c.heads) {
+        case 1: pool_warp_scored_kernel<bf16, 8, 1, 6><<<g, 256, 0, c.stream>>>(Nn, sc, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 2: pool_warp_scored_kernel<bf16, 8, 2, 6><<<g, 256, 0, c.stream>>>(Nn, sc, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 4: pool_warp_scored_kernel<bf16, 8, 4, 6><<<g, 256, 0, c.stream>>>(Nn, sc, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        case 8: pool_warp_scored_kernel<bf16, 8, 8, 6><<<g, 256, 0, c.stream>>>(Nn, sc, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+        default: pool_warp_scored_kernel<bf16, 8, 16, 6><<<g, 256, 0, c.stream>>>(Nn, sc, c.check_ptr, c.P, c.E, K, c.D, groups, pooled); break;
+    }
+}
+
 // ---- grouped GEMMs of the Q >= D path ----------------------------------------------------------
 void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, int nb, int K, int groups,
               const int* cnt, const int* arow, const int* alpha, int max_seg, const int* out_row, int out_rows_per_bin,
@@ -698,7 +724,7 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, rows * D * 2.0 * (mean_seg + 1));
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
     CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
-    using Lay = tc::SmemLayout<256>;
+    using Lay = tc::SmemLayout<256, 0>;
     static bool attr_set = false;
     if (!attr_set) {
         ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
@@ -730,7 +756,15 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
     for (int li = 0; li < c.N; ++li) {
         const LayerW& lw = c.lw[li];
         // Module A (denoiser.cpp:141-160)
-        Epi e = epi(EP_LBAR);
+        Epi e;
+        if (c.bf16 && 32 % K == 0 && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
+            // intermediate logits and demixing in one kernel: Lambda-bar never leaves the chip
+            e = epi(EP_DEMIX);
+            e.out_t = w.Aq; e.ldo = Q; e.S = S; e.L = L; e.K = K; e.beta = float(c.md.evidence_scale);
+            e.inv_tau = 1.0f / float(c.md.tau_demix); // as demix_block_kernel computes it
+            gemm(c, "gemm_demix", w.Zt, D, nullptr, 0, c.W, Ms, Q, e);
+        } else {
+        e = epi(EP_LBAR);
         e.out_f = w.lbar; e.ldo = Q; e.S = S; e.L = L; e.K = K; e.beta = float(c.md.evidence_scale);
         gemm(c, "gemm_lbar", w.Zt, D, nullptr, 0, c.W, Ms, Q, e);
         {
@@ -738,6 +772,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             if (c.bf16) run_demix<bf16>(c, w.lbar, S, int64_t(nb) * L, K, (bf16*)w.Aq);
             else run_demix<float>(c, w.lbar, S, int64_t(nb) * L, K, (float*)w.Aq);
             check_launch("demix");
+        }
         }
         e = epi(EP_STORE);
         e.out_f = w.ef; e.out_t = c.bf16 ? w.et : nullptr; e.ldo = D; // (ef is null in BF16 mode)
@@ -765,7 +800,16 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             e.out_t = w.Nn; e.ldo = D;
             gemm(c, "gemm_backproj", w.Ae, Q, nullptr, 0, c.Wt, Me, D, e);
         }
-        if (pool_fast(c)) {
+        if (pool_scored(c, lw)) {
+            // head scores on the tensor cores, then a streaming leave-one-out softmax pool
+            float* sc = (float*)wsbuf(c, "scores", size_t(round_up(size_t(Me), 128)) * c.heads * 4);
+            e = epi(EP_SCORES);
+            e.out_f = sc; e.ldo = c.heads; e.K = c.heads;
+            gemm(c, "gemm_scores", w.Nn, D, nullptr, 0, lw.aus, Me, 64, e);
+            Launch lg(c, "pool_attn", 2.0 * double(Me) * D * c.max_check_deg, double(Me) * D * 2 * c.act_size);
+            run_pool_scored(c, (const bf16*)w.Nn, sc, nb, K, (bf16*)w.pooled);
+            check_launch("pool");
+        } else if (pool_fast(c)) {
             Launch lg(c, c.heads ? "pool_attn" : "pool_sum", 2.0 * double(Me) * D * (c.heads + c.max_check_deg),
                       double(Me) * D * 2 * c.act_size);
             if (c.bf16) run_pool<bf16>(c, lw, (const bf16*)w.Nn, nb, K, (bf16*)w.pooled);
@@ -1072,6 +1116,7 @@ void upload_model(cider_ctx& c, const float* w) {
         L.ak = nullptr;
         L.aq = nullptr;
         L.au = nullptr;
+        L.aus = nullptr;
     }
     if (c.heads)
         for (int l = 0; l < c.N; ++l) {
@@ -1092,6 +1137,21 @@ void upload_model(cider_ctx& c, const float* w) {
             DevBuf& b = wbuf(c, u.size() * 4);
             ck(cudaMemcpy(b.p, u.data(), u.size() * 4, cudaMemcpyHostToDevice), "upload");
             c.lw[l].au = b.as<float>();
+            if (c.bf16 && c.heads <= 16) {
+                // hi + lo bf16 split: the score GEMM recovers u . n to ~2^-16 relative (fp32-grade)
+                const float scale = 1.0f / std::sqrt(float(dh));
+                std::vector<bf16> m(size_t(64) * D, __float2bfloat16_rn(0.0f));
+                for (int h = 0; h < c.heads; ++h)
+                    for (int col = 0; col < D; ++col) {
+                        const float x = u[size_t(h) * D + col] * scale;
+                        const bf16 hi = __float2bfloat16_rn(x);
+                        m[size_t(h) * D + col] = hi;
+                        m[size_t(16 + h) * D + col] = __float2bfloat16_rn(x - __bfloat162float(hi));
+                    }
+                DevBuf& bs = wbuf(c, m.size() * 2);
+                ck(cudaMemcpy(bs.p, m.data(), m.size() * 2, cudaMemcpyHostToDevice), "upload");
+                c.lw[l].aus = bs.p;
+            }
         }
 }
 

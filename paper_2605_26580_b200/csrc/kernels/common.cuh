@@ -31,6 +31,9 @@ enum EpKind : int {
     EP_RESID = 3,  // out = z + acc + bias                                (Module B fusion, denoiser.cpp:224)
     EP_LBAR = 4,   // out = acc + beta * S[bin, slot, n]                  (intermediate logits, denoiser.cpp:96)
     EP_LOGITS = 5, // row statistics of final logits: kappa(tau), argmax  (refine.cpp:61-78); optional f32 logits
+    EP_SCORES = 6, // attention head scores: out[m][h] = acc[h] + acc[16 + h], h < K (hi + lo bf16 split of u_h)
+    EP_DEMIX = 7,  // Module A demix fused on the intermediate logits x = acc + beta S: per (bin, slot) group of K
+                   // rows, out = softmax_k(x / tau) * S, normaliser in 2^-26 fixed point (= demix_block_kernel)
 };
 
 // Everything an epilogue may need. Pointers the kind does not use are ignored.

@@ -48,7 +48,7 @@ constexpr int GRP_THREADS = 320; // producer, MMA, 8 epilogue warps (two per TME
 __global__ void __launch_bounds__(GRP_THREADS, 1)
 gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
     constexpr int BN = 256;
-    using Lay = SmemLayout<BN>;
+    using Lay = SmemLayout<BN, 0>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);

@@ -110,18 +110,36 @@ struct Args {
     Epi ep;
 };
 
-template <int BN>
+// EPW epilogue warps (0 = layout without the EP_DEMIX staging, for gemm_grp.cuh); kernels with more
+// than 4 epilogue warps use a 2-stage ring to make room for the per-warp staging blocks.
+template <int BN, int EPW = 4>
 struct SmemLayout {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    // ring depth: as deep as ~192 KB allows (narrow-N GEMMs are A-stream bound), 2 with > 4 epilogue warps
+    static constexpr int NST_FIT = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
+    static constexpr int NST = EPW > 4 ? 2 : EPW == 0 ? STAGES : NST_FIT;
+    // EP_DEMIX transpose staging per epilogue warp: [32][33] fp32 (padded: conflict-free rows and
+    // columns) + [32][32] bf16 results
+    static constexpr int STG_WARP = 32 * 33 * 4 + 32 * 32 * 2;
+    static constexpr int STG_OFF = NST * STAGE_BYTES;
+    static constexpr int BAR_OFF = STG_OFF + EPW * STG_WARP;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024; // barriers + 1 KB alignment slack
     static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+    static_assert(TOTAL <= 232448, "gemm_tc shared memory");
 };
 
 // 32 consecutive output columns of one row through the shared epilogue, vectorised.
 __device__ __forceinline__ void epi_row32(const Epi& ep, int m, int n0, float* v) {
+    if (ep.kind == EP_SCORES) { // columns [0,16) hold hi(u_h).n, [16,32) lo(u_h).n; the rest is padding
+        if (n0 == 0) {
+#pragma unroll
+            for (int h = 0; h < 16; ++h) // static indices: v stays in registers
+                if (h < ep.K) ep.out_f[size_t(m) * ep.ldo + h] = v[h] + v[16 + h];
+        }
+        return;
+    }
     if (ep.bias) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
@@ -197,16 +215,46 @@ __device__ __forceinline__ void epi_row32(const Epi& ep, int m, int n0, float* v
     }
 }
 
-template <int BN>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// EP_DEMIX column pass: lane = column n0 + lane, the warp's 32 rows in groups of KK (= one
+// (bin, slot) row each); arithmetic identical to demix_block_kernel (path.cuh).
+template <int KK>
+__device__ __forceinline__ void demix_cols(const float* xs, bf16* os, const Epi& ep, int m0, int n0, int lane, float scale2) {
+#pragma unroll
+    for (int g0 = 0; g0 < 32; g0 += KK) {
+        if (m0 + g0 >= ep.M) break;
+        float xv[KK];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < KK; ++k) { xv[k] = xs[(g0 + k) * 33 + lane]; mx = fmaxf(mx, xv[k]); }
+        uint32_t den = 0;
+#pragma unroll
+        for (int k = 0; k < KK; ++k) {
+            const float e = exp2f((xv[k] - mx) * scale2);
+            xv[k] = e;
+            den += __float2uint_rn(e * 67108864.0f); // 2^26
+        }
+        const float rden = 1.0f / (float(den) * (1.0f / 67108864.0f));
+        const float sv = __ldg(ep.S + size_t((m0 + g0) / KK) * ep.N + n0 + lane);
+#pragma unroll
+        for (int k = 0; k < KK; ++k) os[(g0 + k) * 32 + lane] = __float2bfloat16_rn((xv[k] * rden) * sv);
+    }
+}
+
+// EPW epilogue warps: 4 = one per TMEM lane quarter (row statistics need whole rows); 16 = four
+// per quarter splitting the columns (EP_DEMIX, whose per-element work would otherwise leave one warp
+// per scheduler latency-bound).
+template <int BN, int EPW>
+__global__ void __launch_bounds__(64 + 32 * EPW, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                const __grid_constant__ CUtensorMap tmB, const Args args) {
-    using Lay = SmemLayout<BN>;
+    using Lay = SmemLayout<BN, EPW>;
+    constexpr int NST = Lay::NST;
+    constexpr int CSTEP = (EPW / 4) * 32; // column stride of one warp's 32-column chunks
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -214,8 +262,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     const int kblocks = args.K / BK;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+        for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * EPW); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA1)) : "memory");
@@ -248,7 +296,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                     else
                         tma_load_2d(sa, &tmA1, &full[stage], k - args.K0, mb * BM);
                     tma_load_2d(sb, &tmB, &full[stage], k, nb * BN);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -271,7 +319,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                     for (int kk = 0; kk < BK / 16; ++kk)
                         mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
                     mma_commit(&empty[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -280,6 +328,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     } else {
         // epilogue: warp w may only touch TMEM lanes [32*(w%4), 32*(w%4)+32)
         const int quarter = warp % 4;
+        const int sub = (warp - 2) / 4; // column share of this warp among the EPW / 4 of its quarter
         const int row = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -317,9 +366,83 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                     ep.kappa[m] = 1.0f / s;
                     ep.amax[m] = bi;
                 }
+            } else if (ep.kind == EP_DEMIX) {
+                // rows of a (bin, slot) group are K consecutive lanes of this warp (K | 32): write
+                // x = acc + beta S row-wise, then each lane runs one column over the warp's groups
+                // (same arithmetic as demix_block_kernel), results transposed back for whole-row stores
+                float* xs = reinterpret_cast<float*>(smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP);
+                bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP + 32 * 33 * 4);
+                const int K = ep.K, m0 = mb * BM + quarter * 32;
+                const float scale2 = ep.inv_tau * 1.4426950408889634f;
+                float v[32];
+                for (int c0 = sub * 32; c0 < BN; c0 += CSTEP) {
+                    tmem_ld32(tbase + c0, v);
+                    const int n0 = nb * BN + c0;
+                    if (m < ep.M) {
+                        const float* srow = ep.S + size_t(m / K) * ep.N + n0;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) xs[lane * 33 + i] = v[i] + ep.beta * __ldg(srow + i);
+                    }
+                    __syncwarp();
+                    switch (K) {
+                        case 1: demix_cols<1>(xs, os, ep, m0, n0, lane, scale2); break;
+                        case 2: demix_cols<2>(xs, os, ep, m0, n0, lane, scale2); break;
+                        case 4: demix_cols<4>(xs, os, ep, m0, n0, lane, scale2); break;
+                        case 8: demix_cols<8>(xs, os, ep, m0, n0, lane, scale2); break;
+                        case 16: demix_cols<16>(xs, os, ep, m0, n0, lane, scale2); break;
+                        default: demix_cols<32>(xs, os, ep, m0, n0, lane, scale2); break;
+                    }
+                    __syncwarp();
+                    bf16* ot = reinterpret_cast<bf16*>(ep.out_t);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int r = i * 8 + lane / 4;
+                        if (m0 + r < ep.M)
+                            *reinterpret_cast<uint4*>(ot + size_t(m0 + r) * ep.ldo + n0 + (lane % 4) * 8) =
+                                *reinterpret_cast<const uint4*>(os + r * 32 + (lane % 4) * 8);
+                    }
+                    __syncwarp();
+                }
+            } else if (ep.kind == EP_STORE && ep.out_t && !ep.out_f) {
+                // bf16 store through the warp's staging block: whole 64-byte row segments per lane group
+                bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP);
+                const int m0 = mb * BM + quarter * 32;
+                bf16* ot = reinterpret_cast<bf16*>(ep.out_t);
+                float v[32];
+                for (int c0 = sub * 32; c0 < BN; c0 += CSTEP) {
+                    tmem_ld32(tbase + c0, v);
+                    const int n0 = nb * BN + c0;
+                    if (ep.bias) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + i));
+                            v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+                        }
+                    }
+                    // row `lane`, 16-byte chunk j at (j ^ (lane & 3)) of its 64-byte row: conflict-free
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            __nv_bfloat162 p = __floats2bfloat162_rn(v[j * 8 + 2 * t], v[j * 8 + 2 * t + 1]);
+                            pk[t] = *reinterpret_cast<uint32_t*>(&p);
+                        }
+                        *reinterpret_cast<uint4*>(os + lane * 32 + ((j ^ (lane & 3)) * 8)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int r = i * 8 + lane / 4, j = lane % 4;
+                        if (m0 + r < ep.M)
+                            *reinterpret_cast<uint4*>(ot + size_t(m0 + r) * ep.ldo + n0 + j * 8) =
+                                *reinterpret_cast<const uint4*>(os + r * 32 + ((j ^ (r & 3)) * 8));
+                    }
+                    __syncwarp();
+                }
             } else {
                 float v[32];
-                for (int c0 = 0; c0 < BN; c0 += 32) {
+                for (int c0 = sub * 32; c0 < BN; c0 += CSTEP) {
                     tmem_ld32(tbase + c0, v);
                     if (m < ep.M) epi_row32(ep, m, nb * BN + c0, v);
                 }

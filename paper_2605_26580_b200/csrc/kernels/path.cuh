@@ -394,6 +394,58 @@ pool_warp_fixed_kernel(const T* __restrict__ Nn, const float* __restrict__ U, co
     }
 }
 
+// Streaming variant of pool_warp_fixed_kernel: the head scores come precomputed from a tensor-core
+// GEMM (scores = N . [hi(u) | lo(u)]^T, EP_SCORES), so a warp only loads its check's DEG rows and
+// its lane's head score per row, forms the DEG leave-one-out softmaxes and writes DEG rows.
+template <typename T, int V, int NH, int DEG>
+__global__ void __launch_bounds__(256)
+pool_warp_scored_kernel(const T* __restrict__ Nn, const float* __restrict__ scores, const int* __restrict__ check_ptr,
+                        int P, int E, int K, int D, int64_t n_groups, T* __restrict__ pooled) {
+    const int64_t g = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int lane = threadIdx.x % 32;
+    if (g >= n_groups) return;
+    const int k = int(g % K);
+    const int64_t bj = g / K;
+    const int j = int(bj % P);
+    const int64_t b = bj / P;
+    const int e0 = check_ptr[j];
+    const int c0 = lane * V;
+    const int h = lane * NH / 32; // the head this lane's columns belong to
+    float f[DEG][V];
+    float sc[DEG];
+#pragma unroll
+    for (int i = 0; i < DEG; ++i) {
+        const int64_t r = (b * E + e0 + i) * K + k;
+        load_v<T, V>(Nn + r * D + c0, f[i]);
+        sc[i] = __ldg(scores + r * NH + h);
+    }
+#pragma unroll
+    for (int i = 0; i < DEG; ++i) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i2 = 0; i2 < DEG; ++i2)
+            if (i2 != i) mx = fmaxf(mx, sc[i2]);
+        float ex[DEG], den = 0.0f;
+#pragma unroll
+        for (int i2 = 0; i2 < DEG; ++i2) {
+            ex[i2] = i2 != i ? __expf(sc[i2] - mx) : 0.0f;
+            den += ex[i2];
+        }
+        const float fct = float(DEG - 1) / den;
+        float out[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) out[v] = 0.0f;
+#pragma unroll
+        for (int i2 = 0; i2 < DEG; ++i2) {
+            if (i2 == i) continue;
+            const float w = ex[i2] * fct;
+#pragma unroll
+            for (int v = 0; v < V; ++v) out[v] = fmaf(w, f[i2][v], out[v]);
+        }
+        store_v<T, V>(pooled + ((b * E + e0 + i) * K + k) * D + c0, out);
+    }
+}
+
 // Pi_alpha gather, one edge row per warp, V = Q/32 symbols per lane.
 template <typename T, int V>
 __global__ void __launch_bounds__(256)
