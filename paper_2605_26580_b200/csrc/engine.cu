@@ -724,13 +724,26 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, rows * D * 2.0 * (mean_seg + 1));
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
     CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
+    const int tiles = a.groups * a.mtiles;
+    static const bool no_res = std::getenv("CIDER_NO_TRES") != nullptr;
+    if (max_seg == 1 && D == 256 && !no_res) {
+        // single-segment groups: T-resident kernel (T loaded once per group change per CTA)
+        static bool attr_res = false;
+        if (!attr_res) {
+            ck(cudaFuncSetAttribute(tc::gemm_grp_res_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::GrpResLayout::TOTAL), "smem attr");
+            attr_res = true;
+        }
+        tc::gemm_grp_res_kernel<<<std::min(tiles, c.sm_count), tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, a);
+        check_launch(tag);
+        return;
+    }
     using Lay = tc::SmemLayout<256, 0>;
     static bool attr_set = false;
     if (!attr_set) {
         ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
         attr_set = true;
     }
-    const int tiles = a.groups * a.mtiles;
     tc::gemm_grp_kernel<<<std::min(tiles, c.sm_count), tc::GRP_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
     check_launch(tag);
 }

@@ -175,5 +175,171 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
 }
 
+// ---- T-resident variant for single-segment groups (the normalise GEMM, group = edge) ------------
+// Each CTA walks a contiguous range of (group, m-tile) work, group-major, so its coefficient action
+// T_alpha (D x D bf16, 128 KB for D = 256) is loaded ONCE per group change and stays resident; only
+// the gathered A rows stream (64 KB per 128-row tile against 2K cycles of MMA). The epilogue stages
+// each warp's 32 x 32 bf16 block in SMEM and writes whole 64-byte row segments.
+struct GrpResLayout {
+    static constexpr int T_OFF = 0;                 // 4 k-blocks x (256 x 64 bf16)
+    static constexpr int A_OFF = 4 * 32768;         // ring of A k-blocks, 16 KB each
+    static constexpr int NST = 4;
+    static constexpr int STG_OFF = A_OFF + NST * 16384;
+    static constexpr int BAR_OFF = STG_OFF + 8 * 2048;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(GRP_THREADS, 1)
+gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
+    using Lay = GrpResLayout;
+    constexpr int BN = 256;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
+    uint64_t* empty = full + Lay::NST;
+    uint64_t* t_full = empty + Lay::NST;
+    uint64_t* t_empty = t_full + 1;
+    uint64_t* afull = t_empty + 1;   // [2] accumulator ready
+    uint64_t* aempty = afull + 2;    // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int total = args.groups * args.mtiles;
+    const int t_begin = int(int64_t(blockIdx.x) * total / gridDim.x);
+    const int t_end = int(int64_t(blockIdx.x + 1) * total / gridDim.x);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Lay::NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(t_full, 1);
+        mbar_init(t_empty, 1);
+        for (int a = 0; a < 2; ++a) { mbar_init(&afull[a], 1); mbar_init(&aempty[a], 256); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int a_bytes = args.K * args.bb * 128;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0, cur = -1;
+            uint32_t phase = 0, teph = 0;
+            for (int t = t_begin; t < t_end; ++t) {
+                const int g = t / args.mtiles, mt = t % args.mtiles;
+                const int alpha = args.seg_alpha[g * args.max_seg];
+                if (alpha != cur) { // new coefficient action: wait until the MMAs on the old one retired
+                    if (cur >= 0) { mbar_wait(t_empty, teph); teph ^= 1; }
+                    mbar_expect_tx(t_full, 4 * 32768);
+                    for (int kb = 0; kb < 4; ++kb) tma_load_3d(smem + Lay::T_OFF + kb * 32768, &tmT, t_full, kb * 64, 0, alpha);
+                    cur = alpha;
+                }
+                const int arow = args.seg_arow[g * args.max_seg];
+                for (int kb = 0; kb < 4; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], a_bytes);
+                    tma_load_3d(smem + Lay::A_OFF + stage * 16384, &tmA, &full[stage], kb * 64, arow * args.K, mt * args.bb);
+                    if (++stage == Lay::NST) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+            int stage = 0, acc = 0, cur = -1;
+            uint32_t phase = 0, acc_phase = 0, tfph = 0;
+            for (int t = t_begin; t < t_end; ++t) {
+                const int g = t / args.mtiles;
+                const int alpha = args.seg_alpha[g * args.max_seg];
+                if (alpha != cur) {
+                    if (cur >= 0) mma_commit(t_empty); // fires once every MMA on the old T has completed
+                    mbar_wait(t_full, tfph);
+                    tfph ^= 1;
+                    fence_after();
+                    cur = alpha;
+                }
+                mbar_wait(&aempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < 4; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint64_t da = sw128_desc(smem + Lay::A_OFF + stage * 16384);
+                    const uint64_t db = sw128_desc(smem + Lay::T_OFF + kb * 32768);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
+                    mma_commit(&empty[stage]);
+                    if (++stage == Lay::NST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&afull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        const int quarter = warp % 4;
+        const int half = (warp - 2) / 4; // column half of every row
+        bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * 2048);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = t_begin; t < t_end; ++t) {
+            const int g = t / args.mtiles, mt = t % args.mtiles;
+            mbar_wait(&afull[acc], acc_phase);
+            fence_after();
+            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+            const int rows_live = args.K * args.bb;
+            auto orow_of = [&](int r /* tile row */, bool& ok) -> size_t {
+                const int b = mt * args.bb + r / args.K, k = r % args.K;
+                ok = r < rows_live && b < args.bins;
+                return (size_t(b) * args.out_rows_per_bin + args.out_row[g]) * args.K + k;
+            };
+            for (int c0 = half * (args.D / 2); c0 < (half + 1) * (args.D / 2); c0 += 32) {
+                float v[32];
+                tmem_ld32(tbase + c0, v);
+                if (args.out_f) {
+                    bool ok;
+                    const size_t orow = orow_of(quarter * 32 + lane, ok);
+                    if (ok) {
+                        float* o = args.out_f + orow * args.D + c0;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        __nv_bfloat162 p = __floats2bfloat162_rn(v[j * 8 + 2 * q], v[j * 8 + 2 * q + 1]);
+                        pk[q] = *reinterpret_cast<uint32_t*>(&p);
+                    }
+                    *reinterpret_cast<uint4*>(os + lane * 32 + ((j ^ (lane & 3)) * 8)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int r = i * 8 + lane / 4, j = lane % 4;
+                    bool ok;
+                    const size_t orow = orow_of(quarter * 32 + r, ok);
+                    if (ok)
+                        *reinterpret_cast<uint4*>(args.out_t + orow * args.D + c0 + j * 8) =
+                            *reinterpret_cast<const uint4*>(os + r * 32 + ((j ^ (r & 3)) * 8));
+                }
+                __syncwarp();
+            }
+            fence_before();
+            mbar_arrive(&aempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
 } // namespace tc
 } // namespace cider
