@@ -14,6 +14,7 @@ KEYS = [
     ("dram_rd_MB", "dram__bytes_read.sum"),
     ("dram_wr_MB", "dram__bytes_write.sum"),
     ("tensor_pct", "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+    ("tcgen05_bf16_pct", "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed"),
     ("hmma_pct", "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active"),
     ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
     ("lts_pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed"),
