@@ -388,7 +388,9 @@ void gemm(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1,
     static const int epw_demix = std::getenv("CIDER_EPW_DEMIX") ? std::atoi(std::getenv("CIDER_EPW_DEMIX")) : 16;
     static const int epw_store = std::getenv("CIDER_EPW_STORE") ? std::atoi(std::getenv("CIDER_EPW_STORE")) : 4;
     static const int epw_scores = std::getenv("CIDER_EPW_SCORES") ? std::atoi(std::getenv("CIDER_EPW_SCORES")) : 4;
-    const int epw = ep.kind == EP_DEMIX ? epw_demix : ep.kind == EP_STORE ? epw_store : ep.kind == EP_SCORES ? epw_scores : 4;
+    const int epw = ep.kind == EP_DEMIX ? (epw_demix == 8 ? 8 : 16) // the demix epilogue needs the > 4-warp staging
+                    : ep.kind == EP_STORE ? epw_store : ep.kind == EP_SCORES ? epw_scores : 4;
+    if (ep.kind == EP_DEMIX && BN != 256) throw InvalidInput("fused demix epilogue needs Q % 256 == 0");
     if (BN == 256 && epw == 16) launch_tc<256, 16>(c, a0, a1, b, args);
     else if (BN == 256 && epw == 8) launch_tc<256, 8>(c, a0, a1, b, args);
     else if (BN == 64 && epw == 8) launch_tc<64, 8>(c, a0, a1, b, args);
@@ -770,7 +772,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         const LayerW& lw = c.lw[li];
         // Module A (denoiser.cpp:141-160)
         Epi e;
-        if (c.bf16 && 32 % K == 0 && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
+        if (c.bf16 && 32 % K == 0 && K >= 4 && Q % 256 == 0 && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
             // intermediate logits and demixing in one kernel: Lambda-bar never leaves the chip
             e = epi(EP_DEMIX);
             e.out_t = w.Aq; e.ldo = Q; e.S = S; e.L = L; e.K = K; e.beta = float(c.md.evidence_scale);

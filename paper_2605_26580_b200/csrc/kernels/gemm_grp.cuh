@@ -50,7 +50,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     constexpr int BN = 256;
     using Lay = SmemLayout<BN, 0>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -194,7 +194,7 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     using Lay = GrpResLayout;
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
     uint64_t* empty = full + Lay::NST;
     uint64_t* t_full = empty + Lay::NST;

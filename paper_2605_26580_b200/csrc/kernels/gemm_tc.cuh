@@ -122,7 +122,8 @@ struct SmemLayout {
     static constexpr int NST = EPW > 4 ? 2 : EPW == 0 ? STAGES : NST_FIT;
     // EP_DEMIX transpose staging per epilogue warp: [32][33] fp32 (padded: conflict-free rows and
     // columns) + [32][32] bf16 results
-    static constexpr int STG_WARP = 32 * 33 * 4 + 32 * 32 * 2;
+    // (EPW <= 4 kernels only stage bf16 stores: [32][32] bf16; EP_DEMIX runs with EPW > 4)
+    static constexpr int STG_WARP = EPW > 4 ? 32 * 33 * 4 + 32 * 32 * 2 : 32 * 32 * 2;
     static constexpr int STG_OFF = NST * STAGE_BYTES;
     static constexpr int BAR_OFF = STG_OFF + EPW * STG_WARP;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024; // barriers + 1 KB alignment slack
@@ -251,7 +252,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     constexpr int NST = Lay::NST;
     constexpr int CSTEP = (EPW / 4) * 32; // column stride of one warp's 32-column chunks
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
     uint64_t* empty = full + NST;
     uint64_t* tfull = empty + NST;
@@ -339,7 +340,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
             fence_after();
             const int m = mb * BM + row;
             const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-            if (ep.kind == EP_LOGITS) {
+            if (EPW <= 4 && ep.kind == EP_LOGITS) {
                 // whole row in this tile (N == BN): argmax (lowest index on ties) then
                 // kappa = 1 / sum exp((x - max) / tau)   (refine.cpp:61-78)
                 float bv = -INFINITY;
@@ -366,7 +367,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                     ep.kappa[m] = 1.0f / s;
                     ep.amax[m] = bi;
                 }
-            } else if (ep.kind == EP_DEMIX) {
+            } else if (EPW > 4 && ep.kind == EP_DEMIX) {
                 // rows of a (bin, slot) group are K consecutive lanes of this warp (K | 32): write
                 // x = acc + beta S row-wise, then each lane runs one column over the warp's groups
                 // (same arithmetic as demix_block_kernel), results transposed back for whole-row stores
@@ -376,17 +377,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                 const float scale2 = ep.inv_tau * 1.4426950408889634f;
                 float v[32];
                 for (int c0 = sub * 32; c0 < BN; c0 += CSTEP) {
-                    tmem_ld32(tbase + c0, v);
                     const int n0 = nb * BN + c0;
+                    tmem_ld32(tbase + c0, v);
                     if (m < ep.M) {
-                        const float* srow = ep.S + size_t(m / K) * ep.N + n0;
+                        const float4* srow = reinterpret_cast<const float4*>(ep.S + size_t(m / K) * ep.N + n0);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) xs[lane * 33 + i] = v[i] + ep.beta * __ldg(srow + i);
+                        for (int i = 0; i < 8; ++i) {
+                            const float4 s4 = __ldg(srow + i); // this row's (bin, slot) S segment
+                            xs[lane * 33 + 4 * i] = v[4 * i] + ep.beta * s4.x;
+                            xs[lane * 33 + 4 * i + 1] = v[4 * i + 1] + ep.beta * s4.y;
+                            xs[lane * 33 + 4 * i + 2] = v[4 * i + 2] + ep.beta * s4.z;
+                            xs[lane * 33 + 4 * i + 3] = v[4 * i + 3] + ep.beta * s4.w;
+                        }
                     }
                     __syncwarp();
                     switch (K) {
-                        case 1: demix_cols<1>(xs, os, ep, m0, n0, lane, scale2); break;
-                        case 2: demix_cols<2>(xs, os, ep, m0, n0, lane, scale2); break;
                         case 4: demix_cols<4>(xs, os, ep, m0, n0, lane, scale2); break;
                         case 8: demix_cols<8>(xs, os, ep, m0, n0, lane, scale2); break;
                         case 16: demix_cols<16>(xs, os, ep, m0, n0, lane, scale2); break;
@@ -403,7 +408,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                     }
                     __syncwarp();
                 }
-            } else if (ep.kind == EP_STORE && ep.out_t && !ep.out_f) {
+            } else if (EPW <= 4 && ep.kind == EP_STORE && ep.out_t && !ep.out_f) {
                 // bf16 store through the warp's staging block: whole 64-byte row segments per lane group
                 bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP);
                 const int m0 = mb * BM + quarter * 32;
@@ -440,7 +445,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                     }
                     __syncwarp();
                 }
-            } else {
+            } else if (EPW <= 4) {
                 float v[32];
                 for (int c0 = sub * 32; c0 < BN; c0 += CSTEP) {
                     tmem_ld32(tbase + c0, v);

@@ -174,7 +174,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     constexpr int KB1 = Lay::KB1, KB2 = Lay::KB2, NS = Lay::NS;
     constexpr int KBD = D / 64; // output k-blocks = final-epilogue steps (half h takes k-blocks h, h+2, ...)
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
     uint8_t* xs = smem;
     uint8_t* ring = smem + Lay::R_OFF;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
