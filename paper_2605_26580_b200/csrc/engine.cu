@@ -32,6 +32,7 @@
 #include "kernels/mlp_tc.cuh"
 #include "kernels/mlp_tc2.cuh"
 #include "kernels/gemm_grp.cuh"
+#include "kernels/pool_mma.cuh"
 #include "kernels/wht.cuh"
 #include "kernels/path.cuh"
 
@@ -161,6 +162,7 @@ struct LayerW {
     void *g1, *g2, *a1, *a2, *f1, *f2, *ak;
     float *gb1, *gb2, *ab1, *ab2, *fb1, *fb2, *aq;
     float* au; // heads x D: u_h = Wk_h^T q_h, the attention score vectors
+    void* aus16; // BF16 mode, heads <= 8, D = 256: 16 x D, rows h = hi(u_h / sqrt(D/heads)), 8 + h = lo (pool_mma)
     void* aus; // BF16 mode, heads <= 16: 64 x D bf16 score matrix, rows h = hi(u_h / sqrt(D/heads)),
                // rows 16 + h = the bf16 remainder (lo), zero elsewhere: scores = N . aus^T (EP_SCORES)
 };
@@ -682,6 +684,25 @@ void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* poo
     else run_pool_v<T, 2>(c, lw, Nn, K, groups, pooled);
 }
 
+// BF16, check-regular degree 6, D = 256, heads in {1, 2, 4, 8}, 6K <= 48 rows per (bin, check) block (K = 4 or 8)
+bool pool_mma_ok(const cider_ctx& c, const LayerW& lw, int K) {
+    return c.bf16 && lw.aus16 && c.D == 256 && c.max_check_deg == 6 && c.min_check_deg == 6 && 8 % c.heads == 0 &&
+           6 * K <= 48 && (6 * K) % 8 == 0 && !std::getenv("CIDER_NO_POOL_MMA");
+}
+const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, int ld, int box_rows);
+void run_pool_mma(cider_ctx& c, const LayerW& lw, const void* Nn, int64_t Me, int nb, int K, void* pooled) {
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(pool_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PoolMmaLayout::TOTAL), "smem attr");
+        attr = true;
+    }
+    const CUtensorMap& tm = map_for(c, Nn, Me, c.D, c.D, 6 * K);
+    const int64_t blocks = int64_t(nb) * c.P;
+    const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count) * 2));
+    pool_mma_kernel<<<grid, PM_THREADS, PoolMmaLayout::TOTAL, c.stream>>>(tm, (const bf16*)lw.aus16, c.check_ptr, c.P, c.E, K,
+                                                                          c.heads, blocks, (bf16*)pooled);
+}
+
 // BF16, check-regular degree 6, D = 256, 1..16 heads dividing 32 lanes: scores from EP_SCORES
 bool pool_scored(const cider_ctx& c, const LayerW& lw) {
     return c.bf16 && lw.aus && c.D == 256 && c.max_check_deg == 6 && c.min_check_deg == 6 && 32 % c.heads == 0 &&
@@ -815,7 +836,12 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             e.out_t = w.Nn; e.ldo = D;
             gemm(c, "gemm_backproj", w.Ae, Q, nullptr, 0, c.Wt, Me, D, e);
         }
-        if (pool_scored(c, lw)) {
+        if (pool_mma_ok(c, lw, K)) {
+            // one pass: TMA block loads, mma.sync head scores, leave-one-out softmax pool
+            Launch lg(c, "pool_attn", 2.0 * double(Me) * D * (32 + c.max_check_deg), double(Me) * D * 2 * c.act_size);
+            run_pool_mma(c, lw, w.Nn, Me, nb, K, w.pooled);
+            check_launch("pool");
+        } else if (pool_scored(c, lw)) {
             // head scores on the tensor cores, then a streaming leave-one-out softmax pool
             float* sc = (float*)wsbuf(c, "scores", size_t(round_up(size_t(Me), 128)) * c.heads * 4);
             e = epi(EP_SCORES);
@@ -1132,6 +1158,7 @@ void upload_model(cider_ctx& c, const float* w) {
         L.aq = nullptr;
         L.au = nullptr;
         L.aus = nullptr;
+        L.aus16 = nullptr;
     }
     if (c.heads)
         for (int l = 0; l < c.N; ++l) {
@@ -1166,6 +1193,17 @@ void upload_model(cider_ctx& c, const float* w) {
                 DevBuf& bs = wbuf(c, m.size() * 2);
                 ck(cudaMemcpy(bs.p, m.data(), m.size() * 2, cudaMemcpyHostToDevice), "upload");
                 c.lw[l].aus = bs.p;
+                if (c.heads <= 8) { // the same split, 16 rows: hi at h, lo at 8 + h
+                    std::vector<bf16> m16(size_t(16) * D, __float2bfloat16_rn(0.0f));
+                    for (int h = 0; h < c.heads; ++h)
+                        for (int col = 0; col < D; ++col) {
+                            m16[size_t(h) * D + col] = m[size_t(h) * D + col];
+                            m16[size_t(8 + h) * D + col] = m[size_t(16 + h) * D + col];
+                        }
+                    DevBuf& b16 = wbuf(c, m16.size() * 2);
+                    ck(cudaMemcpy(b16.p, m16.data(), m16.size() * 2, cudaMemcpyHostToDevice), "upload");
+                    c.lw[l].aus16 = b16.p;
+                }
             }
         }
 }

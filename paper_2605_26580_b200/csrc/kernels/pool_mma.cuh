@@ -1,0 +1,197 @@
+// pool_mma.cuh — Module B extrinsic attention pooling (denoiser.cpp:196-203
+// with the attention Psi of DESIGN.md §4) in ONE pass over the edge rows, BF16 mode.
+//
+// For a check-regular code (every check has DEG = 6 edges, all BASELINE codes) the DEG x K edge rows
+// (b, e0..e0+5, k) of one (bin, check) block are contiguous in HBM. A persistent CTA streams blocks:
+//   1. TMA (SWIZZLE_128B boxes of 64 columns) brings the block into SMEM, double-buffered;
+//   2. head scores s = n . [hi(u_h) | lo(u_h)] on the tensor cores with mma.sync m16n8k16 (bf16 in,
+//      fp32 accumulate; the hi/lo split of u_h keeps the scores fp32-grade), fragments by ldmatrix;
+//   3. per (k, 8-column chunk) thread: leave-one-out softmax over the other DEG-1 edges of its head and
+//      the weighted sum (DEG-1) sum_{i2 != i} w n_{i2}, written as whole 512-byte rows.
+// N is read once and pooled written once: the kernel is an HBM stream (the scores GEMM and its second
+// read of N are gone).
+#pragma once
+
+#include "gemm_tc.cuh"
+
+namespace cider {
+
+constexpr int PM_THREADS = 256;
+constexpr int PM_DEG = 6;
+constexpr int PM_NBUF = 4;            // blocks in flight per CTA (two CTAs per SM)
+constexpr int PM_BUF = 4 * 48 * 128;  // 4 k-blocks x 6K rows x 128 B, K <= 8 (k-block stride R x 128, 1 KB aligned)
+struct PoolMmaLayout {
+    static constexpr int U_OFF = PM_NBUF * PM_BUF;     // 16 x 256 bf16 score matrix, swizzled
+    static constexpr int S_OFF = U_OFF + 16 * 512;     // per-warp score scratch [16 rows][8] fp32
+    static constexpr int BAR_OFF = S_OFF + 8 * 128 * 4;
+    static constexpr int TOTAL = BAR_OFF + 64 + 1024;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& b0, uint32_t& b1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0, %1}, [%2];" : "=r"(b0), "=r"(b1) : "r"(addr));
+}
+__device__ __forceinline__ void mma_16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+                 "{%0, %1, %2, %3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Nn: edge rows [(b*E + e)*K + k][256] bf16 through tmN (box {64, 6K}); Uhl: [16][256] bf16, rows
+// h < NH = hi(u_h / sqrt(D/NH)), rows 8 + h = the bf16 remainder; n_blocks = bins * P.
+// Two independent 4-warp groups per CTA alternate blocks (each with PM_NBUF / 2 buffers and its own
+// named barrier); warp w of a group owns rows k = 2w, 2w + 1 of a block: it computes their DEG x 2 head
+// scores (one m16 tile, 12 real rows) and pools them, so no CTA-wide barrier sits between the phases.
+__global__ void __launch_bounds__(PM_THREADS, 2)
+pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict__ Uhl, const int* __restrict__ check_ptr,
+                int P, int E, int K, int NH, int64_t n_blocks, bf16* __restrict__ pooled) {
+    using Lay = PoolMmaLayout;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* us = smem + Lay::U_OFF;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int grp = warp / 4, wg = warp % 4;         // group, warp within the group
+    float* ss = reinterpret_cast<float*>(smem + Lay::S_OFF) + warp * 128; // per-warp [12 rows][8 heads + pad]
+    const int R = PM_DEG * K;        // rows per block (<= 48)
+    const int KBS = R * 128;         // k-block stride inside a block buffer
+    constexpr int GB = PM_NBUF / 2;  // buffers per group
+
+    // score matrix into SMEM: 16-byte chunk c of row n at (c & ~7) | ((c ^ n) & 7) (ldmatrix conflict-free)
+    for (int i = tid; i < 16 * 32; i += PM_THREADS) {
+        const int n = i / 32, c = i % 32;
+        *reinterpret_cast<uint4*>(us + n * 512 + (((c & ~7) | ((c ^ n) & 7)) * 16)) =
+            *reinterpret_cast<const uint4*>(Uhl + n * 256 + c * 8);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < PM_NBUF; ++s) tc::mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // this group's blocks: blockIdx.x + (2 i + grp) * gridDim.x, i = 0, 1, ...
+    const int64_t stride = 2 * int64_t(gridDim.x);
+    const int64_t first = int64_t(blockIdx.x) + int64_t(grp) * gridDim.x;
+    auto issue = [&](int64_t blk, int slot) { // one thread of the group: the block's 4 column boxes
+        const int64_t b = blk / P;
+        const int j = int(blk % P);
+        const int row0 = int((b * E + check_ptr[j]) * K);
+        uint64_t* bar = &full[grp * GB + slot];
+        tc::mbar_expect_tx(bar, 4 * R * 128);
+        for (int kb = 0; kb < 4; ++kb)
+            tc::tma_load_2d(smem + (grp * GB + slot) * PM_BUF + kb * KBS, &tmN, bar, kb * 64, row0);
+    };
+    const bool leader = wg == 0 && lane == 0;
+    if (leader)
+        for (int s = 0; s < GB - 1; ++s)
+            if (first + s * stride < n_blocks) issue(first + s * stride, s);
+    // rows of this warp's m16 tile: q < 12 -> (i = q % 6, k = 2 wg + q / 6); q >= 12 pads with q = 0
+    const int q = lane & 15;
+    const int qa = q < 2 * PM_DEG ? q : 0;
+    const int k_of_q = 2 * wg + qa / PM_DEG, i_of_q = qa % PM_DEG;
+    const int arow = i_of_q * K + k_of_q;
+    const int h = (lane * 8) / (256 / NH); // pooling: lane = 8-column chunk of head h
+    int slot = 0;
+    uint32_t ph = 0; // bit s: phase of this group's full[s]
+    for (int64_t blk = first; blk < n_blocks; blk += stride) {
+        const int64_t nxt = blk + (GB - 1) * stride;
+        if (leader && nxt < n_blocks) issue(nxt, (slot + GB - 1) % GB); // released by the last group barrier
+        tc::mbar_wait(&full[grp * GB + slot], (ph >> slot) & 1u);
+        ph ^= 1u << slot;
+        const uint8_t* nb = smem + (grp * GB + slot) * PM_BUF;
+        const int64_t b = blk / P;
+        const int e0 = check_ptr[int(blk % P)];
+        if (2 * wg < K) {
+            // (1) head scores of the warp's 12 rows: n-tile 0 = hi(u), 1 = lo(u)
+            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll 4
+            for (int ks = 0; ks < 16; ++ks) {
+                const int kc = ks * 2 + (lane >> 4);
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4(tc::smem_u32(nb + (kc >> 3) * KBS + arow * 128 + (((kc & 7) ^ (arow & 7)) * 16)), a0, a1, a2, a3);
+                const int kc2 = ks * 2 + ((lane >> 3) & 1);
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const int n = nt * 8 + (lane & 7);
+                    uint32_t b0, b1;
+                    ldsm_x2(tc::smem_u32(us + n * 512 + (((kc2 & ~7) | ((kc2 ^ n) & 7)) * 16)), b0, b1);
+                    mma_16816(acc[nt], a0, a1, a2, a3, b0, b1);
+                }
+            }
+            // C rows lane/4 (+8), cols 2 (lane % 4) (+1): scores = hi + lo, into the warp's scratch
+            const int r0 = lane >> 2, c0 = (lane & 3) * 2;
+            ss[r0 * 8 + c0] = acc[0][0] + acc[1][0];
+            ss[r0 * 8 + c0 + 1] = acc[0][1] + acc[1][1];
+            if (r0 + 8 < 2 * PM_DEG) {
+                ss[(r0 + 8) * 8 + c0] = acc[0][2] + acc[1][2];
+                ss[(r0 + 8) * 8 + c0 + 1] = acc[0][3] + acc[1][3];
+            }
+            __syncwarp();
+            // (2) pooling of rows k = 2 wg + kk
+#pragma unroll 1
+            for (int kk = 0; kk < 2 && 2 * wg + kk < K; ++kk) {
+                const int k = 2 * wg + kk;
+                float2 f[PM_DEG][4];
+                float sc[PM_DEG];
+#pragma unroll
+                for (int i = 0; i < PM_DEG; ++i) {
+                    const int r = i * K + k;
+                    sc[i] = ss[(kk * PM_DEG + i) * 8 + h];
+                    const uint4 u = *reinterpret_cast<const uint4*>(nb + (lane >> 3) * KBS + r * 128 + (((lane & 7) ^ (r & 7)) * 16));
+                    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) f[i][v] = __bfloat1622float2(p2[v]);
+                }
+                // leave-one-out softmax: max over the edges other than i is the overall max M1 for every
+                // i except the (first) argmax i1, whose max over the others is the runner-up M2 — the same
+                // values as taking the max per i, with 12 exponentials instead of 36.
+                int i1 = 0;
+                float m1 = sc[0];
+#pragma unroll
+                for (int i2 = 1; i2 < PM_DEG; ++i2)
+                    if (sc[i2] > m1) { m1 = sc[i2]; i1 = i2; }
+                float m2 = -INFINITY;
+#pragma unroll
+                for (int i2 = 0; i2 < PM_DEG; ++i2)
+                    if (i2 != i1) m2 = fmaxf(m2, sc[i2]);
+                float e1[PM_DEG], e2[PM_DEG];
+#pragma unroll
+                for (int i2 = 0; i2 < PM_DEG; ++i2) {
+                    e1[i2] = __expf(sc[i2] - m1);
+                    e2[i2] = __expf(sc[i2] - m2);
+                }
+#pragma unroll
+                for (int i = 0; i < PM_DEG; ++i) {
+                    float den = 0.0f; // ascending over the other edges
+#pragma unroll
+                    for (int i2 = 0; i2 < PM_DEG; ++i2)
+                        if (i2 != i) den += i == i1 ? e2[i2] : e1[i2];
+                    const float fct = __fdividef(float(PM_DEG - 1), den);
+                    float2 out[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                    for (int i2 = 0; i2 < PM_DEG; ++i2) {
+                        if (i2 == i) continue;
+                        const float w = (i == i1 ? e2[i2] : e1[i2]) * fct;
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) out[v] = __ffma2_rn(make_float2(w, w), f[i2][v], out[v]);
+                    }
+                    uint4 o;
+                    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) po[v] = __floats2bfloat162_rn(out[v].x, out[v].y);
+                    *reinterpret_cast<uint4*>(pooled + ((b * E + e0 + i) * K + k) * 256 + lane * 8) = o;
+                }
+            }
+        }
+        if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory"); // the group is done with this buffer
+        else asm volatile("bar.sync 2, 128;" ::: "memory");
+        slot = (slot + 1) % GB;
+    }
+}
+
+} // namespace cider
