@@ -783,7 +783,9 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
     const int64_t Ms = int64_t(nb) * L * K, Me = int64_t(nb) * E * K;
     {
         Launch lg(c, "embed", 0, double(Ms) * D * (4 + c.act_size));
-        if (c.bf16)
+        if (c.bf16 && D % 8 == 0)
+            embed_bf16x8_kernel<<<blocks_for(Ms * (D / 8)), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, (bf16*)w.Zt);
+        else if (c.bf16)
             embed_kernel<bf16><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, nullptr, (bf16*)w.Zt);
         else
             embed_kernel<float><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, w.Zf, nullptr);

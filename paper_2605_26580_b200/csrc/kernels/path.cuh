@@ -26,6 +26,27 @@ __global__ void embed_kernel(const int* __restrict__ X, const float* __restrict_
     if (Zt) Zt[i] = from_f<T>(v);
 }
 
+// Vectorised BF16 variant (D % 8 == 0): 8 columns per thread, one 16-byte store.
+__global__ void embed_bf16x8_kernel(const int* __restrict__ X, const float* __restrict__ Etab, int Q, int D, int64_t M,
+                                    bf16* __restrict__ Zt) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int cpr = D / 8; // 16-byte chunks per row
+    if (i >= M * cpr) return;
+    const int64_t m = i / cpr;
+    const int c = int(i - m * cpr);
+    const int tok = __ldg(X + m);
+    const int row = (tok < 0 || tok >= Q) ? Q : tok;
+    const float4* src = reinterpret_cast<const float4*>(Etab + size_t(row) * D + c * 8);
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    uint4 o;
+    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+    po[0] = __floats2bfloat162_rn(a.x, a.y);
+    po[1] = __floats2bfloat162_rn(a.z, a.w);
+    po[2] = __floats2bfloat162_rn(b.x, b.y);
+    po[3] = __floats2bfloat162_rn(b.z, b.w);
+    *reinterpret_cast<uint4*>(Zt + m * D + c * 8) = o;
+}
+
 // ---- demix_responsibilities x S (denoiser.cpp:103-122, 130) -------------------------------
 // r_{k,l,a} = softmax over the K rows of lbar/tau; out = r * S_{l,a}. The normaliser is summed in
 // 2^-52 fixed point (exact integer adds), which is order-independent: the same bitwise
