@@ -144,6 +144,26 @@ int cider_refine_device(cider_ctx* ctx, int B, int K, const float* S_device,
 int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const int32_t* coeffs, double* c2v,
                            int device);
 
+/* ---- batched GF(Q) FFT-BP decoder -------------------------------------- */
+/* A code-only context: GF(2^m) tables and the Tanner graph on one device. */
+typedef struct cider_bp_ctx cider_bp_ctx;
+/* ura::BpConfig (bp.hpp:20-25) with the WHT backend (bp.cpp:222-269). */
+typedef struct {
+    int max_iters;        /* >= 1 */
+    double message_floor; /* > 0 */
+    int early_exit;       /* stop a bin at its first zero-syndrome iteration */
+} cider_bp_config;
+int cider_bp_create(int m, uint32_t prim_poly, const cider_code_desc* code, int device, cider_bp_ctx** out);
+void cider_bp_destroy(cider_bp_ctx* ctx);
+/* = ura::bp_decode (bp.cpp:271-347) for B independent belief sets: lambda B x L x Q (fp64), hard B x L,
+ * marginals B x L x Q (nullable), converged / iters B (nullable). Host buffers. */
+int cider_bp_decode(cider_bp_ctx* ctx, int B, const double* lambda, const cider_bp_config* cfg, int32_t* hard,
+                    double* marginals, int32_t* converged, int32_t* iters);
+/* = ura::sic_decode (bp.cpp:349-368): S B x L x Q (fp64 evidence), grid B x K x L (rows in decode order),
+ * stage_converged / stage_iters B x K (nullable). cancel_value NaN -> log(K/Q) (bp.cpp:352-353). */
+int cider_sic_decode(cider_bp_ctx* ctx, int B, int K, const double* S, const cider_bp_config* cfg, double cancel_value,
+                     int32_t* grid, int32_t* stage_converged, int32_t* stage_iters);
+
 /* ---- device plumbing used by the benchmark (no PyTorch on the path) --------------------- */
 int cider_device_count(int* n);
 int cider_device_alloc(cider_ctx* ctx, size_t bytes, void** ptr);

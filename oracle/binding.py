@@ -51,6 +51,9 @@ def _load(path: str, prefix: str) -> C.CDLL:
         h.ref_infer_temperature.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double]
         h.ref_infer_temperature.restype = C.c_double
         h.ref_remask_steps.argtypes = [C.c_int, C.c_int, C.c_int]
+        h.ref_bp_decode.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, P, C.c_int, C.c_double, C.c_int, P, P, P, P]
+        h.ref_sic_decode.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.c_int, C.c_double, C.c_int,
+                                     C.c_double, P, P, P]
     _handles[path] = h
     return h
 
@@ -173,6 +176,35 @@ class Reference(Checker):
         out = np.empty(1 << m, np.float64)
         self._check(self.h.ref_check_update_direct(m, inc.shape[0], _p(inc), _p(cf), target, _p(out)))
         return out
+
+
+    def bp_decode(self, m: int, edges: np.ndarray, checks: int, slots: int, lam: np.ndarray, max_iters: int = 50,
+                  message_floor: float = 1e-30, early_exit: bool = True):
+        """ura::bp_decode (bp.cpp:271-347), WHT backend, per bin: (hard, marginals, converged, iters)."""
+        cd, _e = code_desc(edges, checks, slots)
+        lam = np.ascontiguousarray(lam, np.float64)
+        B, q = lam.shape[0], 1 << m
+        hard = np.empty((B, slots), np.int32)
+        marg = np.empty((B, slots, q), np.float64)
+        conv = np.empty(B, np.int32)
+        its = np.empty(B, np.int32)
+        self._check(self.h.ref_bp_decode(m, C.byref(cd), B, _p(lam), max_iters, message_floor, int(early_exit), _p(hard),
+                                         _p(marg), _p(conv), _p(its)))
+        return hard, marg, conv, its
+
+    def sic_decode(self, m: int, edges: np.ndarray, checks: int, slots: int, S: np.ndarray, k: int,
+                   max_iters: int = 50, message_floor: float = 1e-30, early_exit: bool = True,
+                   cancel_value: float = float("nan")):
+        """ura::sic_decode (bp.cpp:349-368) per bin: (grid B x K x L, stage converged, stage iters)."""
+        cd, _e = code_desc(edges, checks, slots)
+        S = np.ascontiguousarray(S, np.float64)
+        B = S.shape[0]
+        grid = np.empty((B, k, slots), np.int32)
+        sc = np.empty((B, k), np.int32)
+        si = np.empty((B, k), np.int32)
+        self._check(self.h.ref_sic_decode(m, C.byref(cd), B, k, _p(S), max_iters, message_floor, int(early_exit),
+                                          cancel_value, _p(grid), _p(sc), _p(si)))
+        return grid, sc, si
 
 
 def derive_seed(master: int, index: int) -> int:

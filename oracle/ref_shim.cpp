@@ -460,6 +460,62 @@ int ref_check_update_direct(int m, int n_in, const double* incoming, const int32
     });
 }
 
+// Reference FFT-BP decoders (bp.cpp:271-368), WHT backend, for B independent inputs: the oracle of
+// the GPU decoder behind cider_bp_decode / cider_sic_decode.
+int ref_bp_decode(int m, const cider_code_desc* code, int B, const double* lambda, int max_iters,
+                  double message_floor, int early_exit, int32_t* hard, double* marginals, int32_t* converged,
+                  int32_t* iters) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        const int q = gf.q();
+        auto h = make_h(q, code);
+        const int L = h.slots();
+        ura::BpConfig cfg;
+        cfg.max_iters = max_iters;
+        cfg.message_floor = message_floor;
+        cfg.early_exit = early_exit != 0;
+        cfg.backend = ura::CheckBackend::wht;
+        for (int b = 0; b < B; ++b) {
+            std::vector<std::vector<double>> lam(L, std::vector<double>(q));
+            for (int l = 0; l < L; ++l)
+                std::copy(lambda + (size_t(b) * L + l) * q, lambda + (size_t(b) * L + l + 1) * q, lam[l].begin());
+            auto r = ura::bp_decode(lam, gf, h, cfg);
+            for (int l = 0; l < L; ++l) {
+                hard[size_t(b) * L + l] = r.hard[l];
+                if (marginals) std::copy(r.marginals[l].begin(), r.marginals[l].end(), marginals + (size_t(b) * L + l) * q);
+            }
+            if (converged) converged[b] = r.converged ? 1 : 0;
+            if (iters) iters[b] = r.iters_used;
+        }
+    });
+}
+
+int ref_sic_decode(int m, const cider_code_desc* code, int B, int K, const double* S, int max_iters,
+                   double message_floor, int early_exit, double cancel_value, int32_t* grid, int32_t* stage_converged,
+                   int32_t* stage_iters) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        const int q = gf.q();
+        auto h = make_h(q, code);
+        const int L = h.slots();
+        ura::BpConfig cfg;
+        cfg.max_iters = max_iters;
+        cfg.message_floor = message_floor;
+        cfg.early_exit = early_exit != 0;
+        cfg.backend = ura::CheckBackend::wht;
+        for (int b = 0; b < B; ++b) {
+            ura::EvidenceMatrix ev(L, q);
+            std::copy(S + size_t(b) * L * q, S + size_t(b + 1) * L * q, ev.v.begin());
+            auto r = ura::sic_decode(ev, gf, h, K, cfg, cancel_value);
+            for (int k = 0; k < K; ++k) {
+                for (int l = 0; l < L; ++l) grid[(size_t(b) * K + k) * L + l] = r.grid.at(k, l);
+                if (stage_converged) stage_converged[size_t(b) * K + k] = r.stages[k].converged ? 1 : 0;
+                if (stage_iters) stage_iters[size_t(b) * K + k] = r.stages[k].iters_used;
+            }
+        }
+    });
+}
+
 int ref_cosine_target(int t, int steps, int initially_masked, int base) {
     return base + int(std::lround(ura::cosine_fraction(t, steps) * initially_masked));
 }

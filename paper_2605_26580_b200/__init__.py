@@ -39,6 +39,10 @@ class ModelDesc(C.Structure):
                 ("evidence_scale", C.c_double), ("precision", C.c_int)]
 
 
+class BpConfigDesc(C.Structure):
+    _fields_ = [("max_iters", C.c_int), ("message_floor", C.c_double), ("early_exit", C.c_int)]
+
+
 class CodeDesc(C.Structure):
     _fields_ = [("checks", C.c_int), ("slots", C.c_int), ("n_edges", C.c_int), ("edges", C.POINTER(C.c_int32))]
 
@@ -111,6 +115,10 @@ def lib() -> C.CDLL:
         h.cider_workload_bins.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
         h.cider_ser_cer.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         h.cider_check_update_wht.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, C.c_int]
+        h.cider_bp_create.argtypes = [C.c_int, C.c_uint32, C.POINTER(CodeDesc), C.c_int, C.POINTER(C.c_void_p)]
+        h.cider_bp_destroy.argtypes = [P]
+        h.cider_bp_decode.argtypes = [P, C.c_int, P, C.POINTER(BpConfigDesc), P, P, P, P]
+        h.cider_sic_decode.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(BpConfigDesc), C.c_double, P, P, P]
         _lib_handle = h
     return _lib_handle
 
@@ -409,6 +417,63 @@ def check_update_wht(m: int, v2c: np.ndarray, coeffs: np.ndarray, device: int = 
     out = np.empty_like(v)
     _check(lib().cider_check_update_wht(m, n, d, _ptr(v), _ptr(cf), _ptr(out), device))
     return out
+
+
+@dataclass
+class BpConfig:
+    """ura::BpConfig (bp.hpp:20-25); the device decoder implements the WHT backend."""
+    max_iters: int = 50
+    message_floor: float = 1e-30
+    early_exit: bool = True
+
+    def desc(self) -> BpConfigDesc:
+        return BpConfigDesc(self.max_iters, self.message_floor, int(self.early_exit))
+
+
+class BpDecoder:
+    """Batched GF(Q) FFT-BP on the device: the reference's bp_decode / sic_decode
+    (bp.cpp:271-368) for many bins at once, WHT-domain check updates (double-double spectra)."""
+
+    def __init__(self, m: int, edges: np.ndarray, checks: int, slots: int, device: int = 0, prim_poly: int = 0):
+        self.m, self.q, self.slots = m, 1 << m, slots
+        cd, self._keep = code_desc(edges, checks, slots)
+        h = C.c_void_p()
+        _check(lib().cider_bp_create(m, prim_poly, C.byref(cd), device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cider_bp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def bp_decode(self, lam: np.ndarray, cfg: BpConfig = BpConfig()):
+        """lam: B x L x Q slot beliefs -> (hard B x L, marginals B x L x Q, converged B, iters B)."""
+        lam = np.ascontiguousarray(lam, np.float64)
+        B = lam.shape[0]
+        hard = np.empty((B, self.slots), np.int32)
+        marg = np.empty((B, self.slots, self.q), np.float64)
+        conv = np.empty(B, np.int32)
+        its = np.empty(B, np.int32)
+        d = cfg.desc()
+        _check(lib().cider_bp_decode(self.h, B, _ptr(lam), C.byref(d), _ptr(hard), _ptr(marg), _ptr(conv), _ptr(its)))
+        return hard, marg, conv.astype(bool), its
+
+    def sic_decode(self, S: np.ndarray, k: int, cfg: BpConfig = BpConfig(), cancel_value: float = float("nan")):
+        """S: B x L x Q evidence -> (grid B x k x L in decode order, stage converged B x k, stage iters B x k)."""
+        S = np.ascontiguousarray(S, np.float64)
+        B = S.shape[0]
+        grid = np.empty((B, k, self.slots), np.int32)
+        sc = np.empty((B, k), np.int32)
+        si = np.empty((B, k), np.int32)
+        d = cfg.desc()
+        _check(lib().cider_sic_decode(self.h, B, k, _ptr(S), C.byref(d), cancel_value, _ptr(grid), _ptr(sc), _ptr(si)))
+        return grid, sc.astype(bool), si
 
 
 def device_count() -> int:

@@ -34,6 +34,7 @@
 #include "kernels/gemm_grp.cuh"
 #include "kernels/pool_mma.cuh"
 #include "kernels/wht.cuh"
+#include "kernels/bp.cuh"
 #include "kernels/path.cuh"
 
 namespace cider {
@@ -1336,6 +1337,96 @@ cider_ctx::~cider_ctx() {
     if (stream) cudaStreamDestroy(stream);
 }
 
+// ---- batched GF(Q) FFT-BP (bp.cpp:271-368) ----------------------------------
+struct cider_bp_ctx {
+    int device = 0, Q = 0, L = 0, P = 0, E = 0;
+    std::unique_ptr<Gf> gf;
+    std::unique_ptr<Tanner> tg;
+    cudaStream_t stream = nullptr;
+    DevBuf check_ptr, e_slot, e_coef, slot_ptr, slot_edge, mul;
+    DevBuf lambda, v2c, c2v, beliefs, residual, hard, active, conv, iters, nact, grid;
+    int64_t cap_bins = 0;
+    std::mutex mu;
+    ~cider_bp_ctx() {
+        if (stream) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+    }
+};
+
+namespace {
+template <typename T>
+void bp_upload(cider_bp_ctx& c, DevBuf& b, const std::vector<T>& v) {
+    b.ensure(std::max<size_t>(v.size() * sizeof(T), 16));
+    if (!v.empty()) ck(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+}
+void bp_reserve(cider_bp_ctx& c, int64_t B, int K) {
+    const size_t rq = size_t(B) * c.L * c.Q, eq = size_t(B) * c.E * c.Q;
+    c.lambda.ensure(rq * 8);
+    c.beliefs.ensure(rq * 8);
+    c.residual.ensure(rq * 8);
+    c.v2c.ensure(eq * 8);
+    c.c2v.ensure(eq * 8);
+    c.hard.ensure(size_t(B) * c.L * 4);
+    c.active.ensure(size_t(B) * 4);
+    c.conv.ensure(size_t(B) * 4);
+    c.iters.ensure(size_t(B) * 4);
+    c.nact.ensure(16);
+    c.grid.ensure(size_t(B) * std::max(K, 1) * c.L * 4);
+}
+void bp_validate(const cider_bp_config* cfg) {
+    if (!cfg) throw InvalidInput("bp_decode: null config");
+    if (cfg->max_iters < 1) throw InvalidInput("bp_decode: need max_iters >= 1");
+    if (!(cfg->message_floor > 0.0)) throw InvalidInput("bp_decode: message_floor must be positive");
+}
+// bp_decode over B bins whose slot beliefs are in c.lambda; leaves hard / beliefs / conv / iters
+void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
+    const int Q = c.Q, L = c.L, E = c.E, P = c.P;
+    const int64_t rows = B * L;
+    bp::bp_init_kernel<<<blocks_for(B * E * Q), 256, 0, c.stream>>>(c.lambda.as<double>(), c.e_slot.as<int>(), L, E, Q,
+                                                                    B * E * Q, c.v2c.as<double>(), c.c2v.as<double>());
+    std::vector<int> ones(size_t(B), 1);
+    ck(cudaMemcpyAsync(c.active.p, ones.data(), size_t(B) * 4, cudaMemcpyHostToDevice, c.stream), "h2d");
+    int max_deg = 0;
+    for (int j = 0; j < P; ++j) max_deg = std::max(max_deg, c.tg->check_ptr[j + 1] - c.tg->check_ptr[j]);
+    const size_t smem = size_t(2) * max_deg * Q * sizeof(bp::dd);
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(bp::bp_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
+        attr = true;
+    }
+    if (smem > 200 * 1024) throw InvalidInput("bp_decode: check degree x Q too large for one CTA");
+    const int cthreads = std::min(256, std::max(32, Q));
+    for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+        ck(cudaMemsetAsync(c.nact.p, 0, 4, c.stream), "memset");
+        bp::bp_check_kernel<<<unsigned(B * P), cthreads, smem, c.stream>>>(c.v2c.as<double>(), c.check_ptr.as<int>(),
+                                                                          c.e_coef.as<int>(), c.mul.as<uint8_t>(), P, E, Q,
+                                                                          c.active.as<int>(), c.c2v.as<double>());
+        bp::bp_belief_kernel<<<blocks_for(rows, 64), 64, 0, c.stream>>>(c.lambda.as<double>(), c.c2v.as<double>(),
+                                                                        c.slot_ptr.as<int>(), c.slot_edge.as<int>(), L, E, Q,
+                                                                        c.active.as<int>(), rows, c.beliefs.as<double>(),
+                                                                        c.hard.as<int>());
+        bp::bp_syndrome_kernel<<<blocks_for(B * 32), 256, 0, c.stream>>>(
+            c.hard.as<int>(), c.check_ptr.as<int>(), c.e_slot.as<int>(), c.e_coef.as<int>(), c.mul.as<uint8_t>(), P, L, Q,
+            iter, cfg.max_iters, cfg.early_exit, B, c.active.as<int>(), c.conv.as<int>(), c.iters.as<int>(),
+            c.nact.as<int>());
+        bp::bp_var_kernel<<<blocks_for(rows, 64), 64, 0, c.stream>>>(c.lambda.as<double>(), c.c2v.as<double>(),
+                                                                     c.slot_ptr.as<int>(), c.slot_edge.as<int>(), L, E, Q,
+                                                                     cfg.message_floor, c.active.as<int>(), rows,
+                                                                     c.v2c.as<double>());
+        check_launch("bp iteration");
+        if (iter % 4 == 0 || iter == cfg.max_iters) { // stop once every bin has exited
+            int n = 0;
+            ck(cudaMemcpyAsync(&n, c.nact.p, 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+            ck(cudaStreamSynchronize(c.stream), "bp");
+            if (n == 0) break;
+        }
+    }
+}
+} // namespace
+
+
 extern "C" {
 
 const char* cider_last_error(void) {
@@ -1636,6 +1727,96 @@ int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const 
         ck(cudaStreamSynchronize(st), "wht");
         cudaStreamDestroy(st);
         din.release(); dout.release(); dcf.release(); dmul.release();
+    });
+}
+
+int cider_bp_create(int m, uint32_t prim_poly, const cider_code_desc* code, int device, cider_bp_ctx** out) {
+    return guard([&] {
+        *out = nullptr;
+        if (m < 1 || m > 8) throw InvalidInput("bp: GF(2^m) needs 1 <= m <= 8");
+        auto c = std::make_unique<cider_bp_ctx>();
+        c->gf = std::make_unique<Gf>(m, prim_poly);
+        c->Q = c->gf->q;
+        c->tg = std::make_unique<Tanner>(code, c->Q);
+        c->L = c->tg->slots;
+        c->P = c->tg->checks;
+        c->E = c->tg->n_edges();
+        require_device();
+        c->device = device;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        std::vector<uint8_t> mul(size_t(c->Q) * c->Q);
+        for (int a = 0; a < c->Q; ++a)
+            for (int b = 0; b < c->Q; ++b) mul[size_t(a) * c->Q + b] = uint8_t(c->gf->mul(a, b));
+        bp_upload(*c, c->check_ptr, c->tg->check_ptr);
+        bp_upload(*c, c->e_slot, c->tg->slot);
+        bp_upload(*c, c->e_coef, c->tg->coef);
+        bp_upload(*c, c->slot_ptr, c->tg->slot_ptr);
+        bp_upload(*c, c->slot_edge, c->tg->slot_edge);
+        bp_upload(*c, c->mul, mul);
+        *out = c.release();
+    });
+}
+
+void cider_bp_destroy(cider_bp_ctx* c) { delete c; }
+
+int cider_bp_decode(cider_bp_ctx* c, int B, const double* lambda, const cider_bp_config* cfg, int32_t* hard,
+                    double* marginals, int32_t* converged, int32_t* iters) {
+    return guard([&] {
+        if (!c) throw InvalidInput("bp_decode: null context");
+        bp_validate(cfg);
+        if (B < 0) throw InvalidInput("bp_decode: negative batch");
+        if (B == 0) return;
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        bp_reserve(*c, B, 1);
+        const size_t rq = size_t(B) * c->L * c->Q;
+        ck(cudaMemcpyAsync(c->lambda.p, lambda, rq * 8, cudaMemcpyHostToDevice, c->stream), "h2d");
+        bp_run(*c, B, *cfg);
+        ck(cudaMemcpyAsync(hard, c->hard.p, size_t(B) * c->L * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        if (marginals) ck(cudaMemcpyAsync(marginals, c->beliefs.p, rq * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        if (converged) ck(cudaMemcpyAsync(converged, c->conv.p, size_t(B) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        if (iters) ck(cudaMemcpyAsync(iters, c->iters.p, size_t(B) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "bp_decode");
+    });
+}
+
+int cider_sic_decode(cider_bp_ctx* c, int B, int K, const double* S, const cider_bp_config* cfg, double cancel_value,
+                     int32_t* grid, int32_t* stage_converged, int32_t* stage_iters) {
+    return guard([&] {
+        if (!c) throw InvalidInput("sic_decode: null context");
+        if (K < 1) throw InvalidInput("sic_decode: need K >= 1");
+        bp_validate(cfg);
+        if (B < 0) throw InvalidInput("sic_decode: negative batch");
+        if (B == 0) return;
+        if (std::isnan(cancel_value)) cancel_value = std::log(static_cast<double>(K) / c->Q); // bp.cpp:352-353
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        bp_reserve(*c, B, K);
+        const int64_t rows = int64_t(B) * c->L;
+        ck(cudaMemcpyAsync(c->residual.p, S, size_t(rows) * c->Q * 8, cudaMemcpyHostToDevice, c->stream), "h2d");
+        std::vector<int32_t> conv{}, its{};
+        conv.resize(static_cast<size_t>(B));
+        its.resize(static_cast<size_t>(B));
+        for (int stage = 0; stage < K; ++stage) {
+            bp::slot_beliefs_kernel<<<blocks_for(rows, 64), 64, 0, c->stream>>>(c->residual.as<double>(), rows, c->Q,
+                                                                                c->lambda.as<double>());
+            bp_run(*c, B, *cfg);
+            bp::sic_cancel_kernel<<<blocks_for(rows), 256, 0, c->stream>>>(c->hard.as<int>(), c->L, c->Q, cancel_value, rows,
+                                                                          c->residual.as<double>(), c->grid.as<int>(), K, stage);
+            check_launch("sic stage");
+            if (stage_converged || stage_iters) {
+                ck(cudaMemcpyAsync(conv.data(), c->conv.p, size_t(B) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+                ck(cudaMemcpyAsync(its.data(), c->iters.p, size_t(B) * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+                ck(cudaStreamSynchronize(c->stream), "sic");
+                for (int b = 0; b < B; ++b) {
+                    if (stage_converged) stage_converged[size_t(b) * K + stage] = conv[b];
+                    if (stage_iters) stage_iters[size_t(b) * K + stage] = its[b];
+                }
+            }
+        }
+        ck(cudaMemcpyAsync(grid, c->grid.p, size_t(B) * K * c->L * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "sic_decode");
     });
 }
 
