@@ -1396,14 +1396,14 @@ void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
         ck(cudaFuncSetAttribute(bp::bp_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
         attr = true;
     }
-    if (smem > 200 * 1024) throw InvalidInput("bp_decode: check degree x Q too large for one CTA");
+    if (smem > 200 * 1024 || max_deg > 32) throw InvalidInput("bp_decode: check degree x Q too large for one CTA");
     const int cthreads = std::min(256, std::max(32, Q));
     for (int iter = 1; iter <= cfg.max_iters; ++iter) {
         ck(cudaMemsetAsync(c.nact.p, 0, 4, c.stream), "memset");
         bp::bp_check_kernel<<<unsigned(B * P), cthreads, smem, c.stream>>>(c.v2c.as<double>(), c.check_ptr.as<int>(),
                                                                           c.e_coef.as<int>(), c.mul.as<uint8_t>(), P, E, Q,
                                                                           c.active.as<int>(), c.c2v.as<double>());
-        bp::bp_belief_kernel<<<blocks_for(rows, 64), 64, 0, c.stream>>>(c.lambda.as<double>(), c.c2v.as<double>(),
+        bp::bp_belief_kernel<<<unsigned((rows + 7) / 8), 256, 0, c.stream>>>(c.lambda.as<double>(), c.c2v.as<double>(),
                                                                         c.slot_ptr.as<int>(), c.slot_edge.as<int>(), L, E, Q,
                                                                         c.active.as<int>(), rows, c.beliefs.as<double>(),
                                                                         c.hard.as<int>());
@@ -1411,7 +1411,7 @@ void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
             c.hard.as<int>(), c.check_ptr.as<int>(), c.e_slot.as<int>(), c.e_coef.as<int>(), c.mul.as<uint8_t>(), P, L, Q,
             iter, cfg.max_iters, cfg.early_exit, B, c.active.as<int>(), c.conv.as<int>(), c.iters.as<int>(),
             c.nact.as<int>());
-        bp::bp_var_kernel<<<blocks_for(rows, 64), 64, 0, c.stream>>>(c.lambda.as<double>(), c.c2v.as<double>(),
+        bp::bp_var_kernel<<<unsigned((rows + 7) / 8), 256, 0, c.stream>>>(c.lambda.as<double>(), c.c2v.as<double>(),
                                                                      c.slot_ptr.as<int>(), c.slot_edge.as<int>(), L, E, Q,
                                                                      cfg.message_floor, c.active.as<int>(), rows,
                                                                      c.v2c.as<double>());
@@ -1733,7 +1733,7 @@ int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const 
 int cider_bp_create(int m, uint32_t prim_poly, const cider_code_desc* code, int device, cider_bp_ctx** out) {
     return guard([&] {
         *out = nullptr;
-        if (m < 1 || m > 8) throw InvalidInput("bp: GF(2^m) needs 1 <= m <= 8");
+        if (m < 1 || m > 8) throw InvalidInput("bp: GF(2^m) needs 1 <= m <= 8"); // Q <= 256 (BP_QMAX)
         auto c = std::make_unique<cider_bp_ctx>();
         c->gf = std::make_unique<Gf>(m, prim_poly);
         c->Q = c->gf->q;

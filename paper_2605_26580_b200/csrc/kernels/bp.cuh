@@ -137,42 +137,79 @@ __global__ void bp_check_kernel(const double* __restrict__ v2c, const int* __res
         }
     }
     wht_rows_dd(sp, d, Q);
-    // out[a] = max(double(spec[map[a]] / Q), 0), then normalize_or_uniform per edge
-    double* out = c2v + (b * E + e0) * Q;
+    // out[a] = max(double(spec[map[a]] / Q), 0) staged in SMEM (over the dead y rows), then
+    // normalize_or_uniform per edge (sequential sums, one thread per edge) and a coalesced write
+    double* xo = reinterpret_cast<double*>(y);
+    __shared__ double inv_s[32];
     const double scale = 1.0 / Q;
     for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
         const int i = idx / Q, a = idx % Q;
         const dd v = sp[size_t(i) * Q + mul[e_coef[e0 + i] * Q + a]];
         const double x = (v.hi + v.lo) * scale; // scale is a power of two: exact
-        out[idx] = fmax(x, 0.0);
+        xo[idx] = fmax(x, 0.0);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < d; i += blockDim.x) normalize_row_seq(out + size_t(i) * Q, Q);
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        double t = 0.0;
+        for (int a = 0; a < Q; ++a) t += xo[size_t(i) * Q + a];
+        inv_s[i] = t > 0.0 ? 1.0 / t : -1.0;
+    }
+    __syncthreads();
+    double* out = c2v + (b * E + e0) * Q;
+    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
+        const double iv = inv_s[idx / Q];
+        out[idx] = iv < 0.0 ? 1.0 / Q : xo[idx] * iv;
+    }
+}
+
+// Sequential (symbol-order) normaliser of a row a warp holds in SMEM: lane 0 sums, all lanes scale
+// their own symbols (normalize_or_uniform, bp.cpp:11-19, in the reference's summation order).
+__device__ __forceinline__ double warp_row_inv(const double* row, int Q, int lane) {
+    double s = 0.0;
+    if (lane == 0)
+        for (int a = 0; a < Q; ++a) s += row[a];
+    s = __shfl_sync(0xffffffffu, s, 0);
+    return s > 0.0 ? 1.0 / s : -1.0; // -1: uniform
 }
 
 // Beliefs and hard decision (bp.cpp:306-313): b = lambda * prod over slot edges (in slot order) of
-// c2v, normalised, argmax with ties to the lowest symbol. One thread per (bin, slot).
-__global__ void bp_belief_kernel(const double* __restrict__ lambda, const double* __restrict__ c2v,
+// c2v, normalised, argmax with ties to the lowest symbol. One warp per (bin, slot), lanes over symbols.
+constexpr int BP_QMAX = 256;
+__global__ void __launch_bounds__(256) bp_belief_kernel(const double* __restrict__ lambda, const double* __restrict__ c2v,
                                  const int* __restrict__ slot_ptr, const int* __restrict__ slot_edge, int L, int E,
                                  int Q, const int* __restrict__ active, int64_t rows, double* __restrict__ beliefs,
                                  int* __restrict__ hard) {
-    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    __shared__ double rowbuf[8][BP_QMAX];
+    const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t r = int64_t(blockIdx.x) * 8 + wib;
     if (r >= rows) return;
     const int l = int(r % L);
     const int64_t b = r / L;
     if (!active[b]) return;
-    double* bl = beliefs + r * Q;
+    double* sb = rowbuf[wib];
     const double* lam = lambda + r * Q;
-    for (int a = 0; a < Q; ++a) bl[a] = lam[a];
-    for (int p = slot_ptr[l]; p < slot_ptr[l + 1]; ++p) {
-        const double* m = c2v + (b * E + slot_edge[p]) * Q;
-        for (int a = 0; a < Q; ++a) bl[a] *= m[a];
+    const int p0 = slot_ptr[l], p1 = slot_ptr[l + 1];
+    for (int a = lane; a < Q; a += 32) {
+        double v = lam[a];
+        for (int p = p0; p < p1; ++p) v *= c2v[(b * E + slot_edge[p]) * Q + a];
+        sb[a] = v;
     }
-    normalize_row_seq(bl, Q);
-    int best = 0;
-    for (int a = 1; a < Q; ++a)
-        if (bl[a] > bl[best]) best = a;
-    hard[r] = best;
+    __syncwarp();
+    const double inv = warp_row_inv(sb, Q, lane);
+    double* bl = beliefs + r * Q;
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int a = lane; a < Q; a += 32) {
+        const double v = inv < 0.0 ? 1.0 / Q : sb[a] * inv;
+        bl[a] = v;
+        if (v > best) { best = v; bi = a; } // ascending a within the lane: first maximum kept
+    }
+    for (int o = 16; o; o >>= 1) { // lowest index among equal maxima
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) hard[r] = bi;
 }
 
 // Syndrome test and the per-bin control flow of one iteration (bp.cpp:315-318): one warp per bin.
@@ -200,28 +237,34 @@ __global__ void bp_syndrome_kernel(const int* __restrict__ hard, const int* __re
 }
 
 // Variable update (bp.cpp:320-344) for the bins still active: extrinsic prefix/suffix products over
-// the slot's edges, floored at message_floor, normalised. One thread per (bin, slot).
-__global__ void bp_var_kernel(const double* __restrict__ lambda, const double* __restrict__ c2v,
+// the slot's edges, floored at message_floor, normalised. One warp per (bin, slot), lanes over symbols.
+__global__ void __launch_bounds__(256) bp_var_kernel(const double* __restrict__ lambda, const double* __restrict__ c2v,
                               const int* __restrict__ slot_ptr, const int* __restrict__ slot_edge, int L, int E, int Q,
                               double floor_v, const int* __restrict__ active, int64_t rows, double* __restrict__ v2c) {
-    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    __shared__ double rowbuf[8][BP_QMAX];
+    const int wib = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t r = int64_t(blockIdx.x) * 8 + wib;
     if (r >= rows) return;
     const int l = int(r % L);
     const int64_t b = r / L;
     if (!active[b]) return;
+    double* sb = rowbuf[wib];
     const int p0 = slot_ptr[l], d = slot_ptr[l + 1] - p0;
     const double* lam = lambda + r * Q;
     for (int i = 0; i < d; ++i) {
         double* out = v2c + (b * E + slot_edge[p0 + i]) * Q;
-        for (int a = 0; a < Q; ++a) {
+        for (int a = lane; a < Q; a += 32) {
             double pre = lam[a]; // pre[i] = lambda * c2v[e_0] ... c2v[e_{i-1}]
             for (int t = 0; t < i; ++t) pre *= c2v[(b * E + slot_edge[p0 + t]) * Q + a];
             double suf = 1.0;    // suf[i+1] = c2v[e_{d-1}] ... c2v[e_{i+1}], built right to left
             for (int t = d - 1; t > i; --t) suf *= c2v[(b * E + slot_edge[p0 + t]) * Q + a];
             const double x = pre * suf;
-            out[a] = x < floor_v ? floor_v : x;
+            sb[a] = x < floor_v ? floor_v : x;
         }
-        normalize_row_seq(out, Q);
+        __syncwarp();
+        const double inv = warp_row_inv(sb, Q, lane);
+        for (int a = lane; a < Q; a += 32) out[a] = inv < 0.0 ? 1.0 / Q : sb[a] * inv;
+        __syncwarp();
     }
 }
 
