@@ -10,12 +10,16 @@
 //       the whole T-step loop on the device, batched over bins.
 //   cider::make_bin_decoder -> ura::BinDecoder            (protocol.hpp:32-40)
 //       for run_protocol_frame (protocol.cpp:73).
+//   cider::GpuBp::bp_decode / sic_decode                  (bp.hpp:72-93)
+//       the reference's FFT-BP / SIC-BP decoders (WHT backend) on the device, batched over bins;
+//   cider::make_sic_bin_decoder -> ura::BinDecoder        SIC-BP per bin for run_protocol_frame.
 //
 // Errors: status 3 -> std::domain_error, 4 -> std::runtime_error, with the library's message
 // (which keeps the reference's prefixes, e.g. "embed_grid: token out of range").
 #pragma once
 
 #include <cmath>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -23,6 +27,7 @@
 #include <vector>
 
 #include "cider.h"
+#include "ura/bp.hpp"
 #include "ura/denoiser.hpp"
 #include "ura/protocol.hpp"
 #include "ura/refine.hpp"
@@ -181,6 +186,80 @@ inline ura::BinDecoder make_bin_decoder(std::shared_ptr<Context> ctx, ura::Revea
         if (per_load_remask) rm.thresholds = ura::default_remask_thresholds(t.load);
         return refiner->run_with_remasking(t.evidence, t.h, sched, rm, t.load);
     };
+}
+
+// The device FFT-BP decoder for one code (cider_bp_* in cider.h). Implements the WHT backend
+// (bp.cpp:222-269); a direct-backend config is refused rather than silently substituted.
+class GpuBp {
+public:
+    GpuBp(const ura::GfContext& gf, const ura::ParityCheckMatrix& h, int device = 0)
+        : slots_(h.slots()), q_(gf.q()) {
+        const auto e = edges_of(h);
+        cider_code_desc cd{h.checks(), h.slots(), int(e.size() / 3), e.data()};
+        cider_bp_ctx* c = nullptr;
+        check(cider_bp_create(gf.m(), gf.prim_poly(), &cd, device, &c));
+        ctx_.reset(c, cider_bp_destroy);
+    }
+
+    // = ura::bp_decode (bp.cpp:271-347); final_state is not exported by the device decoder
+    ura::BpResult bp_decode(const std::vector<std::vector<double>>& lambda, const ura::BpConfig& cfg) const {
+        if (static_cast<int>(lambda.size()) != slots_) throw std::domain_error("bp_decode: belief count must equal slot count");
+        std::vector<double> lam(size_t(slots_) * q_);
+        for (int l = 0; l < slots_; ++l) std::copy(lambda[l].begin(), lambda[l].end(), lam.begin() + size_t(l) * q_);
+        std::vector<int32_t> hard(slots_);
+        std::vector<double> marg(lam.size());
+        int32_t conv = 0, its = 0;
+        const cider_bp_config c = config(cfg);
+        check(cider_bp_decode(ctx_.get(), 1, lam.data(), &c, hard.data(), marg.data(), &conv, &its));
+        ura::BpResult r;
+        r.hard.assign(hard.begin(), hard.end());
+        r.marginals.assign(slots_, std::vector<double>(q_));
+        for (int l = 0; l < slots_; ++l) std::copy(marg.begin() + size_t(l) * q_, marg.begin() + size_t(l + 1) * q_, r.marginals[l].begin());
+        r.converged = conv != 0;
+        r.iters_used = its;
+        return r;
+    }
+
+    // = ura::sic_decode (bp.cpp:349-368) for many bins in one device batch
+    std::vector<ura::SicResult> sic_decode_batch(const std::vector<const ura::EvidenceMatrix*>& bins, int k,
+                                                 const ura::BpConfig& cfg,
+                                                 double cancel_value = std::numeric_limits<double>::quiet_NaN()) const {
+        const int B = static_cast<int>(bins.size());
+        std::vector<double> S(size_t(B) * slots_ * q_);
+        for (int b = 0; b < B; ++b) {
+            if (bins[b]->slots != slots_ || bins[b]->q != q_) throw std::domain_error("sic_decode: evidence shape mismatch");
+            std::copy(bins[b]->v.begin(), bins[b]->v.end(), S.begin() + size_t(b) * slots_ * q_);
+        }
+        std::vector<int32_t> grid(size_t(B) * k * slots_), sc(size_t(B) * k), si(size_t(B) * k);
+        const cider_bp_config c = config(cfg);
+        check(cider_sic_decode(ctx_.get(), B, k, S.data(), &c, cancel_value, grid.data(), sc.data(), si.data()));
+        std::vector<ura::SicResult> out(B);
+        for (int b = 0; b < B; ++b) {
+            out[b].grid = ura::SymbolGrid(k, slots_);
+            for (int r = 0; r < k; ++r) {
+                for (int l = 0; l < slots_; ++l) out[b].grid.at(r, l) = grid[(size_t(b) * k + r) * slots_ + l];
+                out[b].stages.push_back({sc[size_t(b) * k + r] != 0, si[size_t(b) * k + r]});
+            }
+        }
+        return out;
+    }
+    ura::SicResult sic_decode(const ura::EvidenceMatrix& s, int k, const ura::BpConfig& cfg,
+                              double cancel_value = std::numeric_limits<double>::quiet_NaN()) const {
+        return sic_decode_batch({&s}, k, cfg, cancel_value)[0];
+    }
+
+private:
+    static cider_bp_config config(const ura::BpConfig& cfg) {
+        if (cfg.backend != ura::CheckBackend::wht) throw std::domain_error("cider: the device BP decoder implements the WHT backend");
+        return cider_bp_config{cfg.max_iters, cfg.message_floor, cfg.early_exit ? 1 : 0};
+    }
+    int slots_, q_;
+    std::shared_ptr<cider_bp_ctx> ctx_;
+};
+
+// ura::BinDecoder running SIC-BP on the device for bins of load K (the paper's FFT-BP baseline).
+inline ura::BinDecoder make_sic_bin_decoder(std::shared_ptr<GpuBp> bp, ura::BpConfig cfg = {}) {
+    return [bp, cfg](const ura::BinTask& t) { return bp->sic_decode(t.evidence, t.load, cfg).grid; };
 }
 
 } // namespace cider

@@ -7,6 +7,7 @@
 //   (2) ura::run_refinement + cider::GpuStructuredDenoiser   (reference loop, B200 forward)
 //   (3) cider::GpuRefiner::run_refinement                    (whole loop on the B200)
 //   (4) ura::run_with_remasking vs GpuRefiner::run_with_remasking, and a BinDecoder call
+//   (5) ura::sic_decode vs cider::GpuBp::sic_decode (FFT-BP, WHT backend), and a SIC BinDecoder
 // on fp32-rounded parameters and evidence (FP32 mode), and requires identical grids.
 // Exit code = number of failed checks.
 #include <cmath>
@@ -75,6 +76,37 @@ int main() {
         const bool shape_ok = out.rows == 2 && out.cols == 16;
         std::printf("BinDecoder call: %s\n", shape_ok ? "ok" : "FAILED");
         fails += !shape_ok;
+        // (5) SIC-BP: ura::sic_decode vs cider::GpuBp (bp.hpp:72-93), same evidence, identical grids
+        {
+            cider::GpuBp gbp(gf, h);
+            std::mt19937_64 r3(7);
+            std::normal_distribution<double> nd(0.0, 1.0);
+            ura::BpConfig bcfg;
+            bcfg.max_iters = 20;
+            std::vector<ura::EvidenceMatrix> ev(6, ura::EvidenceMatrix(16, 64));
+            std::vector<const ura::EvidenceMatrix*> ptrs;
+            for (auto& m : ev) {
+                for (double& x : m.v) x = 1.5 * nd(r3);
+                ptrs.push_back(&m);
+            }
+            auto gpu_res = gbp.sic_decode_batch(ptrs, 2, bcfg);
+            int same = 0;
+            for (size_t b = 0; b < ev.size(); ++b) {
+                auto ref_res = ura::sic_decode(ev[b], gf, h, 2, bcfg);
+                bool ok = ref_res.grid.v == gpu_res[b].grid.v;
+                for (int st = 0; st < 2; ++st)
+                    ok = ok && ref_res.stages[st].converged == gpu_res[b].stages[st].converged &&
+                         ref_res.stages[st].iters_used == gpu_res[b].stages[st].iters_used;
+                same += ok;
+            }
+            std::printf("GPU SIC-BP vs reference:       %d/%d identical grids + stage stats\n", same, int(ev.size()));
+            fails += same != int(ev.size());
+            auto sdec = cider::make_sic_bin_decoder(std::make_shared<cider::GpuBp>(gf, h), bcfg);
+            ura::BinTask t2{gf, h, ev[0], truth, 2};
+            const bool sic_ok = sdec(t2).v == gpu_res[0].grid.v;
+            std::printf("SIC BinDecoder call: %s\n", sic_ok ? "ok" : "FAILED");
+            fails += !sic_ok;
+        }
         // error contract: a different H must be rejected like a bad input
         auto rng2 = ura::make_rng(99);
         auto h2 = ura::build_random_ldpc(gf, 16, 8, 3, rng2);
