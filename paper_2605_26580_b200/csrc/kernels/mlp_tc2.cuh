@@ -439,6 +439,20 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             const bool live = m < ep.M;
             const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
             if (trf) args.trace[512 + it * 4 + 0] = clock64();
+            // z (and e) of this row's first output k-block are requested before waiting for the
+            // accumulator (their latency hides behind the last MMA2); later k-blocks at loop top
+            uint32_t zr[reads_z ? 32 : 1], er[reads_e ? 32 : 1];
+            auto load_ze = [&](int kb) {
+                const bf16* zp = ep.zb + size_t(m) * ep.ldz + kb * 64;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) ld_global_v8(zp + q * 16, zr + q * 8);
+                if (reads_e) {
+                    const bf16* eptr = ep.eb + size_t(m) * ep.ldz + kb * 64;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) ld_global_v8(eptr + q * 16, er + q * 8);
+                }
+            };
+            if (reads_z && live && half < KBD) load_ze(half);
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
             fence_after();
@@ -446,20 +460,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #pragma unroll 1
             for (int kb = half; kb < KBD; kb += 2) {
                 const int n0 = kb * 64;
-                uint32_t zr[reads_z ? 32 : 1], er[reads_e ? 32 : 1];
-                if (reads_z && (args.dbg & 2)) { // timing experiment: no z / e loads
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) { zr[q] = 0; if (reads_e) er[q] = 0; }
-                } else if (reads_z && live) {
-                    const bf16* zp = ep.zb + size_t(m) * ep.ldz + n0;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) ld_global_v8(zp + q * 16, zr + q * 8);
-                    if (reads_e) {
-                        const bf16* eptr = ep.eb + size_t(m) * ep.ldz + n0;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) ld_global_v8(eptr + q * 16, er + q * 8);
-                    }
-                }
+                if (reads_z && live && kb != half) load_ze(kb);
                 uint32_t pkl[reads_z ? 1 : 32];
                 uint32_t* pk = reads_z ? zr : pkl; // results packed over the consumed z registers
 #pragma unroll
