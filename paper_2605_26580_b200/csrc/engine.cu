@@ -346,17 +346,17 @@ const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, 
     return c.maps.emplace(key, make_map(p, rows, cols, ld, box_rows)).first->second;
 }
 
-template <int BN, int EPW = 4>
+template <int BN, int EPW = 4, bool BRES = false>
 void launch_tc(cider_ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const tc::Args& args) {
-    using Lay = tc::SmemLayout<BN, EPW>;
+    using Lay = tc::SmemLayout<BN, EPW, BRES>;
     static bool attr_set = false; // per process; same attribute for every device
     if (!attr_set) {
-        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, EPW>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+        ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, EPW, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
         attr_set = true;
     }
     int grid = std::min(args.tiles, c.sm_count);
-    tc::gemm_tc_kernel<BN, EPW><<<grid, 64 + 32 * EPW, Lay::TOTAL, c.stream>>>(a0, a1, b, args);
+    tc::gemm_tc_kernel<BN, EPW, BRES><<<grid, 64 + 32 * EPW, Lay::TOTAL, c.stream>>>(a0, a1, b, args);
 }
 
 // C[M x N] = [A0 (M x K0) | A1 (M x K1)] . B[N x (K0+K1)]^T, then the epilogue.
@@ -394,7 +394,13 @@ void gemm(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1,
     const int epw = ep.kind == EP_DEMIX ? (epw_demix == 8 ? 8 : 16) // the demix epilogue needs the > 4-warp staging
                     : ep.kind == EP_STORE ? epw_store : ep.kind == EP_SCORES ? epw_scores : 4;
     if (ep.kind == EP_DEMIX && BN != 256) throw InvalidInput("fused demix epilogue needs Q % 256 == 0");
-    if (BN == 256 && epw == 16) launch_tc<256, 16>(c, a0, a1, b, args);
+    // B-resident variants: one N tile, K <= 256 (W, W^T, V^T against 128-row A tiles)
+    static const bool no_bres = std::getenv("CIDER_NO_BRES") != nullptr;
+    const bool bres = !no_bres && BN == 256 && N == 256 && K <= 256;
+    // (the fused demix is epilogue-bound: it keeps 16 epilogue warps and a streamed B, measured faster
+    // than 8 warps with B resident)
+    if (bres && epw == 4) launch_tc<256, 4, true>(c, a0, a1, b, args);
+    else if (BN == 256 && epw == 16) launch_tc<256, 16>(c, a0, a1, b, args);
     else if (BN == 256 && epw == 8) launch_tc<256, 8>(c, a0, a1, b, args);
     else if (BN == 64 && epw == 8) launch_tc<64, 8>(c, a0, a1, b, args);
     else if (BN == 256) launch_tc<256>(c, a0, a1, b, args);

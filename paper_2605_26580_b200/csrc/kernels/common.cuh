@@ -22,6 +22,12 @@ template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __flo
 
 // erf-form GELU and logistic sigmoid, as the reference (denoiser.cpp:13-15)
 __device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// 2^x on the MUFU unit (BF16-mode softmaxes; FP32 mode keeps expf)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + expf(-x)); }
 
 enum EpKind : int {

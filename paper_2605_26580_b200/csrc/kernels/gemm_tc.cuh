@@ -110,24 +110,29 @@ struct Args {
     Epi ep;
 };
 
-// EPW epilogue warps (0 = layout without the EP_DEMIX staging, for gemm_grp.cuh); kernels with more
-// than 4 epilogue warps use a 2-stage ring to make room for the per-warp staging blocks.
-template <int BN, int EPW = 4>
+// EPW epilogue warps (0 = layout without the EP_DEMIX staging, for gemm_grp.cuh). BRES: the whole
+// B operand (N = BN, K <= 256: at most 4 k-blocks) is loaded once per CTA and stays resident; the
+// ring then streams only A tiles (the tall-skinny GEMMs against W, W^T, V^T re-read 128 KB of B per
+// 128-row tile otherwise). Kernels with more than 4 epilogue warps and a streamed B use a 2-stage ring.
+template <int BN, int EPW = 4, bool BRES = false>
 struct SmemLayout {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    // ring depth: as deep as ~192 KB allows (narrow-N GEMMs are A-stream bound), 2 with > 4 epilogue warps
-    static constexpr int NST_FIT = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
-    static constexpr int NST = EPW > 4 ? 2 : EPW == 0 ? STAGES : NST_FIT;
+    static constexpr int BRES_BYTES = BRES ? 4 * B_BYTES : 0;
+    static constexpr int STAGE_BYTES = BRES ? A_BYTES : A_BYTES + B_BYTES;
     // EP_DEMIX transpose staging per epilogue warp: [32][33] fp32 (padded: conflict-free rows and
-    // columns) + [32][32] bf16 results
-    // (EPW <= 4 kernels only stage bf16 stores: [32][32] bf16; EP_DEMIX runs with EPW > 4)
+    // columns) + [32][32] bf16 results; EPW <= 4 kernels only stage bf16 stores ([32][32] bf16)
     static constexpr int STG_WARP = EPW > 4 ? 32 * 33 * 4 + 32 * 32 * 2 : 32 * 32 * 2;
-    static constexpr int STG_OFF = NST * STAGE_BYTES;
+    static constexpr int FREE = 232448 - 1024 - 256 - BRES_BYTES - EPW * STG_WARP;
+    static constexpr int NST_FIT = (FREE / STAGE_BYTES) > 8 ? 8 : (FREE / STAGE_BYTES);
+    static constexpr int NST_STREAM = (196608 / STAGE_BYTES) > 8 ? 8 : (196608 / STAGE_BYTES);
+    static constexpr int NST = BRES ? NST_FIT : EPW > 4 ? 2 : EPW == 0 ? STAGES : NST_STREAM;
+    static constexpr int RING_OFF = BRES_BYTES;
+    static constexpr int STG_OFF = RING_OFF + NST * STAGE_BYTES;
     static constexpr int BAR_OFF = STG_OFF + EPW * STG_WARP;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024; // barriers + 1 KB alignment slack
     static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+    static_assert(NST >= 2, "gemm_tc ring");
     static_assert(TOTAL <= 232448, "gemm_tc shared memory");
 };
 
@@ -219,7 +224,8 @@ __device__ __forceinline__ void epi_row32(const Epi& ep, int m, int n0, float* v
 // EP_DEMIX column pass: lane = column n0 + lane, the warp's 32 rows in groups of KK (= one
 // (bin, slot) row each); arithmetic identical to demix_block_kernel (path.cuh).
 template <int KK>
-__device__ __forceinline__ void demix_cols(const float* xs, bf16* os, const Epi& ep, int m0, int n0, int lane, float scale2) {
+__device__ __forceinline__ void demix_cols(const float* xs, bf16* os, const Epi& ep, int m0, const float* svs, int lane,
+                                           float scale2) {
 #pragma unroll
     for (int g0 = 0; g0 < 32; g0 += KK) {
         if (m0 + g0 >= ep.M) break;
@@ -230,12 +236,12 @@ __device__ __forceinline__ void demix_cols(const float* xs, bf16* os, const Epi&
         uint32_t den = 0;
 #pragma unroll
         for (int k = 0; k < KK; ++k) {
-            const float e = exp2f((xv[k] - mx) * scale2);
+            const float e = ex2_approx((xv[k] - mx) * scale2);
             xv[k] = e;
             den += __float2uint_rn(e * 67108864.0f); // 2^26
         }
         const float rden = 1.0f / (float(den) * (1.0f / 67108864.0f));
-        const float sv = __ldg(ep.S + size_t((m0 + g0) / KK) * ep.N + n0 + lane);
+        const float sv = svs[g0 / KK]; // S[(bin, slot)][n0 + lane], requested at the chunk start
 #pragma unroll
         for (int k = 0; k < KK; ++k) os[(g0 + k) * 32 + lane] = __float2bfloat16_rn((xv[k] * rden) * sv);
     }
@@ -244,11 +250,11 @@ __device__ __forceinline__ void demix_cols(const float* xs, bf16* os, const Epi&
 // EPW epilogue warps: 4 = one per TMEM lane quarter (row statistics need whole rows); 16 = four
 // per quarter splitting the columns (EP_DEMIX, whose per-element work would otherwise leave one warp
 // per scheduler latency-bound).
-template <int BN, int EPW>
+template <int BN, int EPW, bool BRES>
 __global__ void __launch_bounds__(64 + 32 * EPW, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                const __grid_constant__ CUtensorMap tmB, const Args args) {
-    using Lay = SmemLayout<BN, EPW>;
+    using Lay = SmemLayout<BN, EPW, BRES>;
     constexpr int NST = Lay::NST;
     constexpr int CSTEP = (EPW / 4) * 32; // column stride of one warp's 32-column chunks
     extern __shared__ uint8_t smem_raw[];
@@ -257,7 +263,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     uint64_t* empty = full + NST;
     uint64_t* tfull = empty + NST;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* bfull = tempty + 2; // BRES: resident B landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int kblocks = args.K / BK;
@@ -265,6 +272,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 32 * EPW); }
+        mbar_init(bfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA0)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA1)) : "memory");
@@ -284,11 +292,15 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            if (BRES) { // the whole B (one N tile) once
+                mbar_expect_tx(bfull, kblocks * Lay::B_BYTES);
+                for (int kb = 0; kb < kblocks; ++kb) tma_load_2d(smem + kb * Lay::B_BYTES, &tmB, bfull, kb * BK, 0);
+            }
             for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x) {
                 const int mb = tile / args.tiles_n, nb = tile % args.tiles_n;
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
+                    uint8_t* sa = smem + Lay::RING_OFF + stage * Lay::STAGE_BYTES;
                     uint8_t* sb = sa + Lay::A_BYTES;
                     mbar_expect_tx(&full[stage], Lay::STAGE_BYTES);
                     const int k = kb * BK;
@@ -296,7 +308,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                         tma_load_2d(sa, &tmA0, &full[stage], k, mb * BM);
                     else
                         tma_load_2d(sa, &tmA1, &full[stage], k - args.K0, mb * BM);
-                    tma_load_2d(sb, &tmB, &full[stage], k, nb * BN);
+                    if (!BRES) tma_load_2d(sb, &tmB, &full[stage], k, nb * BN);
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
             }
@@ -306,6 +318,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
+            if (BRES) mbar_wait(bfull, 0);
             for (int tile = blockIdx.x; tile < args.tiles; tile += gridDim.x) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 fence_after();
@@ -313,8 +326,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     fence_after();
-                    uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
-                    uint8_t* sb = sa + Lay::A_BYTES;
+                    uint8_t* sa = smem + Lay::RING_OFF + stage * Lay::STAGE_BYTES;
+                    uint8_t* sb = BRES ? smem + kb * Lay::B_BYTES : sa + Lay::A_BYTES;
                     const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)
@@ -369,8 +382,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                 }
             } else if (EPW > 4 && ep.kind == EP_DEMIX) {
                 // rows of a (bin, slot) group are K consecutive lanes of this warp (K | 32): write
-                // x = acc + beta S row-wise, then each lane runs one column over the warp's groups
-                // (same arithmetic as demix_block_kernel), results transposed back for whole-row stores
+                // the logits row-wise, then each lane runs one column over the warp's groups
+                // (demix_block_kernel's arithmetic), results transposed back for whole-row stores
                 float* xs = reinterpret_cast<float*>(smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP);
                 bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP + 32 * 33 * 4);
                 const int K = ep.K, m0 = mb * BM + quarter * 32;
@@ -378,24 +391,23 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
                 float v[32];
                 for (int c0 = sub * 32; c0 < BN; c0 += CSTEP) {
                     const int n0 = nb * BN + c0;
-                    tmem_ld32(tbase + c0, v);
-                    if (m < ep.M) {
-                        const float4* srow = reinterpret_cast<const float4*>(ep.S + size_t(m / K) * ep.N + n0);
+                    float svs[8]; // this lane's column of S for the warp's (<= 8) groups, in flight during the row pass
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const float4 s4 = __ldg(srow + i); // this row's (bin, slot) S segment
-                            xs[lane * 33 + 4 * i] = v[4 * i] + ep.beta * s4.x;
-                            xs[lane * 33 + 4 * i + 1] = v[4 * i + 1] + ep.beta * s4.y;
-                            xs[lane * 33 + 4 * i + 2] = v[4 * i + 2] + ep.beta * s4.z;
-                            xs[lane * 33 + 4 * i + 3] = v[4 * i + 3] + ep.beta * s4.w;
-                        }
+                    for (int gi = 0; gi < 8; ++gi)
+                        svs[gi] = (gi * K < 32 && m0 + gi * K < ep.M) ? __ldg(ep.S + size_t((m0 + gi * K) / K) * ep.N + n0 + lane) : 0.0f;
+                    tmem_ld32(tbase + c0, v);
+                    // beta S[(bin, slot), n] is the same for the K rows of a group: a constant shift
+                    // inside softmax_k that the max subtraction removes, so only acc is staged
+                    if (m < ep.M) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) xs[lane * 33 + i] = v[i];
                     }
                     __syncwarp();
                     switch (K) {
-                        case 4: demix_cols<4>(xs, os, ep, m0, n0, lane, scale2); break;
-                        case 8: demix_cols<8>(xs, os, ep, m0, n0, lane, scale2); break;
-                        case 16: demix_cols<16>(xs, os, ep, m0, n0, lane, scale2); break;
-                        default: demix_cols<32>(xs, os, ep, m0, n0, lane, scale2); break;
+                        case 4: demix_cols<4>(xs, os, ep, m0, svs, lane, scale2); break;
+                        case 8: demix_cols<8>(xs, os, ep, m0, svs, lane, scale2); break;
+                        case 16: demix_cols<16>(xs, os, ep, m0, svs, lane, scale2); break;
+                        default: demix_cols<32>(xs, os, ep, m0, svs, lane, scale2); break;
                     }
                     __syncwarp();
                     bf16* ot = reinterpret_cast<bf16*>(ep.out_t);

@@ -534,7 +534,7 @@ demix_block_kernel(const float* __restrict__ lbar, const float* __restrict__ S, 
 #pragma unroll 8
         for (int k = 0; k < K; ++k) {
             float e;
-            if constexpr (sizeof(T) == 2) e = exp2f((xv[k] - mx) * (inv_tau * 1.4426950408889634f));
+            if constexpr (sizeof(T) == 2) e = ex2_approx((xv[k] - mx) * (inv_tau * 1.4426950408889634f));
             else e = expf((xv[k] - mx) / tau);
             xv[k] = e;
             den += __float2uint_rn(e * 67108864.0f); // 2^26
