@@ -211,6 +211,12 @@ int cider_workload_code(const cider_workload_desc* w, int32_t* edges);
 /* Bins [first, first+n): truth (n x K x L, = sample_codewords) and S (n x L x Q fp32). */
 int cider_workload_bins(const cider_workload_desc* w, const int32_t* edges, int64_t first, int n,
                         int32_t* truth, float* S, int threads);
+/* The same bins generated on the device, into device buffers (truth_device n x K x L,
+ * S_device n x L x Q, e.g. from cider_device_alloc): one thread per bin replays the host generator's
+ * mt19937_64 stream and libstdc++ distributions; S equal to cider_workload_bins' up to the last ulp
+ * of a double exp/log (float results identical in practice). Synchronous. */
+int cider_workload_bins_device(const cider_workload_desc* w, const int32_t* edges, int64_t first, int n,
+                               int32_t* truth_device, float* S_device, int device);
 /* Permutation-invariant SER/CER (= ura::ser_cer, metrics.cpp:124-145) summed over n bins. */
 int cider_ser_cer(int n, int K, int L, const int32_t* truth, const int32_t* pred, double* ser_sum,
                   double* cer_sum);

@@ -113,6 +113,7 @@ def lib() -> C.CDLL:
         h.cider_nccl_allgather.argtypes = [P, P, P, C.c_size_t]
         h.cider_workload_code.argtypes = [C.POINTER(WorkloadDesc), P]
         h.cider_workload_bins.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
+        h.cider_workload_bins_device.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
         h.cider_ser_cer.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         h.cider_check_update_wht.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, C.c_int]
         h.cider_bp_create.argtypes = [C.c_int, C.c_uint32, C.POINTER(CodeDesc), C.c_int, C.POINTER(C.c_void_p)]
@@ -254,6 +255,7 @@ class Context:
         cd, self._edges = code_desc(edges, checks, slots)
         md = model.desc()
         h = C.c_void_p()
+        self.device = device
         _check(lib().cider_create(C.byref(md), _ptr(self._w), C.byref(cd), device, C.byref(h)))
         self.h = h
 
@@ -393,6 +395,28 @@ class Workload:
         truth = np.empty((n, self.k, self.slots), dtype=np.int32)
         S = out_S if out_S is not None else np.empty((n, self.slots, 1 << self.m), dtype=np.float32)
         _check(lib().cider_workload_bins(C.byref(d), _ptr(edges), first, n, _ptr(truth), _ptr(S), threads))
+        return truth, S
+
+    def bins_device(self, ctx: "Context", edges: np.ndarray, first: int, n: int, copy_back: bool = True):
+        """The same bins generated on the device into buffers of `ctx`; returns host
+        copies (truth, S) or, with copy_back=False, the device pointers (the caller frees them)."""
+        d = self.desc()
+        edges = np.ascontiguousarray(edges, dtype=np.int32)
+        q = 1 << self.m
+        tb, sb = n * self.k * self.slots * 4, n * self.slots * q * 4
+        dt, ds = C.c_void_p(), C.c_void_p()
+        _check(lib().cider_device_alloc(ctx.h, tb, C.byref(dt)))
+        _check(lib().cider_device_alloc(ctx.h, sb, C.byref(ds)))
+        _check(lib().cider_workload_bins_device(C.byref(d), _ptr(edges), first, n, dt, ds, ctx.device))
+        if not copy_back:
+            return dt, ds
+        truth = np.empty((n, self.k, self.slots), dtype=np.int32)
+        S = np.empty((n, self.slots, q), dtype=np.float32)
+        _check(lib().cider_memcpy_d2h(ctx.h, _ptr(truth), dt, tb))
+        _check(lib().cider_memcpy_d2h(ctx.h, _ptr(S), ds, sb))
+        _check(lib().cider_synchronize(ctx.h))
+        _check(lib().cider_device_free(ctx.h, dt))
+        _check(lib().cider_device_free(ctx.h, ds))
         return truth, S
 
 

@@ -35,6 +35,7 @@
 #include "kernels/pool_mma.cuh"
 #include "kernels/wht.cuh"
 #include "kernels/bp.cuh"
+#include "kernels/workload.cuh"
 #include "kernels/path.cuh"
 
 namespace cider {
@@ -1823,6 +1824,42 @@ int cider_sic_decode(cider_bp_ctx* c, int B, int K, const double* S, const cider
         }
         ck(cudaMemcpyAsync(grid, c->grid.p, size_t(B) * K * c->L * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
         ck(cudaStreamSynchronize(c->stream), "sic_decode");
+    });
+}
+
+int cider_workload_bins_device(const cider_workload_desc* w, const int32_t* edges, int64_t first, int n,
+                               int32_t* truth_device, float* S_device, int device) {
+    return guard([&] {
+        Gf gf(w->m, 0);
+        const int L = w->slots, P = w->checks, K = w->k, Q = gf.q;
+        if (K < 1) throw InvalidInput("sample_codewords: need K >= 1");
+        if (K > wl::WL_MAXK || Q > wl::WL_MAXQ || L > wl::WL_MAXL) throw InvalidInput("workload_bins_device: shape too large");
+        if (n <= 0) return;
+        cider_code_desc cd{P, L, L * w->col_weight, edges};
+        Tanner t(&cd, Q);
+        std::vector<int> info, pivot;
+        std::vector<uint8_t> red, mul(size_t(Q) * Q);
+        systematic_tables(gf, t, info, pivot, red);
+        for (int a = 0; a < Q; ++a)
+            for (int b = 0; b < Q; ++b) mul[size_t(a) * Q + b] = uint8_t(gf.mul(a, b));
+        require_device();
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        DevBuf di, dp, dr, dm;
+        auto up = [&](DevBuf& b, const void* src, size_t bytes) {
+            b.ensure(std::max<size_t>(bytes, 16));
+            if (bytes) ck(cudaMemcpy(b.p, src, bytes, cudaMemcpyHostToDevice), "upload");
+        };
+        up(di, info.data(), info.size() * 4);
+        up(dp, pivot.data(), pivot.size() * 4);
+        up(dr, red.data(), red.size());
+        up(dm, mul.data(), mul.size());
+        wl::Sys sys{int(info.size()), int(pivot.size()), di.as<int>(), dp.as<int>(), dr.as<uint8_t>(), dm.as<uint8_t>()};
+        const double sigma = std::pow(10.0, -w->snr_db / 20.0);
+        wl::workload_bins_kernel<<<unsigned((n + 63) / 64), 64>>>(sys, L, K, Q, sigma, w->p_erase, w->p_false,
+                                                                  w->master_seed, first, n, truth_device, S_device);
+        check_launch("workload_bins");
+        ck(cudaDeviceSynchronize(), "workload_bins");
+        di.release(); dp.release(); dr.release(); dm.release();
     });
 }
 

@@ -325,6 +325,17 @@ int guard(F&& f) {
 
 } // namespace
 
+void systematic_tables(const Gf& gf, const Tanner& t, std::vector<int>& info, std::vector<int>& pivot,
+                       std::vector<uint8_t>& red) {
+    Systematic s = systematic_form(gf, t);
+    info = s.info;
+    pivot = s.pivot;
+    red.assign(s.pivot.size() * s.info.size(), 0);
+    for (size_t i = 0; i < s.pivot.size(); ++i)
+        for (size_t j = 0; j < s.info.size(); ++j) red[i * s.info.size() + j] = uint8_t(s.red[i][j]);
+}
+
+
 const char* host_last_error() { return g_host_err.c_str(); }
 
 } // namespace cider

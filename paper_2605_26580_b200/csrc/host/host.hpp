@@ -52,6 +52,11 @@ struct Tanner {
     int n_edges() const { return int(chk.size()); }
 };
 
+// systematic encoder of H (info slots, pivot slots, pivot-row coefficients [pivot][info]) for the
+// device workload generator (kernels/workload.cuh)
+void systematic_tables(const Gf& gf, const Tanner& t, std::vector<int>& info, std::vector<int>& pivot,
+                       std::vector<uint8_t>& red);
+
 size_t weights_count(const cider_model_desc* m);
 void validate_model(const cider_model_desc* m);
 

@@ -357,3 +357,22 @@ def test_bp_errors_like_the_reference(P):
         dec.bp_decode(lam, P.BpConfig(message_floor=0.0))
     with pytest.raises(ValueError, match="K >= 1"):
         dec.sic_decode(np.zeros((1, wl.slots, 16)), 0)
+
+
+# ---- the BASELINE evidence generator on the device --------------------------------
+@pytest.mark.parametrize("name,first,n", [("c1", 0, 64), ("c2", 7, 48), ("c3", 3, 12), ("c4", 0, 6), ("c5", 100, 8)])
+def test_device_workload_matches_host_generator(P, name, first, n):
+    """Device bins (one thread per bin, mt19937_64 + the libstdc++ distributions restated) vs the
+    host generator: identical codewords; S identical except where a double exp/log differs from
+    glibc in the last ulp (then within one float ulp)."""
+    cfg = P.configs()[name]
+    wl = cfg.workload
+    e = wl.code()
+    ctx = P.Context(P.Model(m=wl.m, dim=64, hidden=64, precision=P.FP32), P.weights_init(P.Model(m=wl.m, dim=64, hidden=64), 1),
+                    e, wl.checks, wl.slots)
+    th, Sh = wl.bins(e, first, n)
+    td, Sd = wl.bins_device(ctx, e, first, n)
+    assert np.array_equal(th, td)
+    diff = Sd != Sh
+    assert diff.mean() < 1e-4
+    assert np.all(np.abs(Sd - Sh) <= np.spacing(np.abs(Sh)) * 1.0001)
