@@ -80,6 +80,23 @@ __device__ __forceinline__ void mma_bf16_2sm_ts(uint32_t d_tmem, uint32_t a_tmem
         "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) { // 16 columns, waited
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -160,6 +177,7 @@ struct Mlp2Layout {
     static_assert(KB1 % W1_PER_SLOT == 0, "input width must be a multiple of 128");
 };
 
+constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hidden columns = one MMA2 k-step)
 constexpr int MLP2_MMA2_WARP = 10;
 constexpr int MLP2_XLOAD_WARP = 11;
 constexpr int MLP2_THREADS = 384; // ring producer, MMA1 issuer, 8 epilogue warps (2-9), MMA2 issuer, X producer
@@ -183,8 +201,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint64_t* r_full = x_empty + KB1;
     uint64_t* r_empty = r_full + NS;
     uint64_t* a1_full = r_empty + NS;   // [2] first-layer accumulator ready
-    uint64_t* h_full = a1_full + 2;     // [2][2] GELU group g of acc1[b] packed (leader copy counts both CTAs)
-    uint64_t* a1_free = h_full + 4;     // [2] MMA2 done reading acc1[b] (leader only)
+    uint64_t* h_full = a1_full + 2;     // [2][GG] GELU group g of acc1[b] packed (leader copy counts both CTAs)
+    uint64_t* a1_free = h_full + 2 * MLP2_GG; // [2] MMA2 done reading acc1[b] (leader only)
     uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
@@ -206,8 +224,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&a1_full[b], 1);
-            mbar_init(&h_full[2 * b], EPI_ARRIVALS);
-            mbar_init(&h_full[2 * b + 1], EPI_ARRIVALS);
+            for (int g = 0; g < MLP2_GG; ++g) mbar_init(&h_full[MLP2_GG * b + g], EPI_ARRIVALS);
             mbar_init(&a1_free[b], 1);
         }
         mbar_init(a2_full, 1);
@@ -337,14 +354,14 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     for (int c = 0; c < NC; ++c, ++n) {
                         const int b = n & 1;
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 0] = clock64();
-                        // acc2 += H(c) . W2(c)^T with A = bf16 hidden in TMEM. Hidden columns [64 kb + 32 g,
-                        // +32) are GELU group g of warp-half kb, packed at TMEM cols 64 kb + 16 g: k-steps
-                        // 2g, 2g+1 of W2 slot kb. Group 0 of both halves is issued as soon as it lands.
+                        // acc2 += H(c) . W2(c)^T with A = bf16 hidden in TMEM. Hidden columns [64 kb + 16 g, +16)
+                        // are GELU group g of warp-half kb, packed in place at TMEM cols 64 kb + 8 g: k-step g
+                        // of W2 slot kb, issued as soon as that group lands in both CTAs.
                         const uint32_t a_base = tmem + 256 + b * MLP_HC;
                         int slots[S2];
 #pragma unroll
-                        for (int g = 0; g < 2; ++g) {
-                            mbar_wait(&h_full[2 * b + g], (hph >> b) & 1u);
+                        for (int g = 0; g < MLP2_GG; ++g) {
+                            mbar_wait(&h_full[MLP2_GG * b + g], (hph >> b) & 1u);
                             fence_after();
                             if (g == 0) {
                                 if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
@@ -363,10 +380,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                     fence_after();
                                 }
                                 const uint64_t db = sw128_desc(ring + slots[kb] * Lay::SLOT);
-#pragma unroll
-                                for (int kk = 2 * g; kk < 2 * g + 2; ++kk)
-                                    mma_bf16_2sm_ts(tmem, a_base + kb * 64 + kk * 8, db + uint64_t(kk * 2), id2, (c | kb | kk) != 0);
-                                if (g == 1) mma_commit_2sm(&r_empty[slots[kb]]);
+                                mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, (c | kb | g) != 0);
+                                if (g == MLP2_GG - 1) mma_commit_2sm(&r_empty[slots[kb]]);
                             }
                         }
                         hph ^= 1u << b;
@@ -405,29 +420,26 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 e1ph ^= 1u << b;
                 fence_after();
                 if (tr) args.trace[it * 64 + c * 8 + 3] = clock64();
-                // fp32 columns [64 half, 64 half + 64) -> GELU -> bf16 pairs packed into the first 32
-                // of those columns (32 g .. ): every column is read before it is overwritten.
+                // fp32 columns [64 half, 64 half + 64) -> GELU -> bf16 pairs packed IN PLACE, group g (16
+                // columns) at [8 g, 8 g + 8): every column is read (by this warp) before it is overwritten.
                 const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 64;
 #pragma unroll
-                for (int g = 0; g < ((args.dbg & 1) ? 0 : 2); ++g) {
-                    float v[32];
-                    tmem_ld32(base + g * 32, v);
-                    uint32_t pk[16];
+                for (int g = 0; g < MLP2_GG; ++g) {
+                    if (!(args.dbg & 1)) {
+                        float v[16];
+                        tmem_ld16(base + g * 16, v);
+                        uint32_t pk[8];
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        const float4 bb = bias4[g * 8 + i / 4];
-                        pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
-                        pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 bb = bias4[g * 4 + i / 4];
+                            pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
+                            pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
+                        }
+                        tmem_st8(base + g * 8, pk);
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     }
-                    tmem_st16(base + g * 16, pk);
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     fence_before();
-                    release(L_h_full0 + (2 * b + g) * 8); // group g of both halves -> MMA2 k-steps 2g, 2g+1
-                }
-                if (args.dbg & 1) { // timing experiment (GELU skipped): still release both groups
-                    fence_before();
-                    release(L_h_full0 + (2 * b) * 8);
-                    release(L_h_full0 + (2 * b + 1) * 8);
+                    release(L_h_full0 + (MLP2_GG * b + g) * 8); // group g of both halves -> MMA2 k-step g
                 }
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
