@@ -131,6 +131,14 @@ int cider_denoise(cider_ctx* ctx, int B, int K, const int32_t* X, const float* S
 int cider_refine(cider_ctx* ctx, int B, int K, const float* S, const cider_schedule* sched,
                  const cider_remask* remask, int32_t* grid, float* final_logits, cider_trace* trace);
 
+/* Ragged loads (the protocol's bins carry K_chi in 1..k_max, protocol.cpp:41-88):
+ * B bins with loads[b] users each, S: B x L x Q; bins are bucketed by load and each bucket runs as
+ * one device batch with sched_by_load[K-1] / remask_by_load[K-1] (nullable: no remasking), the
+ * per-load tables of run_protocol's DecoderBank. grids: the bins' K x L grids concatenated in input
+ * order (sum(loads) x L). Results equal per-bin cider_refine calls. */
+int cider_refine_ragged(cider_ctx* ctx, int B, const int32_t* loads, const float* S, int k_max,
+                        const cider_schedule* sched_by_load, const cider_remask* remask_by_load, int32_t* grids);
+
 /* Same, with S and grid in device memory (allocated by cider_device_alloc); async on the
  * context stream; trace ignored. */
 int cider_refine_device(cider_ctx* ctx, int B, int K, const float* S_device,

@@ -166,6 +166,47 @@ public:
         return out;
     }
 
+    // ragged loads in one call (cider_refine_ragged): bin b has loads[b] users, decoded with the
+    // reference's per-load schedule and remask thresholds (default_steps_for_load /
+    // default_remask_thresholds, refine.cpp:28-46) — what a DecoderBank of make_bin_decoder applies
+    // bin by bin inside run_protocol_frame (protocol.cpp:41-88), as one batch per load
+    std::vector<ura::SymbolGrid> run_ragged(const std::vector<const ura::EvidenceMatrix*>& ss, const std::vector<int>& loads,
+                                            const ura::ParityCheckMatrix& h, int k_max, bool per_load_remask = true) const {
+        ctx_->require_same(h);
+        const int B = int(ss.size()), L = ctx_->slots(), Q = ctx_->q();
+        if (int(loads.size()) != B) throw std::domain_error("run_ragged: one load per bin");
+        std::vector<float> S(size_t(B) * L * Q);
+        for (int b = 0; b < B; ++b)
+            for (size_t i = 0; i < size_t(L) * Q; ++i) S[size_t(b) * L * Q + i] = float(ss[b]->v[i]);
+        std::vector<cider_schedule> sc(k_max);
+        std::vector<cider_remask> rm(k_max);
+        for (int k = 1; k <= k_max; ++k) {
+            sc[k - 1] = cider_schedule{ura::default_steps_for_load(k), 1.0, 1.0, 1};
+            rm[k - 1] = cider_remask{};
+            rm[k - 1].mode = CIDER_REMASK_NONE;
+            if (per_load_remask) {
+                const auto th = ura::default_remask_thresholds(k);
+                if (th.size() > CIDER_MAX_THRESHOLDS) throw std::domain_error("remask: too many thresholds");
+                rm[k - 1].mode = th.empty() ? CIDER_REMASK_NONE : CIDER_REMASK_THRESHOLD;
+                rm[k - 1].n_thresholds = int(th.size());
+                for (size_t i = 0; i < th.size(); ++i) rm[k - 1].thresholds[i] = th[i];
+            }
+        }
+        std::vector<int32_t> ld(loads.begin(), loads.end());
+        size_t rows = 0;
+        for (int k : loads) rows += size_t(k);
+        std::vector<int32_t> g(rows * L);
+        check(cider_refine_ragged(ctx_->get(), B, ld.data(), S.data(), k_max, sc.data(), rm.data(), g.data()));
+        std::vector<ura::SymbolGrid> out;
+        size_t o = 0;
+        for (int b = 0; b < B; ++b) {
+            out.emplace_back(loads[b], L);
+            std::copy(g.begin() + o * L, g.begin() + (o + loads[b]) * L, out.back().v.begin());
+            o += size_t(loads[b]);
+        }
+        return out;
+    }
+
 private:
     ura::SymbolGrid run(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h, const ura::RevealSchedule& sched,
                         const cider_remask* rm, int k) const {

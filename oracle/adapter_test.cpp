@@ -76,6 +76,28 @@ int main() {
         const bool shape_ok = out.rows == 2 && out.cols == 16;
         std::printf("BinDecoder call: %s\n", shape_ok ? "ok" : "FAILED");
         fails += !shape_ok;
+        // (4b) ragged loads: one GpuRefiner::run_ragged call == per-bin BinDecoder calls (per-load defaults)
+        {
+            auto bank_dec = cider::make_bin_decoder(ctx);
+            std::mt19937_64 r4(11);
+            std::normal_distribution<double> nd(0.0, 1.0);
+            std::vector<ura::EvidenceMatrix> ev(6, ura::EvidenceMatrix(16, 64));
+            std::vector<const ura::EvidenceMatrix*> ptrs;
+            const std::vector<int> loads{1, 2, 3, 3, 1, 2};
+            for (auto& m : ev) {
+                for (double& x : m.v) x = double(float(1.2 * nd(r4)));
+                ptrs.push_back(&m);
+            }
+            auto rag = refiner.run_ragged(ptrs, loads, h, 3);
+            int same = 0;
+            for (size_t b = 0; b < ev.size(); ++b) {
+                ura::SymbolGrid tk(loads[b], 16);
+                auto one = bank_dec(ura::BinTask{gf, h, ev[b], tk, loads[b]});
+                same += one.v == rag[b].v && one.rows == rag[b].rows;
+            }
+            std::printf("ragged batch vs per-bin decoder: %d/%d identical grids\n", same, int(ev.size()));
+            fails += same != int(ev.size());
+        }
         // (5) SIC-BP: ura::sic_decode vs cider::GpuBp (bp.hpp:72-93), same evidence, identical grids
         {
             cider::GpuBp gbp(gf, h);

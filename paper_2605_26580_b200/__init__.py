@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
         h.cider_denoise.argtypes = [P, C.c_int, C.c_int, P, P, P, P]
         h.cider_refine.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P, P,
                                    C.POINTER(TraceDesc)]
+        h.cider_refine_ragged.argtypes = [P, C.c_int, P, P, C.c_int, P, P, P]
         h.cider_refine_device.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P]
         h.cider_device_count.argtypes = [C.POINTER(C.c_int)]
         h.cider_device_alloc.argtypes = [P, C.c_size_t, C.POINTER(C.c_void_p)]
@@ -306,6 +307,26 @@ class Context:
         if want_trace:
             out.append(tr)
         return out[0] if len(out) == 1 else tuple(out)
+
+    def refine_ragged(self, S: np.ndarray, loads, sched_by_load, remask_by_load=None):
+        """Bins of different loads K (1..k_max) in one call (cider_refine_ragged):
+        sched_by_load[K-1] / remask_by_load[K-1] as a DecoderBank's per-load configs; returns the
+        bins' K x L grids in input order."""
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        B, L, _q = S.shape
+        ld = np.ascontiguousarray(loads, dtype=np.int32)
+        k_max = len(sched_by_load)
+        sd = (ScheduleDesc * k_max)(*[x.desc() for x in sched_by_load])
+        rd = None
+        if remask_by_load is not None:
+            rd = (RemaskDesc * k_max)(*[(x or RemaskConfig()).desc() for x in remask_by_load])
+        flat = np.empty((int(ld.sum()), L), dtype=np.int32)
+        _check(lib().cider_refine_ragged(self.h, B, _ptr(ld), _ptr(S), k_max, sd, rd, _ptr(flat)))
+        out, o = [], 0
+        for k in ld:
+            out.append(flat[o:o + k])
+            o += int(k)
+        return out
 
     # instrumentation
     def launch_count(self) -> int:

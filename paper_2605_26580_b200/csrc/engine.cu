@@ -1607,6 +1607,35 @@ int cider_refine(cider_ctx* c, int B, int K, const float* S, const cider_schedul
     });
 }
 
+int cider_refine_ragged(cider_ctx* c, int B, const int32_t* loads, const float* S, int k_max,
+                        const cider_schedule* sched_by_load, const cider_remask* remask_by_load, int32_t* grids) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        if (B < 0 || k_max < 1) throw InvalidInput("refine_ragged: need B >= 0 and k_max >= 1");
+        if (!sched_by_load) throw InvalidInput("refine_ragged: null schedule table");
+        std::vector<int64_t> off(size_t(B) + 1, 0);
+        for (int b = 0; b < B; ++b) {
+            if (loads[b] < 1 || loads[b] > k_max) throw InvalidInput("refine_ragged: bin load outside 1..k_max");
+            off[b + 1] = off[b] + int64_t(loads[b]) * c->L;
+        }
+        const size_t srow = size_t(c->L) * c->Q;
+        std::lock_guard<std::mutex> lk(c->mu);
+        for (int k = 1; k <= k_max; ++k) { // one device batch per load (BinTask's load, protocol.hpp:32-40)
+            std::vector<int> idx;
+            for (int b = 0; b < B; ++b)
+                if (loads[b] == k) idx.push_back(b);
+            if (idx.empty()) continue;
+            const int n = int(idx.size());
+            std::vector<float> Sb(size_t(n) * srow);
+            for (int i = 0; i < n; ++i) std::copy(S + size_t(idx[i]) * srow, S + size_t(idx[i] + 1) * srow, Sb.begin() + size_t(i) * srow);
+            std::vector<int32_t> g(size_t(n) * k * c->L);
+            refine_impl(c, n, k, Sb.data(), false, &sched_by_load[k - 1], remask_by_load ? &remask_by_load[k - 1] : nullptr,
+                        g.data(), false, nullptr, nullptr);
+            for (int i = 0; i < n; ++i) std::copy(g.begin() + size_t(i) * k * c->L, g.begin() + size_t(i + 1) * k * c->L, grids + off[idx[i]]);
+        }
+    });
+}
+
 int cider_refine_device(cider_ctx* c, int B, int K, const float* S_device, const cider_schedule* sched,
                         const cider_remask* rm, int32_t* grid_device) {
     return guard([&] {

@@ -376,3 +376,26 @@ def test_device_workload_matches_host_generator(P, name, first, n):
     diff = Sd != Sh
     assert diff.mean() < 1e-4
     assert np.all(np.abs(Sd - Sh) <= np.spacing(np.abs(Sh)) * 1.0001)
+
+
+# ---- ragged per-bin loads (protocol bins carry K_chi in 1..k_max) -----------------
+def test_refine_ragged_equals_per_load_calls(P):
+    """cider_refine_ragged buckets bins by load and runs each bucket with its own schedule / remask
+    (a DecoderBank's per-load configs); every bin's grid equals a uniform-K call on that bin."""
+    cfg = P.configs()["c2"]
+    wl = cfg.workload
+    e = wl.code()
+    model = P.Model(m=wl.m, dim=64, hidden=128, layers=1, heads=2, precision=P.FP32)
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    rng = np.random.default_rng(5)
+    loads = rng.integers(1, 5, size=12).astype(np.int32)
+    _, S = wl.bins(e, 0, 12)
+    scheds = [P.RevealSchedule(steps=2 + k) for k in range(4)]
+    rms = [None, P.RemaskConfig(thresholds=[0.5]), None, P.RemaskConfig(thresholds=[0.6, 0.3])]
+    grids = ctx.refine_ragged(S, loads, scheds, rms)
+    for b in range(12):
+        k = int(loads[b])
+        ref = ctx.refine(S[b:b + 1], k, scheds[k - 1], rms[k - 1])
+        assert grids[b].shape == (k, wl.slots) and np.array_equal(grids[b], ref[0])
+    with pytest.raises(ValueError, match="load outside"):
+        ctx.refine_ragged(S[:1], np.array([5], np.int32), scheds, rms)
