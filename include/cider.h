@@ -225,6 +225,13 @@ int cider_workload_bins(const cider_workload_desc* w, const int32_t* edges, int6
  * of a double exp/log (float results identical in practice). Synchronous. */
 int cider_workload_bins_device(const cider_workload_desc* w, const int32_t* edges, int64_t first, int n,
                                int32_t* truth_device, float* S_device, int device);
+/* Parity-check files (= ura::save_parity_file / load_parity_file, ldpc.cpp:197-226).
+ * load: edges (max_edges x 3, sorted (check, slot)) + header fields; a malformed or invalid file is
+ * CIDER_ERUNTIME with the reference's messages ("load_parity_file: malformed header in ..."). */
+int cider_save_parity_file(const char* path, const cider_code_desc* code, int q, int col_weight, uint32_t prim_poly,
+                           uint64_t seed);
+int cider_load_parity_file(const char* path, int max_edges, int32_t* edges, int* n_edges, int* checks, int* slots, int* q,
+                           int* col_weight, uint32_t* prim_poly, uint64_t* seed);
 /* Permutation-invariant SER/CER (= ura::ser_cer, metrics.cpp:124-145) summed over n bins. */
 int cider_ser_cer(int n, int K, int L, const int32_t* truth, const int32_t* pred, double* ser_sum,
                   double* cer_sum);

@@ -51,6 +51,8 @@ def _load(path: str, prefix: str) -> C.CDLL:
         h.ref_infer_temperature.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double]
         h.ref_infer_temperature.restype = C.c_double
         h.ref_remask_steps.argtypes = [C.c_int, C.c_int, C.c_int]
+        h.ref_save_parity_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_uint32, C.c_uint64]
+        h.ref_load_parity_file.argtypes = [C.c_char_p, C.c_int, P, P, P, P, P, P, P, P]
         h.ref_bp_decode.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, P, C.c_int, C.c_double, C.c_int, P, P, P, P]
         h.ref_sic_decode.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.c_int, C.c_double, C.c_int,
                                      C.c_double, P, P, P]
@@ -177,6 +179,18 @@ class Reference(Checker):
         self._check(self.h.ref_check_update_direct(m, inc.shape[0], _p(inc), _p(cf), target, _p(out)))
         return out
 
+
+    def save_parity_file(self, path: str, m: int, edges, checks: int, slots: int, col_weight: int, prim_poly: int, seed: int):
+        cd, _e = code_desc(edges, checks, slots)
+        self._check(self.h.ref_save_parity_file(path.encode(), m, C.byref(cd), col_weight, prim_poly, seed))
+
+    def load_parity_file(self, path: str, max_edges: int = 1 << 16):
+        e = np.empty((max_edges, 3), np.int32)
+        v = [C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_uint32(), C.c_uint64()]
+        self._check(self.h.ref_load_parity_file(path.encode(), max_edges, _p(e), *[C.byref(x) for x in v]))
+        n = v[0].value
+        return {"edges": e[:n].copy(), "checks": v[1].value, "slots": v[2].value, "q": v[3].value,
+                "col_weight": v[4].value, "prim_poly": v[5].value, "seed": v[6].value}
 
     def bp_decode(self, m: int, edges: np.ndarray, checks: int, slots: int, lam: np.ndarray, max_iters: int = 50,
                   message_floor: float = 1e-30, early_exit: bool = True):

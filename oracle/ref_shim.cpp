@@ -516,6 +516,36 @@ int ref_sic_decode(int m, const cider_code_desc* code, int B, int K, const doubl
     });
 }
 
+// ura::save_parity_file / load_parity_file (ldpc.cpp:197-226): the F4 file-format oracle
+int ref_save_parity_file(const char* path, int m, const cider_code_desc* code, int col_weight, uint32_t prim_poly,
+                         uint64_t seed) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        auto h = make_h(gf.q(), code);
+        ura::save_parity_file(path, h, ura::LdpcFileMeta{col_weight, prim_poly, seed});
+    });
+}
+int ref_load_parity_file(const char* path, int max_edges, int32_t* edges, int* n_edges, int* checks, int* slots, int* q,
+                         int* col_weight, uint32_t* prim_poly, uint64_t* seed) {
+    return guarded([&] {
+        ura::LdpcFileMeta meta;
+        auto h = ura::load_parity_file(path, &meta);
+        if (h.edge_count() > max_edges) throw std::runtime_error("ref_load_parity_file: buffer too small");
+        for (int e = 0; e < h.edge_count(); ++e) {
+            edges[3 * e] = h.edge(e).check;
+            edges[3 * e + 1] = h.edge(e).slot;
+            edges[3 * e + 2] = h.edge(e).coeff;
+        }
+        *n_edges = h.edge_count();
+        *checks = h.checks();
+        *slots = h.slots();
+        *q = h.q();
+        *col_weight = meta.col_weight;
+        *prim_poly = meta.prim_poly;
+        *seed = meta.seed;
+    });
+}
+
 int ref_cosine_target(int t, int steps, int initially_masked, int base) {
     return base + int(std::lround(ura::cosine_fraction(t, steps) * initially_masked));
 }

@@ -114,6 +114,8 @@ def lib() -> C.CDLL:
         h.cider_nccl_allgather.argtypes = [P, P, P, C.c_size_t]
         h.cider_workload_code.argtypes = [C.POINTER(WorkloadDesc), P]
         h.cider_workload_bins.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
+        h.cider_save_parity_file.argtypes = [C.c_char_p, C.POINTER(CodeDesc), C.c_int, C.c_int, C.c_uint32, C.c_uint64]
+        h.cider_load_parity_file.argtypes = [C.c_char_p, C.c_int, P, P, P, P, P, P, P, P]
         h.cider_workload_bins_device.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
         h.cider_ser_cer.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         h.cider_check_update_wht.argtypes = [C.c_int, C.c_int, C.c_int, P, P, P, C.c_int]
@@ -439,6 +441,23 @@ class Workload:
         _check(lib().cider_device_free(ctx.h, dt))
         _check(lib().cider_device_free(ctx.h, ds))
         return truth, S
+
+
+def save_parity_file(path: str, edges, checks: int, slots: int, q: int, col_weight: int = 0, prim_poly: int = 0,
+                     seed: int = 0) -> None:
+    """ura::save_parity_file (ldpc.cpp:197-205)."""
+    cd, _e = code_desc(edges, checks, slots)
+    _check(lib().cider_save_parity_file(path.encode(), C.byref(cd), q, col_weight, prim_poly, seed))
+
+
+def load_parity_file(path: str, max_edges: int = 1 << 16) -> dict:
+    """ura::load_parity_file (ldpc.cpp:207-226): edges sorted (check, slot) + header fields."""
+    e = np.empty((max_edges, 3), np.int32)
+    v = [C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_uint32(), C.c_uint64()]
+    _check(lib().cider_load_parity_file(path.encode(), max_edges, _ptr(e), *[C.byref(x) for x in v]))
+    n = v[0].value
+    return {"edges": e[:n].copy(), "checks": v[1].value, "slots": v[2].value, "q": v[3].value,
+            "col_weight": v[4].value, "prim_poly": v[5].value, "seed": v[6].value}
 
 
 def ser_cer(truth: np.ndarray, pred: np.ndarray):

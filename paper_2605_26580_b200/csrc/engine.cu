@@ -44,6 +44,7 @@ const char* host_last_error();
 namespace {
 
 thread_local std::string g_err;
+thread_local uint64_t g_err_tick = 0;
 
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
@@ -237,9 +238,11 @@ int guard(F&& f) {
         return CIDER_OK;
     } catch (const std::domain_error& e) {
         g_err = e.what();
+        g_err_tick = error_tick();
         return CIDER_EINVAL;
     } catch (const std::exception& e) {
         g_err = e.what();
+        g_err_tick = error_tick();
         return CIDER_ERUNTIME;
     }
 }
@@ -1437,7 +1440,7 @@ void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
 extern "C" {
 
 const char* cider_last_error(void) {
-    if (!g_err.empty()) return g_err.c_str();
+    if (g_err_tick >= host_error_tick()) return g_err.c_str(); // the later failure of this thread
     return host_last_error();
 }
 

@@ -8,6 +8,7 @@
 // tests/test_workload.py against oracle/_ref (the reference's own code).
 #include <algorithm>
 #include <atomic>
+#include <fstream>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -308,6 +309,7 @@ void assignment(int K, const std::vector<int>& cost, std::vector<int>& perm, int
 }
 
 thread_local std::string g_host_err;
+thread_local uint64_t g_host_err_tick = 0;
 
 template <class F>
 int guard(F&& f) {
@@ -316,9 +318,11 @@ int guard(F&& f) {
         return CIDER_OK;
     } catch (const std::domain_error& e) {
         g_host_err = e.what();
+        g_host_err_tick = error_tick();
         return CIDER_EINVAL;
     } catch (const std::exception& e) {
         g_host_err = e.what();
+        g_host_err_tick = error_tick();
         return CIDER_ERUNTIME;
     }
 }
@@ -337,6 +341,11 @@ void systematic_tables(const Gf& gf, const Tanner& t, std::vector<int>& info, st
 
 
 const char* host_last_error() { return g_host_err.c_str(); }
+uint64_t host_error_tick() { return g_host_err_tick; }
+uint64_t error_tick() { // per-thread order of failures across the host and engine halves of the ABI
+    static thread_local uint64_t t = 0;
+    return ++t;
+}
 
 } // namespace cider
 
@@ -417,6 +426,56 @@ int cider_workload_bins(const cider_workload_desc* w, const int32_t* edges, int6
                     for (int a = 0; a < Q; ++a) S[(size_t(i) * L + l) * Q + a] = float(y[a] - lse);
             }
         });
+    });
+}
+
+// Parity-check file (ldpc.cpp:197-226): header "P L Q col_weight prim_poly seed",
+// then one "check slot coeff" line per edge; load validates like ParityCheckMatrix (ldpc.cpp:11-30).
+int cider_save_parity_file(const char* path, const cider_code_desc* code, int q, int col_weight, uint32_t prim_poly,
+                           uint64_t seed) {
+    return guard([&] {
+        Tanner t(code, q); // validates and sorts (check, slot) like the reference's constructor
+        std::ofstream out(path);
+        if (!out) throw std::runtime_error(std::string("save_parity_file: cannot open ") + path);
+        out << t.checks << ' ' << t.slots << ' ' << q << ' ' << col_weight << ' ' << prim_poly << ' ' << seed << '\n';
+        for (int e = 0; e < t.n_edges(); ++e) out << t.chk[e] << ' ' << t.slot[e] << ' ' << t.coef[e] << '\n';
+        if (!out) throw std::runtime_error(std::string("save_parity_file: write failed for ") + path);
+    });
+}
+
+int cider_load_parity_file(const char* path, int max_edges, int32_t* edges, int* n_edges, int* checks, int* slots, int* q,
+                           int* col_weight, uint32_t* prim_poly, uint64_t* seed) {
+    return guard([&] {
+        std::ifstream in(path);
+        if (!in) throw std::runtime_error(std::string("load_parity_file: cannot open ") + path);
+        int p = 0, l = 0, qq = 0, w = 0;
+        uint32_t poly = 0;
+        uint64_t sd = 0;
+        if (!(in >> p >> l >> qq >> w >> poly >> sd))
+            throw std::runtime_error(std::string("load_parity_file: malformed header in ") + path);
+        std::vector<int32_t> e;
+        int a, b, c;
+        while (in >> a >> b >> c) e.insert(e.end(), {a, b, c});
+        if (!in.eof()) throw std::runtime_error(std::string("load_parity_file: malformed entry line in ") + path);
+        cider_code_desc cd{p, l, int(e.size() / 3), e.data()};
+        try {
+            Tanner t(&cd, qq);
+            if (t.n_edges() > max_edges) throw std::runtime_error("load_parity_file: edge buffer too small");
+            for (int i = 0; i < t.n_edges(); ++i) {
+                edges[3 * i] = t.chk[i];
+                edges[3 * i + 1] = t.slot[i];
+                edges[3 * i + 2] = t.coef[i];
+            }
+            *n_edges = t.n_edges();
+        } catch (const InvalidInput& err) {
+            throw std::runtime_error(std::string("load_parity_file: invalid matrix in ") + path + ": " + err.what());
+        }
+        *checks = p;
+        *slots = l;
+        *q = qq;
+        *col_weight = w;
+        *prim_poly = poly;
+        *seed = sd;
     });
 }
 

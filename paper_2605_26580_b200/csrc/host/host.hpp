@@ -52,6 +52,10 @@ struct Tanner {
     int n_edges() const { return int(chk.size()); }
 };
 
+// failure ordering for cider_last_error (the most recent message of either half of the ABI)
+uint64_t error_tick();
+uint64_t host_error_tick();
+
 // systematic encoder of H (info slots, pivot slots, pivot-row coefficients [pivot][info]) for the
 // device workload generator (kernels/workload.cuh)
 void systematic_tables(const Gf& gf, const Tanner& t, std::vector<int>& info, std::vector<int>& pivot,
