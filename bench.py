@@ -53,6 +53,29 @@ def peaks():
         return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "fallback": True}
 
 
+def kernel_rooflines(st, tot_ms, pk):
+    """Per kernel class of one profiled step: algorithmic work (engine's Launch accounting: executed
+    2MNK FLOPs, compulsory HBM bytes) over CUDA-event time, against the bound its arithmetic
+    intensity implies (ridge = measured bf16 sustained / HBM)."""
+    peak_t, peak_b = pk.get("bf16_tflops_sustained", 1360.2), pk.get("hbm_gbs", 6539.2)
+    ridge = peak_t * 1e12 / (peak_b * 1e9)
+    out = {}
+    for k, v in sorted(st.items(), key=lambda kv: -kv[1]["ms"]):
+        if v["ms"] <= 0 or 100 * v["ms"] / max(tot_ms, 1e-9) < 0.5:
+            continue
+        fl, by, sec = v["flops"], v["bytes"], v["ms"] / 1e3
+        tensor = fl > 0 and (by <= 0 or fl / by >= ridge)
+        if tensor:
+            ach = fl / sec / 1e12
+            out[k] = {"ms": round(v["ms"], 2), "share": round(v["ms"] / tot_ms, 4), "bound": "tensor",
+                      "achieved": round(ach, 1), "unit": "TFLOP/s", "frac": round(ach / peak_t, 4)}
+        elif by > 0:
+            ach = by / sec / 1e9
+            out[k] = {"ms": round(v["ms"], 2), "share": round(v["ms"] / tot_ms, 4), "bound": "hbm",
+                      "achieved": round(ach, 1), "unit": "GB/s", "frac": round(ach / peak_b, 4)}
+    return out
+
+
 DEFAULT_BINS = {"c1": 64, "c2": 4096, "c3": 2048, "c4": 1024, "c5": 2048}
 
 
@@ -380,7 +403,8 @@ def main():
                                    "share_of_step": round(g_ms / max(tot_ms, 1e-9), 4)},
             "step_algorithmic_tflops": round(step_tflops, 1),
             "step_frac": round(step_tflops / pk.get("bf16_tflops_sustained", 1360.2) / world, 4),
-            "top_kernels_ms": {k: round(v["ms"], 2) for k, v in top}}
+            "top_kernels_ms": {k: round(v["ms"], 2) for k, v in top},
+            "kernels": kernel_rooflines(st, tot_ms, pk)}
 
     line = {"metric": METRIC, "value": round(value, 2), "unit": "bins/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(t_max / a.steps, 2), "higher_is_better": True, "scaling": "weak",
