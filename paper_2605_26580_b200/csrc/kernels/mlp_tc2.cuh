@@ -487,29 +487,32 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     for (int i = 0; i < 32; i += 4) {
                         const float4 bb = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + s2 * 32 + i))
                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-                        v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
+                        const float2 lo = __fadd2_rn(make_float2(v[i], v[i + 1]), make_float2(bb.x, bb.y));
+                        const float2 hi = __fadd2_rn(make_float2(v[i + 2], v[i + 3]), make_float2(bb.z, bb.w));
+                        v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;
                     }
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
+                    for (int i = 0; i < 32; i += 2) { // element pairs with the packed fp32 ops
                         const int w = s2 * 16 + i / 2; // packed-pair index within the k-block
-                        float a0 = v[i], a1 = v[i + 1];
+                        float2 a = make_float2(v[i], v[i + 1]);
                         if (reads_z) {
                             const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zr[w]));
                             if (reads_e) {
                                 const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&er[w]));
-                                const float g0 = sigmoid_fast(a0), g1 = sigmoid_fast(a1);
-                                a0 = fmaf(g0, z2.x - e2.x, e2.x); // g z + (1 - g) e
-                                a1 = fmaf(g1, z2.y - e2.y, e2.y);
+                                // g = 0.5 tanh(a / 2) + 0.5;  out = g (z - e) + e
+                                const float2 h = __fmul2_rn(a, make_float2(0.5f, 0.5f));
+                                const float2 g = __ffma2_rn(make_float2(tanh_approx(h.x), tanh_approx(h.y)), make_float2(0.5f, 0.5f),
+                                                            make_float2(0.5f, 0.5f));
+                                a = __ffma2_rn(g, __fadd2_rn(z2, make_float2(-e2.x, -e2.y)), e2);
                             } else {
-                                a0 += z2.x;
-                                a1 += z2.y;
+                                a = __fadd2_rn(a, z2);
                             }
                         }
                         if (ep.out_f && live) {
-                            v[i] = a0;
-                            v[i + 1] = a1;
+                            v[i] = a.x;
+                            v[i + 1] = a.y;
                         }
-                        __nv_bfloat162 p = __floats2bfloat162_rn(a0, a1);
+                        __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
                         pk[w] = *reinterpret_cast<uint32_t*>(&p);
                     }
                     if (ep.out_f && live) {
