@@ -99,11 +99,11 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int cols, int ld, int box_ro
 }
 
 // W1 of the 2-SM MLP as {64 cols, rows, k-blocks}: one box = box_rows rows x 2 k-blocks (16 KB)
-CUtensorMap make_map_w1_3d(const void* ptr, int64_t rows, int cols, int box_rows) {
+CUtensorMap make_map_w1_3d(const void* ptr, int64_t rows, int cols, int box_rows, int box_kb = 2) {
     CUtensorMap m;
     cuuint64_t dims[3] = {64, cuuint64_t(rows), cuuint64_t(cols / 64)};
     cuuint64_t strides[2] = {cuuint64_t(cols) * 2, 128};
-    cuuint32_t box[3] = {64, cuuint32_t(box_rows), 2};
+    cuuint32_t box[3] = {64, cuuint32_t(box_rows), cuuint32_t(box_kb)};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -440,7 +440,7 @@ void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, cons
 template <int KIN, int D, int EPK>
 void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
                  const CUtensorMap& w2, const tc::MlpArgs& a) {
-    using Lay = tc::Mlp2Layout<KIN, D>;
+    using Lay = tc::Mlp2LayoutFor<KIN, D, EPK>;
     static bool attr_set = false;
     if (!attr_set) {
         ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D, EPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
@@ -449,11 +449,36 @@ void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, con
     }
     static const int cap = std::getenv("CIDER_MLP_PAIRS") ? std::atoi(std::getenv("CIDER_MLP_PAIRS")) : 0;
     const int pairs = std::min(a.tiles, cap > 0 ? cap : c.sm_count / 2);
-    tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::MLP2_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
+    tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
 }
 
 bool mlp_fusable(const cider_ctx& c, int Kin) {
     return c.bf16 && c.H % tc::MLP_HC == 0 && (c.D == 64 || c.D == 128 || c.D == 256) && (Kin == c.D || Kin == 2 * c.D);
+}
+
+void dump_mlp_trace(cider_ctx& c, const char* tag, int64_t M, int H, bool pair, long long* tbuf) {
+    {
+        long long h[1024];
+        cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, c.stream);
+        cudaStreamSynchronize(c.stream);
+        const long long t0 = h[2];
+        std::fprintf(stderr, "[mlp trace %s M=%lld pair=%d] chunk: mma1_wait_free mma1_issued | mma2_wait_h mma2_got_h mma2_issued | epi_wait_a1 epi_got_a1 epi_done\n", tag, (long long)M, int(pair));
+        for (int it = 0; it < (pair ? 4 : 1); ++it)
+            for (int ch = 0; ch < H / tc::MLP_HC; ++ch) {
+                const long long* r = h + it * 64 + ch * 8;
+                std::fprintf(stderr, "  t%d c%d: %8lld %8lld | %8lld %8lld %8lld | %8lld %8lld %8lld\n", it, ch, r[6] - t0, r[7] - t0,
+                             r[0] - t0, r[1] - t0, r[5] - t0, r[2] - t0, r[3] - t0, r[4] - t0);
+            }
+        for (int it = 0; it < (pair ? 4 : 0); ++it) {
+            std::fprintf(stderr, "  t%d mma1 got_free:", it);
+            for (int ch = 0; ch < H / tc::MLP_HC; ++ch) std::fprintf(stderr, " %lld", h[896 + it * 8 + ch] - t0);
+            std::fprintf(stderr, "\n");
+            std::fprintf(stderr, "\n");
+        }
+        for (int it = 0; it < (pair ? 4 : 0); ++it)
+            std::fprintf(stderr, "  t%d final epilogue: wait %lld got %lld done %lld\n", it, h[512 + it * 4] - t0, h[512 + it * 4 + 1] - t0,
+                         h[512 + it * 4 + 2] - t0);
+    }
 }
 
 // Y = ep(GELU([A0|A1] W1^T + b1) W2^T + b2); falls back to two GEMMs through the `hid` buffer.
@@ -512,28 +537,7 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     else if (D == 128) { if (Kin == 256) launch_mlp<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp<128, 128>(c, x0, x1, w1, w2, a); }
     else { if (Kin == 128) launch_mlp<128, 64>(c, x0, x1, w1, w2, a); else launch_mlp<64, 64>(c, x0, x1, w1, w2, a); }
     check_launch(tag);
-    if (tbuf) {
-        long long h[1024];
-        cudaMemcpyAsync(h, tbuf, sizeof(h), cudaMemcpyDeviceToHost, c.stream);
-        cudaStreamSynchronize(c.stream);
-        const long long t0 = h[2];
-        std::fprintf(stderr, "[mlp trace %s M=%lld pair=%d] chunk: mma1_wait_free mma1_issued | mma2_wait_h mma2_got_h mma2_issued | epi_wait_a1 epi_got_a1 epi_done\n", tag, (long long)M, int(pair));
-        for (int it = 0; it < (pair ? 4 : 1); ++it)
-            for (int ch = 0; ch < H / tc::MLP_HC; ++ch) {
-                const long long* r = h + it * 64 + ch * 8;
-                std::fprintf(stderr, "  t%d c%d: %8lld %8lld | %8lld %8lld %8lld | %8lld %8lld %8lld\n", it, ch, r[6] - t0, r[7] - t0,
-                             r[0] - t0, r[1] - t0, r[5] - t0, r[2] - t0, r[3] - t0, r[4] - t0);
-            }
-        for (int it = 0; it < (pair ? 4 : 0); ++it) {
-            std::fprintf(stderr, "  t%d mma1 got_free:", it);
-            for (int ch = 0; ch < H / tc::MLP_HC; ++ch) std::fprintf(stderr, " %lld", h[896 + it * 8 + ch] - t0);
-            std::fprintf(stderr, "\n");
-            std::fprintf(stderr, "\n");
-        }
-        for (int it = 0; it < (pair ? 4 : 0); ++it)
-            std::fprintf(stderr, "  t%d final epilogue: wait %lld got %lld done %lld\n", it, h[512 + it * 4] - t0, h[512 + it * 4 + 1] - t0,
-                         h[512 + it * 4 + 2] - t0);
-    }
+    if (tbuf) dump_mlp_trace(c, tag, M, H, pair, tbuf);
 }
 
 // ---- workspace ------------------------------------------------------------------------------
@@ -782,6 +786,42 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     check_launch(tag);
 }
 
+// ---- Module A evidence path in one kernel: e = (softmax_k(Z W^T / tau) (x) S) V ------------------
+// (intermediate_logits + demix_responsibilities + evidence_embed, denoiser.cpp:86-139): the 2-SM
+// fused two-layer kernel with hidden = the Q symbol columns and the demix as its hidden activation.
+bool demix_evid_ok(const cider_ctx& c, int K) {
+    static const bool off = std::getenv("CIDER_NO_DEMIX_EVID") != nullptr;
+    return !off && c.bf16 && c.D == 256 && c.Q == 256 && (K == 4 || K == 8) && !std::getenv("CIDER_MLP_1SM");
+}
+void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K, bf16* e_out) {
+    const int D = c.D, Q = c.Q;
+    Epi ep = epi(EP_DEMIX);
+    ep.M = int(Ms); ep.N = D; ep.out_t = e_out; ep.ldo = D; ep.S = S; ep.L = c.L; ep.K = K;
+    ep.beta = float(c.md.evidence_scale);
+    ep.inv_tau = 1.0f / float(c.md.tau_demix); // as demix_block_kernel computes it
+    Launch lg(c, "demix_evid", 2.0 * double(Ms) * Q * (D + D), double(Ms) * (2 * D * c.act_size) + double(Ms / K) * Q * 4);
+    const CUtensorMap x0 = make_map_w1_3d(Zt, Ms, D, 128, D / 64); // the whole 128-row tile in one box
+    const CUtensorMap w1 = make_map_w1_3d(c.W, Q, D, tc::MLP_HC / 2);
+    const CUtensorMap& w2 = map_for(c, c.Vt, D, Q, Q, D / 2);
+    tc::MlpArgs a;
+    a.M = int(Ms);
+    a.K0 = D;
+    a.H = Q;
+    a.tiles = int((Ms + 255) / 256);
+    a.b1 = nullptr;
+    a.ep = ep;
+    a.trace = nullptr;
+    a.dbg = 0;
+    static const bool trace_on = std::getenv("CIDER_TRACE_MLP") != nullptr;
+    if (trace_on) {
+        a.trace = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
+        cudaMemsetAsync(a.trace, 0, 8 * 1024, c.stream);
+    }
+    launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, a);
+    check_launch("demix_evid");
+    if (a.trace) dump_mlp_trace(c, "demix_evid", Ms, Q, true, a.trace);
+}
+
 // ---- one denoiser forward over nb bins (denoiser.cpp:253-259) -------------------------------
 struct FwdOpts {
     float tau = 1.0f;
@@ -806,6 +846,10 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         const LayerW& lw = c.lw[li];
         // Module A (denoiser.cpp:141-160)
         Epi e;
+        if (demix_evid_ok(c, K)) {
+            // Lambda-bar, demix and the evidence embedding in one 2-SM kernel (e is its only output)
+            demix_evid(c, w.Zt, S, Ms, K, (bf16*)w.et);
+        } else {
         if (c.bf16 && 32 % K == 0 && K >= 4 && Q % 256 == 0 && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
             // intermediate logits and demixing in one kernel: Lambda-bar never leaves the chip
             e = epi(EP_DEMIX);
@@ -826,6 +870,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         e = epi(EP_STORE);
         e.out_f = w.ef; e.out_t = c.bf16 ? w.et : nullptr; e.ldo = D; // (ef is null in BF16 mode)
         gemm(c, "gemm_evid", w.Aq, Q, nullptr, 0, c.Vt, Ms, D, e);
+        }
         e = epi(EP_GATE);
         e.bias = lw.gb2; e.z = w.Zf; e.e = w.ef; e.zb = (const bf16*)w.Zt; e.eb = (const bf16*)w.et; e.ldz = D;
         e.out_f = w.Ztf; e.out_t = c.bf16 ? w.Ztt : nullptr; e.ldo = D;

@@ -153,8 +153,9 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
         : "memory");
 }
 
-template <int KIN, int D>
+template <int KIN, int D, int STGW = 4096, int EW = 8>
 struct Mlp2Layout {
+    static constexpr int STG_WARP = STGW;
     static constexpr int KB1 = KIN / 64;
     static constexpr int KB2 = MLP_HC / 64;
     static constexpr int W1_HALF = (MLP_HC / 2) * 64 * 2;   // 8 KB: this CTA's 64 rows of a W1 k-block
@@ -165,7 +166,7 @@ struct Mlp2Layout {
     static constexpr int FIXED = 1024 + 512;
     // output staging for coalesced stores: one 32-row x 64-column bf16 block per epilogue warp (the
     // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
-    static constexpr int STG_BYTES = KIN == D ? 8 * 4096 : 0;
+    static constexpr int STG_BYTES = KIN == D ? EW * STGW : 0;
     static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - X_BYTES - STG_BYTES) / SLOT;
     static constexpr int NS = NS_RAW > 16 ? 16 : NS_RAW;
     static constexpr int STG_OFF = X_BYTES;
@@ -177,19 +178,146 @@ struct Mlp2Layout {
     static_assert(KB1 % W1_PER_SLOT == 0, "input width must be a multiple of 128");
 };
 
+// EP_DEMIX runs 16 epilogue warps (4 per TMEM lane quarter, 32 hidden columns each) with one
+// [16][33] fp32 staging block per warp; the GELU variants run 8 with 4 KB each.
+constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
+constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : 8; }
+constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
+template <int KIN, int D, int EPK>
+using Mlp2LayoutFor = Mlp2Layout<KIN, D, EPK == EP_DEMIX ? DEMIX_STG_WARP : 4096, mlp2_epi_warps(EPK)>;
+
 constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hidden columns = one MMA2 k-step)
-constexpr int MLP2_MMA2_WARP = 10;
-constexpr int MLP2_XLOAD_WARP = 11;
-constexpr int MLP2_THREADS = 384; // ring producer, MMA1 issuer, 8 epilogue warps (2-9), MMA2 issuer, X producer
+
+// EP_DEMIX hidden phase of one epilogue warp: its 32 rows (= 32 / KK (bin, slot) groups of KK rows)
+// x 32 intermediate-logit columns of a chunk, in two passes of 16 columns. Per pass the fp32
+// accumulator rows go to SMEM (column-major [16][33], conflict-free both ways); each lane then takes
+// one column over half of the rows and applies demix_responsibilities (denoiser.cpp:103-122): softmax
+// over the KK rows of each group at 1/tau with a fixed-point normaliser (2^-22 units, rounded by the
+// 2^23 magic add, summed as integers: bitwise invariant to the order of the rows), times
+// S[(bin, slot)][column]. The bf16 results come back row-wise through the same SMEM block and are
+// packed IN PLACE into the warp's own TMEM columns as the A operand of the V GEMM. beta S is a
+// per-group constant shift of the logits and cancels inside softmax_k (not applied).
+template <int KK>
+__device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, uint32_t base, uint64_t* a1_full_b, uint32_t ph,
+                                           uint32_t l_h_full, int m0, int col0, int lane, long long* tr) {
+    constexpr int NGL = 16 / KK; // row groups per lane (lanes 0-15: rows 0-15, lanes 16-31: rows 16-31)
+    const Epi& ep = args.ep;
+    float* xs = reinterpret_cast<float*>(stg); // [16 columns][33] fp32; then [32 rows][32 B] bf16
+    const int cl = lane & 15, rh = lane >> 4;
+    const float scale2 = ep.inv_tau * 1.4426950408889634f;
+    float sv[2][NGL]; // S[(bin, slot)][column] for this lane's column and groups, both passes
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int t = 0; t < NGL; ++t) {
+            const int r0 = m0 + rh * 16 + t * KK;
+            sv[p][t] = r0 < ep.M ? __ldg(ep.S + size_t(r0 / KK) * args.H + col0 + p * 16 + cl) : 0.0f;
+        }
+    if (tr) tr[2] = clock64();
+    mbar_wait(a1_full_b, ph);
+    fence_after();
+    if (tr) tr[3] = clock64();
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        {
+            float v[16];
+            tmem_ld16(base + p * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) xs[j * 33 + lane] = v[j]; // row `lane`, column j
+        }
+        __syncwarp();
+        float xv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xv[i] = xs[cl * 33 + rh * 16 + i];
+        __syncwarp(); // xs is reused for the bf16 results below
+        uint8_t* os = stg;
+#pragma unroll
+        for (int t = 0; t < NGL; ++t) {
+            float mx = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < KK; ++k) mx = fmaxf(mx, xv[t * KK + k]);
+            const float nmx = -mx * scale2;
+            uint32_t den = 0;
+#pragma unroll
+            for (int k = 0; k < KK; ++k) {
+                const float e = ex2_approx(fmaf(xv[t * KK + k], scale2, nmx));
+                xv[t * KK + k] = e;
+                den += __float_as_uint(fmaf(e, 4194304.0f, 8388608.0f)) - 0x4B000000u; // round(e 2^22)
+            }
+            const float rs = (4194304.0f / float(den)) * sv[p][t];
+#pragma unroll
+            for (int k = 0; k < KK; ++k) {
+                const int r = rh * 16 + t * KK + k;
+                *reinterpret_cast<bf16*>(os + r * 32 + (((cl >> 3) ^ ((r >> 2) & 1)) * 16) + (cl & 7) * 2) =
+                    __float2bfloat16_rn(xv[t * KK + k] * rs);
+            }
+        }
+        __syncwarp();
+        const uint4 p0 = *reinterpret_cast<const uint4*>(os + lane * 32 + ((0 ^ ((lane >> 2) & 1)) * 16));
+        const uint4 p1 = *reinterpret_cast<const uint4*>(os + lane * 32 + ((1 ^ ((lane >> 2) & 1)) * 16));
+        const uint32_t pk[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+        tmem_st8(base + p * 8, pk); // pass p's 16 columns packed in place (fp32 columns [0, 16) were read in pass 0)
+        __syncwarp(); // the next pass overwrites the staging block
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cl(l_h_full); // the warp's 32 hidden columns -> MMA2 k-steps 2 sub, 2 sub + 1
+    if (tr) tr[4] = clock64();
+}
+
+// EP_DEMIX final epilogue of one warp: output k-block kb (64 columns of e) of its 32 rows, as bf16,
+// through a [32 rows][64 B] staging block per 32 columns (16-byte chunks swizzled) so that every
+// store instruction writes whole 64-byte row segments (direct per-row 32-byte stores measured slower:
+// they also slow the concurrent demix warps).
+__device__ __forceinline__ void demix_final(const Epi& ep, uint8_t* stg, uint32_t acc, int kb, int mrow0, int lane,
+                                            uint32_t l_a2_empty) {
+    bf16* ot = reinterpret_cast<bf16*>(ep.out_t);
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+        float v[32];
+        tmem_ld32(acc + kb * 64 + s2 * 32, v);
+        if (s2 == 1) {
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cl(l_a2_empty); // this warp's accumulator columns drained
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * j + 2 * t], v[8 * j + 2 * t + 1]);
+                pk[t] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16))),
+                         "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
+                         : "memory");
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + lane / 4, j = lane & 3;
+            const uint4 u = *reinterpret_cast<const uint4*>(stg + r * 64 + ((j ^ ((r >> 1) & 3)) * 16));
+            if (mrow0 + r < ep.M)
+                *reinterpret_cast<uint4*>(ot + size_t(mrow0 + r) * ep.ldo + kb * 64 + s2 * 32 + j * 8) = u;
+        }
+        __syncwarp();
+    }
+}
+
+// warps: ring producer, MMA1 issuer, epilogue warps (2 .. EW + 1), MMA2 issuer, X producer
 
 // EPK: final-epilogue kind (EP_STORE, EP_GATE or EP_RESID), a template parameter so each variant
 // carries only the registers its epilogue needs.
 template <int KIN, int D, int EPK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MLP2_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mlp2_threads(EPK), 1)
 mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2, const MlpArgs args) {
-    using Lay = Mlp2Layout<KIN, D>;
+    using Lay = Mlp2LayoutFor<KIN, D, EPK>;
     constexpr int KB1 = Lay::KB1, KB2 = Lay::KB2, NS = Lay::NS;
+    constexpr int EW = mlp2_epi_warps(EPK);              // epilogue warps 2 .. EW + 1
+    constexpr int MMA2_WARP = EW + 2, XLOAD_WARP = EW + 3;
     constexpr int KBD = D / 64; // output k-blocks = final-epilogue steps (half h takes k-blocks h, h+2, ...)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
@@ -212,7 +340,10 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     const bool leader = rank == 0;
     const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int NC = args.H / MLP_HC;
-    constexpr int EPI_ARRIVALS = 2 * 8; // one elected lane per epilogue warp, both CTAs
+    constexpr int EPI_ARRIVALS = 2 * EW; // one elected lane per epilogue warp, both CTAs
+    // hidden group g: GELU = 16 columns of both 64-column warp halves (all epilogue warps); demix =
+    // the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
+    constexpr int H_ARRIVALS = EPK == EP_DEMIX ? 8 : EPI_ARRIVALS;
 
     // Gate / fusion epilogues read z (and e) from global memory (L2: the same rows were just TMA'd
     // into X), so every X k-block is free once the tile's last MMA1 has read it and the next tile's
@@ -224,7 +355,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&a1_full[b], 1);
-            for (int g = 0; g < MLP2_GG; ++g) mbar_init(&h_full[MLP2_GG * b + g], EPI_ARRIVALS);
+            for (int g = 0; g < MLP2_GG; ++g) mbar_init(&h_full[MLP2_GG * b + g], H_ARRIVALS);
             mbar_init(&a1_free[b], 1);
         }
         mbar_init(a2_full, 1);
@@ -285,11 +416,18 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
             }
         }
-    } else if (warp == MLP2_XLOAD_WARP) {
+    } else if (warp == XLOAD_WARP) {
         if (lane == 0) { // row-tile producer, one k-block at a time
             uint32_t eph = 0;
             for (int tile = pair; tile < args.tiles; tile += npairs) {
                 const int row0 = tile * 256 + int(rank) * 128;
+                if constexpr (EPK == EP_DEMIX) { // tmX0 is 3-D: the whole row tile in ONE box, on x_full[0]
+                    for (int kb = 0; kb < KB1; ++kb) mbar_wait(&x_empty[kb], eph ^ 1);
+                    if (leader) mbar_expect_tx(&x_full[0], 2 * KB1 * 16384);
+                    tma_load_3d_2sm(xs, &tmX0, L_x_full0, 0, row0, 0);
+                    eph ^= 1;
+                    continue;
+                }
                 for (int kb = 0; kb < KB1; ++kb) {
                     mbar_wait(&x_empty[kb], eph ^ 1);
                     if (leader) mbar_expect_tx(&x_full[kb], 2 * 16384);
@@ -300,7 +438,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 eph ^= 1;
             }
         }
-    } else if (warp == 1 || warp == MLP2_MMA2_WARP) {
+    } else if (warp == 1 || warp == MMA2_WARP) {
         // Two MMA issuers on the leader: the tensor pipe queues only ~50 cycles of work, so every
         // barrier wait of a single issuing thread is a pipe bubble (tools/mma_bench.cu issue2_kernel:
         // 200-cycle waits per slot cost 22% with one issuer, 11% with two). Warp 1 issues the first
@@ -324,7 +462,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         for (int sg = 0; sg < S1; ++sg) {
                             uint32_t ph;
                             const int slot = ring_slot(it * per_tile + pos_w1(c) + sg, ph);
-                            if (c == 0) // the tile's k-blocks arrive one by one
+                            if (c == 0 && EPK == EP_DEMIX && sg == 0) mbar_wait(&x_full[0], xph); // one box
+                            else if (c == 0 && EPK != EP_DEMIX) // the tile's k-blocks arrive one by one
                                 for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[sg * Lay::W1_PER_SLOT + j], xph);
                             mbar_wait(&r_full[slot], ph);
                             fence_after();
@@ -358,6 +497,32 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         // are GELU group g of warp-half kb, packed in place at TMEM cols 64 kb + 8 g: k-step g
                         // of W2 slot kb, issued as soon as that group lands in both CTAs.
                         const uint32_t a_base = tmem + 256 + b * MLP_HC;
+                        if constexpr (EPK == EP_DEMIX) {
+                            // group g = hidden columns [32 g, 32 g + 32) of every quarter, packed at TMEM
+                            // columns 32 g + [0, 16): k-steps 2 g, 2 g + 1 of W2 k-block g / 2
+#pragma unroll
+                            for (int g = 0; g < MLP2_GG; ++g) {
+                                mbar_wait(&h_full[MLP2_GG * b + g], (hph >> b) & 1u);
+                                fence_after();
+                                if (g == 0 && c == 0) {
+                                    mbar_wait(a2_empty, a2ph ^ 1);
+                                    a2ph ^= 1;
+                                    fence_after();
+                                }
+                                uint32_t ph;
+                                const int slot = ring_slot(it * per_tile + pos_w2(c) + g / 2, ph);
+                                if (g % 2 == 0) {
+                                    mbar_wait(&r_full[slot], ph);
+                                    fence_after();
+                                }
+                                const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
+#pragma unroll
+                                for (int j = 0; j < 2; ++j)
+                                    mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
+                                                    (c | g | j) != 0);
+                                if (g % 2 == 1) mma_commit_2sm(&r_empty[slot]);
+                            }
+                        } else {
                         int slots[S2];
 #pragma unroll
                         for (int g = 0; g < MLP2_GG; ++g) {
@@ -384,6 +549,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                 if (g == MLP2_GG - 1) mma_commit_2sm(&r_empty[slots[kb]]);
                             }
                         }
+                        }
                         hph ^= 1u << b;
                         mma_commit_2sm_mask(&a1_free[b], 1);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 5] = clock64();
@@ -408,6 +574,33 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         int n = 0; // chunk counter across tiles: acc1 buffer = n & 1
         for (int tile = pair; tile < args.tiles; tile += npairs) {
             const int it = (tile - pair) / npairs;
+            if constexpr (EPK == EP_DEMIX) {
+                // Module A intermediate logits -> demix -> evidence embedding (denoiser.cpp:86-139) with
+                // Lambda-bar and r (x) S never leaving the chip: hidden = the Q symbol columns
+                uint8_t* stg = smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP;
+                const int m0 = tile * 256 + int(rank) * 128 + quarter * 32;
+                for (int c = 0; c < NC; ++c, ++n) {
+                    long long* tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0 ? args.trace + it * 64 + c * 8 : nullptr;
+                    const int b = n & 1;
+                    const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 32;
+                    if (ep.K == 8)
+                        demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, m0,
+                                      c * MLP_HC + half * 32, lane, tr);
+                    else
+                        demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, m0,
+                                      c * MLP_HC + half * 32, lane, tr);
+                    e1ph ^= 1u << b;
+                }
+                const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
+                if (trf) args.trace[512 + it * 4 + 0] = clock64();
+                mbar_wait(a2_full, e2ph);
+                e2ph ^= 1;
+                fence_after();
+                if (trf) args.trace[512 + it * 4 + 1] = clock64();
+                demix_final(ep, stg, tmem + lane_off, half, m0, lane, L_a2_empty);
+                if (trf) args.trace[512 + it * 4 + 2] = clock64();
+                continue;
+            } else
             for (int c = 0; c < NC; ++c, ++n) {
                 const int b = n & 1;
                 const float* b1 = args.b1 + c * MLP_HC + half * 64;
@@ -526,7 +719,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     if constexpr (Lay::STG_BYTES > 0) {
                         // this row's 128 B into the warp's staging block (chunk j of row r at j ^ (r & 7)),
                         // then the warp copies 4 whole rows (4 x 128 B) per store instruction
-                        uint8_t* stg = smem + Lay::STG_OFF + (warp - 2) * 4096;
+                        uint8_t* stg = smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP;
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
                             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + lane * 128 + ((j ^ (lane & 7)) * 16))),
