@@ -57,7 +57,9 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int grp = warp / 4, wg = warp % 4;         // group, warp within the group
-    float* ss = reinterpret_cast<float*>(smem + Lay::S_OFF) + warp * 128; // per-warp [12 rows][8 heads + pad]
+    // per-group score scratch [48 block rows][8 heads]: warp wg scores block rows [12 wg, 12 wg + 12)
+    // (consecutive rows: distinct SW128 phases, conflict-free ldmatrix) and pools rows k = 2 wg, 2 wg + 1
+    float* ss = reinterpret_cast<float*>(smem + Lay::S_OFF) + grp * 512;
     const int R = PM_DEG * K;        // rows per block (<= 48)
     const int KBS = R * 128;         // k-block stride inside a block buffer
     constexpr int GB = PM_NBUF / 2;  // buffers per group
@@ -75,12 +77,13 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     __syncthreads();
 
     // this group's blocks: blockIdx.x + (2 i + grp) * gridDim.x, i = 0, 1, ...
-    const int64_t stride = 2 * int64_t(gridDim.x);
-    const int64_t first = int64_t(blockIdx.x) + int64_t(grp) * gridDim.x;
-    auto issue = [&](int64_t blk, int slot) { // one thread of the group: the block's 4 column boxes
-        const int64_t b = blk / P;
-        const int j = int(blk % P);
-        const int row0 = int((b * E + check_ptr[j]) * K);
+    const int stride = 2 * int(gridDim.x);
+    const int first = int(blockIdx.x) + grp * int(gridDim.x);
+    const int nblk = int(n_blocks);
+    auto issue = [&](int blk, int slot) { // one thread of the group: the block's 4 column boxes
+        const int b = blk / P;
+        const int j = blk - b * P;
+        const int row0 = (b * E + check_ptr[j]) * K;
         uint64_t* bar = &full[grp * GB + slot];
         tc::mbar_expect_tx(bar, 4 * R * 128);
         for (int kb = 0; kb < 4; ++kb)
@@ -89,24 +92,22 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     const bool leader = wg == 0 && lane == 0;
     if (leader)
         for (int s = 0; s < GB - 1; ++s)
-            if (first + s * stride < n_blocks) issue(first + s * stride, s);
-    // rows of this warp's m16 tile: q < 12 -> (i = q % 6, k = 2 wg + q / 6); q >= 12 pads with q = 0
+            if (first + s * stride < nblk) issue(first + s * stride, s);
+    // rows of this warp's m16 tile: block rows 12 wg + q for q < 12
     const int q = lane & 15;
-    const int qa = q < 2 * PM_DEG ? q : 0;
-    const int k_of_q = 2 * wg + qa / PM_DEG, i_of_q = qa % PM_DEG;
-    const int arow = i_of_q * K + k_of_q;
+    const int arow = 12 * wg + (q < 2 * PM_DEG ? q : q - 4); // pad lanes repeat rows 8-11 (same address: broadcast)
     const int h = (lane * 8) / (256 / NH); // pooling: lane = 8-column chunk of head h
     int slot = 0;
     uint32_t ph = 0; // bit s: phase of this group's full[s]
-    for (int64_t blk = first; blk < n_blocks; blk += stride) {
-        const int64_t nxt = blk + (GB - 1) * stride;
-        if (leader && nxt < n_blocks) issue(nxt, (slot + GB - 1) % GB); // released by the last group barrier
+    for (int blk = first; blk < nblk; blk += stride) {
+        const int nxt = blk + (GB - 1) * stride;
+        if (leader && nxt < nblk) issue(nxt, (slot + GB - 1) % GB); // released by the last group barrier
         tc::mbar_wait(&full[grp * GB + slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
         const uint8_t* nb = smem + (grp * GB + slot) * PM_BUF;
-        const int64_t b = blk / P;
-        const int e0 = check_ptr[int(blk % P)];
-        if (2 * wg < K) {
+        const int b = blk / P;
+        const int e0 = check_ptr[blk - b * P];
+        if (12 * wg < PM_DEG * K) {
             // (1) head scores of the warp's 12 rows: n-tile 0 = hi(u), 1 = lo(u)
             float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll 4
@@ -123,15 +124,18 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                     mma_16816(acc[nt], a0, a1, a2, a3, b0, b1);
                 }
             }
-            // C rows lane/4 (+8), cols 2 (lane % 4) (+1): scores = hi + lo, into the warp's scratch
+            // C rows lane/4 (+8), cols 2 (lane % 4) (+1): scores = hi + lo, into the group's scratch
             const int r0 = lane >> 2, c0 = (lane & 3) * 2;
-            ss[r0 * 8 + c0] = acc[0][0] + acc[1][0];
-            ss[r0 * 8 + c0 + 1] = acc[0][1] + acc[1][1];
+            ss[(12 * wg + r0) * 8 + c0] = acc[0][0] + acc[1][0];
+            ss[(12 * wg + r0) * 8 + c0 + 1] = acc[0][1] + acc[1][1];
             if (r0 + 8 < 2 * PM_DEG) {
-                ss[(r0 + 8) * 8 + c0] = acc[0][2] + acc[1][2];
-                ss[(r0 + 8) * 8 + c0 + 1] = acc[0][3] + acc[1][3];
+                ss[(12 * wg + r0 + 8) * 8 + c0] = acc[0][2] + acc[1][2];
+                ss[(12 * wg + r0 + 8) * 8 + c0 + 1] = acc[0][3] + acc[1][3];
             }
-            __syncwarp();
+        }
+        if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory"); // the group's scores are in
+        else asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (2 * wg < K) {
             // (2) pooling of rows k = 2 wg + kk
 #pragma unroll 1
             for (int kk = 0; kk < 2 && 2 * wg + kk < K; ++kk) {
@@ -141,7 +145,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
 #pragma unroll
                 for (int i = 0; i < PM_DEG; ++i) {
                     const int r = i * K + k;
-                    sc[i] = ss[(kk * PM_DEG + i) * 8 + h];
+                    sc[i] = ss[r * 8 + h];
                     const uint4 u = *reinterpret_cast<const uint4*>(nb + (lane >> 3) * KBS + r * 128 + (((lane & 7) ^ (r & 7)) * 16));
                     const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
