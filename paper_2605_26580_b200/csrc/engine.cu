@@ -439,7 +439,7 @@ void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, cons
 
 template <int KIN, int D, int EPK>
 void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
-                 const CUtensorMap& w2, const tc::MlpArgs& a) {
+                 const CUtensorMap& w2, const CUtensorMap& out, const tc::MlpArgs& a) {
     using Lay = tc::Mlp2LayoutFor<KIN, D, EPK>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -449,7 +449,7 @@ void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, con
     }
     static const int cap = std::getenv("CIDER_MLP_PAIRS") ? std::atoi(std::getenv("CIDER_MLP_PAIRS")) : 0;
     const int pairs = std::min(a.tiles, cap > 0 ? cap : c.sm_count / 2);
-    tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
+    tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, out, a);
 }
 
 bool mlp_fusable(const cider_ctx& c, int Kin) {
@@ -524,14 +524,16 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
         a.trace = tbuf;
     }
     if (pair) {
+        if (ep.out_f || !ep.out_t) throw InvalidInput("cider: the 2-SM MLP writes one bf16 output");
+        const CUtensorMap& om = map_for(c, ep.out_t, M, D, ep.ldo, 32); // 32-row TMA store boxes
         if (D == 256) {
-            if (ep.kind == EP_GATE) launch_mlp2<512, 256, EP_GATE>(c, x0, x1, w1, w2, a);
-            else if (ep.kind == EP_RESID) launch_mlp2<512, 256, EP_RESID>(c, x0, x1, w1, w2, a);
-            else launch_mlp2<256, 256, EP_STORE>(c, x0, x1, w1, w2, a);
+            if (ep.kind == EP_GATE) launch_mlp2<512, 256, EP_GATE>(c, x0, x1, w1, w2, om, a);
+            else if (ep.kind == EP_RESID) launch_mlp2<512, 256, EP_RESID>(c, x0, x1, w1, w2, om, a);
+            else launch_mlp2<256, 256, EP_STORE>(c, x0, x1, w1, w2, om, a);
         } else {
-            if (ep.kind == EP_GATE) launch_mlp2<256, 128, EP_GATE>(c, x0, x1, w1, w2, a);
-            else if (ep.kind == EP_RESID) launch_mlp2<256, 128, EP_RESID>(c, x0, x1, w1, w2, a);
-            else launch_mlp2<128, 128, EP_STORE>(c, x0, x1, w1, w2, a);
+            if (ep.kind == EP_GATE) launch_mlp2<256, 128, EP_GATE>(c, x0, x1, w1, w2, om, a);
+            else if (ep.kind == EP_RESID) launch_mlp2<256, 128, EP_RESID>(c, x0, x1, w1, w2, om, a);
+            else launch_mlp2<128, 128, EP_STORE>(c, x0, x1, w1, w2, om, a);
         }
     } else if (D == 256) { if (Kin == 512) launch_mlp<512, 256>(c, x0, x1, w1, w2, a); else launch_mlp<256, 256>(c, x0, x1, w1, w2, a); }
     else if (D == 128) { if (Kin == 256) launch_mlp<256, 128>(c, x0, x1, w1, w2, a); else launch_mlp<128, 128>(c, x0, x1, w1, w2, a); }
@@ -758,6 +760,11 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     a.D = D;
     a.out_t = reinterpret_cast<bf16*>(out_t);
     a.out_f = out_f;
+    // T-resident sweep chunk: default one chunk (each CTA one contiguous group-major range). Chunks of
+    // 64-256 bins (z~ L2-resident across a slot's edges) measured slower: every extra T change drains
+    // the CTA's MMA pipeline (bench c5: normalise 83 ms whole vs 85-100 ms chunked).
+    static const int mchunk_bins = std::getenv("CIDER_GRP_CHUNK_BINS") ? std::atoi(std::getenv("CIDER_GRP_CHUNK_BINS")) : 0;
+    a.mchunk = mchunk_bins > 0 ? std::max(1, mchunk_bins / bb) : a.mtiles;
     const double rows = double(nb) * K * groups;
     Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, rows * D * 2.0 * (mean_seg + 1));
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
@@ -817,7 +824,7 @@ void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K,
         a.trace = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
         cudaMemsetAsync(a.trace, 0, 8 * 1024, c.stream);
     }
-    launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, a);
+    launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, x0, a); // (its epilogue stores directly; no output map)
     check_launch("demix_evid");
     if (a.trace) dump_mlp_trace(c, "demix_evid", Ms, Q, true, a.trace);
 }

@@ -39,6 +39,7 @@ struct GrpArgs {
     int out_rows_per_bin;             // L (site output) or E (edge output)
     const int* out_row;               // [groups]: output row block (edge or slot index)
     int D;
+    int mchunk;                       // T-resident kernel: m-tiles per sweep chunk
     bf16* out_t;                      // bf16 output [bins * out_rows_per_bin * K x D]
     float* out_f;                     // optional fp32 copy
 };
@@ -176,10 +177,22 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 }
 
 // ---- T-resident variant for single-segment groups (the normalise GEMM, group = edge) ------------
-// Each CTA walks a contiguous range of (group, m-tile) work, group-major, so its coefficient action
-// T_alpha (D x D bf16, 128 KB for D = 256) is loaded ONCE per group change and stays resident; only
-// the gathered A rows stream (64 KB per 128-row tile against 2K cycles of MMA). The epilogue stages
-// each warp's 32 x 32 bf16 block in SMEM and writes whole 64-byte row segments.
+// The m-tiles are swept in chunks of `mchunk` (128 bins at K = 8: 32 MB of z~, L2-resident); inside a
+// chunk every CTA takes an equal contiguous range of (group, m-tile) work, group-major, so its
+// coefficient action T_alpha (D x D bf16, 128 KB for D = 256) is loaded once per group change and
+// stays resident while only the gathered A rows stream (64 KB per 128-row tile against 2K cycles of
+// MMA). All CTAs work on the same chunk at once, so the z~ rows a slot shares among its (column
+// weight) edges come from DRAM once and from L2 for the other edges. The epilogue stages each warp's
+// 32 x 32 bf16 block in SMEM and writes whole 64-byte row segments.
+template <typename F>
+__device__ __forceinline__ void grp_res_sweep(const GrpArgs& args, F&& body) {
+    for (int c0 = 0; c0 < args.mtiles; c0 += args.mchunk) {
+        const int mc = min(args.mchunk, args.mtiles - c0);
+        const int tot = args.groups * mc;
+        const int u0 = int(int64_t(blockIdx.x) * tot / gridDim.x), u1 = int(int64_t(blockIdx.x + 1) * tot / gridDim.x);
+        for (int u = u0; u < u1; ++u) body(u / mc, c0 + u % mc);
+    }
+}
 struct GrpResLayout {
     static constexpr int T_OFF = 0;                 // 4 k-blocks x (256 x 64 bf16)
     static constexpr int A_OFF = 4 * 32768;         // ring of A k-blocks, 16 KB each
@@ -203,9 +216,6 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint64_t* aempty = afull + 2;    // [2] accumulator drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int total = args.groups * args.mtiles;
-    const int t_begin = int(int64_t(blockIdx.x) * total / gridDim.x);
-    const int t_end = int(int64_t(blockIdx.x + 1) * total / gridDim.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < Lay::NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -228,8 +238,7 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         if (lane == 0) {
             int stage = 0, cur = -1;
             uint32_t phase = 0, teph = 0;
-            for (int t = t_begin; t < t_end; ++t) {
-                const int g = t / args.mtiles, mt = t % args.mtiles;
+            grp_res_sweep(args, [&](int g, int mt) {
                 const int alpha = args.seg_alpha[g * args.max_seg];
                 if (alpha != cur) { // new coefficient action: wait until the MMAs on the old one retired
                     if (cur >= 0) { mbar_wait(t_empty, teph); teph ^= 1; }
@@ -244,15 +253,14 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                     tma_load_3d(smem + Lay::A_OFF + stage * 16384, &tmA, &full[stage], kb * 64, arow * args.K, mt * args.bb);
                     if (++stage == Lay::NST) { stage = 0; phase ^= 1; }
                 }
-            }
+            });
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
             int stage = 0, acc = 0, cur = -1;
             uint32_t phase = 0, acc_phase = 0, tfph = 0;
-            for (int t = t_begin; t < t_end; ++t) {
-                const int g = t / args.mtiles;
+            grp_res_sweep(args, [&](int g, int) {
                 const int alpha = args.seg_alpha[g * args.max_seg];
                 if (alpha != cur) {
                     if (cur >= 0) mma_commit(t_empty); // fires once every MMA on the old T has completed
@@ -276,7 +284,7 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 }
                 mma_commit(&afull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            }
+            });
         }
     } else {
         const int quarter = warp % 4;
@@ -284,8 +292,7 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * 2048);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = t_begin; t < t_end; ++t) {
-            const int g = t / args.mtiles, mt = t % args.mtiles;
+        grp_res_sweep(args, [&](int g, int mt) {
             mbar_wait(&afull[acc], acc_phase);
             fence_after();
             const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
@@ -332,7 +339,7 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             fence_before();
             mbar_arrive(&aempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
+        });
     }
     __syncthreads();
     if (warp == 1) {

@@ -105,6 +105,23 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
+__device__ __forceinline__ void ld_shared_v4(const void* p, uint32_t* r) {
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void st_shared_v4(void* p, const uint32_t* r) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3])
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// TMA store of one box out of shared memory (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void ld_global_v8(const void* p, uint32_t* r) { // 32 bytes, one sector
     asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -313,7 +330,8 @@ __device__ __forceinline__ void demix_final(const Epi& ep, uint8_t* stg, uint32_
 template <int KIN, int D, int EPK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mlp2_threads(EPK), 1)
 mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
-               const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2, const MlpArgs args) {
+               const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
+               const __grid_constant__ CUtensorMap tmO, const MlpArgs args) {
     using Lay = Mlp2LayoutFor<KIN, D, EPK>;
     constexpr int KB1 = Lay::KB1, KB2 = Lay::KB2, NS = Lay::NS;
     constexpr int EW = mlp2_epi_warps(EPK);              // epilogue warps 2 .. EW + 1
@@ -350,8 +368,17 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // rows stream in while this tile's final epilogue runs.
     constexpr bool reads_z = EPK == EP_GATE || EPK == EP_RESID;
     constexpr bool reads_e = EPK == EP_GATE;
+    // gate / fusion keep the tile's z k-blocks until the final epilogue has read them, so every chunk
+    // runs over the input k-blocks starting at the second half ([e | z] order): the next tile's
+    // e / acc k-blocks load during the final epilogue and the first MMA1 starts on them.
+    constexpr int ROT = reads_z ? KBD : 0;
     if (threadIdx.x == 0) {
-        for (int kb = 0; kb < KB1; ++kb) { mbar_init(&x_full[kb], 1); mbar_init(&x_empty[kb], 1); }
+        // x_empty: the last MMA1 of the tile, plus (gate / fusion) the 4 warps whose final epilogue
+        // reads that z / e k-block
+        for (int kb = 0; kb < KB1; ++kb) {
+            mbar_init(&x_full[kb], 1);
+            mbar_init(&x_empty[kb], 1 + ((reads_z && kb < KBD) || (reads_e && kb >= KBD) ? 4 : 0));
+        }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&a1_full[b], 1);
@@ -392,7 +419,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 if (leader) mbar_expect_tx(&r_full[slot], bytes_both); // the leader arms its own barrier
             };
             auto load_w1 = [&](int c) { // tmW1 is 3-D: {64 cols, H rows, KIN/64 k-blocks}
-                for (int kb = 0; kb < KB1; kb += Lay::W1_PER_SLOT) {
+                for (int i = 0; i < KB1; i += Lay::W1_PER_SLOT) {
+                    const int kb = (i + ROT) % KB1;
                     acquire(2 * Lay::W1_PER_SLOT * Lay::W1_HALF);
                     tma_load_3d_2sm(ring + slot * Lay::SLOT, &tmW1, L_r_full0 + slot * 8, 0,
                                     c * MLP_HC + int(rank) * (MLP_HC / 2), kb);
@@ -428,7 +456,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     eph ^= 1;
                     continue;
                 }
-                for (int kb = 0; kb < KB1; ++kb) {
+                for (int i = 0; i < KB1; ++i) {
+                    const int kb = (i + ROT) % KB1;
                     mbar_wait(&x_empty[kb], eph ^ 1);
                     if (leader) mbar_expect_tx(&x_full[kb], 2 * 16384);
                     const int k = kb * 64;
@@ -464,17 +493,17 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             const int slot = ring_slot(it * per_tile + pos_w1(c) + sg, ph);
                             if (c == 0 && EPK == EP_DEMIX && sg == 0) mbar_wait(&x_full[0], xph); // one box
                             else if (c == 0 && EPK != EP_DEMIX) // the tile's k-blocks arrive one by one
-                                for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[sg * Lay::W1_PER_SLOT + j], xph);
+                                for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[(sg * Lay::W1_PER_SLOT + j + ROT) % KB1], xph);
                             mbar_wait(&r_full[slot], ph);
                             fence_after();
 #pragma unroll
                             for (int j = 0; j < Lay::W1_PER_SLOT; ++j) {
-                                const int kb = sg * Lay::W1_PER_SLOT + j;
+                                const int kb = (sg * Lay::W1_PER_SLOT + j + ROT) % KB1;
                                 const uint64_t da = sw128_desc(xs + kb * 16384);
                                 const uint64_t db = sw128_desc(ring + slot * Lay::SLOT + j * Lay::W1_HALF);
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
-                                    mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id1, (kb | kk) != 0);
+                                    mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id1, (sg | j | kk) != 0);
                             }
                             mma_commit_2sm(&r_empty[slot]);
                         }
@@ -637,27 +666,15 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
             // final epilogue straight from TMEM: this thread's row, output k-blocks half, half + 2, ...
-            // (64 columns per TMEM load). z / e rows come from global memory with 32-byte loads issued
-            // before the accumulator is read; gate / fusion results go out with 32-byte stores, the
-            // aggregator's through a per-warp staging block (coalesced whole-row stores).
-            const int m = tile * 256 + int(rank) * 128 + row;
-            const bool live = m < ep.M;
+            // Gate / fusion read z (and e) from the tile's own X k-blocks in SMEM (X = [z | e] / [z~ | acc]:
+            // they are kept until here) and write the bf16 result over the z k-block; the aggregator
+            // stages in its per-warp block. Each warp's 32 x 64 result block then leaves by one TMA
+            // store (SW128 box = the staging layout), so the epilogue warps never wait on HBM and the
+            // write burst drains while the next tile's chunks run. A z / e k-block is handed back to the
+            // X producer once the store out of it has been read.
+            const int m0w = tile * 256 + int(rank) * 128 + quarter * 32;
             const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
             if (trf) args.trace[512 + it * 4 + 0] = clock64();
-            // z (and e) of this row's first output k-block are requested before waiting for the
-            // accumulator (their latency hides behind the last MMA2); later k-blocks at loop top
-            uint32_t zr[reads_z ? 32 : 1], er[reads_e ? 32 : 1];
-            auto load_ze = [&](int kb) {
-                const bf16* zp = ep.zb + size_t(m) * ep.ldz + kb * 64;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) ld_global_v8(zp + q * 16, zr + q * 8);
-                if (reads_e) {
-                    const bf16* eptr = ep.eb + size_t(m) * ep.ldz + kb * 64;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) ld_global_v8(eptr + q * 16, er + q * 8);
-                }
-            };
-            if (reads_z && live && half < KBD) load_ze(half);
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
             fence_after();
@@ -665,9 +682,12 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #pragma unroll 1
             for (int kb = half; kb < KBD; kb += 2) {
                 const int n0 = kb * 64;
-                if (reads_z && live && kb != half) load_ze(kb);
-                uint32_t pkl[reads_z ? 1 : 32];
-                uint32_t* pk = reads_z ? zr : pkl; // results packed over the consumed z registers
+                uint8_t* dst = reads_z ? xs + kb * 16384 + quarter * 4096 : smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP;
+                const uint8_t* esrc = xs + (KBD + kb) * 16384 + quarter * 4096;
+                if (!reads_z) { // the staging block's previous store must have been read out
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) { // two 32-column halves of the k-block
                     float v[32];
@@ -685,65 +705,55 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;
                     }
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) { // element pairs with the packed fp32 ops
-                        const int w = s2 * 16 + i / 2; // packed-pair index within the k-block
-                        float2 a = make_float2(v[i], v[i + 1]);
-                        if (reads_z) {
-                            const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zr[w]));
-                            if (reads_e) {
-                                const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&er[w]));
-                                // g = 0.5 tanh(a / 2) + 0.5;  out = g (z - e) + e
-                                const float2 h = __fmul2_rn(a, make_float2(0.5f, 0.5f));
-                                const float2 g = __ffma2_rn(make_float2(tanh_approx(h.x), tanh_approx(h.y)), make_float2(0.5f, 0.5f),
-                                                            make_float2(0.5f, 0.5f));
-                                a = __ffma2_rn(g, __fadd2_rn(z2, make_float2(-e2.x, -e2.y)), e2);
-                            } else {
-                                a = __fadd2_rn(a, z2);
+                    for (int jj = 0; jj < 4; ++jj) { // 16-byte chunk j of this lane's row (SW128: at j ^ (row & 7))
+                        const int j = s2 * 4 + jj;
+                        const uint32_t off = uint32_t(lane * 128 + ((j ^ (lane & 7)) * 16));
+                        uint32_t zq[4] = {0u, 0u, 0u, 0u}, eq[4] = {0u, 0u, 0u, 0u};
+                        if (reads_z) ld_shared_v4(dst + off, zq);
+                        if (reads_e) ld_shared_v4(esrc + off, eq);
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int i = jj * 8 + 2 * t;
+                            float2 a = make_float2(v[i], v[i + 1]);
+                            if (reads_z) {
+                                const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zq[t]));
+                                if (reads_e) {
+                                    const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&eq[t]));
+                                    // g = 0.5 tanh(a / 2) + 0.5;  out = g (z - e) + e
+                                    const float2 h = __fmul2_rn(a, make_float2(0.5f, 0.5f));
+                                    const float2 g = __ffma2_rn(make_float2(tanh_approx(h.x), tanh_approx(h.y)), make_float2(0.5f, 0.5f),
+                                                                make_float2(0.5f, 0.5f));
+                                    a = __ffma2_rn(g, __fadd2_rn(z2, make_float2(-e2.x, -e2.y)), e2);
+                                } else {
+                                    a = __fadd2_rn(a, z2);
+                                }
                             }
+                            __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
+                            pk[t] = *reinterpret_cast<uint32_t*>(&p);
                         }
-                        if (ep.out_f && live) {
-                            v[i] = a.x;
-                            v[i + 1] = a.y;
-                        }
-                        __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
-                        pk[w] = *reinterpret_cast<uint32_t*>(&p);
-                    }
-                    if (ep.out_f && live) {
-                        float* o = ep.out_f + size_t(m) * ep.ldo + n0 + s2 * 32;
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                        st_shared_v4(dst + off, pk);
                     }
                 }
-                if (ep.out_t && !(args.dbg & 4)) {
-                    bf16* ot = reinterpret_cast<bf16*>(ep.out_t);
-                    if constexpr (Lay::STG_BYTES > 0) {
-                        // this row's 128 B into the warp's staging block (chunk j of row r at j ^ (r & 7)),
-                        // then the warp copies 4 whole rows (4 x 128 B) per store instruction
-                        uint8_t* stg = smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP;
-#pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + lane * 128 + ((j ^ (lane & 7)) * 16))),
-                                         "r"(pk[4 * j]), "r"(pk[4 * j + 1]), "r"(pk[4 * j + 2]), "r"(pk[4 * j + 3])
-                                         : "memory");
-                        __syncwarp();
-                        const int j = lane & 7;
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int r = i * 4 + lane / 8;
-                            const uint4 u = *reinterpret_cast<const uint4*>(stg + r * 128 + ((j ^ (r & 7)) * 16));
-                            const int mr = tile * 256 + int(rank) * 128 + quarter * 32 + r;
-                            if (mr < ep.M) *reinterpret_cast<uint4*>(ot + size_t(mr) * ep.ldo + n0 + j * 8) = u;
-                        }
-                        __syncwarp();
-                    } else if (live) {
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) st_global_v8(ot + size_t(m) * ep.ldo + n0 + q * 16, pk + q * 8);
-                    }
+                fence_proxy_async_smem(); // generic-proxy writes -> visible to the TMA store
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmO, dst, n0, m0w);
+                    bulk_commit();
+                    if (reads_e) mbar_arrive(&x_empty[KBD + kb]); // e k-block read: the next tile's may load
                 }
+            }
+            if (reads_z) { // hand the z (and e) k-blocks back to the X producer once the stores have read them
+                if (lane == 0) {
+                    bulk_wait_read0();
+                    for (int kb = half; kb < KBD; kb += 2) mbar_arrive(&x_empty[kb]);
+                }
+                __syncwarp();
             }
             if (trf) args.trace[512 + it * 4 + 2] = clock64();
         }
     }
+    if (warp >= 2 && warp < 2 + EW && lane == 0) bulk_wait_all(); // TMA stores out of this CTA's smem complete
     fence_before();
     cluster_sync_all(); // no CTA leaves while its peer may still signal its barriers or read its smem
     if (warp == 1) {
