@@ -98,6 +98,20 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int cols, int ld, int box_ro
     return m;
 }
 
+// 2-D bf16 map with an explicit box and swizzle (TMA store boxes of the fused MLP epilogues)
+CUtensorMap make_map_box(const void* ptr, int64_t rows, int cols, int ld, int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+    cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (box) failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
 // W1 of the 2-SM MLP as {64 cols, rows, k-blocks}: one box = box_rows rows x 2 k-blocks (16 KB)
 CUtensorMap make_map_w1_3d(const void* ptr, int64_t rows, int cols, int box_rows, int box_kb = 2) {
     CUtensorMap m;
@@ -475,9 +489,12 @@ void dump_mlp_trace(cider_ctx& c, const char* tag, int64_t M, int H, bool pair, 
             std::fprintf(stderr, "\n");
             std::fprintf(stderr, "\n");
         }
-        for (int it = 0; it < (pair ? 4 : 0); ++it)
-            std::fprintf(stderr, "  t%d final epilogue: wait %lld got %lld done %lld\n", it, h[512 + it * 4] - t0, h[512 + it * 4 + 1] - t0,
+        for (int it = 0; it < (pair ? 4 : 0); ++it) {
+            std::fprintf(stderr, "  t%d final epilogue: wait %lld got %lld done %lld |", it, h[512 + it * 4] - t0, h[512 + it * 4 + 1] - t0,
                          h[512 + it * 4 + 2] - t0);
+            for (int k = 1; k < 10; ++k) std::fprintf(stderr, " %lld", h[256 + it * 16 + k] ? h[256 + it * 16 + k] - t0 : -1);
+            std::fprintf(stderr, "\n");
+        }
     }
 }
 
@@ -525,7 +542,8 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     }
     if (pair) {
         if (ep.out_f || !ep.out_t) throw InvalidInput("cider: the 2-SM MLP writes one bf16 output");
-        const CUtensorMap& om = map_for(c, ep.out_t, M, D, ep.ldo, 32); // 32-row TMA store boxes
+        // one TMA store box (SW128) per 128-row x 64-column output k-block staged in the tile's X
+        const CUtensorMap om = make_map_box(ep.out_t, M, D, ep.ldo, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         if (D == 256) {
             if (ep.kind == EP_GATE) launch_mlp2<512, 256, EP_GATE>(c, x0, x1, w1, w2, om, a);
             else if (ep.kind == EP_RESID) launch_mlp2<512, 256, EP_RESID>(c, x0, x1, w1, w2, om, a);

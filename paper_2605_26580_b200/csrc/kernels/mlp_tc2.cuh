@@ -170,9 +170,10 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
         : "memory");
 }
 
-template <int KIN, int D, int STGW = 4096, int EW = 8>
+template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1>
 struct Mlp2Layout {
     static constexpr int STG_WARP = STGW;
+    static constexpr int XBUF = NXB; // row-tile buffers (2: the next tile's rows load during this tile)
     static constexpr int KB1 = KIN / 64;
     static constexpr int KB2 = MLP_HC / 64;
     static constexpr int W1_HALF = (MLP_HC / 2) * 64 * 2;   // 8 KB: this CTA's 64 rows of a W1 k-block
@@ -184,13 +185,14 @@ struct Mlp2Layout {
     // output staging for coalesced stores: one 32-row x 64-column bf16 block per epilogue warp (the
     // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
     static constexpr int STG_BYTES = KIN == D ? EW * STGW : 0;
-    static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - X_BYTES - STG_BYTES) / SLOT;
+    static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - NXB * X_BYTES - STG_BYTES) / SLOT;
     static constexpr int NS = NS_RAW > 16 ? 16 : NS_RAW;
-    static constexpr int STG_OFF = X_BYTES;
-    static constexpr int R_OFF = X_BYTES + STG_BYTES;
+    static constexpr int STG_OFF = NXB * X_BYTES;
+    static constexpr int R_OFF = NXB * X_BYTES + STG_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
     static constexpr int TOTAL = BAR_OFF + 512 + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
+    static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 4 + 2 + 2 + NXB * (D / 64)) * 8 + 4 <= 512, "barrier block");
     static_assert(D % 32 == 0 && D <= 256 && W2_HALF <= SLOT, "output width must be <= 256");
     static_assert(KB1 % W1_PER_SLOT == 0, "input width must be a multiple of 128");
 };
@@ -200,8 +202,11 @@ struct Mlp2Layout {
 constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
 constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : 8; }
 constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
+// The GELU variants stage their output in the tile's own X k-blocks (no staging region); the
+// aggregator (input = output width) double-buffers its row tile.
 template <int KIN, int D, int EPK>
-using Mlp2LayoutFor = Mlp2Layout<KIN, D, EPK == EP_DEMIX ? DEMIX_STG_WARP : 4096, mlp2_epi_warps(EPK)>;
+using Mlp2LayoutFor = Mlp2Layout<KIN, D, EPK == EP_DEMIX ? DEMIX_STG_WARP : 0, mlp2_epi_warps(EPK),
+                                 (KIN == D && EPK == EP_STORE) ? 2 : 1>;
 
 constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hidden columns = one MMA2 k-step)
 
@@ -342,16 +347,18 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint8_t* xs = smem;
     uint8_t* ring = smem + Lay::R_OFF;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
-    uint64_t* x_full = bar;             // [KB1] row-tile k-block landed (leader copy counts both CTAs)
-    uint64_t* x_empty = x_full + KB1;   // [KB1] k-block free: last MMA1 read it (+ final-epilogue readers)
-    uint64_t* r_full = x_empty + KB1;
+    constexpr int NXB = Lay::XBUF;
+    uint64_t* x_full = bar;             // [NXB][KB1] row-tile k-block landed (leader copy counts both CTAs)
+    uint64_t* x_empty = x_full + NXB * KB1; // [NXB][KB1] k-block free: last MMA1 read it (+ final-epilogue readers)
+    uint64_t* r_full = x_empty + NXB * KB1;
     uint64_t* r_empty = r_full + NS;
     uint64_t* a1_full = r_empty + NS;   // [2] first-layer accumulator ready
     uint64_t* h_full = a1_full + 2;     // [2][GG] GELU group g of acc1[b] packed (leader copy counts both CTAs)
     uint64_t* a1_free = h_full + 2 * MLP2_GG; // [2] MMA2 done reading acc1[b] (leader only)
     uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
+    uint64_t* o_full = a2_empty + 1;    // [NXB][KBD] output block staged in X k-block kb (4 quarter warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + NXB * KBD);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
@@ -373,11 +380,11 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // e / acc k-blocks load during the final epilogue and the first MMA1 starts on them.
     constexpr int ROT = reads_z ? KBD : 0;
     if (threadIdx.x == 0) {
-        // x_empty: the last MMA1 of the tile, plus (gate / fusion) the 4 warps whose final epilogue
-        // reads that z / e k-block
-        for (int kb = 0; kb < KB1; ++kb) {
+        // x_empty: the last MMA1 of the tile (+ the gate's 4 warps that read that e k-block); the
+        // output k-blocks are refilled by the X producer itself after storing them (o_full)
+        for (int kb = 0; kb < NXB * KB1; ++kb) {
             mbar_init(&x_full[kb], 1);
-            mbar_init(&x_empty[kb], 1 + ((reads_z && kb < KBD) || (reads_e && kb >= KBD) ? 4 : 0));
+            mbar_init(&x_empty[kb], 1 + (reads_e && kb % KB1 >= KBD ? 4 : 0));
         }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
@@ -387,6 +394,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         }
         mbar_init(a2_full, 1);
         mbar_init(a2_empty, EPI_ARRIVALS);
+        for (int kb = 0; kb < NXB * KBD; ++kb) mbar_init(&o_full[kb], 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -447,8 +455,12 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     } else if (warp == XLOAD_WARP) {
         if (lane == 0) { // row-tile producer, one k-block at a time
             uint32_t eph = 0;
-            for (int tile = pair; tile < args.tiles; tile += npairs) {
+            int itx = 0;
+            for (int tile = pair; tile < args.tiles; tile += npairs, ++itx) {
                 const int row0 = tile * 256 + int(rank) * 128;
+                const int xb = itx % NXB;
+                uint8_t* xsb = xs + xb * Lay::X_BYTES;
+                if (NXB > 1 && itx > 0 && xb == 0) eph ^= 1; // buffer 0's phase flips every NXB tiles
                 if constexpr (EPK == EP_DEMIX) { // tmX0 is 3-D: the whole row tile in ONE box, on x_full[0]
                     for (int kb = 0; kb < KB1; ++kb) mbar_wait(&x_empty[kb], eph ^ 1);
                     if (leader) mbar_expect_tx(&x_full[0], 2 * KB1 * 16384);
@@ -456,15 +468,46 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     eph ^= 1;
                     continue;
                 }
-                for (int i = 0; i < KB1; ++i) {
-                    const int kb = (i + ROT) % KB1;
-                    mbar_wait(&x_empty[kb], eph ^ 1);
-                    if (leader) mbar_expect_tx(&x_full[kb], 2 * 16384);
+                // The final epilogue stages the previous tile of this buffer in its k-blocks [0, KBD):
+                // this thread stores them (one TMA box per k-block, two at a time as the epilogue's two
+                // rounds finish) and refills them once the stores have read them out.
+                const int prev_row0 = row0 - NXB * npairs * 256;
+                const uint32_t oph = uint32_t((itx / NXB - 1) & 1);
+                auto load_kb = [&](int kb) {
+                    const int xk = xb * KB1 + kb;
+                    mbar_wait(&x_empty[xk], eph ^ 1);
+                    if (leader) mbar_expect_tx(&x_full[xk], 2 * 16384);
                     const int k = kb * 64;
-                    if (k < args.K0) tma_load_2d_2sm(xs + kb * 16384, &tmX0, L_x_full0 + kb * 8, k, row0);
-                    else tma_load_2d_2sm(xs + kb * 16384, &tmX1, L_x_full0 + kb * 8, k - args.K0, row0);
+                    if (k < args.K0) tma_load_2d_2sm(xsb + kb * 16384, &tmX0, L_x_full0 + xk * 8, k, row0);
+                    else tma_load_2d_2sm(xsb + kb * 16384, &tmX1, L_x_full0 + xk * 8, k - args.K0, row0);
+                };
+                for (int kb = KBD; kb < KB1; ++kb) load_kb(kb); // e / acc k-blocks (gate / fusion) first
+                for (int kb0 = 0; kb0 < KBD; kb0 += 2) {
+                    if (itx >= NXB) {
+                        for (int kb = kb0; kb < kb0 + 2 && kb < KBD; ++kb) {
+                            mbar_wait(&o_full[xb * KBD + kb], oph);
+                            tma_store_2d(&tmO, xsb + kb * 16384, kb * 64, prev_row0);
+                        }
+                        bulk_commit();
+                        bulk_wait_read0();
+                    }
+                    for (int kb = kb0; kb < kb0 + 2 && kb < KBD; ++kb) load_kb(kb);
                 }
-                eph ^= 1;
+                if (NXB == 1) eph ^= 1;
+            }
+            if constexpr (EPK != EP_DEMIX) { // the last NXB tiles' outputs
+                for (int q = 0; q < NXB; ++q) {
+                    const int itl = itx - NXB + q; // tile index (per CTA) whose output is still staged
+                    if (itl < 0) continue;
+                    const int xb = itl % NXB;
+                    const int row0 = (pair + itl * npairs) * 256 + int(rank) * 128;
+                    for (int kb = 0; kb < KBD; ++kb) {
+                        mbar_wait(&o_full[xb * KBD + kb], uint32_t((itl / NXB) & 1));
+                        tma_store_2d(&tmO, xs + xb * Lay::X_BYTES + kb * 16384, kb * 64, row0);
+                    }
+                    bulk_commit();
+                }
+                bulk_wait_all();
             }
         }
     } else if (warp == 1 || warp == MMA2_WARP) {
@@ -480,6 +523,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 uint32_t xph = 0, fph = 0; // fph bit b: phase of a1_free[b]
                 int n = 0, it = 0;
                 for (int tile = pair; tile < args.tiles; tile += npairs, ++it) {
+                    const int xb = it % NXB;
+                    if (NXB > 1 && it > 0 && xb == 0) xph ^= 1;
                     for (int c = 0; c < NC; ++c, ++n) {
                         const int b = n & 1;
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 6] = clock64();
@@ -493,13 +538,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             const int slot = ring_slot(it * per_tile + pos_w1(c) + sg, ph);
                             if (c == 0 && EPK == EP_DEMIX && sg == 0) mbar_wait(&x_full[0], xph); // one box
                             else if (c == 0 && EPK != EP_DEMIX) // the tile's k-blocks arrive one by one
-                                for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[(sg * Lay::W1_PER_SLOT + j + ROT) % KB1], xph);
+                                for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[xb * KB1 + (sg * Lay::W1_PER_SLOT + j + ROT) % KB1], xph);
                             mbar_wait(&r_full[slot], ph);
                             fence_after();
 #pragma unroll
                             for (int j = 0; j < Lay::W1_PER_SLOT; ++j) {
                                 const int kb = (sg * Lay::W1_PER_SLOT + j + ROT) % KB1;
-                                const uint64_t da = sw128_desc(xs + kb * 16384);
+                                const uint64_t da = sw128_desc(xs + xb * Lay::X_BYTES + kb * 16384);
                                 const uint64_t db = sw128_desc(ring + slot * Lay::SLOT + j * Lay::W1_HALF);
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
@@ -509,10 +554,10 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         }
                         mma_commit_2sm(&a1_full[b]);
                         if (c == NC - 1)
-                            for (int kb = 0; kb < KB1; ++kb) mma_commit_2sm(&x_empty[kb]);
+                            for (int kb = 0; kb < KB1; ++kb) mma_commit_2sm(&x_empty[xb * KB1 + kb]);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 7] = clock64();
                     }
-                    xph ^= 1;
+                    if (NXB == 1) xph ^= 1;
                 }
             } else {
                 constexpr uint32_t id2 = idesc_bf16(256, D);
@@ -673,6 +718,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             // write burst drains while the next tile's chunks run. A z / e k-block is handed back to the
             // X producer once the store out of it has been read.
             const int m0w = tile * 256 + int(rank) * 128 + quarter * 32;
+            uint8_t* xcur = xs + (it % NXB) * Lay::X_BYTES; // this tile's row buffer
             const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
             if (trf) args.trace[512 + it * 4 + 0] = clock64();
             mbar_wait(a2_full, e2ph);
@@ -682,16 +728,14 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #pragma unroll 1
             for (int kb = half; kb < KBD; kb += 2) {
                 const int n0 = kb * 64;
-                uint8_t* dst = reads_z ? xs + kb * 16384 + quarter * 4096 : smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP;
-                const uint8_t* esrc = xs + (KBD + kb) * 16384 + quarter * 4096;
-                if (!reads_z) { // the staging block's previous store must have been read out
-                    if (lane == 0) bulk_wait_read0();
-                    __syncwarp();
-                }
+                // this warp's 32 rows of X k-block kb: z in (gate / fusion), the output block out (all)
+                uint8_t* dst = xcur + kb * 16384 + quarter * 4096;
+                const uint8_t* esrc = xcur + (KBD + kb) * 16384 + quarter * 4096;
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) { // two 32-column halves of the k-block
                     float v[32];
                     tmem_ld32(tmem + lane_off + n0 + s2 * 32, v);
+                    if (trf) args.trace[256 + it * 16 + (kb / 2) * 5 + 1 + s2] = clock64();
                     if (s2 == 1 && kb + 2 >= KBD) {
                         fence_before();
                         release(L_a2_empty); // accumulator drained: next tile's MMA2 may start
@@ -735,25 +779,17 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         st_shared_v4(dst + off, pk);
                     }
                 }
-                fence_proxy_async_smem(); // generic-proxy writes -> visible to the TMA store
+                if (trf) args.trace[256 + it * 16 + (kb / 2) * 5 + 3] = clock64();
+                fence_proxy_async_smem(); // generic-proxy writes -> visible to the X producer's TMA store
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tmO, dst, n0, m0w);
-                    bulk_commit();
                     if (reads_e) mbar_arrive(&x_empty[KBD + kb]); // e k-block read: the next tile's may load
+                    mbar_arrive(&o_full[(it % NXB) * KBD + kb]);   // output block staged
                 }
-            }
-            if (reads_z) { // hand the z (and e) k-blocks back to the X producer once the stores have read them
-                if (lane == 0) {
-                    bulk_wait_read0();
-                    for (int kb = half; kb < KBD; kb += 2) mbar_arrive(&x_empty[kb]);
-                }
-                __syncwarp();
             }
             if (trf) args.trace[512 + it * 4 + 2] = clock64();
         }
     }
-    if (warp >= 2 && warp < 2 + EW && lane == 0) bulk_wait_all(); // TMA stores out of this CTA's smem complete
     fence_before();
     cluster_sync_all(); // no CTA leaves while its peer may still signal its barriers or read its smem
     if (warp == 1) {
