@@ -181,7 +181,8 @@ struct Mlp2Layout {
     static constexpr int SLOT = 16384;
     static constexpr int W1_PER_SLOT = SLOT / W1_HALF;       // 2
     static constexpr int X_BYTES = KB1 * 128 * 64 * 2;
-    static constexpr int FIXED = 1024 + 512;
+    static constexpr int FIXED = 1024 + 512 + 4 * D; // alignment slack, barriers, output bias
+    static constexpr int BIAS_OFF_FROM_BAR = 512;      // output bias [D] fp32 right after the barriers
     // output staging for coalesced stores: one 32-row x 64-column bf16 block per epilogue warp (the
     // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
     static constexpr int STG_BYTES = KIN == D ? EW * STGW : 0;
@@ -190,7 +191,7 @@ struct Mlp2Layout {
     static constexpr int STG_OFF = NXB * X_BYTES;
     static constexpr int R_OFF = NXB * X_BYTES + STG_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
-    static constexpr int TOTAL = BAR_OFF + 512 + 1024;
+    static constexpr int TOTAL = BAR_OFF + 512 + 4 * D + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
     static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 4 + 2 + 2 + NXB * (D / 64)) * 8 + 4 <= 512, "barrier block");
     static_assert(D % 32 == 0 && D <= 256 && W2_HALF <= SLOT, "output width must be <= 256");
@@ -200,7 +201,10 @@ struct Mlp2Layout {
 // EP_DEMIX runs 16 epilogue warps (4 per TMEM lane quarter, 32 hidden columns each) with one
 // [16][33] fp32 staging block per warp; the GELU variants run 8 with 4 KB each.
 constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
-constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : 8; }
+// 16 epilogue warps in every variant: demix = 16 warps on every phase; GELU variants = warps 2-9 on
+// the hidden chunks and warps 10-17 on the final epilogue (which then overlaps the next tile's chunks)
+constexpr int mlp2_epi_warps(int) { return 16; }
+constexpr int MLP2_FIN_WARP0 = 10;
 constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
 // The GELU variants stage their output in the tile's own X k-blocks (no staging region); the
 // aggregator (input = output width) double-buffers its row tile.
@@ -368,7 +372,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     constexpr int EPI_ARRIVALS = 2 * EW; // one elected lane per epilogue warp, both CTAs
     // hidden group g: GELU = 16 columns of both 64-column warp halves (all epilogue warps); demix =
     // the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
-    constexpr int H_ARRIVALS = EPK == EP_DEMIX ? 8 : EPI_ARRIVALS;
+    constexpr int H_ARRIVALS = EPK == EP_DEMIX ? 8 : 8 * 2; // demix: one warp per quarter x 2 CTAs; GELU: the 8 hidden warps x 2 CTAs
+    constexpr int A2_ARRIVALS = EPK == EP_DEMIX ? EPI_ARRIVALS : 8 * 2; // warps that drain acc2
 
     // Gate / fusion epilogues read z (and e) from global memory (L2: the same rows were just TMA'd
     // into X), so every X k-block is free once the tile's last MMA1 has read it and the next tile's
@@ -393,7 +398,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             mbar_init(&a1_free[b], 1);
         }
         mbar_init(a2_full, 1);
-        mbar_init(a2_empty, EPI_ARRIVALS);
+        mbar_init(a2_empty, A2_ARRIVALS);
         for (int kb = 0; kb < NXB * KBD; ++kb) mbar_init(&o_full[kb], 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -402,6 +407,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     fence_before();
+    float* bias_s = reinterpret_cast<float*>(smem + Lay::BAR_OFF + Lay::BIAS_OFF_FROM_BAR); // final-epilogue bias
+    for (int i = threadIdx.x; i < D; i += blockDim.x) bias_s[i] = args.ep.bias ? args.ep.bias[i] : 0.0f;
     cluster_sync_all(); // barriers of both CTAs initialised before any remote signal
     fence_after();
     const uint32_t tmem = *tmem_slot;
@@ -636,7 +643,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // 8 epilogue warps: TMEM lane quarter = warp % 4; the two warps of a quarter own the two
         // 64-column halves of every hidden chunk, and alternate 64-column k-blocks of the output.
         const int quarter = warp % 4;
-        const int half = (warp - 2) / 4;
+        const bool fin = EPK != EP_DEMIX && warp >= MLP2_FIN_WARP0; // final-epilogue warp (GELU variants)
+        const int half = fin ? (warp - MLP2_FIN_WARP0) / 4 : (warp - 2) / 4;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         uint32_t e1ph = 0, e2ph = 0; // e1ph bit b: phase of a1_full[b]
@@ -674,13 +682,11 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 demix_final(ep, stg, tmem + lane_off, half, m0, lane, L_a2_empty);
                 if (trf) args.trace[512 + it * 4 + 2] = clock64();
                 continue;
-            } else
+            }
+            if (!fin)
             for (int c = 0; c < NC; ++c, ++n) {
                 const int b = n & 1;
                 const float* b1 = args.b1 + c * MLP_HC + half * 64;
-                float4 bias4[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + q);
                 const bool tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
                 if (tr) args.trace[it * 64 + c * 8 + 2] = clock64();
                 mbar_wait(&a1_full[b], (e1ph >> b) & 1u);
@@ -693,12 +699,15 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #pragma unroll
                 for (int g = 0; g < MLP2_GG; ++g) {
                     if (!(args.dbg & 1)) {
+                        float4 bias4[4]; // this group's 16 hidden biases (L1-resident)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
                         float v[16];
                         tmem_ld16(base + g * 16, v);
                         uint32_t pk[8];
 #pragma unroll
                         for (int i = 0; i < 16; i += 4) {
-                            const float4 bb = bias4[g * 4 + i / 4];
+                            const float4 bb = bias4[i / 4];
                             pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
                             pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
                         }
@@ -710,6 +719,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
+            if (!fin) continue;
             // final epilogue straight from TMEM: this thread's row, output k-blocks half, half + 2, ...
             // Gate / fusion read z (and e) from the tile's own X k-blocks in SMEM (X = [z | e] / [z~ | acc]:
             // they are kept until here) and write the bf16 result over the z k-block; the aggregator
@@ -719,7 +729,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             // X producer once the store out of it has been read.
             const int m0w = tile * 256 + int(rank) * 128 + quarter * 32;
             uint8_t* xcur = xs + (it % NXB) * Lay::X_BYTES; // this tile's row buffer
-            const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
+            const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == MLP2_FIN_WARP0 + 2 && lane == 0;
             if (trf) args.trace[512 + it * 4 + 0] = clock64();
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
@@ -742,8 +752,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     }
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {
-                        const float4 bb = ep.bias ? __ldg(reinterpret_cast<const float4*>(ep.bias + n0 + s2 * 32 + i))
-                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 bb = *reinterpret_cast<const float4*>(bias_s + n0 + s2 * 32 + i); // SMEM broadcast
                         const float2 lo = __fadd2_rn(make_float2(v[i], v[i + 1]), make_float2(bb.x, bb.y));
                         const float2 hi = __fadd2_rn(make_float2(v[i + 2], v[i + 3]), make_float2(bb.z, bb.w));
                         v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;
