@@ -781,8 +781,10 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     // T-resident sweep chunk: default one chunk (each CTA one contiguous group-major range). Chunks of
     // 64-256 bins (z~ L2-resident across a slot's edges) measured slower: every extra T change drains
     // the CTA's MMA pipeline (bench c5: normalise 83 ms whole vs 85-100 ms chunked).
-    static const int mchunk_bins = std::getenv("CIDER_GRP_CHUNK_BINS") ? std::atoi(std::getenv("CIDER_GRP_CHUNK_BINS")) : 0;
-    a.mchunk = mchunk_bins > 0 ? std::max(1, mchunk_bins / bb) : a.mtiles;
+    // CIDER_GRP_CHUNK_BINS: -1 = laps (default), 0 = one contiguous group-major range per CTA, > 0 =
+    // chunked sweeps of that many bins
+    static const int mchunk_bins = std::getenv("CIDER_GRP_CHUNK_BINS") ? std::atoi(std::getenv("CIDER_GRP_CHUNK_BINS")) : -1;
+    a.mchunk = mchunk_bins < 0 ? -1 : mchunk_bins > 0 ? std::max(1, mchunk_bins / bb) : a.mtiles;
     const double rows = double(nb) * K * groups;
     Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, rows * D * 2.0 * (mean_seg + 1));
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
@@ -797,7 +799,9 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
                                     tc::GrpResLayout::TOTAL), "smem attr");
             attr_res = true;
         }
-        tc::gemm_grp_res_kernel<<<std::min(tiles, c.sm_count), tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, a);
+        // laps: one CTA per SM, at most one per group
+        const int grid = a.mchunk < 0 ? std::min(groups, c.sm_count) : std::min(tiles, c.sm_count);
+        tc::gemm_grp_res_kernel<<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, a);
         check_launch(tag);
         return;
     }

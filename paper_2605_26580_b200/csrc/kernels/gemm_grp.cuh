@@ -184,8 +184,30 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 // MMA). All CTAs work on the same chunk at once, so the z~ rows a slot shares among its (column
 // weight) edges come from DRAM once and from L2 for the other edges. The epilogue stages each warp's
 // 32 x 32 bf16 block in SMEM and writes whole 64-byte row segments.
+//
+// mchunk < 0 (default): "laps" — CTA c takes group c of each full lap of gridDim.x groups over ALL
+// m-tiles (groups are slot-major, so the column-weight edges of a slot run on neighbouring CTAs at
+// the same m-tile at the same time and share the gathered z~ rows through L2: DRAM reads them once
+// instead of once per edge), then the remaining groups split their m-tile range across the CTAs.
+// One T_alpha per lap per CTA.
 template <typename F>
 __device__ __forceinline__ void grp_res_sweep(const GrpArgs& args, F&& body) {
+    if (args.mchunk < 0) {
+        const int G = args.groups, C = int(gridDim.x), c = int(blockIdx.x);
+        int g0 = 0;
+        for (; G - g0 >= C; g0 += C)
+            for (int mt = 0; mt < args.mtiles; ++mt) body(g0 + c, mt);
+        const int rem = G - g0;
+        if (rem > 0) {
+            const int R = max(1, C / rem);
+            if (c < rem * R) {
+                const int part = c / rem, g = g0 + c % rem;
+                const int m0 = int(int64_t(part) * args.mtiles / R), m1 = int(int64_t(part + 1) * args.mtiles / R);
+                for (int mt = m0; mt < m1; ++mt) body(g, mt);
+            }
+        }
+        return;
+    }
     for (int c0 = 0; c0 < args.mtiles; c0 += args.mchunk) {
         const int mc = min(args.mchunk, args.mtiles - c0);
         const int tot = args.groups * mc;
@@ -297,11 +319,20 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             fence_after();
             const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
             const int rows_live = args.K * args.bb;
+            const int orow_g = __ldg(args.out_row + g); // once per tile (was reloaded per stored row)
             auto orow_of = [&](int r /* tile row */, bool& ok) -> size_t {
                 const int b = mt * args.bb + r / args.K, k = r % args.K;
                 ok = r < rows_live && b < args.bins;
-                return (size_t(b) * args.out_rows_per_bin + args.out_row[g]) * args.K + k;
+                return (size_t(b) * args.out_rows_per_bin + orow_g) * args.K + k;
             };
+            // the 4 rows this lane copies out of the staging block in every 32-column chunk
+            bf16* orow_ptr[4];
+            bool orow_ok[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const size_t orow = orow_of(quarter * 32 + i * 8 + lane / 4, orow_ok[i]);
+                orow_ptr[i] = args.out_t + orow * args.D + (lane % 4) * 8;
+            }
             for (int c0 = half * (args.D / 2); c0 < (half + 1) * (args.D / 2); c0 += 32) {
                 float v[32];
                 tmem_ld32(tbase + c0, v);
@@ -328,11 +359,8 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int r = i * 8 + lane / 4, j = lane % 4;
-                    bool ok;
-                    const size_t orow = orow_of(quarter * 32 + r, ok);
-                    if (ok)
-                        *reinterpret_cast<uint4*>(args.out_t + orow * args.D + c0 + j * 8) =
-                            *reinterpret_cast<const uint4*>(os + r * 32 + ((j ^ (r & 3)) * 8));
+                    if (orow_ok[i])
+                        *reinterpret_cast<uint4*>(orow_ptr[i] + c0) = *reinterpret_cast<const uint4*>(os + r * 32 + ((j ^ (r & 3)) * 8));
                 }
                 __syncwarp();
             }
