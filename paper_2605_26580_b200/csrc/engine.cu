@@ -141,11 +141,11 @@ CUtensorMap make_map_rows3d(const void* ptr, int bins, int rows_per_bin, int col
     return m;
 }
 // The T table [alpha][n][k] as {k, n, alpha}, box {64, 256, 1}.
-CUtensorMap make_map_ttab(const void* ptr, int D, int Q) {
+CUtensorMap make_map_ttab(const void* ptr, int D, int Q, int box_rows = 0) {
     CUtensorMap m;
     cuuint64_t dims[3] = {cuuint64_t(D), cuuint64_t(D), cuuint64_t(Q)};
     cuuint64_t strides[2] = {cuuint64_t(D) * 2, cuuint64_t(D) * D * 2};
-    cuuint32_t box[3] = {64, cuuint32_t(D), 1};
+    cuuint32_t box[3] = {64, cuuint32_t(box_rows > 0 ? box_rows : D), 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -806,6 +806,34 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         return;
     }
     using Lay = tc::SmemLayout<256, 0>;
+    static const int grp_mode = std::getenv("CIDER_GRP_MODE") ? std::atoi(std::getenv("CIDER_GRP_MODE")) : 2;
+    if (grp_mode == 2 && a.mtiles >= 2 && c.sm_count >= 2 && D == 256) {
+        // CTA pairs, one cta_group::2 MMA over two m-tiles: each SM pulls half of every T k-block
+        static bool attr2 = false;
+        if (!attr2) {
+            ck(cudaFuncSetAttribute(tc::gemm_grp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::GRP2_SMEM), "smem attr");
+            attr2 = true;
+        }
+        const int supers = a.groups * ((a.mtiles + 1) / 2);
+        const int grid = 2 * std::min(supers, c.sm_count / 2);
+        const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
+        tc::gemm_grp2_kernel<<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, a);
+        check_launch(tag);
+        return;
+    }
+    if (grp_mode == 1 && a.mtiles >= 2 && c.sm_count >= 2) {
+        // cluster pairs: T_alpha multicast into both CTAs (two m-tiles of the same group)
+        static bool attr_mc = false;
+        if (!attr_mc) {
+            ck(cudaFuncSetAttribute(tc::gemm_grp_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
+            attr_mc = true;
+        }
+        const int supers = a.groups * ((a.mtiles + 1) / 2);
+        const int grid = 2 * std::min(supers, c.sm_count / 2);
+        tc::gemm_grp_mc_kernel<<<grid, tc::GRP_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
+        check_launch(tag);
+        return;
+    }
     static bool attr_set = false;
     if (!attr_set) {
         ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");

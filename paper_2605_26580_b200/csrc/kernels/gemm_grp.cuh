@@ -17,6 +17,7 @@
 #pragma once
 
 #include "gemm_tc.cuh"
+#include "mlp_tc2.cuh" // 2-SM TMA / MMA / commit helpers
 
 namespace cider {
 namespace tc {
@@ -175,6 +176,316 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Lay::TMEM_COLS));
     }
 }
+
+// ---- cluster-pair variant (the message GEMM, group = slot, segments = its edges) -----------------
+// The kernel is L2-bound on the T_alpha stream (per 128-row tile 3 x 128 KB of T against 3 x 64 KB of
+// gathered A). Two CTAs of a cluster take the same group for two neighbouring m-tiles: rank 0 loads
+// each T k-block ONCE with a cluster multicast into both CTAs' stage, each CTA loads its own A rows
+// and runs its own 1-SM MMAs; a stage is refilled once BOTH CTAs' MMAs have read it (every MMA commit
+// arrives on the empty barrier of both CTAs). Half the T bytes per tile leave L2.
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GRP_THREADS, 1)
+gemm_grp_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
+    constexpr int BN = 256;
+    using Lay = SmemLayout<BN, 0>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // same offset in both CTAs
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cl_rank();
+    const int cid = int(blockIdx.x) / 2, ncl = int(gridDim.x) / 2;
+    const int mpairs = (args.mtiles + 1) / 2;
+    const int supers = args.groups * mpairs;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 2); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 256); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(Lay::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    cl_sync(); // both CTAs' barriers initialised before any multicast lands
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int a_bytes = args.K * args.bb * 128;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int st = cid; st < supers; st += ncl) {
+                const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
+                const int nseg = args.seg_count[g];
+                for (int sg = 0; sg < nseg; ++sg) {
+                    const int arow = args.seg_arow[g * args.max_seg + sg];
+                    const int alpha = args.seg_alpha[g * args.max_seg + sg];
+                    for (int kk = 0; kk < args.kb_per_seg; ++kk) {
+                        mbar_wait(&empty[stage], phase ^ 1); // both CTAs' MMAs are done with this stage
+                        uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
+                        uint8_t* sb = sa + Lay::A_BYTES;
+                        mbar_expect_tx(&full[stage], a_bytes + Lay::B_BYTES);
+                        tma_load_3d(sa, &tmA, &full[stage], kk * 64, arow * args.K, mt * args.bb); // (zero rows past the bins)
+                        if (rank == 0) tma_load_3d_mc(sb, &tmT, &full[stage], kk * 64, 0, alpha, uint16_t(3));
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int st = cid; st < supers; st += ncl) {
+                const int g = st % args.groups;
+                const int kblocks = args.seg_count[g] * args.kb_per_seg;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
+                    uint8_t* sb = sa + Lay::A_BYTES;
+                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
+                    mma_commit_mc(&empty[stage], uint16_t(3)); // both CTAs may refill (T lands in both)
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        const int quarter = warp % 4;
+        const int half = (warp - 2) / 4; // the two warps of a lane quarter split the columns
+        const int row = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int st = cid; st < supers; st += ncl) {
+            const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
+            mbar_wait(&tfull[acc], acc_phase);
+            fence_after();
+            const int b = mt * args.bb + row / args.K, k = row % args.K;
+            const bool live = row < args.K * args.bb && b < args.bins;
+            const size_t orow = (size_t(b) * args.out_rows_per_bin + __ldg(args.out_row + g)) * args.K + k;
+            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+            const int cw = args.D / 2;
+            for (int c0 = half * cw; c0 < (half + 1) * cw; c0 += 32) {
+                float v[32];
+                tmem_ld32(tbase + c0, v);
+                if (!live) continue;
+                if (args.out_f) {
+                    float* o = args.out_f + orow * args.D + c0;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                }
+                bf16* o = args.out_t + orow * args.D + c0;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
+                    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+                    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
+                    __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+                    uint4 u;
+                    u.x = *reinterpret_cast<uint32_t*>(&p0);
+                    u.y = *reinterpret_cast<uint32_t*>(&p1);
+                    u.z = *reinterpret_cast<uint32_t*>(&p2);
+                    u.w = *reinterpret_cast<uint32_t*>(&p3);
+                    *reinterpret_cast<uint4*>(o + i) = u;
+                }
+            }
+            fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    fence_before();
+    cl_sync(); // the peer may still multicast into this CTA's stages or arrive on its barriers
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Lay::TMEM_COLS));
+    }
+}
+
+// ---- CTA-pair variant: one cta_group::2 MMA over two m-tiles ---------------------------------------
+// Per SM the message GEMM is bound by the bytes it must pull into SMEM (per 128-row tile 3 x 64 KB of
+// gathered A rows + 3 x 128 KB of T). With M = 256 tiles on a CTA pair each CTA loads its own A rows
+// and only HALF of every T k-block (the N-half the pair's MMA reads from it): 3 x (64 + 64) KB per SM
+// per tile. Protocol as the 2-SM MLP (mlp_tc2.cuh): both producers signal the leader's full barrier,
+// the leader arms it and issues the MMAs, its commits multicast to both CTAs; the epilogue warps of
+// both CTAs release the accumulator on the leader's barrier.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GRP_THREADS, 1)
+gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
+    constexpr int BN = 256;
+    constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of a k-block
+    constexpr int B_HALF = (BN / 2) * BK * 2;       // 16 KB: this CTA's N-half of a T k-block
+    constexpr int STAGE = A_BYTES + B_HALF;
+    constexpr int NST = 6;
+    constexpr int BAR_OFF = NST * STAGE;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // same offset in both CTAs
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = int(blockIdx.x) / 2, npairs = int(gridDim.x) / 2;
+    const int mpairs = (args.mtiles + 1) / 2;
+    const int supers = args.groups * mpairs;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * 8); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    fence_before();
+    cluster_sync_all();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int a_bytes = args.K * args.bb * 128; // the A box actually filled (<= 16 KB)
+    const uint32_t L_full0 = mapa_u32(smem_u32(&full[0]), 0);
+    const uint32_t L_tempty0 = mapa_u32(smem_u32(&tempty[0]), 0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int st = pair; st < supers; st += npairs) {
+                const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
+                const int nseg = args.seg_count[g];
+                for (int sg = 0; sg < nseg; ++sg) {
+                    const int arow = args.seg_arow[g * args.max_seg + sg];
+                    const int alpha = args.seg_alpha[g * args.max_seg + sg];
+                    for (int kk = 0; kk < args.kb_per_seg; ++kk) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        if (leader) mbar_expect_tx(&full[stage], 2 * (a_bytes + B_HALF)); // both CTAs' bytes
+                        uint8_t* sa = smem + stage * STAGE;
+                        // (rows past the bins: zero-filled box, bytes still counted)
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                                smem_u32(sa)),
+                            "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(L_full0 + stage * 8), "r"(kk * 64), "r"(arow * args.K), "r"(mt * args.bb)
+                            : "memory");
+                        tma_load_3d_2sm(sa + A_BYTES, &tmT, L_full0 + stage * 8, kk * 64, int(rank) * (BN / 2), alpha);
+                        if (++stage == NST) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(256, BN);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int st = pair; st < supers; st += npairs) {
+                const int g = st % args.groups;
+                const int kblocks = args.seg_count[g] * args.kb_per_seg;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    uint8_t* sa = smem + stage * STAGE;
+                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + A_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
+                    mma_commit_2sm(&empty[stage]);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit_2sm(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        const int quarter = warp % 4;
+        const int half = (warp - 2) / 4; // the two warps of a lane quarter split the columns
+        const int row = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int st = pair; st < supers; st += npairs) {
+            const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
+            mbar_wait(&tfull[acc], acc_phase);
+            fence_after();
+            const int b = mt * args.bb + row / args.K, k = row % args.K;
+            const bool live = row < args.K * args.bb && b < args.bins;
+            const size_t orow = (size_t(b) * args.out_rows_per_bin + __ldg(args.out_row + g)) * args.K + k;
+            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+            const int cw = args.D / 2;
+            for (int c0 = half * cw; c0 < (half + 1) * cw; c0 += 32) {
+                float v[32];
+                tmem_ld32(tbase + c0, v);
+                if (!live) continue;
+                if (args.out_f) {
+                    float* o = args.out_f + orow * args.D + c0;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                }
+                uint32_t pk[16];
+#pragma unroll
+                for (int t = 0; t < 16; ++t) {
+                    __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * t], v[2 * t + 1]);
+                    pk[t] = *reinterpret_cast<uint32_t*>(&p);
+                }
+                bf16* o = args.out_t + orow * args.D + c0;
+                st_global_v8(o, pk);
+                st_global_v8(o + 16, pk + 8);
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cl(L_tempty0 + acc * 8);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    fence_before();
+    cluster_sync_all(); // no CTA leaves while its peer may still signal its barriers or read its smem
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+constexpr int GRP2_SMEM = 6 * (BM * BK * 2 + 128 * BK * 2) + 256 + 1024;
 
 // ---- T-resident variant for single-segment groups (the normalise GEMM, group = edge) ------------
 // The m-tiles are swept in chunks of `mchunk` (128 bins at K = 8: 32 MB of z~, L2-resident); inside a
