@@ -801,7 +801,9 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         }
         // laps: one CTA per SM, at most one per group
         const int grid = a.mchunk < 0 ? std::min(groups, c.sm_count) : std::min(tiles, c.sm_count);
-        tc::gemm_grp_res_kernel<<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, a);
+        if (out_f || !out_t) throw InvalidInput("cider: the T-resident grouped GEMM writes one bf16 output");
+        const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb); // TMA store boxes
+        tc::gemm_grp_res_kernel<<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, to, a);
         check_launch(tag);
         return;
     }

@@ -530,13 +530,14 @@ struct GrpResLayout {
     static constexpr int T_OFF = 0;                 // 4 k-blocks x (256 x 64 bf16)
     static constexpr int A_OFF = 4 * 32768;         // ring of A k-blocks, 16 KB each
     static constexpr int NST = 4;
-    static constexpr int STG_OFF = A_OFF + NST * 16384;
-    static constexpr int BAR_OFF = STG_OFF + 8 * 2048;
+    static constexpr int STG_OFF = A_OFF + NST * 16384; // 2 x 16 KB output k-block staging (SW128, TMA store)
+    static constexpr int BAR_OFF = STG_OFF + 2 * 16384;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
 __global__ void __launch_bounds__(GRP_THREADS, 1)
-gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
+gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
+                    const __grid_constant__ CUtensorMap tmO, const GrpArgs args) {
     using Lay = GrpResLayout;
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
@@ -621,64 +622,55 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
     } else {
         const int quarter = warp % 4;
-        const int half = (warp - 2) / 4; // column half of every row
-        bf16* os = reinterpret_cast<bf16*>(smem + Lay::STG_OFF + (warp - 2) * 2048);
-        int acc = 0;
+        const int half = (warp - 2) / 4; // 32-column half of every 64-column output k-block
+        const bool issuer = warp == 2 && lane == 0;
+        int acc = 0, step = 0;
         uint32_t acc_phase = 0;
+        // Output k-block kb (128 rows x 64 columns) is staged by all 8 warps in a 16 KB SW128 block
+        // (double-buffered) and leaves as ONE TMA store of the 3-D rows box {64, K, bb} (whole
+        // 128-byte lines; was 64-byte segments per 4 lanes). Named barrier 1 (the 256 epilogue
+        // threads): staged -> store issued and the buffer of two steps ago read out.
         grp_res_sweep(args, [&](int g, int mt) {
             mbar_wait(&afull[acc], acc_phase);
             fence_after();
             const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-            const int rows_live = args.K * args.bb;
-            const int orow_g = __ldg(args.out_row + g); // once per tile (was reloaded per stored row)
-            auto orow_of = [&](int r /* tile row */, bool& ok) -> size_t {
-                const int b = mt * args.bb + r / args.K, k = r % args.K;
-                ok = r < rows_live && b < args.bins;
-                return (size_t(b) * args.out_rows_per_bin + orow_g) * args.K + k;
-            };
-            // the 4 rows this lane copies out of the staging block in every 32-column chunk
-            bf16* orow_ptr[4];
-            bool orow_ok[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const size_t orow = orow_of(quarter * 32 + i * 8 + lane / 4, orow_ok[i]);
-                orow_ptr[i] = args.out_t + orow * args.D + (lane % 4) * 8;
-            }
-            for (int c0 = half * (args.D / 2); c0 < (half + 1) * (args.D / 2); c0 += 32) {
+            const int orow_g = __ldg(args.out_row + g);
+            const int r = quarter * 32 + lane; // this thread's tile row
+#pragma unroll 1
+            for (int kb = 0; kb < args.D / 64; ++kb, ++step) {
                 float v[32];
-                tmem_ld32(tbase + c0, v);
-                if (args.out_f) {
-                    bool ok;
-                    const size_t orow = orow_of(quarter * 32 + lane, ok);
-                    if (ok) {
-                        float* o = args.out_f + orow * args.D + c0;
-#pragma unroll
-                        for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                    }
+                tmem_ld32(tbase + kb * 64 + half * 32, v);
+                if (kb == args.D / 64 - 1) { // accumulator drained
+                    fence_before();
+                    mbar_arrive(&aempty[acc]);
                 }
+                uint8_t* stg = smem + Lay::STG_OFF + (step & 1) * 16384;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int jj = 0; jj < 4; ++jj) {
                     uint32_t pk[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        __nv_bfloat162 p = __floats2bfloat162_rn(v[j * 8 + 2 * q], v[j * 8 + 2 * q + 1]);
+                        __nv_bfloat162 p = __floats2bfloat162_rn(v[jj * 8 + 2 * q], v[jj * 8 + 2 * q + 1]);
                         pk[q] = *reinterpret_cast<uint32_t*>(&p);
                     }
-                    *reinterpret_cast<uint4*>(os + lane * 32 + ((j ^ (lane & 3)) * 8)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    const int j = half * 4 + jj;
+                    *reinterpret_cast<uint4*>(stg + r * 128 + ((j ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int r = i * 8 + lane / 4, j = lane % 4;
-                    if (orow_ok[i])
-                        *reinterpret_cast<uint4*>(orow_ptr[i] + c0) = *reinterpret_cast<const uint4*>(os + r * 32 + ((j ^ (r & 3)) * 8));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (issuer) {
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                     reinterpret_cast<uint64_t>(&tmO)),
+                                 "r"(smem_u32(stg)), "r"(kb * 64), "r"(orow_g * args.K), "r"(mt * args.bb)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); // the other buffer is free
                 }
-                __syncwarp();
+                asm volatile("bar.sync 1, 256;" ::: "memory");
             }
-            fence_before();
-            mbar_arrive(&aempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         });
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     __syncthreads();
     if (warp == 1) {
