@@ -819,7 +819,9 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         const int supers = a.groups * ((a.mtiles + 1) / 2);
         const int grid = 2 * std::min(supers, c.sm_count / 2);
         const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
-        tc::gemm_grp2_kernel<<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, a);
+        if (!out_t) throw InvalidInput("cider: the paired grouped GEMM writes a bf16 output");
+        const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb); // TMA store boxes
+        tc::gemm_grp2_kernel<<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, to, a);
         check_launch(tag);
         return;
     }

@@ -348,13 +348,15 @@ gemm_grp_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 // the leader arms it and issues the MMAs, its commits multicast to both CTAs; the epilogue warps of
 // both CTAs release the accumulator on the leader's barrier.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GRP_THREADS, 1)
-gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
+gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
+                 const __grid_constant__ CUtensorMap tmO, const GrpArgs args) {
     constexpr int BN = 256;
     constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of a k-block
     constexpr int B_HALF = (BN / 2) * BK * 2;       // 16 KB: this CTA's N-half of a T k-block
     constexpr int STAGE = A_BYTES + B_HALF;
     constexpr int NST = 6;
-    constexpr int BAR_OFF = NST * STAGE;
+    constexpr int STG_OFF = NST * STAGE;       // 2 x 16 KB output k-block staging (SW128, TMA store)
+    constexpr int BAR_OFF = STG_OFF + 2 * 16384;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // same offset in both CTAs
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
@@ -439,10 +441,14 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
     } else {
+        // epilogue: output k-block kb (128 rows x 64 columns) staged by all 8 warps (SW128, double
+        // buffered) and sent by one 3-D TMA store, as in gemm_grp_res_kernel; the optional fp32 copy
+        // (incoming messages) is written directly
         const int quarter = warp % 4;
-        const int half = (warp - 2) / 4; // the two warps of a lane quarter split the columns
+        const int half = (warp - 2) / 4; // 32-column half of every 64-column output k-block
         const int row = quarter * 32 + lane;
-        int acc = 0;
+        const bool issuer = warp == 2 && lane == 0;
+        int acc = 0, step = 0;
         uint32_t acc_phase = 0;
         for (int st = pair; st < supers; st += npairs) {
             const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
@@ -450,33 +456,51 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             fence_after();
             const int b = mt * args.bb + row / args.K, k = row % args.K;
             const bool live = row < args.K * args.bb && b < args.bins;
-            const size_t orow = (size_t(b) * args.out_rows_per_bin + __ldg(args.out_row + g)) * args.K + k;
+            const int orow_g = __ldg(args.out_row + g);
+            const size_t orow = (size_t(b) * args.out_rows_per_bin + orow_g) * args.K + k;
             const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-            const int cw = args.D / 2;
-            for (int c0 = half * cw; c0 < (half + 1) * cw; c0 += 32) {
+#pragma unroll 1
+            for (int kb = 0; kb < args.D / 64; ++kb, ++step) {
+                const int c0 = kb * 64 + half * 32;
                 float v[32];
                 tmem_ld32(tbase + c0, v);
-                if (!live) continue;
-                if (args.out_f) {
+                if (kb == args.D / 64 - 1) { // accumulator drained
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cl(L_tempty0 + acc * 8);
+                }
+                if (args.out_f && live) {
                     float* o = args.out_f + orow * args.D + c0;
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                 }
-                uint32_t pk[16];
+                uint8_t* stg = smem + STG_OFF + (step & 1) * 16384;
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * t], v[2 * t + 1]);
-                    pk[t] = *reinterpret_cast<uint32_t*>(&p);
+                for (int jj = 0; jj < 4; ++jj) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        __nv_bfloat162 p = __floats2bfloat162_rn(v[jj * 8 + 2 * q], v[jj * 8 + 2 * q + 1]);
+                        pk[q] = *reinterpret_cast<uint32_t*>(&p);
+                    }
+                    const int j = half * 4 + jj;
+                    *reinterpret_cast<uint4*>(stg + row * 128 + ((j ^ (row & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                 }
-                bf16* o = args.out_t + orow * args.D + c0;
-                st_global_v8(o, pk);
-                st_global_v8(o + 16, pk + 8);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (issuer) {
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                     reinterpret_cast<uint64_t>(&tmO)),
+                                 "r"(smem_u32(stg)), "r"(kb * 64), "r"(orow_g * args.K), "r"(mt * args.bb)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); // the other buffer is free
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");
             }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cl(L_tempty0 + acc * 8);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     fence_before();
     cluster_sync_all(); // no CTA leaves while its peer may still signal its barriers or read its smem
@@ -485,7 +509,7 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
 }
-constexpr int GRP2_SMEM = 6 * (BM * BK * 2 + 128 * BK * 2) + 256 + 1024;
+constexpr int GRP2_SMEM = 6 * (BM * BK * 2 + 128 * BK * 2) + 2 * 16384 + 256 + 1024;
 
 // ---- T-resident variant for single-segment groups (the normalise GEMM, group = edge) ------------
 // The m-tiles are swept in chunks of `mchunk` (128 bins at K = 8: 32 MB of z~, L2-resident); inside a
