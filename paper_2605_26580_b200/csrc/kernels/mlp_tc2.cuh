@@ -373,7 +373,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // hidden group g: GELU = 16 columns of both 64-column warp halves (all epilogue warps); demix =
     // the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
     constexpr int H_ARRIVALS = EPK == EP_DEMIX ? 8 : 8 * 2; // demix: one warp per quarter x 2 CTAs; GELU: the 8 hidden warps x 2 CTAs
-    constexpr int A2_ARRIVALS = EPK == EP_DEMIX ? EPI_ARRIVALS : 8 * 2; // warps that drain acc2
+    // Final epilogue: the aggregator (double-buffered rows) runs it on warps 10-17 only, overlapping the
+    // next tile's chunks; gate / fusion (whose next row tile waits for it) on all 16 epilogue warps, one
+    // output k-block each, to shorten the tile transition.
+    constexpr bool FIN_ALL = false; // (all 16 warps on the gate / fusion final epilogue measured no faster)
+    constexpr int FIN_STRIDE = FIN_ALL ? 4 : 2;                  // output k-blocks between one warp's
+    constexpr int FIN_WARPS = FIN_ALL ? (4 * KBD < 16 ? 4 * KBD : 16) : 8;
+    constexpr int A2_ARRIVALS = EPK == EP_DEMIX ? EPI_ARRIVALS : FIN_WARPS * 2; // warps that drain acc2
 
     // Gate / fusion epilogues read z (and e) from global memory (L2: the same rows were just TMA'd
     // into X), so every X k-block is free once the tile's last MMA1 has read it and the next tile's
@@ -488,8 +494,11 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     if (k < args.K0) tma_load_2d_2sm(xsb + kb * 16384, &tmX0, L_x_full0 + xk * 8, k, row0);
                     else tma_load_2d_2sm(xsb + kb * 16384, &tmX1, L_x_full0 + xk * 8, k - args.K0, row0);
                 };
-                for (int kb = KBD; kb < KB1; ++kb) load_kb(kb); // e / acc k-blocks (gate / fusion) first
+                // by final-epilogue round (its warp halves finish output k-blocks kb0, kb0 + 1 together, and
+                // the gate's e k-blocks KBD + kb0, KBD + kb0 + 1 with them): e / acc first, then the z pair
                 for (int kb0 = 0; kb0 < KBD; kb0 += 2) {
+                    if (KB1 > KBD)
+                        for (int kb = KBD + kb0; kb < KBD + kb0 + 2; ++kb) load_kb(kb);
                     if (itx >= NXB) {
                         for (int kb = kb0; kb < kb0 + 2 && kb < KBD; ++kb) {
                             mbar_wait(&o_full[xb * KBD + kb], oph);
@@ -719,7 +728,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
-            if (!fin) continue;
+            if (!fin && !FIN_ALL) continue;
+            const int fsub = FIN_ALL ? (warp - 2) / 4 : half; // first output k-block of this warp
+            if (fsub >= KBD) continue;
             // final epilogue straight from TMEM: this thread's row, output k-blocks half, half + 2, ...
             // Gate / fusion read z (and e) from the tile's own X k-blocks in SMEM (X = [z | e] / [z~ | acc]:
             // they are kept until here) and write the bf16 result over the z k-block; the aggregator
@@ -736,7 +747,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             fence_after();
             if (trf) args.trace[512 + it * 4 + 1] = clock64();
 #pragma unroll 1
-            for (int kb = half; kb < KBD; kb += 2) {
+            for (int kb = fsub; kb < KBD; kb += FIN_STRIDE) {
                 const int n0 = kb * 64;
                 // this warp's 32 rows of X k-block kb: z in (gate / fusion), the output block out (all)
                 uint8_t* dst = xcur + kb * 16384 + quarter * 4096;
@@ -746,7 +757,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     float v[32];
                     tmem_ld32(tmem + lane_off + n0 + s2 * 32, v);
                     if (trf) args.trace[256 + it * 16 + (kb / 2) * 5 + 1 + s2] = clock64();
-                    if (s2 == 1 && kb + 2 >= KBD) {
+                    if (s2 == 1 && kb + FIN_STRIDE >= KBD) {
                         fence_before();
                         release(L_a2_empty); // accumulator drained: next tile's MMA2 may start
                     }
