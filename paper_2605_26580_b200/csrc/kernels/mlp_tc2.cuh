@@ -223,22 +223,34 @@ constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hi
 // S[(bin, slot)][column]. The bf16 results come back row-wise through the same SMEM block and are
 // packed IN PLACE into the warp's own TMEM columns as the A operand of the V GEMM. beta S is a
 // per-group constant shift of the logits and cancels inside softmax_k (not applied).
+// S[(bin, slot)][column] for this lane's column and row groups of one warp chunk (both passes),
+// requested one chunk ahead of its use
 template <int KK>
-__device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, uint32_t base, uint64_t* a1_full_b, uint32_t ph,
-                                           uint32_t l_h_full, int m0, int col0, int lane, long long* tr) {
-    constexpr int NGL = 16 / KK; // row groups per lane (lanes 0-15: rows 0-15, lanes 16-31: rows 16-31)
-    const Epi& ep = args.ep;
-    float* xs = reinterpret_cast<float*>(stg); // [16 columns][33] fp32; then [32 rows][32 B] bf16
+__device__ __forceinline__ void demix_load_sv(const MlpArgs& args, int m0, int col0, int lane, float* sv) {
+    constexpr int NGL = 16 / KK;
     const int cl = lane & 15, rh = lane >> 4;
-    const float scale2 = ep.inv_tau * 1.4426950408889634f;
-    float sv[2][NGL]; // S[(bin, slot)][column] for this lane's column and groups, both passes
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
         for (int t = 0; t < NGL; ++t) {
             const int r0 = m0 + rh * 16 + t * KK;
-            sv[p][t] = r0 < ep.M ? __ldg(ep.S + size_t(r0 / KK) * args.H + col0 + p * 16 + cl) : 0.0f;
+            sv[p * NGL + t] = r0 < args.ep.M ? __ldg(args.ep.S + size_t(r0 / KK) * args.H + col0 + p * 16 + cl) : 0.0f;
         }
+}
+
+template <int KK>
+__device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, uint32_t base, uint64_t* a1_full_b, uint32_t ph,
+                                           uint32_t l_h_full, const float* svin, int lane, long long* tr) {
+    constexpr int NGL = 16 / KK; // row groups per lane (lanes 0-15: rows 0-15, lanes 16-31: rows 16-31)
+    const Epi& ep = args.ep;
+    float* xs = reinterpret_cast<float*>(stg); // [16 columns][33] fp32; then [32 rows][32 B] bf16
+    const int cl = lane & 15, rh = lane >> 4;
+    const float scale2 = ep.inv_tau * 1.4426950408889634f;
+    float sv[2][NGL];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int t = 0; t < NGL; ++t) sv[p][t] = svin[p * NGL + t];
     if (tr) tr[2] = clock64();
     mbar_wait(a1_full_b, ph);
     fence_after();
@@ -663,6 +675,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             if (lane == 0) mbar_arrive_cl(leader_bar);
         };
         int n = 0; // chunk counter across tiles: acc1 buffer = n & 1
+        float svn[8]; // EP_DEMIX: the next chunk's S values
         for (int tile = pair; tile < args.tiles; tile += npairs) {
             const int it = (tile - pair) / npairs;
             if constexpr (EPK == EP_DEMIX) {
@@ -670,16 +683,28 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 // Lambda-bar and r (x) S never leaving the chip: hidden = the Q symbol columns
                 uint8_t* stg = smem + Lay::STG_OFF + (warp - 2) * Lay::STG_WARP;
                 const int m0 = tile * 256 + int(rank) * 128 + quarter * 32;
+                const int m0n = m0 + npairs * 256; // the next tile's rows
+                if (tile == pair) { // first tile: nothing was prefetched
+                    if (ep.K == 8) demix_load_sv<8>(args, m0, half * 32, lane, svn);
+                    else demix_load_sv<4>(args, m0, half * 32, lane, svn);
+                }
                 for (int c = 0; c < NC; ++c, ++n) {
                     long long* tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0 ? args.trace + it * 64 + c * 8 : nullptr;
                     const int b = n & 1;
                     const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 32;
+                    float svc[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) svc[i] = svn[i];
+                    // the next chunk's S (this tile's, or the next tile's first)
+                    const int cn = c + 1 < NC ? c + 1 : 0, mn = c + 1 < NC ? m0 : m0n;
+                    if (c + 1 < NC || tile + npairs < args.tiles) {
+                        if (ep.K == 8) demix_load_sv<8>(args, mn, cn * MLP_HC + half * 32, lane, svn);
+                        else demix_load_sv<4>(args, mn, cn * MLP_HC + half * 32, lane, svn);
+                    }
                     if (ep.K == 8)
-                        demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, m0,
-                                      c * MLP_HC + half * 32, lane, tr);
+                        demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, svc, lane, tr);
                     else
-                        demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, m0,
-                                      c * MLP_HC + half * 32, lane, tr);
+                        demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, svc, lane, tr);
                     e1ph ^= 1u << b;
                 }
                 const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
