@@ -203,8 +203,14 @@ struct Mlp2Layout {
 constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
 // 16 epilogue warps in every variant: demix = 16 warps on every phase; GELU variants = warps 2-9 on
 // the hidden chunks and warps 10-17 on the final epilogue (which then overlaps the next tile's chunks)
-constexpr int mlp2_epi_warps(int) { return 16; }
-constexpr int MLP2_FIN_WARP0 = 10;
+// MLP2_GELU16: the GELU variants run 16 hidden-chunk warps (4 per lane quarter, 32 columns each, the
+// demix layout) + 8 final-epilogue warps; else 8 hidden-chunk warps (64 columns each) + 8 final.
+#ifndef MLP2_GELU16
+#define MLP2_GELU16 0 // measured slower (c5: agg 356 -> 390 ms; the 72-register cap of 896 threads)
+#endif
+constexpr int MLP2_HW = MLP2_GELU16 ? 16 : 8;            // hidden-chunk warps of the GELU variants
+constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : MLP2_HW + 8; }
+constexpr int MLP2_FIN_WARP0 = 2 + MLP2_HW;
 constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
 // The GELU variants stage their output in the tile's own X k-blocks (no staging region); the
 // aggregator (input = output width) double-buffers its row tile.
@@ -384,7 +390,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     constexpr int EPI_ARRIVALS = 2 * EW; // one elected lane per epilogue warp, both CTAs
     // hidden group g: GELU = 16 columns of both 64-column warp halves (all epilogue warps); demix =
     // the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
-    constexpr int H_ARRIVALS = EPK == EP_DEMIX ? 8 : 8 * 2; // demix: one warp per quarter x 2 CTAs; GELU: the 8 hidden warps x 2 CTAs
+    // hidden group g: one warp per quarter x 2 CTAs (32-column warps), or the 8 hidden warps x 2 CTAs
+    constexpr bool W32 = EPK == EP_DEMIX || MLP2_GELU16; // 32-column hidden warps
+    constexpr int H_ARRIVALS = W32 ? 8 : 8 * 2;
     // Final epilogue: the aggregator (double-buffered rows) runs it on warps 10-17 only, overlapping the
     // next tile's chunks; gate / fusion (whose next row tile waits for it) on all 16 epilogue warps, one
     // output k-block each, to shorten the tile transition.
@@ -599,7 +607,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         // are GELU group g of warp-half kb, packed in place at TMEM cols 64 kb + 8 g: k-step g
                         // of W2 slot kb, issued as soon as that group lands in both CTAs.
                         const uint32_t a_base = tmem + 256 + b * MLP_HC;
-                        if constexpr (EPK == EP_DEMIX) {
+                        if constexpr (W32) {
                             // group g = hidden columns [32 g, 32 g + 32) of every quarter, packed at TMEM
                             // columns 32 g + [0, 16): k-steps 2 g, 2 g + 1 of W2 k-block g / 2
 #pragma unroll
@@ -717,7 +725,41 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 if (trf) args.trace[512 + it * 4 + 2] = clock64();
                 continue;
             }
-            if (!fin)
+            if (!fin && W32)
+            for (int c = 0; c < NC; ++c, ++n) {
+                // 32-column warp: fp32 columns [32 half, 32 half + 32) -> GELU -> bf16 pairs packed IN
+                // PLACE at [32 half, 32 half + 16) (16-column group g' at + 8 g'), then one release
+                const int b = n & 1;
+                const float* b1 = args.b1 + c * MLP_HC + half * 32;
+                const bool tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
+                if (tr) args.trace[it * 64 + c * 8 + 2] = clock64();
+                mbar_wait(&a1_full[b], (e1ph >> b) & 1u);
+                e1ph ^= 1u << b;
+                fence_after();
+                if (tr) args.trace[it * 64 + c * 8 + 3] = clock64();
+                const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 32;
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    float4 bias4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
+                    float v[16];
+                    tmem_ld16(base + g * 16, v);
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        const float4 bb = bias4[i / 4];
+                        pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
+                        pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
+                    }
+                    tmem_st8(base + g * 8, pk);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                fence_before();
+                release(L_h_full0 + (MLP2_GG * b + half) * 8); // this warp's 32 columns -> MMA2 k-steps 2 half, 2 half + 1
+                if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
+            }
+            if (!fin && !W32)
             for (int c = 0; c < NC; ++c, ++n) {
                 const int b = n & 1;
                 const float* b1 = args.b1 + c * MLP_HC + half * 64;
