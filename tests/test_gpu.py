@@ -399,3 +399,42 @@ def test_refine_ragged_equals_per_load_calls(P):
         assert grids[b].shape == (k, wl.slots) and np.array_equal(grids[b], ref[0])
     with pytest.raises(ValueError, match="load outside"):
         ctx.refine_ragged(S[:1], np.array([5], np.int32), scheds, rms)
+
+
+# ---- the fused sm_100a kernels of the BASELINE c3/c5 shapes (Q = D = 256, heads = 8, degree 6) ---
+@pytest.mark.parametrize("k", [4, 8])
+def test_fused_bf16_kernels_parity_and_invariants(P, oracle, k):
+    """The c3/c5 kernel set — Lambda-bar -> demix -> e in one 2-SM kernel, the 2-SM MLPs with
+    X-staged TMA-stored outputs, the one-pass attention pool, the lap-scheduled normalise and the
+    CTA-pair message GEMMs — on a small code: parity with the oracle, bitwise row-permutation
+    equivariance and bitwise extrinsicity of the layer's check messages (SURVEY §4 property tests,
+    test_denoiser.cpp:213-247, 293-326). 40 bins: an odd number of 128-row tiles for K = 8 (the
+    CTA pair's second m-tile falls past the bins)."""
+    wl = P.Workload(m=8, slots=16, checks=8, k=k, snr_db=4.0, p_erase=0.1, p_false=0.1)
+    model = P.Model(m=8, dim=256, hidden=256, layers=1, heads=8, precision=P.BF16)
+    ctx, e, w = ctx_for(P, model, wl)
+    nb = 40
+    _, S = wl.bins(e, 0, nb)
+    rng = np.random.default_rng(5)
+    X = np.where(rng.random((nb, k, wl.slots)) < 0.5, rng.integers(0, model.q, size=(nb, k, wl.slots)), -1).astype(np.int32)
+    X[:, k - 1] = X[:, 0]  # identical rows -> exact ties
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    lg, inc = ctx.denoise(X, S, want_incoming=True)
+    ctx.set_profiling(False)
+    tags = set(ctx.kernel_stats())
+    assert {"demix_evid", "mlp_gate", "pool_attn", "mlp_agg", "grp_normalise", "grp_message", "mlp_fuse"} <= tags, tags
+    wr = as_run(P, model, w)
+    for b in (0, nb - 1):
+        lo, io = oracle.denoise(model, wr, e, wl.checks, wl.slots, X[b], S[b].astype(np.float64), True)
+        assert rel_err(lg[b], lo) < BF16_TOL
+        assert rel_err(inc[b, 0], io[0]) < BF16_TOL
+    assert np.array_equal(lg[:, k - 1], lg[:, 0])
+    p = np.roll(np.arange(k), 1)
+    lgp = ctx.denoise(X[:, p], S)
+    assert np.array_equal(lgp, lg[:, p])
+    for l in (0, 9):
+        Y = X.copy()
+        Y[:, :, l] = (np.maximum(Y[:, :, l], 0) + 7) % model.q
+        _, inc2 = ctx.denoise(Y, S, want_incoming=True)
+        assert np.array_equal(inc2[:, 0][:, :, l], inc[:, 0][:, :, l])
