@@ -786,7 +786,8 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     static const int mchunk_bins = std::getenv("CIDER_GRP_CHUNK_BINS") ? std::atoi(std::getenv("CIDER_GRP_CHUNK_BINS")) : -1;
     a.mchunk = mchunk_bins < 0 ? -1 : mchunk_bins > 0 ? std::max(1, mchunk_bins / bb) : a.mtiles;
     const double rows = double(nb) * K * groups;
-    Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, rows * D * 2.0 * (mean_seg + 1));
+    // compulsory bytes: every A row once (normalise: the site rows its edges share) + the output rows
+    Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, (double(nb) * K * (a_rows_per_bin + out_rows_per_bin)) * D * 2.0);
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
     CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
     const int tiles = a.groups * a.mtiles;
@@ -1596,11 +1597,14 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
         ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
         upload_model(*c, weights);
         upload_code(*c);
-        // Q >= D: Module B through precomputed coefficient actions (gemm_grp.cuh); slots with no
-        // incident check (possible in external codes) would make an empty group -> generic path
+        // D = 256: Module B through precomputed coefficient actions (gemm_grp.cuh). For Q < D (c4)
+        // T_alpha has rank <= Q and the D x D GEMM executes 2-4x the FLOPs of the Q-space route, but
+        // as one fused grouped GEMM without the projection / permutation / back-projection round trips
+        // it is faster (c4: 1093 -> 1197 bins/s). Slots with no incident check (possible in external
+        // codes) would make an empty group -> generic path.
         bool every_slot_checked = true;
         for (int l = 0; l < c->L; ++l) every_slot_checked &= c->tg->slot_ptr[l + 1] > c->tg->slot_ptr[l];
-        if (c->bf16 && c->D == 256 && c->Q >= c->D && every_slot_checked && !std::getenv("CIDER_NO_TPATH"))
+        if (c->bf16 && c->D == 256 && every_slot_checked && !std::getenv("CIDER_NO_TPATH"))
             build_tpath(*c);
         ck(cudaDeviceSynchronize(), "upload");
         *out = c.release();
