@@ -45,8 +45,9 @@ __device__ __forceinline__ void mma_16816(float* d, uint32_t a0, uint32_t a1, ui
 // Nn: edge rows [(b*E + e)*K + k][256] bf16 through tmN (box {64, 6K}); Uhl: [16][256] bf16, rows
 // h < NH = hi(u_h / sqrt(D/NH)), rows 8 + h = the bf16 remainder; n_blocks = bins * P.
 // Two independent 4-warp groups per CTA alternate blocks (each with PM_NBUF / 2 buffers and its own
-// named barrier); warp w of a group owns rows k = 2w, 2w + 1 of a block: it computes their DEG x 2 head
-// scores (one m16 tile, 12 real rows) and pools them, so no CTA-wide barrier sits between the phases.
+// named barrier); warp w of a group computes the head scores of block rows [12 w, 12 w + 12) (one m16
+// tile) into the group's scratch, and after the group barrier pools rows k = w K/4 .. (w + 1) K/4 - 1
+// (all four warps pool, for K = 4 as well as K = 8); no CTA-wide barrier sits between the phases.
 __global__ void __launch_bounds__(PM_THREADS, 2)
 pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict__ Uhl, const int* __restrict__ check_ptr,
                 int P, int E, int K, int NH, int64_t n_blocks, bf16* __restrict__ pooled) {
@@ -135,11 +136,12 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         }
         if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory"); // the group's scores are in
         else asm volatile("bar.sync 2, 128;" ::: "memory");
-        if (2 * wg < K) {
+        const int kpw = (K + 3) / 4; // pooled rows k per warp: every warp of the group pools (K = 4: one each)
+        if (wg * kpw < K) {
             // (2) pooling of rows k = 2 wg + kk
 #pragma unroll 1
-            for (int kk = 0; kk < 2 && 2 * wg + kk < K; ++kk) {
-                const int k = 2 * wg + kk;
+            for (int kk = 0; kk < kpw && wg * kpw + kk < K; ++kk) {
+                const int k = wg * kpw + kk;
                 float2 f[PM_DEG][4];
                 float sc[PM_DEG];
 #pragma unroll
