@@ -48,9 +48,12 @@ __device__ __forceinline__ void mma_16816(float* d, uint32_t a0, uint32_t a1, ui
 // named barrier); warp w of a group computes the head scores of block rows [12 w, 12 w + 12) (one m16
 // tile) into the group's scratch, and after the group barrier pools rows k = w K/4 .. (w + 1) K/4 - 1
 // (all four warps pool, for K = 4 as well as K = 8); no CTA-wide barrier sits between the phases.
+// K (rows per edge, 4 or 8) is a template parameter: block geometry and the pooled-row loop are
+// compile-time, so the per-row address arithmetic folds away (the kernel is issue-bound).
+template <int K>
 __global__ void __launch_bounds__(PM_THREADS, 2)
 pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict__ Uhl, const int* __restrict__ check_ptr,
-                int P, int E, int K, int NH, int64_t n_blocks, bf16* __restrict__ pooled) {
+                int P, int E, int NH, int64_t n_blocks, bf16* __restrict__ pooled) {
     using Lay = PoolMmaLayout;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -61,8 +64,8 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     // per-group score scratch [48 block rows][8 heads]: warp wg scores block rows [12 wg, 12 wg + 12)
     // (consecutive rows: distinct SW128 phases, conflict-free ldmatrix) and pools rows k = 2 wg, 2 wg + 1
     float* ss = reinterpret_cast<float*>(smem + Lay::S_OFF) + grp * 512;
-    const int R = PM_DEG * K;        // rows per block (<= 48)
-    const int KBS = R * 128;         // k-block stride inside a block buffer
+    constexpr int R = PM_DEG * K;    // rows per block (<= 48)
+    constexpr int KBS = R * 128;     // k-block stride inside a block buffer
     constexpr int GB = PM_NBUF / 2;  // buffers per group
 
     // score matrix into SMEM: 16-byte chunk c of row n at (c & ~7) | ((c ^ n) & 7) (ldmatrix conflict-free)
@@ -136,12 +139,13 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         }
         if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory"); // the group's scores are in
         else asm volatile("bar.sync 2, 128;" ::: "memory");
-        const int kpw = (K + 3) / 4; // pooled rows k per warp: every warp of the group pools (K = 4: one each)
+        constexpr int kpw = (K + 3) / 4; // pooled rows k per warp: every warp of the group pools (K = 4: one each)
         if (wg * kpw < K) {
-            // (2) pooling of rows k = 2 wg + kk
+            // (2) pooling of rows k = wg kpw + kk (not unrolled: 128-register cap at 2 CTAs / SM)
 #pragma unroll 1
-            for (int kk = 0; kk < kpw && wg * kpw + kk < K; ++kk) {
+            for (int kk = 0; kk < kpw; ++kk) {
                 const int k = wg * kpw + kk;
+                bf16* orow = pooled + (size_t(b * E + e0) * K + k) * 256 + lane * 8; // edge i at + i K 256 (64-bit)
                 float2 f[PM_DEG][4];
                 float sc[PM_DEG];
 #pragma unroll
@@ -190,7 +194,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                     __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
                     for (int v = 0; v < 4; ++v) po[v] = __floats2bfloat162_rn(out[v].x, out[v].y);
-                    *reinterpret_cast<uint4*>(pooled + ((b * E + e0 + i) * K + k) * 256 + lane * 8) = o;
+                    *reinterpret_cast<uint4*>(orow + i * K * 256) = o;
                 }
             }
         }
