@@ -721,26 +721,31 @@ void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* poo
 
 // BF16, check-regular degree 6, D = 256, heads in {1, 2, 4, 8}, 6K <= 48 rows per (bin, check) block (K = 4 or 8)
 bool pool_mma_ok(const cider_ctx& c, const LayerW& lw, int K) {
-    return c.bf16 && lw.aus16 && c.D == 256 && c.max_check_deg == 6 && c.min_check_deg == 6 && 8 % c.heads == 0 &&
+    return c.bf16 && lw.aus16 && (c.D == 256 || c.D == 128) && c.max_check_deg == 6 && c.min_check_deg == 6 && 8 % c.heads == 0 &&
            (K == 4 || K == 8) && !std::getenv("CIDER_NO_POOL_MMA");
 }
 const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, int ld, int box_rows);
-template <int K>
+template <int K, int D>
 void launch_pool_mma(cider_ctx& c, const LayerW& lw, const CUtensorMap& tm, int64_t blocks, void* pooled) {
     static bool attr = false;
     if (!attr) {
-        ck(cudaFuncSetAttribute(pool_mma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, PoolMmaLayout::TOTAL), "smem attr");
+        ck(cudaFuncSetAttribute(pool_mma_kernel<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, PoolMmaLayout::TOTAL), "smem attr");
         attr = true;
     }
     const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count) * 2));
-    pool_mma_kernel<K><<<grid, PM_THREADS, PoolMmaLayout::TOTAL, c.stream>>>(tm, (const bf16*)lw.aus16, c.check_ptr, c.P, c.E,
+    pool_mma_kernel<K, D><<<grid, PM_THREADS, PoolMmaLayout::TOTAL, c.stream>>>(tm, (const bf16*)lw.aus16, c.check_ptr, c.P, c.E,
                                                                              c.heads, blocks, (bf16*)pooled);
 }
 void run_pool_mma(cider_ctx& c, const LayerW& lw, const void* Nn, int64_t Me, int nb, int K, void* pooled) {
     const CUtensorMap& tm = map_for(c, Nn, Me, c.D, c.D, 6 * K);
     const int64_t blocks = int64_t(nb) * c.P;
-    if (K == 8) launch_pool_mma<8>(c, lw, tm, blocks, pooled);
-    else launch_pool_mma<4>(c, lw, tm, blocks, pooled);
+    if (c.D == 256) {
+        if (K == 8) launch_pool_mma<8, 256>(c, lw, tm, blocks, pooled);
+        else launch_pool_mma<4, 256>(c, lw, tm, blocks, pooled);
+    } else {
+        if (K == 8) launch_pool_mma<8, 128>(c, lw, tm, blocks, pooled);
+        else launch_pool_mma<4, 128>(c, lw, tm, blocks, pooled);
+    }
 }
 
 // BF16, check-regular degree 6, D = 256, 1..16 heads dividing 32 lanes: scores from EP_SCORES

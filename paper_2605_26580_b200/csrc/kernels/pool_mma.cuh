@@ -50,7 +50,7 @@ __device__ __forceinline__ void mma_16816(float* d, uint32_t a0, uint32_t a1, ui
 // (all four warps pool, for K = 4 as well as K = 8); no CTA-wide barrier sits between the phases.
 // K (rows per edge, 4 or 8) is a template parameter: block geometry and the pooled-row loop are
 // compile-time, so the per-row address arithmetic folds away (the kernel is issue-bound).
-template <int K>
+template <int K, int D>
 __global__ void __launch_bounds__(PM_THREADS, 2)
 pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict__ Uhl, const int* __restrict__ check_ptr,
                 int P, int E, int NH, int64_t n_blocks, bf16* __restrict__ pooled) {
@@ -66,13 +66,18 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     float* ss = reinterpret_cast<float*>(smem + Lay::S_OFF) + grp * 512;
     constexpr int R = PM_DEG * K;    // rows per block (<= 48)
     constexpr int KBS = R * 128;     // k-block stride inside a block buffer
+    constexpr int NKB = D / 64;      // 64-column k-blocks per row (4 or 2)
+    constexpr int CPL = D / 32;      // pooled columns per lane (8 or 4)
+    constexpr int V = CPL / 2;       // float2 per lane per row
+    constexpr int RB = D * 2;        // bytes per row of the score matrix
+    static_assert(D == 256 || D == 128, "pool_mma: D = 128 or 256");
     constexpr int GB = PM_NBUF / 2;  // buffers per group
 
     // score matrix into SMEM: 16-byte chunk c of row n at (c & ~7) | ((c ^ n) & 7) (ldmatrix conflict-free)
-    for (int i = tid; i < 16 * 32; i += PM_THREADS) {
-        const int n = i / 32, c = i % 32;
-        *reinterpret_cast<uint4*>(us + n * 512 + (((c & ~7) | ((c ^ n) & 7)) * 16)) =
-            *reinterpret_cast<const uint4*>(Uhl + n * 256 + c * 8);
+    for (int i = tid; i < 16 * (D / 8); i += PM_THREADS) {
+        const int n = i / (D / 8), c = i % (D / 8);
+        *reinterpret_cast<uint4*>(us + n * RB + (((c & ~7) | ((c ^ n) & 7)) * 16)) =
+            *reinterpret_cast<const uint4*>(Uhl + n * D + c * 8);
     }
     if (tid == 0) {
         for (int s = 0; s < PM_NBUF; ++s) tc::mbar_init(&full[s], 1);
@@ -89,8 +94,8 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         const int j = blk - b * P;
         const int row0 = (b * E + check_ptr[j]) * K;
         uint64_t* bar = &full[grp * GB + slot];
-        tc::mbar_expect_tx(bar, 4 * R * 128);
-        for (int kb = 0; kb < 4; ++kb)
+        tc::mbar_expect_tx(bar, NKB * R * 128);
+        for (int kb = 0; kb < NKB; ++kb)
             tc::tma_load_2d(smem + (grp * GB + slot) * PM_BUF + kb * KBS, &tmN, bar, kb * 64, row0);
     };
     const bool leader = wg == 0 && lane == 0;
@@ -100,7 +105,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     // rows of this warp's m16 tile: block rows 12 wg + q for q < 12
     const int q = lane & 15;
     const int arow = 12 * wg + (q < 2 * PM_DEG ? q : q - 4); // pad lanes repeat rows 8-11 (same address: broadcast)
-    const int h = (lane * 8) / (256 / NH); // pooling: lane = 8-column chunk of head h
+    const int h = (lane * CPL) / (D / NH); // pooling: lane = CPL-column slice of head h
     int slot = 0;
     uint32_t ph = 0; // bit s: phase of this group's full[s]
     for (int blk = first; blk < nblk; blk += stride) {
@@ -115,7 +120,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
             // (1) head scores of the warp's 12 rows: n-tile 0 = hi(u), 1 = lo(u)
             float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll 4
-            for (int ks = 0; ks < 16; ++ks) {
+            for (int ks = 0; ks < D / 16; ++ks) {
                 const int kc = ks * 2 + (lane >> 4);
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4(tc::smem_u32(nb + (kc >> 3) * KBS + arow * 128 + (((kc & 7) ^ (arow & 7)) * 16)), a0, a1, a2, a3);
@@ -124,7 +129,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                 for (int nt = 0; nt < 2; ++nt) {
                     const int n = nt * 8 + (lane & 7);
                     uint32_t b0, b1;
-                    ldsm_x2(tc::smem_u32(us + n * 512 + (((kc2 & ~7) | ((kc2 ^ n) & 7)) * 16)), b0, b1);
+                    ldsm_x2(tc::smem_u32(us + n * RB + (((kc2 & ~7) | ((kc2 ^ n) & 7)) * 16)), b0, b1);
                     mma_16816(acc[nt], a0, a1, a2, a3, b0, b1);
                 }
             }
@@ -145,17 +150,25 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
 #pragma unroll 1
             for (int kk = 0; kk < kpw; ++kk) {
                 const int k = wg * kpw + kk;
-                bf16* orow = pooled + (size_t(b * E + e0) * K + k) * 256 + lane * 8; // edge i at + i K 256 (64-bit)
-                float2 f[PM_DEG][4];
+                bf16* orow = pooled + (size_t(b * E + e0) * K + k) * D + lane * CPL; // edge i at + i K D (64-bit)
+                float2 f[PM_DEG][V];
                 float sc[PM_DEG];
 #pragma unroll
                 for (int i = 0; i < PM_DEG; ++i) {
                     const int r = i * K + k;
                     sc[i] = ss[r * 8 + h];
-                    const uint4 u = *reinterpret_cast<const uint4*>(nb + (lane >> 3) * KBS + r * 128 + (((lane & 7) ^ (r & 7)) * 16));
-                    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                    if constexpr (V == 4) { // 8 columns = one 16-byte chunk of k-block lane / 8
+                        const uint4 u = *reinterpret_cast<const uint4*>(nb + (lane >> 3) * KBS + r * 128 + (((lane & 7) ^ (r & 7)) * 16));
+                        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) f[i][v] = __bfloat1622float2(p2[v]);
+                        for (int v = 0; v < 4; ++v) f[i][v] = __bfloat1622float2(p2[v]);
+                    } else { // 4 columns = half a chunk of k-block lane / 16
+                        const uint2 u = *reinterpret_cast<const uint2*>(nb + (lane >> 4) * KBS + r * 128 +
+                                                                        ((((lane >> 1) & 7) ^ (r & 7)) * 16) + (lane & 1) * 8);
+                        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                        for (int v = 0; v < 2; ++v) f[i][v] = __bfloat1622float2(p2[v]);
+                    }
                 }
                 // leave-one-out softmax: max over the edges other than i is the overall max M1 for every
                 // i except the (first) argmax i1, whose max over the others is the runner-up M2 — the same
@@ -182,19 +195,21 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                     for (int i2 = 0; i2 < PM_DEG; ++i2)
                         if (i2 != i) den += i == i1 ? e2[i2] : e1[i2];
                     const float fct = __fdividef(float(PM_DEG - 1), den);
-                    float2 out[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                    float2 out[V];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) out[v] = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int i2 = 0; i2 < PM_DEG; ++i2) {
                         if (i2 == i) continue;
                         const float w = (i == i1 ? e2[i2] : e1[i2]) * fct;
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) out[v] = __ffma2_rn(make_float2(w, w), f[i2][v], out[v]);
+                        for (int v = 0; v < V; ++v) out[v] = __ffma2_rn(make_float2(w, w), f[i2][v], out[v]);
                     }
-                    uint4 o;
-                    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
+                    __nv_bfloat162 po[V];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) po[v] = __floats2bfloat162_rn(out[v].x, out[v].y);
-                    *reinterpret_cast<uint4*>(orow + i * K * 256) = o;
+                    for (int v = 0; v < V; ++v) po[v] = __floats2bfloat162_rn(out[v].x, out[v].y);
+                    if constexpr (V == 4) *reinterpret_cast<uint4*>(orow + i * K * D) = *reinterpret_cast<const uint4*>(po);
+                    else *reinterpret_cast<uint2*>(orow + i * K * D) = *reinterpret_cast<const uint2*>(po);
                 }
             }
         }

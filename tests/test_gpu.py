@@ -402,8 +402,8 @@ def test_refine_ragged_equals_per_load_calls(P):
 
 
 # ---- the fused sm_100a kernels of the BASELINE c3/c5 shapes (Q = D = 256, heads = 8, degree 6) ---
-@pytest.mark.parametrize("k", [4, 8])
-def test_fused_bf16_kernels_parity_and_invariants(P, oracle, k):
+@pytest.mark.parametrize("k,dim", [(4, 256), (8, 256), (4, 128)])
+def test_fused_bf16_kernels_parity_and_invariants(P, oracle, k, dim):
     """The c3/c5 kernel set — Lambda-bar -> demix -> e in one 2-SM kernel, the 2-SM MLPs with
     X-staged TMA-stored outputs, the one-pass attention pool, the lap-scheduled normalise and the
     CTA-pair message GEMMs — on a small code: parity with the oracle, bitwise row-permutation
@@ -411,7 +411,7 @@ def test_fused_bf16_kernels_parity_and_invariants(P, oracle, k):
     test_denoiser.cpp:213-247, 293-326). 40 bins: an odd number of 128-row tiles for K = 8 (the
     CTA pair's second m-tile falls past the bins)."""
     wl = P.Workload(m=8, slots=16, checks=8, k=k, snr_db=4.0, p_erase=0.1, p_false=0.1)
-    model = P.Model(m=8, dim=256, hidden=256, layers=1, heads=8, precision=P.BF16)
+    model = P.Model(m=8, dim=dim, hidden=256, layers=1, heads=8, precision=P.BF16)
     ctx, e, w = ctx_for(P, model, wl)
     nb = 40
     _, S = wl.bins(e, 0, nb)
@@ -423,7 +423,10 @@ def test_fused_bf16_kernels_parity_and_invariants(P, oracle, k):
     lg, inc = ctx.denoise(X, S, want_incoming=True)
     ctx.set_profiling(False)
     tags = set(ctx.kernel_stats())
-    assert {"demix_evid", "mlp_gate", "pool_attn", "mlp_agg", "grp_normalise", "grp_message", "mlp_fuse"} <= tags, tags
+    want = {"mlp_gate", "pool_attn", "mlp_agg", "mlp_fuse"}
+    if dim == 256:
+        want |= {"demix_evid", "grp_normalise", "grp_message"}
+    assert want <= tags, tags
     wr = as_run(P, model, w)
     for b in (0, nb - 1):
         lo, io = oracle.denoise(model, wr, e, wl.checks, wl.slots, X[b], S[b].astype(np.float64), True)
