@@ -802,11 +802,13 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
     const int tiles = a.groups * a.mtiles;
     static const bool no_res = std::getenv("CIDER_NO_TRES") != nullptr;
-    if (max_seg == 1 && D == 256 && !no_res) {
+    if (max_seg == 1 && (D == 256 || D == 128) && !no_res) {
         // single-segment groups: T-resident kernel (T loaded once per group change per CTA)
         static bool attr_res = false;
         if (!attr_res) {
-            ck(cudaFuncSetAttribute(tc::gemm_grp_res_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            ck(cudaFuncSetAttribute(tc::gemm_grp_res_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::GrpResLayout::TOTAL), "smem attr");
+            ck(cudaFuncSetAttribute(tc::gemm_grp_res_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     tc::GrpResLayout::TOTAL), "smem attr");
             attr_res = true;
         }
@@ -814,17 +816,20 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         const int grid = a.mchunk < 0 ? std::min(groups, c.sm_count) : std::min(tiles, c.sm_count);
         if (out_f || !out_t) throw InvalidInput("cider: the T-resident grouped GEMM writes one bf16 output");
         const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb); // TMA store boxes
-        tc::gemm_grp_res_kernel<<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, to, a);
+        if (D == 256) tc::gemm_grp_res_kernel<256><<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, to, a);
+        else tc::gemm_grp_res_kernel<128><<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, to, a);
         check_launch(tag);
         return;
     }
     using Lay = tc::SmemLayout<256, 0>;
     static const int grp_mode = std::getenv("CIDER_GRP_MODE") ? std::atoi(std::getenv("CIDER_GRP_MODE")) : 2;
-    if (grp_mode == 2 && a.mtiles >= 2 && c.sm_count >= 2 && D == 256) {
+    if ((grp_mode == 2 && a.mtiles >= 2 && c.sm_count >= 2 && D == 256) || D == 128) {
         // CTA pairs, one cta_group::2 MMA over two m-tiles: each SM pulls half of every T k-block
+        // (D = 128 always: the other grouped kernels are D = 256 only)
         static bool attr2 = false;
         if (!attr2) {
-            ck(cudaFuncSetAttribute(tc::gemm_grp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::GRP2_SMEM), "smem attr");
+            ck(cudaFuncSetAttribute(tc::gemm_grp2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::GRP2_SMEM), "smem attr");
+            ck(cudaFuncSetAttribute(tc::gemm_grp2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::GRP2_SMEM), "smem attr");
             attr2 = true;
         }
         const int supers = a.groups * ((a.mtiles + 1) / 2);
@@ -832,7 +837,8 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
         if (!out_t) throw InvalidInput("cider: the paired grouped GEMM writes a bf16 output");
         const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb); // TMA store boxes
-        tc::gemm_grp2_kernel<<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, to, a);
+        if (D == 256) tc::gemm_grp2_kernel<256><<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, to, a);
+        else tc::gemm_grp2_kernel<128><<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, to, a);
         check_launch(tag);
         return;
     }
@@ -1614,7 +1620,7 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
         // codes) would make an empty group -> generic path.
         bool every_slot_checked = true;
         for (int l = 0; l < c->L; ++l) every_slot_checked &= c->tg->slot_ptr[l + 1] > c->tg->slot_ptr[l];
-        if (c->bf16 && c->D == 256 && every_slot_checked && !std::getenv("CIDER_NO_TPATH"))
+        if (c->bf16 && (c->D == 256 || c->D == 128) && every_slot_checked && !std::getenv("CIDER_NO_TPATH"))
             build_tpath(*c);
         ck(cudaDeviceSynchronize(), "upload");
         *out = c.release();

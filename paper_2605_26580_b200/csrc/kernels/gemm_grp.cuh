@@ -347,10 +347,11 @@ gemm_grp_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 // per tile. Protocol as the 2-SM MLP (mlp_tc2.cuh): both producers signal the leader's full barrier,
 // the leader arms it and issues the MMAs, its commits multicast to both CTAs; the epilogue warps of
 // both CTAs release the accumulator on the leader's barrier.
+template <int D>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GRP_THREADS, 1)
 gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                  const __grid_constant__ CUtensorMap tmO, const GrpArgs args) {
-    constexpr int BN = 256;
+    constexpr int BN = D;
     constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of a k-block
     constexpr int B_HALF = (BN / 2) * BK * 2;       // 16 KB: this CTA's N-half of a T k-block
     constexpr int STAGE = A_BYTES + B_HALF;
@@ -559,11 +560,14 @@ struct GrpResLayout {
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
+template <int D>
 __global__ void __launch_bounds__(GRP_THREADS, 1)
 gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
                     const __grid_constant__ CUtensorMap tmO, const GrpArgs args) {
     using Lay = GrpResLayout;
-    constexpr int BN = 256;
+    constexpr int BN = D;                // N = D (one tile covers the whole row)
+    constexpr int NKB = D / 64;          // k-blocks of A and of T
+    constexpr int TKB = D * 64 * 2;      // bytes of one T k-block (D rows x 64)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
@@ -600,12 +604,12 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 const int alpha = args.seg_alpha[g * args.max_seg];
                 if (alpha != cur) { // new coefficient action: wait until the MMAs on the old one retired
                     if (cur >= 0) { mbar_wait(t_empty, teph); teph ^= 1; }
-                    mbar_expect_tx(t_full, 4 * 32768);
-                    for (int kb = 0; kb < 4; ++kb) tma_load_3d(smem + Lay::T_OFF + kb * 32768, &tmT, t_full, kb * 64, 0, alpha);
+                    mbar_expect_tx(t_full, NKB * TKB);
+                    for (int kb = 0; kb < NKB; ++kb) tma_load_3d(smem + Lay::T_OFF + kb * TKB, &tmT, t_full, kb * 64, 0, alpha);
                     cur = alpha;
                 }
                 const int arow = args.seg_arow[g * args.max_seg];
-                for (int kb = 0; kb < 4; ++kb) {
+                for (int kb = 0; kb < NKB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], a_bytes);
                     tma_load_3d(smem + Lay::A_OFF + stage * 16384, &tmA, &full[stage], kb * 64, arow * args.K, mt * args.bb);
@@ -630,11 +634,11 @@ gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 mbar_wait(&aempty[acc], acc_phase ^ 1);
                 fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
-                for (int kb = 0; kb < 4; ++kb) {
+                for (int kb = 0; kb < NKB; ++kb) {
                     mbar_wait(&full[stage], phase);
                     fence_after();
                     const uint64_t da = sw128_desc(smem + Lay::A_OFF + stage * 16384);
-                    const uint64_t db = sw128_desc(smem + Lay::T_OFF + kb * 32768);
+                    const uint64_t db = sw128_desc(smem + Lay::T_OFF + kb * TKB);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
                     mma_commit(&empty[stage]);
