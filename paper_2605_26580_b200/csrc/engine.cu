@@ -155,6 +155,11 @@ CUtensorMap make_map_ttab(const void* ptr, int D, int Q, int box_rows = 0) {
 }
 
 // ---- device allocations ------------------------------------------------------------------
+// bumped on every device (re)allocation: captured CUDA graphs bake in device pointers
+inline int64_t& alloc_generation() {
+    static int64_t g = 0;
+    return g;
+}
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -165,6 +170,7 @@ struct DevBuf {
         bytes = 0;
         ck(cudaMalloc(&p, n), "cudaMalloc");
         bytes = n;
+        ++alloc_generation();
     }
     void release() {
         if (p) cudaFree(p);
@@ -227,6 +233,14 @@ struct cider_ctx {
     int cap_bins = 0, cap_K = 0;
     std::map<std::string, DevBuf> ws;
     std::map<std::tuple<const void*, int64_t, int, int, int>, CUtensorMap> maps;
+    // CUDA graphs of whole refinement chunks (no-remask / rank-remask passes: no host round trip),
+    // keyed by shape, schedule, buffers and allocation generation; seen once eagerly, then captured
+    struct GraphEntry {
+        int seen = 0;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+    };
+    std::map<std::string, GraphEntry> graphs;
     // instrumentation
     int64_t launches = 0;
     bool profiling = false;
@@ -1461,6 +1475,8 @@ cider_ctx::~cider_ctx() {
     if (nccl_comm) {
         try { nccl_sym<decltype(&ncclCommDestroy)>("ncclCommDestroy")((ncclComm_t)nccl_comm); } catch (...) {}
     }
+    for (auto& [k, g] : graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     for (auto& [k, b] : ws) b.release();
     for (auto& b : wbufs) b.release();
     flush_buf.release();
@@ -1681,6 +1697,45 @@ int cider_denoise(cider_ctx* c, int B, int K, const int32_t* X, const float* S, 
     });
 }
 
+// One refinement chunk through a CUDA graph: the T-step loop, residual forcing, the gamma = 0 pass and
+// the rank-rule remask stage are a fixed launch sequence with no host round trip (~40 launches per
+// forward), so after one eager run per key the whole chunk is captured once and replayed — the host
+// no longer paces small-bin-count configurations (c2). Launches are still counted (gpu_launches).
+static void refine_chunk_graphed(cider_ctx& c, WS& w, int nb, int K, const float* S, const cider_schedule& sc,
+                                 const cider_remask* rm) {
+    char key[256];
+    std::snprintf(key, sizeof(key), "%d/%d/%p/%p/%d/%.17g/%.17g/%d/%d/%.17g/%lld", nb, K, (const void*)S, (void*)w.X, sc.steps,
+                  sc.tau_max, sc.tau_min, sc.first_reveal, rm ? rm->mode : -1, rm ? rm->rank_fraction : 0.0,
+                  (long long)alloc_generation());
+    auto& g = c.graphs[key];
+    if (g.exec) {
+        ck(cudaGraphLaunch(g.exec, c.stream), "cudaGraphLaunch");
+        c.launches += g.launches;
+        return;
+    }
+    if (g.seen++ == 0) { // first time: eager (allocates, sets kernel attributes)
+        refine_chunk(c, w, nb, K, S, w.X, sc, rm, nullptr);
+        return;
+    }
+    const int64_t l0 = c.launches;
+    const int64_t gen0 = alloc_generation();
+    cudaGraph_t graph = nullptr;
+    ck(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+        refine_chunk(c, w, nb, K, S, w.X, sc, rm, nullptr);
+    } catch (...) {
+        cudaStreamEndCapture(c.stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    ck(cudaStreamEndCapture(c.stream, &graph), "cudaStreamEndCapture");
+    if (alloc_generation() != gen0) throw CudaError("cider: device allocation during graph capture");
+    ck(cudaGraphInstantiate(&g.exec, graph, 0), "cudaGraphInstantiate");
+    cudaGraphDestroy(graph);
+    g.launches = c.launches - l0;
+    ck(cudaGraphLaunch(g.exec, c.stream), "cudaGraphLaunch");
+}
+
 static void refine_impl(cider_ctx* c, int B, int K, const float* S, bool S_device, const cider_schedule* sched,
                         const cider_remask* rm, int32_t* grid, bool grid_device, float* final_logits, cider_trace* tr) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
@@ -1697,7 +1752,10 @@ static void refine_impl(cider_ctx* c, int B, int K, const float* S, bool S_devic
             Sd = w.S;
         }
         ChunkTrace ct;
-        refine_chunk(*c, w, nb, K, Sd, w.X, *sched, rm, tr ? &ct : nullptr);
+        static const bool no_graph = std::getenv("CIDER_NO_GRAPH") != nullptr;
+        const bool graphable = !tr && !c->profiling && !no_graph && (!rm || rm->mode != CIDER_REMASK_THRESHOLD);
+        if (graphable) refine_chunk_graphed(*c, w, nb, K, Sd, *sched, rm);
+        else refine_chunk(*c, w, nb, K, Sd, w.X, *sched, rm, tr ? &ct : nullptr);
         const int64_t Ms = int64_t(nb) * n;
         int* gdst = grid_device ? grid + size_t(b0) * n : w.Xio;
         grid_to_ref_kernel<<<blocks_for(Ms), 256, 0, c->stream>>>(w.X, gdst, L, K, Ms);
