@@ -410,12 +410,19 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // runs over the input k-blocks starting at the second half ([e | z] order): the next tile's
     // e / acc k-blocks load during the final epilogue and the first MMA1 starts on them.
     constexpr int ROT = reads_z ? KBD : 0;
+    // MLP2_ZREG: gate / fusion results leave from registers (32-byte stores) and their z / e k-blocks are
+    // released as soon as the final epilogue has read them (no output staging in X); else staged in X
+    // and TMA-stored by the X producer
+#ifndef MLP2_ZREG
+#define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
+#endif
+    constexpr bool XST = EPK != EP_DEMIX && !(reads_z && MLP2_ZREG); // output staged in X
     if (threadIdx.x == 0) {
         // x_empty: the last MMA1 of the tile (+ the gate's 4 warps that read that e k-block); the
         // output k-blocks are refilled by the X producer itself after storing them (o_full)
         for (int kb = 0; kb < NXB * KB1; ++kb) {
             mbar_init(&x_full[kb], 1);
-            mbar_init(&x_empty[kb], 1 + (reads_e && kb % KB1 >= KBD ? 4 : 0));
+            mbar_init(&x_empty[kb], 1 + ((reads_e && kb % KB1 >= KBD) || (!XST && reads_z && kb % KB1 < KBD) ? 4 : 0));
         }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
@@ -519,7 +526,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 for (int kb0 = 0; kb0 < KBD; kb0 += 2) {
                     if (KB1 > KBD)
                         for (int kb = KBD + kb0; kb < KBD + kb0 + 2; ++kb) load_kb(kb);
-                    if (itx >= NXB) {
+                    if (XST && itx >= NXB) {
                         for (int kb = kb0; kb < kb0 + 2 && kb < KBD; ++kb) {
                             mbar_wait(&o_full[xb * KBD + kb], oph);
                             tma_store_2d(&tmO, xsb + kb * 16384, kb * 64, prev_row0);
@@ -531,7 +538,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
                 if (NXB == 1) eph ^= 1;
             }
-            if constexpr (EPK != EP_DEMIX) { // the last NXB tiles' outputs
+            if constexpr (XST) { // the last NXB tiles' outputs
                 for (int q = 0; q < NXB; ++q) {
                     const int itl = itx - NXB + q; // tile index (per CTA) whose output is still staged
                     if (itl < 0) continue;
@@ -863,15 +870,26 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
                             pk[t] = *reinterpret_cast<uint32_t*>(&p);
                         }
-                        st_shared_v4(dst + off, pk);
+                        if constexpr (XST) st_shared_v4(dst + off, pk);
+                        else if (m0w + lane < ep.M) // 16 bytes of this row; the 4 chunks of a half are one 64-byte run
+                            *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(ep.out_t) + size_t(m0w + lane) * ep.ldo + n0 + s2 * 32 + jj * 8) =
+                                make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
                 }
                 if (trf) args.trace[256 + it * 16 + (kb / 2) * 5 + 3] = clock64();
-                fence_proxy_async_smem(); // generic-proxy writes -> visible to the X producer's TMA store
-                __syncwarp();
-                if (lane == 0) {
-                    if (reads_e) mbar_arrive(&x_empty[KBD + kb]); // e k-block read: the next tile's may load
-                    mbar_arrive(&o_full[(it % NXB) * KBD + kb]);   // output block staged
+                if constexpr (XST) {
+                    fence_proxy_async_smem(); // generic-proxy writes -> visible to the X producer's TMA store
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (reads_e) mbar_arrive(&x_empty[KBD + kb]); // e k-block read: the next tile's may load
+                        mbar_arrive(&o_full[(it % NXB) * KBD + kb]);   // output block staged
+                    }
+                } else {
+                    __syncwarp();
+                    if (lane == 0) { // z (and e) k-block read: the next tile's may load
+                        mbar_arrive(&x_empty[kb]);
+                        if (reads_e) mbar_arrive(&x_empty[KBD + kb]);
+                    }
                 }
             }
             if (trf) args.trace[512 + it * 4 + 2] = clock64();
