@@ -909,7 +909,8 @@ void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K,
         a.trace = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
         cudaMemsetAsync(a.trace, 0, 8 * 1024, c.stream);
     }
-    launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, x0, a); // (its epilogue stores directly; no output map)
+    const CUtensorMap om = make_map_box(e_out, Ms, D, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B); // e k-blocks staged in X
+    launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, om, a);
     check_launch("demix_evid");
     if (a.trace) dump_mlp_trace(c, "demix_evid", Ms, Q, true, a.trace);
 }

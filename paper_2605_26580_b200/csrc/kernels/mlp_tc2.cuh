@@ -170,7 +170,7 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
         : "memory");
 }
 
-template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1>
+template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1, int BIASB = 4 * D>
 struct Mlp2Layout {
     static constexpr int STG_WARP = STGW;
     static constexpr int XBUF = NXB; // row-tile buffers (2: the next tile's rows load during this tile)
@@ -181,7 +181,7 @@ struct Mlp2Layout {
     static constexpr int SLOT = 16384;
     static constexpr int W1_PER_SLOT = SLOT / W1_HALF;       // 2
     static constexpr int X_BYTES = KB1 * 128 * 64 * 2;
-    static constexpr int FIXED = 1024 + 512 + 4 * D; // alignment slack, barriers, output bias
+    static constexpr int FIXED = 1024 + 512 + BIASB;  // alignment slack, barriers, output bias
     static constexpr int BIAS_OFF_FROM_BAR = 512;      // output bias [D] fp32 right after the barriers
     // output staging for coalesced stores: one 32-row x 64-column bf16 block per epilogue warp (the
     // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
@@ -191,7 +191,7 @@ struct Mlp2Layout {
     static constexpr int STG_OFF = NXB * X_BYTES;
     static constexpr int R_OFF = NXB * X_BYTES + STG_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
-    static constexpr int TOTAL = BAR_OFF + 512 + 4 * D + 1024;
+    static constexpr int TOTAL = BAR_OFF + 512 + BIASB + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
     static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 4 + 2 + 2 + NXB * (D / 64)) * 8 + 4 <= 512, "barrier block");
     static_assert(D % 32 == 0 && D <= 256 && W2_HALF <= SLOT, "output width must be <= 256");
@@ -216,7 +216,7 @@ constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
 // aggregator (input = output width) double-buffers its row tile.
 template <int KIN, int D, int EPK>
 using Mlp2LayoutFor = Mlp2Layout<KIN, D, EPK == EP_DEMIX ? DEMIX_STG_WARP : 0, mlp2_epi_warps(EPK),
-                                 (KIN == D && EPK == EP_STORE) ? 2 : 1>;
+                                 (KIN == D && (EPK == EP_STORE || EPK == EP_DEMIX)) ? 2 : 1, EPK == EP_DEMIX ? 0 : 4 * D>;
 
 constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hidden columns = one MMA2 k-step)
 
@@ -416,7 +416,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #ifndef MLP2_ZREG
 #define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
 #endif
-    constexpr bool XST = EPK != EP_DEMIX && !(reads_z && MLP2_ZREG); // output staged in X
+    constexpr bool XST = !(reads_z && MLP2_ZREG); // output staged in X (demix: e in the spent Z tile)
     if (threadIdx.x == 0) {
         // x_empty: the last MMA1 of the tile (+ the gate's 4 warps that read that e k-block); the
         // output k-blocks are refilled by the X producer itself after storing them (o_full)
@@ -441,7 +441,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     }
     fence_before();
     float* bias_s = reinterpret_cast<float*>(smem + Lay::BAR_OFF + Lay::BIAS_OFF_FROM_BAR); // final-epilogue bias
-    for (int i = threadIdx.x; i < D; i += blockDim.x) bias_s[i] = args.ep.bias ? args.ep.bias[i] : 0.0f;
+    if constexpr (EPK != EP_DEMIX)
+        for (int i = threadIdx.x; i < D; i += blockDim.x) bias_s[i] = args.ep.bias ? args.ep.bias[i] : 0.0f;
     cluster_sync_all(); // barriers of both CTAs initialised before any remote signal
     fence_after();
     const uint32_t tmem = *tmem_slot;
@@ -501,11 +502,19 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 const int xb = itx % NXB;
                 uint8_t* xsb = xs + xb * Lay::X_BYTES;
                 if (NXB > 1 && itx > 0 && xb == 0) eph ^= 1; // buffer 0's phase flips every NXB tiles
-                if constexpr (EPK == EP_DEMIX) { // tmX0 is 3-D: the whole row tile in ONE box, on x_full[0]
-                    for (int kb = 0; kb < KB1; ++kb) mbar_wait(&x_empty[kb], eph ^ 1);
-                    if (leader) mbar_expect_tx(&x_full[0], 2 * KB1 * 16384);
-                    tma_load_3d_2sm(xs, &tmX0, L_x_full0, 0, row0, 0);
-                    eph ^= 1;
+                if constexpr (EPK == EP_DEMIX) { // tmX0 is 3-D: the whole row tile in ONE box, on x_full[xb KB1]
+                    if (itx >= NXB) { // this buffer holds the e tile of two tiles back: store it out first
+                        const int prev_row0 = row0 - NXB * npairs * 256;
+                        for (int kb = 0; kb < KBD; ++kb) {
+                            mbar_wait(&o_full[xb * KBD + kb], uint32_t((itx / NXB - 1) & 1));
+                            tma_store_2d(&tmO, xsb + kb * 16384, kb * 64, prev_row0);
+                        }
+                        bulk_commit();
+                        bulk_wait_read0();
+                    }
+                    for (int kb = 0; kb < KB1; ++kb) mbar_wait(&x_empty[xb * KB1 + kb], eph ^ 1);
+                    if (leader) mbar_expect_tx(&x_full[xb * KB1], 2 * KB1 * 16384);
+                    tma_load_3d_2sm(xsb, &tmX0, L_x_full0 + xb * KB1 * 8, 0, row0, 0);
                     continue;
                 }
                 // The final epilogue stages the previous tile of this buffer in its k-blocks [0, KBD):
@@ -579,7 +588,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         for (int sg = 0; sg < S1; ++sg) {
                             uint32_t ph;
                             const int slot = ring_slot(it * per_tile + pos_w1(c) + sg, ph);
-                            if (c == 0 && EPK == EP_DEMIX && sg == 0) mbar_wait(&x_full[0], xph); // one box
+                            if (c == 0 && EPK == EP_DEMIX && sg == 0) mbar_wait(&x_full[xb * KB1], xph); // one box
                             else if (c == 0 && EPK != EP_DEMIX) // the tile's k-blocks arrive one by one
                                 for (int j = 0; j < Lay::W1_PER_SLOT; ++j) mbar_wait(&x_full[xb * KB1 + (sg * Lay::W1_PER_SLOT + j + ROT) % KB1], xph);
                             mbar_wait(&r_full[slot], ph);
@@ -728,7 +737,35 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 e2ph ^= 1;
                 fence_after();
                 if (trf) args.trace[512 + it * 4 + 1] = clock64();
-                demix_final(ep, stg, tmem + lane_off, half, m0, lane, L_a2_empty);
+                {
+                    // e k-block `half` of this warp's 32 rows, bf16 SW128, into the spent Z tile of this
+                    // tile's buffer (MMA1 read it before MMA2 could finish); the X producer TMA-stores it
+                    uint8_t* dst = xs + (it % NXB) * Lay::X_BYTES + half * 16384 + quarter * 4096;
+#pragma unroll
+                    for (int s2 = 0; s2 < 2; ++s2) {
+                        float v[32];
+                        tmem_ld32(tmem + lane_off + half * 64 + s2 * 32, v);
+                        if (s2 == 1) {
+                            fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cl(L_a2_empty);
+                        }
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int j = s2 * 4 + jj;
+                            uint32_t pk[4];
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * jj + 2 * t], v[8 * jj + 2 * t + 1]);
+                                pk[t] = *reinterpret_cast<uint32_t*>(&b2);
+                            }
+                            st_shared_v4(dst + lane * 128 + ((j ^ (lane & 7)) * 16), pk);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&o_full[(it % NXB) * KBD + half]);
+                }
                 if (trf) args.trace[512 + it * 4 + 2] = clock64();
                 continue;
             }
