@@ -417,12 +417,17 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
 #endif
     constexpr bool XST = !(reads_z && MLP2_ZREG); // output staged in X (demix: e in the spent Z tile)
+    // gate / fusion: the 8 final warps walk the output k-blocks together (each warp one 32-column half
+    // of every k-block), so k-block 0 is staged, stored and refilled first and the next tile's first
+    // MMA1 is fed k-block by k-block instead of in two rounds
+    constexpr bool KB_SEQ = reads_z && XST;
+    constexpr int O_ARRIVALS = KB_SEQ ? 8 : 4;
     if (threadIdx.x == 0) {
         // x_empty: the last MMA1 of the tile (+ the gate's 4 warps that read that e k-block); the
         // output k-blocks are refilled by the X producer itself after storing them (o_full)
         for (int kb = 0; kb < NXB * KB1; ++kb) {
             mbar_init(&x_full[kb], 1);
-            mbar_init(&x_empty[kb], 1 + ((reads_e && kb % KB1 >= KBD) || (!XST && reads_z && kb % KB1 < KBD) ? 4 : 0));
+            mbar_init(&x_empty[kb], 1 + ((reads_e && kb % KB1 >= KBD) || (!XST && reads_z && kb % KB1 < KBD) ? O_ARRIVALS : 0));
         }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
@@ -432,7 +437,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         }
         mbar_init(a2_full, 1);
         mbar_init(a2_empty, A2_ARRIVALS);
-        for (int kb = 0; kb < NXB * KBD; ++kb) mbar_init(&o_full[kb], 4);
+        for (int kb = 0; kb < NXB * KBD; ++kb) mbar_init(&o_full[kb], O_ARRIVALS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -532,18 +537,19 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 };
                 // by final-epilogue round (its warp halves finish output k-blocks kb0, kb0 + 1 together, and
                 // the gate's e k-blocks KBD + kb0, KBD + kb0 + 1 with them): e / acc first, then the z pair
-                for (int kb0 = 0; kb0 < KBD; kb0 += 2) {
+                constexpr int KSTEP = KB_SEQ ? 1 : 2;
+                for (int kb0 = 0; kb0 < KBD; kb0 += KSTEP) {
                     if (KB1 > KBD)
-                        for (int kb = KBD + kb0; kb < KBD + kb0 + 2; ++kb) load_kb(kb);
+                        for (int kb = KBD + kb0; kb < KBD + kb0 + KSTEP; ++kb) load_kb(kb);
                     if (XST && itx >= NXB) {
-                        for (int kb = kb0; kb < kb0 + 2 && kb < KBD; ++kb) {
+                        for (int kb = kb0; kb < kb0 + KSTEP && kb < KBD; ++kb) {
                             mbar_wait(&o_full[xb * KBD + kb], oph);
                             tma_store_2d(&tmO, xsb + kb * 16384, kb * 64, prev_row0);
                         }
                         bulk_commit();
                         bulk_wait_read0();
                     }
-                    for (int kb = kb0; kb < kb0 + 2 && kb < KBD; ++kb) load_kb(kb);
+                    for (int kb = kb0; kb < kb0 + KSTEP && kb < KBD; ++kb) load_kb(kb);
                 }
                 if (NXB == 1) eph ^= 1;
             }
@@ -858,17 +864,18 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             fence_after();
             if (trf) args.trace[512 + it * 4 + 1] = clock64();
 #pragma unroll 1
-            for (int kb = fsub; kb < KBD; kb += FIN_STRIDE) {
+            for (int kb = KB_SEQ ? 0 : fsub; kb < KBD; kb += KB_SEQ ? 1 : FIN_STRIDE) {
                 const int n0 = kb * 64;
                 // this warp's 32 rows of X k-block kb: z in (gate / fusion), the output block out (all)
                 uint8_t* dst = xcur + kb * 16384 + quarter * 4096;
                 const uint8_t* esrc = xcur + (KBD + kb) * 16384 + quarter * 4096;
 #pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) { // two 32-column halves of the k-block
+                for (int s2i = 0; s2i < (KB_SEQ ? 1 : 2); ++s2i) { // 32-column halves of the k-block
+                    const int s2 = KB_SEQ ? half : s2i;
                     float v[32];
                     tmem_ld32(tmem + lane_off + n0 + s2 * 32, v);
                     if (trf) args.trace[256 + it * 16 + (kb / 2) * 5 + 1 + s2] = clock64();
-                    if (s2 == 1 && kb + FIN_STRIDE >= KBD) {
+                    if (KB_SEQ ? kb == KBD - 1 : (s2 == 1 && kb + FIN_STRIDE >= KBD)) {
                         fence_before();
                         release(L_a2_empty); // accumulator drained: next tile's MMA2 may start
                     }
