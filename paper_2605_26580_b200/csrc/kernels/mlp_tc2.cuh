@@ -119,6 +119,11 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                  "r"(smem_u32(src)), "r"(x), "r"(y)
                  : "memory");
 }
+// L2 prefetch of one TMA box (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -413,6 +418,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // MLP2_ZREG: gate / fusion results leave from registers (32-byte stores) and their z / e k-blocks are
     // released as soon as the final epilogue has read them (no output staging in X); else staged in X
     // and TMA-stored by the X producer
+#ifndef MLP2_XPREFETCH
+#define MLP2_XPREFETCH 0 // no measurable effect on c5 (gate 202 ms either way)
+#endif
 #ifndef MLP2_ZREG
 #define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
 #endif
@@ -550,6 +558,16 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         bulk_wait_read0();
                     }
                     for (int kb = kb0; kb < kb0 + KSTEP && kb < KBD; ++kb) load_kb(kb);
+                }
+                // single-buffered rows: pull the next tile's rows into L2 now, so that its refill at the
+                // tile transition (all CTAs at once) reads L2 instead of bursting on HBM
+                if (NXB == 1 && MLP2_XPREFETCH && tile + npairs < args.tiles) {
+                    const int nrow0 = row0 + npairs * 256;
+                    for (int kb = 0; kb < KB1; ++kb) {
+                        const int k = kb * 64;
+                        if (k < args.K0) tma_prefetch_2d(&tmX0, k, nrow0);
+                        else tma_prefetch_2d(&tmX1, k - args.K0, nrow0);
+                    }
                 }
                 if (NXB == 1) eph ^= 1;
             }
