@@ -1755,6 +1755,10 @@ static void refine_impl(cider_ctx* c, int B, int K, const float* S, bool S_devic
         ChunkTrace ct;
         static const bool no_graph = std::getenv("CIDER_NO_GRAPH") != nullptr;
         const bool graphable = !tr && !c->profiling && !no_graph && (!rm || rm->mode != CIDER_REMASK_THRESHOLD);
+        if (graphable && Sd != w.S) { // the graph reads S from the workspace: one key for every caller buffer
+            ck(cudaMemcpyAsync(w.S, Sd, size_t(nb) * L * Q * 4, cudaMemcpyDeviceToDevice, c->stream), "d2d");
+            Sd = w.S;
+        }
         if (graphable) refine_chunk_graphed(*c, w, nb, K, Sd, *sched, rm);
         else refine_chunk(*c, w, nb, K, Sd, w.X, *sched, rm, tr ? &ct : nullptr);
         const int64_t Ms = int64_t(nb) * n;
