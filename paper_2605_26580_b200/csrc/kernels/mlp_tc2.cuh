@@ -315,45 +315,6 @@ __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, ui
     if (tr) tr[4] = clock64();
 }
 
-// EP_DEMIX final epilogue of one warp: output k-block kb (64 columns of e) of its 32 rows, as bf16,
-// through a [32 rows][64 B] staging block per 32 columns (16-byte chunks swizzled) so that every
-// store instruction writes whole 64-byte row segments (direct per-row 32-byte stores measured slower:
-// they also slow the concurrent demix warps).
-__device__ __forceinline__ void demix_final(const Epi& ep, uint8_t* stg, uint32_t acc, int kb, int mrow0, int lane,
-                                            uint32_t l_a2_empty) {
-    bf16* ot = reinterpret_cast<bf16*>(ep.out_t);
-#pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) {
-        float v[32];
-        tmem_ld32(acc + kb * 64 + s2 * 32, v);
-        if (s2 == 1) {
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cl(l_a2_empty); // this warp's accumulator columns drained
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            uint32_t pk[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * j + 2 * t], v[8 * j + 2 * t + 1]);
-                pk[t] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16))),
-                         "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
-                         : "memory");
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int r = i * 8 + lane / 4, j = lane & 3;
-            const uint4 u = *reinterpret_cast<const uint4*>(stg + r * 64 + ((j ^ ((r >> 1) & 3)) * 16));
-            if (mrow0 + r < ep.M)
-                *reinterpret_cast<uint4*>(ot + size_t(mrow0 + r) * ep.ldo + kb * 64 + s2 * 32 + j * 8) = u;
-        }
-        __syncwarp();
-    }
-}
 
 // warps: ring producer, MMA1 issuer, epilogue warps (2 .. EW + 1), MMA2 issuer, X producer
 
