@@ -815,8 +815,12 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
     CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
     const int tiles = a.groups * a.mtiles;
-    static const bool no_res = std::getenv("CIDER_NO_TRES") != nullptr;
-    if (max_seg == 1 && (D == 256 || D == 128) && !no_res) {
+    // The T-resident kernel (one T_alpha per CTA, lap schedule) measured 5% slower than the CTA-pair
+    // kernel with streamed T halves for the normalise GEMM (c5: 61.5 vs 58.4 ms per step): the pair
+    // kernel's m-tile-major order keeps a slot's z~ rows in L2 for its edges, and its deeper A / T
+    // ring hides the gather latency. CIDER_GRP_RES=1 selects the T-resident kernel.
+    static const bool use_res = std::getenv("CIDER_GRP_RES") != nullptr;
+    if (max_seg == 1 && (D == 256 || D == 128) && use_res) {
         // single-segment groups: T-resident kernel (T loaded once per group change per CTA)
         static bool attr_res = false;
         if (!attr_res) {
