@@ -736,7 +736,7 @@ void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* poo
 // BF16, check-regular degree 6, D = 256, heads in {1, 2, 4, 8}, 6K <= 48 rows per (bin, check) block (K = 4 or 8)
 bool pool_mma_ok(const cider_ctx& c, const LayerW& lw, int K) {
     return c.bf16 && lw.aus16 && (c.D == 256 || c.D == 128) && c.max_check_deg == 6 && c.min_check_deg == 6 && 8 % c.heads == 0 &&
-           (K == 4 || K == 8) && !std::getenv("CIDER_NO_POOL_MMA");
+           (K == 8 || (K == 4 && c.P % 2 == 0)) && !std::getenv("CIDER_NO_POOL_MMA");
 }
 const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, int ld, int box_rows);
 template <int K, int D>
@@ -751,8 +751,8 @@ void launch_pool_mma(cider_ctx& c, const LayerW& lw, const CUtensorMap& tm, int6
                                                                              c.heads, blocks, (bf16*)pooled);
 }
 void run_pool_mma(cider_ctx& c, const LayerW& lw, const void* Nn, int64_t Me, int nb, int K, void* pooled) {
-    const CUtensorMap& tm = map_for(c, Nn, Me, c.D, c.D, 6 * K);
-    const int64_t blocks = int64_t(nb) * c.P;
+    const CUtensorMap& tm = map_for(c, Nn, Me, c.D, c.D, 48); // 48-row blocks: one check at K = 8, two at K = 4
+    const int64_t blocks = int64_t(nb) * c.P / (8 / K);
     if (c.D == 256) {
         if (K == 8) launch_pool_mma<8, 256>(c, lw, tm, blocks, pooled);
         else launch_pool_mma<4, 256>(c, lw, tm, blocks, pooled);

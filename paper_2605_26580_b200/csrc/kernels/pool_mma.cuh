@@ -64,7 +64,8 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     // per-group score scratch [48 block rows][8 heads]: warp wg scores block rows [12 wg, 12 wg + 12)
     // (consecutive rows: distinct SW128 phases, conflict-free ldmatrix) and pools rows k = 2 wg, 2 wg + 1
     float* ss = reinterpret_cast<float*>(smem + Lay::S_OFF) + grp * 512;
-    constexpr int R = PM_DEG * K;    // rows per block (<= 48)
+    constexpr int CPB = 8 / K;       // checks per block (K = 4: two adjacent checks, so blocks stay 48 rows)
+    constexpr int R = PM_DEG * K * CPB; // rows per block (48)
     constexpr int KBS = R * 128;     // k-block stride inside a block buffer
     constexpr int NKB = D / 64;      // 64-column k-blocks per row (4 or 2)
     constexpr int CPL = D / 32;      // pooled columns per lane (8 or 4)
@@ -89,9 +90,10 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     const int stride = 2 * int(gridDim.x);
     const int first = int(blockIdx.x) + grp * int(gridDim.x);
     const int nblk = int(n_blocks);
-    auto issue = [&](int blk, int slot) { // one thread of the group: the block's 4 column boxes
-        const int b = blk / P;
-        const int j = blk - b * P;
+    const int PB = P / CPB; // blocks per bin
+    auto issue = [&](int blk, int slot) { // one thread of the group: the block's column boxes
+        const int b = blk / PB;
+        const int j = (blk - b * PB) * CPB;
         const int row0 = (b * E + check_ptr[j]) * K;
         uint64_t* bar = &full[grp * GB + slot];
         tc::mbar_expect_tx(bar, NKB * R * 128);
@@ -114,9 +116,9 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         tc::mbar_wait(&full[grp * GB + slot], (ph >> slot) & 1u);
         ph ^= 1u << slot;
         const uint8_t* nb = smem + (grp * GB + slot) * PM_BUF;
-        const int b = blk / P;
-        const int e0 = check_ptr[blk - b * P];
-        if (12 * wg < PM_DEG * K) {
+        const int b = blk / PB;
+        const int e0 = check_ptr[(blk - b * PB) * CPB];
+        if (12 * wg < R) {
             // (1) head scores of the warp's 12 rows: n-tile 0 = hi(u), 1 = lo(u)
             float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll 4
@@ -144,18 +146,18 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         }
         if (grp == 0) asm volatile("bar.sync 1, 128;" ::: "memory"); // the group's scores are in
         else asm volatile("bar.sync 2, 128;" ::: "memory");
-        constexpr int kpw = (K + 3) / 4; // pooled rows k per warp: every warp of the group pools (K = 4: one each)
-        if (wg * kpw < K) {
+        constexpr int kpw = 2; // pooled (check, k) rows per warp: 8 = CPB K per block over the 4 warps
+        {
             // (2) pooling of rows k = wg kpw + kk (not unrolled: 128-register cap at 2 CTAs / SM)
 #pragma unroll 1
             for (int kk = 0; kk < kpw; ++kk) {
-                const int k = wg * kpw + kk;
-                bf16* orow = pooled + (size_t(b * E + e0) * K + k) * D + lane * CPL; // edge i at + i K D (64-bit)
+                const int task = wg * kpw + kk, cb = task / K, k = task % K; // check cb of the block, row k
+                bf16* orow = pooled + (size_t(b * E + e0 + cb * PM_DEG) * K + k) * D + lane * CPL; // edge i at + i K D
                 float2 f[PM_DEG][V];
                 float sc[PM_DEG];
 #pragma unroll
                 for (int i = 0; i < PM_DEG; ++i) {
-                    const int r = i * K + k;
+                    const int r = (cb * PM_DEG + i) * K + k;
                     sc[i] = ss[r * 8 + h];
                     if constexpr (V == 4) { // 8 columns = one 16-byte chunk of k-block lane / 8
                         const uint4 u = *reinterpret_cast<const uint4*>(nb + (lane >> 3) * KBS + r * 128 + (((lane & 7) ^ (r & 7)) * 16));
