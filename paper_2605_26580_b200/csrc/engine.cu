@@ -423,9 +423,9 @@ void gemm(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1,
     static const int epw_demix = std::getenv("CIDER_EPW_DEMIX") ? std::atoi(std::getenv("CIDER_EPW_DEMIX")) : 16;
     static const int epw_store = std::getenv("CIDER_EPW_STORE") ? std::atoi(std::getenv("CIDER_EPW_STORE")) : 4;
     static const int epw_scores = std::getenv("CIDER_EPW_SCORES") ? std::atoi(std::getenv("CIDER_EPW_SCORES")) : 4;
-    const int epw = ep.kind == EP_DEMIX ? (epw_demix == 8 ? 8 : 16) // the demix epilogue needs the > 4-warp staging
+    const int epw = ep.kind == EP_DEMIX ? (epw_demix == 8 || BN == 64 ? 8 : 16) // the demix epilogue needs the > 4-warp staging
                     : ep.kind == EP_STORE ? epw_store : ep.kind == EP_SCORES ? epw_scores : 4;
-    if (ep.kind == EP_DEMIX && BN != 256) throw InvalidInput("fused demix epilogue needs Q % 256 == 0");
+    if (ep.kind == EP_DEMIX && BN != 256 && BN != 64) throw InvalidInput("fused demix epilogue needs Q = 64 or Q % 256 == 0");
     // B-resident variants: one N tile, K <= 256 (W, W^T, V^T against 128-row A tiles)
     static const bool no_bres = std::getenv("CIDER_NO_BRES") != nullptr;
     const bool bres = !no_bres && BN == 256 && N == 256 && K <= 256;
@@ -947,7 +947,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             // Lambda-bar, demix and the evidence embedding in one 2-SM kernel (e is its only output)
             demix_evid(c, w.Zt, S, Ms, K, (bf16*)w.et);
         } else {
-        if (c.bf16 && 32 % K == 0 && K >= 4 && Q % 256 == 0 && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
+        if (c.bf16 && 32 % K == 0 && K >= 4 && (Q % 256 == 0 || Q == 64) && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
             // intermediate logits and demixing in one kernel: Lambda-bar never leaves the chip
             e = epi(EP_DEMIX);
             e.out_t = w.Aq; e.ldo = Q; e.S = S; e.L = L; e.K = K; e.beta = float(c.md.evidence_scale);
