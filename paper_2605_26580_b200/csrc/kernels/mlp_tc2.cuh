@@ -221,7 +221,9 @@ constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
 // aggregator (input = output width) double-buffers its row tile.
 template <int KIN, int D, int EPK>
 using Mlp2LayoutFor = Mlp2Layout<KIN, D, EPK == EP_DEMIX ? DEMIX_STG_WARP : 0, mlp2_epi_warps(EPK),
-                                 (KIN == D && (EPK == EP_STORE || EPK == EP_DEMIX)) ? 2 : 1, EPK == EP_DEMIX ? 0 : 4 * D>;
+                                 ((KIN == D && (EPK == EP_STORE || EPK == EP_DEMIX)) || KIN <= 256) ? 2 : 1,
+                                 EPK == EP_DEMIX ? 0 : 4 * D>;
+// (KIN <= 256: the D = 128 gate / fusion row tile is 64 KB, so it double-buffers as well)
 
 constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hidden columns = one MMA2 k-step)
 
@@ -904,14 +906,14 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     fence_proxy_async_smem(); // generic-proxy writes -> visible to the X producer's TMA store
                     __syncwarp();
                     if (lane == 0) {
-                        if (reads_e) mbar_arrive(&x_empty[KBD + kb]); // e k-block read: the next tile's may load
+                        if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]); // e k-block read: the next tile's may load
                         mbar_arrive(&o_full[(it % NXB) * KBD + kb]);   // output block staged
                     }
                 } else {
                     __syncwarp();
                     if (lane == 0) { // z (and e) k-block read: the next tile's may load
-                        mbar_arrive(&x_empty[kb]);
-                        if (reads_e) mbar_arrive(&x_empty[KBD + kb]);
+                        mbar_arrive(&x_empty[(it % NXB) * KB1 + kb]);
+                        if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]);
                     }
                 }
             }
