@@ -172,6 +172,26 @@ int cider_bp_decode(cider_bp_ctx* ctx, int B, const double* lambda, const cider_
 int cider_sic_decode(cider_bp_ctx* ctx, int B, int K, const double* S, const cider_bp_config* cfg, double cancel_value,
                      int32_t* grid, int32_t* stage_converged, int32_t* stage_iters);
 
+/* ---- batched AMP slot detector (the evidence the path consumes) --------- */
+/* A dataset context: the per-slot sensing dictionaries (fixed per dataset, sim.hpp:60-62) on one
+ * device. dicts: L x q x n_s complex (re, im interleaved), each slot column-major as
+ * ura::SensingMatrix::cols (sim.hpp:18-26). */
+typedef struct cider_amp_ctx cider_amp_ctx;
+/* ura::AmpConfig (amp.hpp:14-19) */
+typedef struct {
+    int iters;             /* >= 1 */
+    double rho_bg;         /* in (0, 1) */
+    double sigma_u2;       /* > 0 */
+    double evidence_floor; /* natural log */
+} cider_amp_config;
+int cider_amp_create(int L, int q, int n_s, const double* dicts, int device, cider_amp_ctx** out);
+void cider_amp_destroy(cider_amp_ctx* ctx);
+/* = ura::detect_frame (amp.cpp:133-148) for B independent frames: y B x L x n_s complex (interleaved),
+ * S B x L x q (fp64 evidence rows = evidence_row(amp_detect(...)), amp.cpp:63-131). Host buffers.
+ * Errors as the reference: 3 for an invalid config (std::domain_error), 4 for a non-finite residual
+ * ("amp_detect: non-finite residual at iteration i", std::runtime_error). */
+int cider_amp_detect(cider_amp_ctx* ctx, int B, const double* y, const cider_amp_config* cfg, double* S);
+
 /* ---- device plumbing used by the benchmark (no PyTorch on the path) --------------------- */
 int cider_device_count(int* n);
 int cider_device_alloc(cider_ctx* ctx, size_t bytes, void** ptr);

@@ -221,6 +221,41 @@ class Reference(Checker):
         return grid, sc, si
 
 
+    # ---- AMP slot detector (amp.cpp, sim.cpp) --------------------------------------------------
+    def amp_make_dicts(self, q: int, n_s: int, slots: int, seed: int) -> np.ndarray:
+        """make_dictionaries (sim.cpp:74-80): slots x q x n_s complex."""
+        d = np.empty((slots, q, n_s), np.complex128)
+        self._check(self.h.ref_amp_make_dicts(q, n_s, slots, C.c_uint64(seed), _p(d)))
+        return d
+
+    def amp_observe(self, dicts: np.ndarray, symbols: np.ndarray, p_sym: float, noise_var: float, seed: int) -> np.ndarray:
+        """activity_vector + transmit per slot on make_rng(seed): symbols slots x K -> y slots x n_s complex."""
+        dicts = np.ascontiguousarray(dicts, np.complex128)
+        L, q, n_s = dicts.shape
+        sym = np.ascontiguousarray(symbols, np.int32)
+        y = np.empty((L, n_s), np.complex128)
+        self._check(self.h.ref_amp_observe(q, n_s, L, _p(dicts), sym.shape[1], _p(sym), C.c_double(p_sym),
+                                           C.c_double(noise_var), C.c_uint64(seed), _p(y)))
+        return y
+
+    def amp_detect_frame(self, dicts: np.ndarray, y: np.ndarray, iters: int = 20, rho_bg: float = 0.03125,
+                         sigma_u2: float = 20.0, evidence_floor: float = -40.0) -> np.ndarray:
+        """detect_frame (amp.cpp:133-148): S slots x q."""
+        dicts = np.ascontiguousarray(dicts, np.complex128)
+        L, q, n_s = dicts.shape
+        y = np.ascontiguousarray(y, np.complex128)
+        S = np.empty((L, q), np.float64)
+        self._check(self.h.ref_amp_detect_frame(q, n_s, L, _p(dicts), _p(y), iters, C.c_double(rho_bg),
+                                                C.c_double(sigma_u2), C.c_double(evidence_floor), _p(S)))
+        return S
+
+    def symbol_power(self, eb_db: float, payload_bits: int, slots: int) -> float:
+        f = self.h.ref_symbol_power
+        f.restype = C.c_double
+        f.argtypes = [C.c_double, C.c_int, C.c_int]
+        return f(eb_db, payload_bits, slots)
+
+
 def derive_seed(master: int, index: int) -> int:
     """seeding.hpp:16-22 (pure-Python restatement, used to name fixture seeds)."""
     M = (1 << 64) - 1

@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "ura/amp.hpp"
 #include "ura/bp.hpp"
 #include "ura/denoiser.hpp"
 #include "ura/gf.hpp"
@@ -29,6 +30,7 @@
 #include "ura/parallel.hpp"
 #include "ura/refine.hpp"
 #include "ura/seeding.hpp"
+#include "ura/sim.hpp"
 
 #include "cider.h"
 
@@ -553,5 +555,71 @@ double ref_infer_temperature(int t, int steps, double tmax, double tmin) {
     return ura::infer_temperature(t, steps, tmax, tmin);
 }
 int ref_remask_steps(int steps, int k_low, int k) { return ura::remask_steps(steps, k_low, k); }
+
+// ---- AMP slot detector -----------------------------------------------------
+// make_dictionaries(q, n_s, slots, seed) (sim.cpp:74-80): slots x q x n_s complex, interleaved.
+int ref_amp_make_dicts(int q, int n_s, int slots, uint64_t seed, double* dicts) {
+    return guarded([&] {
+        auto d = ura::make_dictionaries(q, n_s, slots, seed);
+        for (int l = 0; l < slots; ++l)
+            for (size_t i = 0; i < d[l].cols.size(); ++i) {
+                dicts[(size_t(l) * q * n_s + i) * 2] = d[l].cols[i].real();
+                dicts[(size_t(l) * q * n_s + i) * 2 + 1] = d[l].cols[i].imag();
+            }
+    });
+}
+
+static std::vector<ura::SensingMatrix> dicts_from(int q, int n_s, int slots, const double* dicts) {
+    std::vector<ura::SensingMatrix> d(slots);
+    for (int l = 0; l < slots; ++l) {
+        d[l].slot = l;
+        d[l].n_s = n_s;
+        d[l].q = q;
+        d[l].cols.resize(size_t(q) * n_s);
+        for (size_t i = 0; i < d[l].cols.size(); ++i)
+            d[l].cols[i] = ura::cplx(dicts[(size_t(l) * q * n_s + i) * 2], dicts[(size_t(l) * q * n_s + i) * 2 + 1]);
+    }
+    return d;
+}
+
+// Observations of K users' symbols per slot: activity_vector + transmit on make_rng(seed), slot by
+// slot (as generate_frame does after sampling the codewords, sim.cpp:82-103). y: slots x n_s complex.
+int ref_amp_observe(int q, int n_s, int slots, const double* dicts, int k, const int32_t* symbols, double p_sym,
+                    double noise_var, uint64_t seed, double* y) {
+    return guarded([&] {
+        auto d = dicts_from(q, n_s, slots, dicts);
+        auto rng = ura::make_rng(seed);
+        std::vector<int> col(k);
+        for (int l = 0; l < slots; ++l) {
+            for (int j = 0; j < k; ++j) col[j] = symbols[l * k + j];
+            auto yl = ura::transmit(d[l], ura::activity_vector(col, q), p_sym, noise_var, rng);
+            for (int r = 0; r < n_s; ++r) {
+                y[(size_t(l) * n_s + r) * 2] = yl[r].real();
+                y[(size_t(l) * n_s + r) * 2 + 1] = yl[r].imag();
+            }
+        }
+    });
+}
+
+// detect_frame (amp.cpp:133-148): S slots x q.
+int ref_amp_detect_frame(int q, int n_s, int slots, const double* dicts, const double* y, int iters, double rho_bg,
+                         double sigma_u2, double evidence_floor, double* S) {
+    return guarded([&] {
+        auto d = dicts_from(q, n_s, slots, dicts);
+        std::vector<std::vector<ura::cplx>> obs(slots, std::vector<ura::cplx>(n_s));
+        for (int l = 0; l < slots; ++l)
+            for (int r = 0; r < n_s; ++r) obs[l][r] = ura::cplx(y[(size_t(l) * n_s + r) * 2], y[(size_t(l) * n_s + r) * 2 + 1]);
+        ura::AmpConfig cfg;
+        cfg.iters = iters;
+        cfg.rho_bg = rho_bg;
+        cfg.sigma_u2 = sigma_u2;
+        cfg.evidence_floor = evidence_floor;
+        auto ev = ura::detect_frame(obs, d, cfg);
+        for (int l = 0; l < slots; ++l)
+            for (int a = 0; a < q; ++a) S[size_t(l) * q + a] = ev.at(l, a);
+    });
+}
+
+double ref_symbol_power(double eb_db, int payload_bits, int slots) { return ura::symbol_power(eb_db, payload_bits, slots); }
 
 } // extern "C"

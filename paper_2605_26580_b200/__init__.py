@@ -43,6 +43,10 @@ class BpConfigDesc(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("message_floor", C.c_double), ("early_exit", C.c_int)]
 
 
+class AmpConfigDesc(C.Structure):
+    _fields_ = [("iters", C.c_int), ("rho_bg", C.c_double), ("sigma_u2", C.c_double), ("evidence_floor", C.c_double)]
+
+
 class CodeDesc(C.Structure):
     _fields_ = [("checks", C.c_int), ("slots", C.c_int), ("n_edges", C.c_int), ("edges", C.POINTER(C.c_int32))]
 
@@ -123,6 +127,9 @@ def lib() -> C.CDLL:
         h.cider_bp_destroy.argtypes = [P]
         h.cider_bp_decode.argtypes = [P, C.c_int, P, C.POINTER(BpConfigDesc), P, P, P, P]
         h.cider_sic_decode.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(BpConfigDesc), C.c_double, P, P, P]
+        h.cider_amp_create.argtypes = [C.c_int, C.c_int, C.c_int, P, C.c_int, C.POINTER(C.c_void_p)]
+        h.cider_amp_destroy.argtypes = [P]
+        h.cider_amp_detect.argtypes = [P, C.c_int, P, C.POINTER(AmpConfigDesc), P]
         _lib_handle = h
     return _lib_handle
 
@@ -538,6 +545,48 @@ class BpDecoder:
         d = cfg.desc()
         _check(lib().cider_sic_decode(self.h, B, k, _ptr(S), C.byref(d), cancel_value, _ptr(grid), _ptr(sc), _ptr(si)))
         return grid, sc.astype(bool), si
+
+
+@dataclass
+class AmpConfig:
+    """ura::AmpConfig (amp.hpp:14-19); default_amp_config sets rho_bg = K/Q, sigma_u2 = P_sym (amp.cpp:29-36)."""
+    iters: int = 20
+    rho_bg: float = 0.03125
+    sigma_u2: float = 20.0
+    evidence_floor: float = -40.0
+
+    def desc(self) -> AmpConfigDesc:
+        return AmpConfigDesc(self.iters, self.rho_bg, self.sigma_u2, self.evidence_floor)
+
+
+class AmpDetector:
+    """Batched AMP slot detector on the device: the reference's detect_frame
+    (amp.cpp:133-148) for many frames at once. dicts: L x q x n_s complex (the per-slot
+    ura::SensingMatrix columns, fixed per dataset)."""
+
+    def __init__(self, dicts: np.ndarray, device: int = 0):
+        dicts = np.ascontiguousarray(dicts, np.complex128)
+        self.L, self.q, self.n_s = dicts.shape
+        h = C.c_void_p()
+        _check(lib().cider_amp_create(self.L, self.q, self.n_s, _ptr(dicts), device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().cider_amp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def detect(self, y: np.ndarray, cfg: AmpConfig = AmpConfig()) -> np.ndarray:
+        """y: B x L x n_s complex observations -> S: B x L x q evidence rows (fp64)."""
+        y = np.ascontiguousarray(y, np.complex128)
+        B = y.shape[0]
+        S = np.empty((B, self.L, self.q), np.float64)
+        d = cfg.desc()
+        _check(lib().cider_amp_detect(self.h, B, _ptr(y), C.byref(d), _ptr(S)))
+        return S
 
 
 def device_count() -> int:

@@ -37,6 +37,7 @@
 #include "kernels/bp.cuh"
 #include "kernels/workload.cuh"
 #include "kernels/path.cuh"
+#include "kernels/amp.cuh"
 
 namespace cider {
 const char* host_last_error();
@@ -2121,3 +2122,87 @@ int cider_nccl_allgather(cider_ctx* c, const void* send, void* recv, size_t n) {
 }
 
 } // extern "C"
+
+// ---- batched AMP slot detector (amp.cpp:63-148) ---------------------------------
+struct cider_amp_ctx {
+    int device = 0, L = 0, q = 0, n_s = 0;
+    cudaStream_t stream = nullptr;
+    cider::DevBuf At, y, S, bad;
+    std::mutex mu;
+    ~cider_amp_ctx() {
+        if (device >= 0) cudaSetDevice(device);
+        At.release(); y.release(); S.release(); bad.release();
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+using namespace cider;
+
+int cider_amp_create(int L, int q, int n_s, const double* dicts, int device, cider_amp_ctx** out) {
+    return guard([&] {
+        if (!out) throw InvalidInput("amp: null output");
+        *out = nullptr;
+        if (L < 1 || q < 1 || n_s < 1) throw InvalidInput("amp: need L, q, n_s >= 1");
+        if (n_s > q) throw InvalidInput("partial_dft: n_s must not exceed Q"); // sim.cpp:12
+        if (!dicts) throw InvalidInput("amp: null dictionaries");
+        require_device();
+        auto c = std::make_unique<cider_amp_ctx>();
+        c->device = device; c->L = L; c->q = q; c->n_s = n_s;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "props");
+        if (prop.major != 10) throw CudaError("cider: needs an sm_100 (B200) device, found sm_" + std::to_string(prop.major * 10 + prop.minor));
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        // reference layout [l][col][r] -> device [l][r][col] (a thread per column reads rows coalesced)
+        std::vector<double> t(size_t(L) * n_s * q * 2);
+        for (int l = 0; l < L; ++l)
+            for (int col = 0; col < q; ++col)
+                for (int r = 0; r < n_s; ++r)
+                    for (int k = 0; k < 2; ++k)
+                        t[((size_t(l) * n_s + r) * q + col) * 2 + k] = dicts[((size_t(l) * q + col) * n_s + r) * 2 + k];
+        c->At.ensure(t.size() * 8);
+        ck(cudaMemcpy(c->At.p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "upload");
+        c->bad.ensure(16);
+        *out = c.release();
+    });
+}
+
+void cider_amp_destroy(cider_amp_ctx* ctx) { delete ctx; }
+
+int cider_amp_detect(cider_amp_ctx* c, int B, const double* y, const cider_amp_config* cfg, double* S) {
+    return guard([&] {
+        if (!c || !cfg) throw InvalidInput("amp_detect: null argument");
+        if (cfg->iters < 1) throw InvalidInput("amp_detect: need at least one iteration");  // amp.cpp:66
+        if (!(cfg->rho_bg > 0.0 && cfg->rho_bg < 1.0)) throw InvalidInput("amp: rho_bg must lie in (0,1)");
+        if (!(cfg->sigma_u2 > 0.0)) throw InvalidInput("amp: sigma_u2 must be positive"); // amp.cpp:22-27
+        if (B < 0) throw InvalidInput("amp_detect: negative batch");
+        if (B == 0) return;
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const size_t ny = size_t(B) * c->L * c->n_s * 2, ns = size_t(B) * c->L * c->q;
+        c->y.ensure(ny * 8);
+        c->S.ensure(ns * 8);
+        ck(cudaMemcpyAsync(c->y.p, y, ny * 8, cudaMemcpyHostToDevice, c->stream), "h2d");
+        const int big = 1 << 30;
+        ck(cudaMemcpyAsync(c->bad.p, &big, 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+        AmpParams p;
+        p.iters = cfg->iters;
+        p.rho_bg = cfg->rho_bg;
+        p.sigma_u2 = cfg->sigma_u2;
+        p.floor = cfg->evidence_floor;
+        p.log_rho = std::log(cfg->rho_bg);
+        p.log1m_rho = std::log1p(-cfg->rho_bg);
+        const size_t smem = size_t(3 * c->n_s + c->q) * 16 + size_t(c->q) * 8;
+        if (smem > 227 * 1024) throw InvalidInput("amp_detect: q / n_s too large for one CTA");
+        if (smem > 48 * 1024)
+            ck(cudaFuncSetAttribute(amp_detect_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem attr");
+        amp_detect_kernel<256><<<unsigned(int64_t(B) * c->L), 256, smem, c->stream>>>(
+            (const double2*)c->At.p, (const double2*)c->y.p, B, c->L, c->q, c->n_s, p, (double*)c->S.p, (int*)c->bad.p);
+        check_launch("amp_detect");
+        int bad = 0;
+        ck(cudaMemcpyAsync(&bad, c->bad.p, 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaMemcpyAsync(S, c->S.p, ns * 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+        ck(cudaStreamSynchronize(c->stream), "amp_detect");
+        if (bad != (1 << 30)) throw std::runtime_error("amp_detect: non-finite residual at iteration " + std::to_string(bad));
+    });
+}
