@@ -18,10 +18,15 @@
 // (which keeps the reference's prefixes, e.g. "embed_grid: token out of range").
 #pragma once
 
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <future>
 #include <limits>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -227,6 +232,114 @@ inline ura::BinDecoder make_bin_decoder(std::shared_ptr<Context> ctx, ura::Revea
         if (per_load_remask) rm.thresholds = ura::default_remask_thresholds(t.load);
         return refiner->run_with_remasking(t.evidence, t.h, sched, rm, t.load);
     };
+}
+
+// Request-coalescing BinDecoder: run_protocol (protocol.cpp:97-110) calls the decoder bank from
+// parallel_for worker threads, one bin at a time per frame. Each call here enqueues its bin and
+// blocks; a dispatcher thread drains everything pending (after the first request waited `window`, or
+// as soon as `max_batch` bins are queued) into ONE ragged device batch (GpuRefiner::run_ragged: the
+// reference's per-load schedule and remask thresholds) and hands every caller its grid. Results are
+// those of the per-bin make_bin_decoder (run_ragged == per-load calls, tests). Evidence is read
+// during the call only (the caller's BinTask outlives it).
+class BinCoalescer {
+public:
+    BinCoalescer(std::shared_ptr<Context> ctx, int k_max, size_t max_batch = 4096,
+                 std::chrono::microseconds window = std::chrono::microseconds(200), bool per_load_remask = true)
+        : refiner_(std::make_shared<GpuRefiner>(std::move(ctx))), k_max_(k_max), max_batch_(max_batch), window_(window),
+          per_load_remask_(per_load_remask), worker_([this] { loop(); }) {}
+    ~BinCoalescer() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        worker_.join();
+    }
+    BinCoalescer(const BinCoalescer&) = delete;
+    BinCoalescer& operator=(const BinCoalescer&) = delete;
+
+    ura::SymbolGrid decode(const ura::BinTask& t) {
+        if (t.load < 1 || t.load > k_max_) throw std::domain_error("BinCoalescer: load outside 1..k_max");
+        Req r{&t.evidence, &t.h, t.load, {}};
+        auto fut = r.done.get_future();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if (q_.empty()) first_ = std::chrono::steady_clock::now();
+            q_.push_back(&r);
+        }
+        cv_.notify_all();
+        return fut.get(); // rethrows the batch's exception
+    }
+    int64_t batches() const { return batches_; }
+
+private:
+    struct Req {
+        const ura::EvidenceMatrix* s;
+        const ura::ParityCheckMatrix* h;
+        int load;
+        std::promise<ura::SymbolGrid> done;
+    };
+    void loop() {
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+            if (q_.empty() && stop_) return;
+            // gather: until the window since the first pending request has passed, or the batch is full
+            cv_.wait_until(lk, first_ + window_, [this] { return stop_ || q_.size() >= max_batch_; });
+            std::vector<Req*> batch;
+            while (!q_.empty() && batch.size() < max_batch_) {
+                batch.push_back(q_.front());
+                q_.pop_front();
+            }
+            if (!q_.empty()) first_ = std::chrono::steady_clock::now();
+            lk.unlock();
+            run(batch);
+            lk.lock();
+        }
+    }
+    void run(const std::vector<Req*>& batch) {
+        // one code per context: bins whose H differs from the first are decoded (and rejected) alone
+        std::vector<const ura::EvidenceMatrix*> ss;
+        std::vector<int> loads;
+        std::vector<Req*> in;
+        for (Req* r : batch) {
+            if (r->h != batch.front()->h) {
+                try {
+                    r->done.set_value(refiner_->run_ragged({r->s}, {r->load}, *r->h, k_max_, per_load_remask_)[0]);
+                } catch (...) {
+                    r->done.set_exception(std::current_exception());
+                }
+                continue;
+            }
+            ss.push_back(r->s);
+            loads.push_back(r->load);
+            in.push_back(r);
+        }
+        if (in.empty()) return;
+        try {
+            auto out = refiner_->run_ragged(ss, loads, *in.front()->h, k_max_, per_load_remask_);
+            ++batches_;
+            for (size_t i = 0; i < in.size(); ++i) in[i]->done.set_value(std::move(out[i]));
+        } catch (...) {
+            for (Req* r : in) r->done.set_exception(std::current_exception());
+        }
+    }
+    std::shared_ptr<GpuRefiner> refiner_;
+    int k_max_;
+    size_t max_batch_;
+    std::chrono::microseconds window_;
+    bool per_load_remask_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Req*> q_;
+    std::chrono::steady_clock::time_point first_{};
+    bool stop_ = false;
+    int64_t batches_ = 0;
+    std::thread worker_; // last: started after every member above is initialised
+};
+
+inline ura::BinDecoder make_coalescing_bin_decoder(std::shared_ptr<BinCoalescer> c) {
+    return [c](const ura::BinTask& t) { return c->decode(t); };
 }
 
 // The device FFT-BP decoder for one code (cider_bp_* in cider.h). Implements the WHT backend

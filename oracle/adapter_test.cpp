@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <thread>
 
 #include "cider_ura.hpp"
 #include "ura/ldpc.hpp"
@@ -97,6 +98,39 @@ int main() {
             }
             std::printf("ragged batch vs per-bin decoder: %d/%d identical grids\n", same, int(ev.size()));
             fails += same != int(ev.size());
+        }
+        // (4c) request coalescing: 8 threads x 6 bins through one BinCoalescer == per-bin decoder
+        {
+            auto co = std::make_shared<cider::BinCoalescer>(ctx, 3);
+            auto cdec = cider::make_coalescing_bin_decoder(co);
+            auto pdec = cider::make_bin_decoder(ctx);
+            const int T = 8, NB = 6;
+            std::vector<ura::EvidenceMatrix> ev(T * NB, ura::EvidenceMatrix(16, 64));
+            std::mt19937_64 r5(5);
+            std::normal_distribution<double> nd(0.0, 1.0);
+            for (auto& m : ev)
+                for (double& x : m.v) x = double(float(1.2 * nd(r5)));
+            std::vector<ura::SymbolGrid> got(T * NB, ura::SymbolGrid(1, 16));
+            std::vector<std::thread> th;
+            for (int t = 0; t < T; ++t)
+                th.emplace_back([&, t] {
+                    for (int i = 0; i < NB; ++i) {
+                        const int b = t * NB + i, load = 1 + b % 3;
+                        ura::SymbolGrid tk(load, 16);
+                        got[b] = cdec(ura::BinTask{gf, h, ev[b], tk, load});
+                    }
+                });
+            for (auto& x : th) x.join();
+            int same = 0;
+            for (int b = 0; b < T * NB; ++b) {
+                const int load = 1 + b % 3;
+                ura::SymbolGrid tk(load, 16);
+                auto one = pdec(ura::BinTask{gf, h, ev[b], tk, load});
+                same += one.v == got[b].v && one.rows == got[b].rows;
+            }
+            std::printf("coalesced (8 threads, %lld device batches) vs per-bin decoder: %d/%d identical grids\n",
+                        (long long)co->batches(), same, T * NB);
+            fails += same != T * NB;
         }
         // (5) SIC-BP: ura::sic_decode vs cider::GpuBp (bp.hpp:72-93), same evidence, identical grids
         {
