@@ -205,6 +205,25 @@ def test_c2_full_size_properties(P):
     assert 0.0 <= ser <= 1.0 and 0.0 <= cer <= 1.0
 
 
+def test_c3_full_size_properties(P):
+    """BASELINE config 3 at full size (16384 bins, N=6, D=256, H=1024, 8 heads, T=16 + rank-25%
+    remasking, bf16 — the bench's kernel set over several device chunks): valid symbols, and a
+    re-decode of the first 3000 bins in 700-bin chunks (different chunk boundaries, eager and graph
+    runs) reproduces them exactly."""
+    cfg = P.configs()["c3"]
+    wl, model = cfg.workload, cfg.model
+    ctx, e, w = ctx_for(P, model, wl)
+    truth, S = wl.bins(e, 0, cfg.bins)
+    sched = P.RevealSchedule(steps=cfg.steps)
+    g = ctx.refine(S, wl.k, sched, cfg.remask)
+    assert g.shape == (cfg.bins, wl.k, wl.slots) and np.all((g >= 0) & (g < model.q))
+    ctx.set_chunk(700)
+    part = ctx.refine(S[:3000], wl.k, sched, cfg.remask)
+    assert np.array_equal(part, g[:3000])
+    ser, cer = P.ser_cer(truth[:64], g[:64])
+    assert 0.0 <= ser <= 1.0 and 0.0 <= cer <= 1.0
+
+
 # ---- edge cases ---------------------------------------------------------------------------------
 def test_edge_shapes_and_schedules(P, oracle):
     wl = P.Workload(m=4, slots=16, checks=8, k=3, snr_db=6.0)
