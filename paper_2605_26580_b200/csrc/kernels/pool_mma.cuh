@@ -190,28 +190,74 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                     e1[i2] = __expf(sc[i2] - m1);
                     e2[i2] = __expf(sc[i2] - m2);
                 }
+                // Leave-one-out sums by prefix / suffix over the edges (no term of edge i enters output i,
+                // so extrinsicity stays bitwise): for i != i1, out_i = (d-1) (P_i + S_i) / (pd_i + sd_i)
+                // with P_i = sum_{i2 < i} e1 n, S_i = sum_{i2 > i} e1 n (pd, sd the same sums of e1); row
+                // i1 uses e2 and is computed on its own (zero weight on itself: + 0 leaves sums unchanged)
+                // and stored over the e1 value.
+                auto store_row = [&](int i, const float2* out, float fct) {
+                    __nv_bfloat162 po[V];
 #pragma unroll
-                for (int i = 0; i < PM_DEG; ++i) {
-                    float den = 0.0f; // ascending over the other edges
+                    for (int v = 0; v < V; ++v) po[v] = __floats2bfloat162_rn(out[v].x * fct, out[v].y * fct);
+                    if constexpr (V == 4) *reinterpret_cast<uint4*>(orow + i * K * D) = *reinterpret_cast<const uint4*>(po);
+                    else *reinterpret_cast<uint2*>(orow + i * K * D) = *reinterpret_cast<const uint2*>(po);
+                };
+                float2 pre[PM_DEG][V]; // pre[i] = P_i (i >= 1)
+                float pd[PM_DEG];
 #pragma unroll
-                    for (int i2 = 0; i2 < PM_DEG; ++i2)
-                        if (i2 != i) den += i == i1 ? e2[i2] : e1[i2];
-                    const float fct = __fdividef(float(PM_DEG - 1), den);
+                for (int v = 0; v < V; ++v) pre[1][v] = __fmul2_rn(make_float2(e1[0], e1[0]), f[0][v]);
+                pd[1] = e1[0];
+#pragma unroll
+                for (int i = 2; i < PM_DEG; ++i) {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) pre[i][v] = __ffma2_rn(make_float2(e1[i - 1], e1[i - 1]), f[i - 1][v], pre[i - 1][v]);
+                    pd[i] = pd[i - 1] + e1[i - 1];
+                }
+                float2 suf[V]; // running S_i, from the top
+                float sd = 0.0f;
+#pragma unroll
+                for (int i = PM_DEG - 1; i >= 0; --i) {
                     float2 out[V];
+                    float den;
+                    if (i == PM_DEG - 1) {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) out[v] = pre[i][v];
+                        den = pd[i];
+                    } else if (i == 0) {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) out[v] = suf[v];
+                        den = sd;
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < V; ++v) out[v] = __fadd2_rn(pre[i][v], suf[v]);
+                        den = pd[i] + sd;
+                    }
+                    store_row(i, out, __fdividef(float(PM_DEG - 1), den));
+                    if (i > 0) { // S_{i-1} = S_i + e1_i n_i
+                        if (i == PM_DEG - 1) {
+#pragma unroll
+                            for (int v = 0; v < V; ++v) suf[v] = __fmul2_rn(make_float2(e1[i], e1[i]), f[i][v]);
+                            sd = e1[i];
+                        } else {
+#pragma unroll
+                            for (int v = 0; v < V; ++v) suf[v] = __ffma2_rn(make_float2(e1[i], e1[i]), f[i][v], suf[v]);
+                            sd = sd + e1[i];
+                        }
+                    }
+                }
+                { // row i1 with the runner-up max (e2), ascending over the others
+                    float2 out[V];
+                    float den = 0.0f;
 #pragma unroll
                     for (int v = 0; v < V; ++v) out[v] = make_float2(0.f, 0.f);
 #pragma unroll
                     for (int i2 = 0; i2 < PM_DEG; ++i2) {
-                        if (i2 == i) continue;
-                        const float w = (i == i1 ? e2[i2] : e1[i2]) * fct;
+                        const float w = i2 == i1 ? 0.0f : e2[i2];
+                        den += w;
 #pragma unroll
                         for (int v = 0; v < V; ++v) out[v] = __ffma2_rn(make_float2(w, w), f[i2][v], out[v]);
                     }
-                    __nv_bfloat162 po[V];
-#pragma unroll
-                    for (int v = 0; v < V; ++v) po[v] = __floats2bfloat162_rn(out[v].x, out[v].y);
-                    if constexpr (V == 4) *reinterpret_cast<uint4*>(orow + i * K * D) = *reinterpret_cast<const uint4*>(po);
-                    else *reinterpret_cast<uint2*>(orow + i * K * D) = *reinterpret_cast<const uint2*>(po);
+                    store_row(i1, out, __fdividef(float(PM_DEG - 1), den));
                 }
             }
         }
