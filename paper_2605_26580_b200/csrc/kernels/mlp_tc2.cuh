@@ -251,6 +251,30 @@ __device__ __forceinline__ void demix_load_sv(const MlpArgs& args, int m0, int c
         }
 }
 
+// 2^x for x <= 0 (the demix arguments are max-subtracted). MLP2_DEMIX_POLYEXP: every other row group
+// (a whole (bin, slot) group, so the softmax stays bitwise invariant to the order of its rows) on
+// the FMA pipe (Cody-Waite split, degree-5 minimax polynomial on [0,1), exponent by integer add; rel.
+// error < 2e-7, below the bf16 output rounding), the rest on MUFU ex2 — halves the MUFU load.
+#ifndef MLP2_DEMIX_POLYEXP
+#define MLP2_DEMIX_POLYEXP 0 // measured slower (demix_evid 62 -> 67.5 ms per c5 step: not MUFU-bound)
+#endif
+__device__ __forceinline__ float exp2_poly(float x) {
+    x = fmaxf(x, -126.0f);
+    const float fi = floorf(x);
+    const float f = x - fi; // [0, 1)
+    float p = 1.8775767e-3f;
+    p = fmaf(p, f, 8.9893397e-3f);
+    p = fmaf(p, f, 5.5826318e-2f);
+    p = fmaf(p, f, 2.4015361e-1f);
+    p = fmaf(p, f, 6.9315308e-1f);
+    p = fmaf(p, f, 9.9999994e-1f);
+    return __int_as_float(__float_as_int(p) + (int(fi) << 23));
+}
+__device__ __forceinline__ float demix_exp2(float x, int group) {
+    if (MLP2_DEMIX_POLYEXP && (group & 1)) return exp2_poly(x);
+    return ex2_approx(x);
+}
+
 template <int KK>
 __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, uint32_t base, uint64_t* a1_full_b, uint32_t ph,
                                            uint32_t l_h_full, const float* svin, int lane, long long* tr) {
@@ -291,7 +315,7 @@ __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, ui
             uint32_t den = 0;
 #pragma unroll
             for (int k = 0; k < KK; ++k) {
-                const float e = ex2_approx(fmaf(xv[t * KK + k], scale2, nmx));
+                const float e = demix_exp2(fmaf(xv[t * KK + k], scale2, nmx), t); // one method per (bin, slot) group
                 xv[t * KK + k] = e;
                 den += __float_as_uint(fmaf(e, 4194304.0f, 8388608.0f)) - 0x4B000000u; // round(e 2^22)
             }
