@@ -223,6 +223,19 @@ def reference_sample(cfg, sample_s: float, threads: int):
                       f"threads, x{per_bin} forwards/bin; fp64; {cpu_info()[0]}"}
 
 
+def arm_config(cfg, B, world):
+    """The `config` both arms report (the reference arm times a bounded sample of this workload)."""
+    wl, model = cfg.workload, cfg.model
+    return {"workload": f"{cfg.name}: K={wl.k} L={wl.slots} Q={model.q} N={model.layers} D={model.dim} H={model.hidden} "
+                        f"heads={model.heads} T={cfg.steps}"
+                        + (" + rank-25% remask" if cfg.remask else "") + f"; {B} bins/GPU/step",
+            "bins_per_gpu_per_step": B, "global_batch": B * world,
+            "parallelism": f"bin-sharded x{world} (no per-step collective)",
+            "l2": "inputs+working set per step >> 126 MB L2 (no flush needed)",
+            "forwards_per_bin": P.forward_count(cfg), "gflop_per_bin": round(P.flops_per_bin(cfg) / 1e9, 2),
+            "survey_gflop_per_bin": round(P.survey_flops_per_bin(cfg) / 1e9, 2)}
+
+
 def run_reference_arm(a, cfg, dist):
     if dist.rank != 0:
         return
@@ -236,7 +249,9 @@ def run_reference_arm(a, cfg, dist):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "bins/s", "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE evidence model)",
-            "config": {"workload": f"{cfg.name}: one denoiser forward per host thread per step"},
+            "config": dict(arm_config(cfg, a.bins_per_step or DEFAULT_BINS[a.config], a.gpus),
+                           reference_sample="each step times one fp64 denoiser forward of this workload's bins per host "
+                                            "thread and scales by the forwards per bin"),
             "cpu_baseline": {"value": v, "unit": "bins/s", "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]},
             "e2e": {"value": v, "unit": "bins/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -410,14 +425,7 @@ def main():
             "warmup": a.warmup, "ms_per_step": round(t_max / a.steps, 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16" if model.precision == P.BF16 else "f32",
             "data": "synthetic (seeded BASELINE evidence model, random-init weights seed 1)",
-            "config": {"workload": f"{cfg.name}: K={K} L={L} Q={Q} N={model.layers} D={model.dim} H={model.hidden} "
-                                   f"heads={model.heads} T={cfg.steps}"
-                                   + (" + rank-25% remask" if cfg.remask else "") + f"; {B} bins/GPU/step",
-                       "bins_per_gpu_per_step": B, "global_batch": B * world,
-                       "parallelism": f"bin-sharded x{world} (no per-step collective)",
-                       "l2": "inputs+working set per step >> 126 MB L2 (no flush needed)",
-                       "forwards_per_bin": P.forward_count(cfg), "gflop_per_bin": round(fpb / 1e9, 2),
-                       "survey_gflop_per_bin": round(P.survey_flops_per_bin(cfg) / 1e9, 2)},
+            "config": arm_config(cfg, B, world),
             "e2e": {"value": round(e2e, 2), "unit": "bins/s", "h2d_bytes_per_step": s_bytes * world,
                     "d2h_bytes_per_step": g_bytes * world, "steps": e2e_steps},
             "gpu_launches": int(launches),
