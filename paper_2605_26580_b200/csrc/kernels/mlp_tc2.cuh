@@ -198,7 +198,7 @@ struct Mlp2Layout {
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
     static constexpr int TOTAL = BAR_OFF + 512 + BIASB + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
-    static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 4 + 2 + 2 + NXB * (D / 64)) * 8 + 4 <= 512, "barrier block");
+    static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 8 + 2 + 2 + NXB * (D / 64)) * 8 + 4 <= 512, "barrier block");
     static_assert(D % 32 == 0 && D <= 256 && W2_HALF <= SLOT, "output width must be <= 256");
     static_assert(KB1 % W1_PER_SLOT == 0, "input width must be a multiple of 128");
 };
@@ -332,12 +332,11 @@ __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, ui
         const uint4 p1 = *reinterpret_cast<const uint4*>(os + lane * 32 + ((1 ^ ((lane >> 2) & 1)) * 16));
         const uint32_t pk[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
         tmem_st8(base + p * 8, pk); // pass p's 16 columns packed in place (fp32 columns [0, 16) were read in pass 0)
-        __syncwarp(); // the next pass overwrites the staging block
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_before();
+        __syncwarp(); // (also: the next pass overwrites the staging block)
+        if (lane == 0) mbar_arrive_cl(l_h_full + p * 8); // pass p -> MMA2 k-step 2 sub + p, as soon as it is packed
     }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cl(l_h_full); // the warp's 32 hidden columns -> MMA2 k-steps 2 sub, 2 sub + 1
     if (tr) tr[4] = clock64();
 }
 
@@ -367,8 +366,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint64_t* r_full = x_empty + NXB * KB1;
     uint64_t* r_empty = r_full + NS;
     uint64_t* a1_full = r_empty + NS;   // [2] first-layer accumulator ready
-    uint64_t* h_full = a1_full + 2;     // [2][GG] GELU group g of acc1[b] packed (leader copy counts both CTAs)
-    uint64_t* a1_free = h_full + 2 * MLP2_GG; // [2] MMA2 done reading acc1[b] (leader only)
+    constexpr int HG = 2 * MLP2_GG;     // hidden-group barriers per acc1 buffer (demix: one per 16-column pass)
+    uint64_t* h_full = a1_full + 2;     // [2][HG] hidden group g of acc1[b] packed (leader copy counts both CTAs)
+    uint64_t* a1_free = h_full + 2 * HG; // [2] MMA2 done reading acc1[b] (leader only)
     uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
     uint64_t* o_full = a2_empty + 1;    // [NXB][KBD] output block staged in X k-block kb (4 quarter warps)
@@ -427,7 +427,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&a1_full[b], 1);
-            for (int g = 0; g < MLP2_GG; ++g) mbar_init(&h_full[MLP2_GG * b + g], H_ARRIVALS);
+            for (int g = 0; g < HG; ++g) mbar_init(&h_full[HG * b + g], H_ARRIVALS);
             mbar_init(&a1_free[b], 1);
         }
         mbar_init(a2_full, 1);
@@ -634,12 +634,38 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         // are GELU group g of warp-half kb, packed in place at TMEM cols 64 kb + 8 g: k-step g
                         // of W2 slot kb, issued as soon as that group lands in both CTAs.
                         const uint32_t a_base = tmem + 256 + b * MLP_HC;
-                        if constexpr (W32) {
+                        if constexpr (EPK == EP_DEMIX) {
+                            // pass j of warp group g = hidden columns [32 g + 16 j, +16), packed at TMEM columns
+                            // 32 g + 8 j: every warp's first pass lands before its second, so the first
+                            // pass of all four groups is issued while the second ones are still computed
+#pragma unroll
+                            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                                for (int g = 0; g < MLP2_GG; ++g) {
+                                    mbar_wait(&h_full[HG * b + 2 * g + j], (hph >> b) & 1u);
+                                    fence_after();
+                                    if (g == 0 && j == 0 && c == 0) {
+                                        mbar_wait(a2_empty, a2ph ^ 1);
+                                        a2ph ^= 1;
+                                        fence_after();
+                                    }
+                                    uint32_t ph;
+                                    const int slot = ring_slot(it * per_tile + pos_w2(c) + g / 2, ph);
+                                    if (j == 0 && g % 2 == 0) {
+                                        mbar_wait(&r_full[slot], ph);
+                                        fence_after();
+                                    }
+                                    const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
+                                    mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
+                                                    (c | g | j) != 0);
+                                    if (j == 1 && g % 2 == 1) mma_commit_2sm(&r_empty[slot]);
+                                }
+                        } else if constexpr (W32) {
                             // group g = hidden columns [32 g, 32 g + 32) of every quarter, packed at TMEM
                             // columns 32 g + [0, 16): k-steps 2 g, 2 g + 1 of W2 k-block g / 2
 #pragma unroll
                             for (int g = 0; g < MLP2_GG; ++g) {
-                                mbar_wait(&h_full[MLP2_GG * b + g], (hph >> b) & 1u);
+                                mbar_wait(&h_full[HG * b + g], (hph >> b) & 1u);
                                 fence_after();
                                 if (g == 0 && c == 0) {
                                     mbar_wait(a2_empty, a2ph ^ 1);
@@ -663,7 +689,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         int slots[S2];
 #pragma unroll
                         for (int g = 0; g < MLP2_GG; ++g) {
-                            mbar_wait(&h_full[MLP2_GG * b + g], (hph >> b) & 1u);
+                            mbar_wait(&h_full[HG * b + g], (hph >> b) & 1u);
                             fence_after();
                             if (g == 0) {
                                 if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
@@ -737,9 +763,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         else demix_load_sv<4>(args, mn, cn * MLP_HC + half * 32, lane, svn);
                     }
                     if (ep.K == 8)
-                        demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, svc, lane, tr);
+                        demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
                     else
-                        demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (MLP2_GG * b + half) * 8, svc, lane, tr);
+                        demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
                     e1ph ^= 1u << b;
                 }
                 const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
@@ -811,7 +837,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 fence_before();
-                release(L_h_full0 + (MLP2_GG * b + half) * 8); // this warp's 32 columns -> MMA2 k-steps 2 half, 2 half + 1
+                release(L_h_full0 + (HG * b + half) * 8); // this warp's 32 columns -> MMA2 k-steps 2 half, 2 half + 1
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
             if (!fin && !W32)
@@ -846,7 +872,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     }
                     fence_before();
-                    release(L_h_full0 + (MLP2_GG * b + g) * 8); // group g of both halves -> MMA2 k-step g
+                    release(L_h_full0 + (HG * b + g) * 8); // group g of both halves -> MMA2 k-step g
                 }
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
