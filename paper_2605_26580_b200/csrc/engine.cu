@@ -842,6 +842,28 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     }
     using Lay = tc::SmemLayout<256, 0>;
     static const int grp_mode = std::getenv("CIDER_GRP_MODE") ? std::atoi(std::getenv("CIDER_GRP_MODE")) : 2;
+    static const bool no_res2 = std::getenv("CIDER_NO_GRP2_RES") != nullptr;
+    if (max_seg == 1 && !no_res2 && c.sm_count >= 2 && D == 256) {
+        // single-segment groups (normalise): CTA pairs with their T halves resident, laps over the pairs
+        // (c5 58.6 -> 55.7 ms, c4 45 -> 41 ms per step; at D = 128 the streamed kernel is as fast)
+        static bool attr_r2 = false;
+        if (!attr_r2) {
+            ck(cudaFuncSetAttribute(tc::gemm_grp2_res_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::grp2_res_smem<256>()), "smem attr");
+            ck(cudaFuncSetAttribute(tc::gemm_grp2_res_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc::grp2_res_smem<128>()), "smem attr");
+            attr_r2 = true;
+        }
+        const int mpairs = (a.mtiles + 1) / 2;
+        const int grid = 2 * std::min(groups * mpairs, c.sm_count / 2);
+        const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
+        if (!out_t || out_f) throw InvalidInput("cider: the paired T-resident grouped GEMM writes one bf16 output");
+        const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb);
+        if (D == 256) tc::gemm_grp2_res_kernel<256><<<grid, tc::GRP_THREADS, tc::grp2_res_smem<256>(), c.stream>>>(ta, tt2, to, a);
+        else tc::gemm_grp2_res_kernel<128><<<grid, tc::GRP_THREADS, tc::grp2_res_smem<128>(), c.stream>>>(ta, tt2, to, a);
+        check_launch(tag);
+        return;
+    }
     if ((grp_mode == 2 && a.mtiles >= 2 && c.sm_count >= 2 && D == 256) || D == 128) {
         // CTA pairs, one cta_group::2 MMA over two m-tiles: each SM pulls half of every T k-block
         // (D = 128 always: the other grouped kernels are D = 256 only)

@@ -512,6 +512,191 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 }
 constexpr int GRP2_SMEM = 6 * (BM * BK * 2 + 128 * BK * 2) + 2 * 16384 + 256 + 1024;
 
+// ---- CTA-pair T-resident variant (single-segment groups: the normalise GEMM) --------------------
+// Each CTA of a pair keeps its N-half of the group's T_alpha resident (64 KB at D = 256) and streams
+// only its gathered A rows (an 8-deep ring), so per 256-row pair tile each SM pulls 64 KB instead of
+// 128 KB. Work = (group, m-tile pair) units in laps over the pairs (groups are slot-major: a slot's
+// edges run on neighbouring pairs at the same m-tiles and share their z~ rows through L2), the
+// remaining groups split their m-tile range; a T change waits for the MMAs on the old T (t_empty).
+template <typename F>
+__device__ __forceinline__ void grp_lap_sweep(int worker, int workers, int groups, int msz, F&& body) {
+    int g0 = 0;
+    for (; groups - g0 >= workers; g0 += workers)
+        for (int m = 0; m < msz; ++m) body(g0 + worker, m);
+    const int rem = groups - g0;
+    if (rem > 0) { // the rest as equal contiguous (group, m) ranges: one T change per worker at most
+        const int tot = rem * msz;
+        const int u0 = int(int64_t(worker) * tot / workers), u1 = int(int64_t(worker + 1) * tot / workers);
+        for (int u = u0; u < u1; ++u) body(g0 + u / msz, u % msz);
+    }
+}
+
+template <int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GRP_THREADS, 1)
+gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
+                     const __grid_constant__ CUtensorMap tmO, const GrpArgs args) {
+    constexpr int BN = D;
+    constexpr int NKB = D / 64;
+    constexpr int A_BYTES = BM * BK * 2;            // 16 KB: this CTA's 128 rows of a k-block
+    constexpr int B_HALF = (BN / 2) * BK * 2;       // this CTA's N-half of a T k-block
+    constexpr int T_OFF = 0, A_OFF = NKB * B_HALF;
+    constexpr int NST = 8;
+    constexpr int STG_OFF = A_OFF + NST * A_BYTES;  // 2 x 16 KB output k-block staging (SW128, TMA store)
+    constexpr int BAR_OFF = STG_OFF + 2 * 16384;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* t_full = tempty + 2;  // resident T half landed (leader copy counts both CTAs)
+    uint64_t* t_empty = t_full + 1; // every MMA on the old T retired
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = int(blockIdx.x) / 2, npairs = int(gridDim.x) / 2;
+    const int mpairs = (args.mtiles + 1) / 2;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * 8); }
+        mbar_init(t_full, 1);
+        mbar_init(t_empty, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    fence_before();
+    cluster_sync_all();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int a_bytes = args.K * args.bb * 128;
+    const uint32_t L_full0 = mapa_u32(smem_u32(&full[0]), 0);
+    const uint32_t L_tfull = mapa_u32(smem_u32(t_full), 0);
+    const uint32_t L_tempty0 = mapa_u32(smem_u32(&tempty[0]), 0);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0, cur = -1;
+            uint32_t phase = 0, teph = 0;
+            grp_lap_sweep(pair, npairs, args.groups, mpairs, [&](int g, int mtp) {
+                const int alpha = args.seg_alpha[g * args.max_seg];
+                if (alpha != cur) { // new coefficient action: after the MMAs on the old one retired
+                    if (cur >= 0) { mbar_wait(t_empty, teph); teph ^= 1; }
+                    if (leader) mbar_expect_tx(t_full, 2 * NKB * B_HALF);
+                    for (int kb = 0; kb < NKB; ++kb)
+                        tma_load_3d_2sm(smem + T_OFF + kb * B_HALF, &tmT, L_tfull, kb * 64, int(rank) * (BN / 2), alpha);
+                    cur = alpha;
+                }
+                const int arow = args.seg_arow[g * args.max_seg];
+                const int mt = 2 * mtp + int(rank);
+                for (int kb = 0; kb < NKB; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_expect_tx(&full[stage], 2 * a_bytes);
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+                            smem_u32(smem + A_OFF + stage * A_BYTES)),
+                        "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(L_full0 + stage * 8), "r"(kb * 64), "r"(arow * args.K), "r"(mt * args.bb)
+                        : "memory");
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+            });
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(256, BN);
+            int stage = 0, acc = 0, cur = -1;
+            uint32_t phase = 0, acc_phase = 0, tfph = 0;
+            grp_lap_sweep(pair, npairs, args.groups, mpairs, [&](int g, int) {
+                const int alpha = args.seg_alpha[g * args.max_seg];
+                if (alpha != cur) {
+                    if (cur >= 0) mma_commit_2sm(t_empty); // fires once every MMA on the old T has completed
+                    mbar_wait(t_full, tfph);
+                    tfph ^= 1;
+                    fence_after();
+                    cur = alpha;
+                }
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                fence_after();
+                const uint32_t d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < NKB; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint64_t da = sw128_desc(smem + A_OFF + stage * A_BYTES), db = sw128_desc(smem + T_OFF + kb * B_HALF);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
+                    mma_commit_2sm(&empty[stage]);
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
+                }
+                mma_commit_2sm(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            });
+        }
+    } else {
+        // epilogue as gemm_grp2_kernel (staged SW128 k-blocks, one 3-D TMA store each)
+        const int quarter = warp % 4;
+        const int half = (warp - 2) / 4;
+        const int row = quarter * 32 + lane;
+        const bool issuer = warp == 2 && lane == 0;
+        int acc = 0, step = 0;
+        uint32_t acc_phase = 0;
+        grp_lap_sweep(pair, npairs, args.groups, mpairs, [&](int g, int mtp) {
+            const int mt = 2 * mtp + int(rank);
+            mbar_wait(&tfull[acc], acc_phase);
+            fence_after();
+            const int orow_g = __ldg(args.out_row + g);
+            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+            for (int kb = 0; kb < NKB; ++kb, ++step) {
+                float v[32];
+                tmem_ld32(tbase + kb * 64 + half * 32, v);
+                if (kb == NKB - 1) { // accumulator drained
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cl(L_tempty0 + acc * 8);
+                }
+                uint8_t* stg = smem + STG_OFF + (step & 1) * 16384;
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        __nv_bfloat162 p = __floats2bfloat162_rn(v[jj * 8 + 2 * q], v[jj * 8 + 2 * q + 1]);
+                        pk[q] = *reinterpret_cast<uint32_t*>(&p);
+                    }
+                    const int j = half * 4 + jj;
+                    *reinterpret_cast<uint4*>(stg + row * 128 + ((j ^ (row & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (issuer) {
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                                     reinterpret_cast<uint64_t>(&tmO)),
+                                 "r"(smem_u32(stg)), "r"(kb * 64), "r"(orow_g * args.K), "r"(mt * args.bb)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                }
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+            }
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        });
+        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+template <int D>
+constexpr int grp2_res_smem() { return (D / 64) * (D / 2) * 64 * 2 + 8 * BM * BK * 2 + 2 * 16384 + 256 + 1024; }
+
 // ---- T-resident variant for single-segment groups (the normalise GEMM, group = edge) ------------
 // The m-tiles are swept in chunks of `mchunk` (128 bins at K = 8: 32 MB of z~, L2-resident); inside a
 // chunk every CTA takes an equal contiguous range of (group, m-tile) work, group-major, so its
