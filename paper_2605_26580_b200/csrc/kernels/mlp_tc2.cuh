@@ -19,6 +19,14 @@
 // read), and the second MMA takes its A operand straight from TMEM (tcgen05.mma [d], [a_tmem], b).
 // SMEM then holds only the resident row tile and a deep weight ring.
 // Ring slot = 16 KB: a W2 half k-block (D/2 x 64) or two W1 half k-blocks (HC/2 x 64 each).
+//
+// Warp roles (640 threads): 0 weight-ring producer, 1 first-layer MMA issuer, 2-9 hidden-chunk
+// epilogue (GELU, packed in place, released in 16-column groups), 10-17 final epilogue (overlaps the
+// next tile's chunks; bias from SMEM; results staged in the tile's own X k-blocks in the SW128 layout),
+// 18 second-layer MMA issuer, 19 row-tile (X) producer, which also TMA-stores the staged outputs and
+// refills those k-blocks. The aggregator and the demix variant double-buffer their 64 KB row tile.
+// EP_DEMIX (Lambda-bar -> demix -> e, hidden = the Q symbol columns) runs all 16 epilogue warps on
+// the demix (16-column passes, each released to the second MMA on its own) and the final epilogue.
 #pragma once
 
 #include "mlp_tc.cuh"
