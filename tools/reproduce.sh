@@ -1,0 +1,21 @@
+#!/bin/bash
+# Reproduce the round's measurements (run from the repo root on a B200).
+set -e
+python -c "import __graft_entry__ as g; g.build()"                       # nvcc sm_100a + CPU checkers
+python -m pytest tests -m "not gpu" -q                                   # oracle / reference / ABI (CPU)
+python -m pytest tests -m gpu -q                                         # device parity
+python -c "import __graft_entry__ as g; g.smoke()"
+python bench.py > profiles/r1/bench_c5_2048bins.json                     # headline line (c5, 2048 bins/step)
+for c in c1 c2 c3 c4; do python bench.py --config $c --no-cpu-baseline --steps 3 > profiles/r1/bench_$c.json; done
+python bench.py --impl reference --steps 1 --warmup 1                    # the reference arm (host cores)
+# launch list (cold-cache, serialised: shares only) and one full capture of each hot kernel
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file launches.csv \
+    python bench.py --bins-per-step 512 --steps 1 --warmup 1 --no-cpu-baseline
+python tools/ncu_summary.py launches launches.csv > profiles/r1/launch_share.txt
+BINS=512 ncu --set full --clock-control none --import-source on -k regex:"mlp_tc2|pool_mma|gemm_grp" \
+    --launch-skip 0 --launch-count 7 -o kernels python tests/mlp_rate.py
+python tools/ncu_summary.py rep kernels.ncu-rep > profiles/r1/kernels_ncu_full.txt
+python tools/make_ncu_summary.py kernels.ncu-rep 512                    # -> profiles/ncu_summary.json (roofline.traffic)
+# per-chunk MLP timelines, side benches of the 8(f) components
+CIDER_TRACE_MLP=1 python tests/trace_mlp.py
+python tools/bench_bp.py --config c3; python tools/bench_workload.py; python tools/bench_amp.py
