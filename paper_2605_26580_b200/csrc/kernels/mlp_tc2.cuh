@@ -416,6 +416,17 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #ifndef MLP2_XPREFETCH
 #define MLP2_XPREFETCH 0 // no measurable effect on c5 (gate 202 ms either way)
 #endif
+// Issue loops run by the whole warp (bit 0: MMA1 issuer, bit 1: MMA2 issuer; lane 0 issues) or by
+// lane 0 alone, per variant
+#ifndef MLP2_WI_AGG
+#define MLP2_WI_AGG 3
+#endif
+#ifndef MLP2_WI_GF
+#define MLP2_WI_GF 0
+#endif
+#ifndef MLP2_WI_DEMIX
+#define MLP2_WI_DEMIX 3
+#endif
 #ifndef MLP2_ZREG
 #define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
 #endif
@@ -586,9 +597,11 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // barrier wait of a single issuing thread is a pipe bubble (tools/mma_bench.cu issue2_kernel:
         // 200-cycle waits per slot cost 22% with one issuer, 11% with two). Warp 1 issues the first
         // layer (acc1 buffers), warp 10 the second (acc2); a1_free orders MMA2(n) before MMA1(n+2).
-        if (leader && lane == 0) {
+        constexpr int WI = EPK == EP_DEMIX ? MLP2_WI_DEMIX : KIN == D ? MLP2_WI_AGG : MLP2_WI_GF;
+        const bool el = lane == 0;
+        if (leader && (el || ((warp == 1 ? WI & 1 : WI & 2) != 0))) {
             auto ring_slot = [&](int gpos, uint32_t& ph) { ph = uint32_t(gpos / NS) & 1u; return gpos % NS; };
-            const bool tr = args.trace && blockIdx.x == 0;
+            const bool tr = args.trace && blockIdx.x == 0 && el;
             if (warp == 1) {
                 constexpr uint32_t id1 = idesc_bf16(256, MLP_HC);
                 uint32_t xph = 0, fph = 0; // fph bit b: phase of a1_free[b]
@@ -619,13 +632,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                 const uint64_t db = sw128_desc(ring + slot * Lay::SLOT + j * Lay::W1_HALF);
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
-                                    mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id1, (sg | j | kk) != 0);
+                                    if (el) mma_bf16_2sm(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), id1, (sg | j | kk) != 0);
                             }
-                            mma_commit_2sm(&r_empty[slot]);
+                            if (el) mma_commit_2sm(&r_empty[slot]);
                         }
-                        mma_commit_2sm(&a1_full[b]);
+                        if (el) mma_commit_2sm(&a1_full[b]);
                         if (c == NC - 1)
-                            for (int kb = 0; kb < KB1; ++kb) mma_commit_2sm(&x_empty[xb * KB1 + kb]);
+                            for (int kb = 0; kb < KB1; ++kb) if (el) mma_commit_2sm(&x_empty[xb * KB1 + kb]);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 7] = clock64();
                     }
                     if (NXB == 1) xph ^= 1;
@@ -664,9 +677,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                         fence_after();
                                     }
                                     const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
-                                    mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
+                                    if (el) mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
                                                     (c | g | j) != 0);
-                                    if (j == 1 && g % 2 == 1) mma_commit_2sm(&r_empty[slot]);
+                                    if (j == 1 && g % 2 == 1) if (el) mma_commit_2sm(&r_empty[slot]);
                                 }
                         } else if constexpr (W32) {
                             // group g = hidden columns [32 g, 32 g + 32) of every quarter, packed at TMEM
@@ -689,9 +702,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                 const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
 #pragma unroll
                                 for (int j = 0; j < 2; ++j)
-                                    mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
+                                    if (el) mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
                                                     (c | g | j) != 0);
-                                if (g % 2 == 1) mma_commit_2sm(&r_empty[slot]);
+                                if (g % 2 == 1) if (el) mma_commit_2sm(&r_empty[slot]);
                             }
                         } else {
                         int slots[S2];
@@ -716,16 +729,16 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                     fence_after();
                                 }
                                 const uint64_t db = sw128_desc(ring + slots[kb] * Lay::SLOT);
-                                mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, (c | kb | g) != 0);
-                                if (g == MLP2_GG - 1) mma_commit_2sm(&r_empty[slots[kb]]);
+                                if (el) mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, (c | kb | g) != 0);
+                                if (g == MLP2_GG - 1) if (el) mma_commit_2sm(&r_empty[slots[kb]]);
                             }
                         }
                         }
                         hph ^= 1u << b;
-                        mma_commit_2sm_mask(&a1_free[b], 1);
+                        if (el) mma_commit_2sm_mask(&a1_free[b], 1);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 5] = clock64();
                     }
-                    mma_commit_2sm(a2_full);
+                    if (el) mma_commit_2sm(a2_full);
                 }
             }
         }
