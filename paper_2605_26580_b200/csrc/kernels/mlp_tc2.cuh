@@ -221,6 +221,11 @@ constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
 #ifndef MLP2_GELU16
 #define MLP2_GELU16 0 // measured slower (c5: agg 356 -> 390 ms; the 72-register cap of 896 threads)
 #endif
+// MLP2_AGG_MERGED: the aggregator runs its 16 epilogue warps on both phases (32 hidden columns per
+// warp per chunk, the demix layout, then one output k-block each): half the GELU latency per chunk
+#ifndef MLP2_AGG_MERGED
+#define MLP2_AGG_MERGED 0 // measured slower (c5: agg 356 -> 415 ms)
+#endif
 constexpr int MLP2_HW = MLP2_GELU16 ? 16 : 8;            // hidden-chunk warps of the GELU variants
 constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : MLP2_HW + 8; }
 constexpr int MLP2_FIN_WARP0 = 2 + MLP2_HW;
@@ -391,12 +396,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // hidden group g: GELU = 16 columns of both 64-column warp halves (all epilogue warps); demix =
     // the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
     // hidden group g: one warp per quarter x 2 CTAs (32-column warps), or the 8 hidden warps x 2 CTAs
-    constexpr bool W32 = EPK == EP_DEMIX || MLP2_GELU16; // 32-column hidden warps
+    constexpr bool MERGED = MLP2_AGG_MERGED && !MLP2_GELU16 && EPK == EP_STORE;
+    constexpr bool W32 = EPK == EP_DEMIX || MLP2_GELU16 || MERGED; // 32-column hidden warps
     constexpr int H_ARRIVALS = W32 ? 8 : 8 * 2;
     // Final epilogue: the aggregator (double-buffered rows) runs it on warps 10-17 only, overlapping the
     // next tile's chunks; gate / fusion (whose next row tile waits for it) on all 16 epilogue warps, one
     // output k-block each, to shorten the tile transition.
-    constexpr bool FIN_ALL = false; // (all 16 warps on the gate / fusion final epilogue measured no faster)
+    constexpr bool FIN_ALL = MERGED; // (all 16 warps on the gate / fusion final epilogue measured no faster)
     constexpr int FIN_STRIDE = FIN_ALL ? 4 : 2;                  // output k-blocks between one warp's
     constexpr int FIN_WARPS = FIN_ALL ? (4 * KBD < 16 ? 4 * KBD : 16) : 8;
     constexpr int A2_ARRIVALS = EPK == EP_DEMIX ? EPI_ARRIVALS : FIN_WARPS * 2; // warps that drain acc2
@@ -746,7 +752,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // 8 epilogue warps: TMEM lane quarter = warp % 4; the two warps of a quarter own the two
         // 64-column halves of every hidden chunk, and alternate 64-column k-blocks of the output.
         const int quarter = warp % 4;
-        const bool fin = EPK != EP_DEMIX && warp >= MLP2_FIN_WARP0; // final-epilogue warp (GELU variants)
+        const bool fin = EPK != EP_DEMIX && !MERGED && warp >= MLP2_FIN_WARP0; // final-epilogue-only warp
         const int half = fin ? (warp - MLP2_FIN_WARP0) / 4 : (warp - 2) / 4;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
