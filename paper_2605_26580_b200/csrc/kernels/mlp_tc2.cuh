@@ -183,6 +183,31 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
         : "memory");
 }
 
+// tcgen05.ld of 32 columns without the wait, and the wait tied to those registers (so no use of
+// them can be scheduled above it): the final epilogue loads k-block kb + 1 while it works on kb
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld32(uint32_t (&r)[32]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                   "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                   "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+                 :
+                 : "memory");
+}
+
 template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1, int BIASB = 4 * D>
 struct Mlp2Layout {
     static constexpr int STG_WARP = STGW;
@@ -223,6 +248,9 @@ constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
 #endif
 // MLP2_AGG_MERGED: the aggregator runs its 16 epilogue warps on both phases (32 hidden columns per
 // warp per chunk, the demix layout, then one output k-block each): half the GELU latency per chunk
+#ifndef MLP2_FIN_PREFETCH
+#define MLP2_FIN_PREFETCH 0 // measured neutral (c5: gate 205 -> 202 ms, fusion unchanged, step within noise)
+#endif
 #ifndef MLP2_AGG_MERGED
 #define MLP2_AGG_MERGED 0 // measured slower (c5: agg 356 -> 415 ms)
 #endif
@@ -921,6 +949,74 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             e2ph ^= 1;
             fence_after();
             if (trf) args.trace[512 + it * 4 + 1] = clock64();
+            if constexpr (KB_SEQ && MLP2_FIN_PREFETCH) {
+                // gate / fusion: this warp's 32 columns of every output k-block in order, the TMEM load
+                // of k-block kb + 1 in flight while k-block kb is combined with z (and e) and staged
+                auto fin_block = [&](int kb, uint32_t (&r)[32]) {
+                    const int n0 = kb * 64;
+                    uint8_t* dst = xcur + kb * 16384 + quarter * 4096;
+                    const uint8_t* esrc = xcur + (KBD + kb) * 16384 + quarter * 4096;
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 bb = *reinterpret_cast<const float4*>(bias_s + n0 + half * 32 + i);
+                        const float2 lo = __fadd2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(bb.x, bb.y));
+                        const float2 hi = __fadd2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), make_float2(bb.z, bb.w));
+                        v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int j = half * 4 + jj;
+                        const uint32_t off = uint32_t(lane * 128 + ((j ^ (lane & 7)) * 16));
+                        uint32_t zq[4], eq[4] = {0u, 0u, 0u, 0u};
+                        ld_shared_v4(dst + off, zq);
+                        if (reads_e) ld_shared_v4(esrc + off, eq);
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int i = jj * 8 + 2 * t;
+                            float2 a = make_float2(v[i], v[i + 1]);
+                            const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zq[t]));
+                            if (reads_e) {
+                                const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&eq[t]));
+                                const float2 h = __fmul2_rn(a, make_float2(0.5f, 0.5f));
+                                const float2 g = __ffma2_rn(make_float2(tanh_approx(h.x), tanh_approx(h.y)), make_float2(0.5f, 0.5f),
+                                                            make_float2(0.5f, 0.5f));
+                                a = __ffma2_rn(g, __fadd2_rn(z2, make_float2(-e2.x, -e2.y)), e2);
+                            } else {
+                                a = __fadd2_rn(a, z2);
+                            }
+                            __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
+                            pk[t] = *reinterpret_cast<uint32_t*>(&p);
+                        }
+                        st_shared_v4(dst + off, pk);
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]);
+                        mbar_arrive(&o_full[(it % NXB) * KBD + kb]);
+                    }
+                };
+                uint32_t ra[32], rb[32];
+                tmem_ld32_nw(tmem + lane_off + half * 32, ra);
+                tmem_wait_ld32(ra);
+#pragma unroll
+                for (int kb = 0; kb < KBD; ++kb) {
+                    uint32_t(&cur)[32] = (kb & 1) ? rb : ra;
+                    uint32_t(&nxt)[32] = (kb & 1) ? ra : rb;
+                    if (kb + 1 < KBD) {
+                        tmem_ld32_nw(tmem + lane_off + (kb + 1) * 64 + half * 32, nxt);
+                    } else {
+                        fence_before();
+                        release(L_a2_empty); // every acc2 load of this warp has completed
+                    }
+                    fin_block(kb, cur);
+                    if (kb + 1 < KBD) tmem_wait_ld32(nxt);
+                }
+                if (trf) args.trace[512 + it * 4 + 2] = clock64();
+                continue;
+            }
 #pragma unroll 1
             for (int kb = KB_SEQ ? 0 : fsub; kb < KBD; kb += KB_SEQ ? 1 : FIN_STRIDE) {
                 const int n0 = kb * 64;
