@@ -231,7 +231,7 @@ struct Mlp2Layout {
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
     static constexpr int TOTAL = BAR_OFF + 512 + BIASB + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
-    static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 8 + 2 + 2 + NXB * (D / 64)) * 8 + 4 <= 512, "barrier block");
+    static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 8 + 2 + 2 + NXB * (D / 64) + 1) * 8 + 4 <= 512, "barrier block");
     static_assert(D % 32 == 0 && D <= 256 && W2_HALF <= SLOT, "output width must be <= 256");
     static_assert(KB1 % W1_PER_SLOT == 0, "input width must be a multiple of 128");
 };
@@ -250,6 +250,16 @@ constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
 // warp per chunk, the demix layout, then one output k-block each): half the GELU latency per chunk
 #ifndef MLP2_FIN_PREFETCH
 #define MLP2_FIN_PREFETCH 0 // measured neutral (c5: gate 205 -> 202 ms, fusion unchanged, step within noise)
+#endif
+// MLP2_FUSE_FOLDZ: the fusion's residual z enters acc2 before the tile's first MMA2 (the final
+// warps tcgen05.st it as fp32 right after draining the previous tile), the output leaves from
+// registers, so the whole row tile is free once the tile's last MMA1 has read it and the next
+// tile's rows load during the last chunks instead of after the final epilogue
+// Measured neutral (c5 fusion 197 -> 199 ms): the transition shrinks (last MMA1 -> next first MMA1
+// 12.4k -> 5.6k cycles), but the final warps' drain + per-row 16-byte global stores + z load take
+// ~9k cycles and the next tile's first MMA2 waits for them (tests/trace_mlp.py)
+#ifndef MLP2_FUSE_FOLDZ
+#define MLP2_FUSE_FOLDZ 0
 #endif
 #ifndef MLP2_AGG_MERGED
 #define MLP2_AGG_MERGED 0 // measured slower (c5: agg 356 -> 415 ms)
@@ -413,7 +423,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
     uint64_t* o_full = a2_empty + 1;    // [NXB][KBD] output block staged in X k-block kb (4 quarter warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + NXB * KBD);
+    uint64_t* z_ready = o_full + NXB * KBD; // FOLDZ: the tile's first MMA1 done (its z k-blocks landed), both CTAs
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(z_ready + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
@@ -464,7 +475,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
 #ifndef MLP2_ZREG
 #define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
 #endif
-    constexpr bool XST = !(reads_z && MLP2_ZREG); // output staged in X (demix: e in the spent Z tile)
+    constexpr bool FOLDZ = MLP2_FUSE_FOLDZ && EPK == EP_RESID && NXB == 1;
+    constexpr bool XST = !(reads_z && MLP2_ZREG) && !FOLDZ; // output staged in X (demix: e in the spent Z tile)
     // gate / fusion: the 8 final warps walk the output k-blocks together (each warp one 32-column half
     // of every k-block), so k-block 0 is staged, stored and refilled first and the next tile's first
     // MMA1 is fed k-block by k-block instead of in two rounds
@@ -475,7 +487,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // output k-blocks are refilled by the X producer itself after storing them (o_full)
         for (int kb = 0; kb < NXB * KB1; ++kb) {
             mbar_init(&x_full[kb], 1);
-            mbar_init(&x_empty[kb], 1 + ((reads_e && kb % KB1 >= KBD) || (!XST && reads_z && kb % KB1 < KBD) ? O_ARRIVALS : 0));
+            mbar_init(&x_empty[kb], 1 + (FOLDZ ? (kb % KB1 < KBD ? 8 : 0)
+                                               : ((reads_e && kb % KB1 >= KBD) || (!XST && reads_z && kb % KB1 < KBD) ? O_ARRIVALS : 0)));
         }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
@@ -486,6 +499,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         mbar_init(a2_full, 1);
         mbar_init(a2_empty, A2_ARRIVALS);
         for (int kb = 0; kb < NXB * KBD; ++kb) mbar_init(&o_full[kb], O_ARRIVALS);
+        mbar_init(z_ready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -671,6 +685,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             if (el) mma_commit_2sm(&r_empty[slot]);
                         }
                         if (el) mma_commit_2sm(&a1_full[b]);
+                        if (FOLDZ && c == 0)
+                            if (el) mma_commit_2sm(z_ready); // this tile's z k-blocks are in both CTAs
                         if (c == NC - 1)
                             for (int kb = 0; kb < KB1; ++kb) if (el) mma_commit_2sm(&x_empty[xb * KB1 + kb]);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 7] = clock64();
@@ -700,7 +716,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                     mbar_wait(&h_full[HG * b + 2 * g + j], (hph >> b) & 1u);
                                     fence_after();
                                     if (g == 0 && j == 0 && c == 0) {
-                                        mbar_wait(a2_empty, a2ph ^ 1);
+                                        mbar_wait(a2_empty, FOLDZ ? a2ph : a2ph ^ 1); // FOLDZ: acc2 = this tile's z first
                                         a2ph ^= 1;
                                         fence_after();
                                     }
@@ -723,7 +739,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                 mbar_wait(&h_full[HG * b + g], (hph >> b) & 1u);
                                 fence_after();
                                 if (g == 0 && c == 0) {
-                                    mbar_wait(a2_empty, a2ph ^ 1);
+                                    mbar_wait(a2_empty, FOLDZ ? a2ph : a2ph ^ 1); // FOLDZ: acc2 = this tile's z first
                                     a2ph ^= 1;
                                     fence_after();
                                 }
@@ -749,7 +765,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             if (g == 0) {
                                 if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
                                 if (c == 0) {
-                                    mbar_wait(a2_empty, a2ph ^ 1);
+                                    mbar_wait(a2_empty, FOLDZ ? a2ph : a2ph ^ 1); // FOLDZ: acc2 = this tile's z first
                                     a2ph ^= 1;
                                     fence_after();
                                 }
@@ -763,7 +779,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                     fence_after();
                                 }
                                 const uint64_t db = sw128_desc(ring + slots[kb] * Lay::SLOT);
-                                if (el) mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, (c | kb | g) != 0);
+                                if (el) mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, FOLDZ || (c | kb | g) != 0);
                                 if (g == MLP2_GG - 1) if (el) mma_commit_2sm(&r_empty[slots[kb]]);
                             }
                         }
@@ -785,6 +801,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         uint32_t e1ph = 0, e2ph = 0; // e1ph bit b: phase of a1_full[b]
+        uint32_t zph = 0;            // FOLDZ: phase of z_ready
         const Epi& ep = args.ep;
         auto release = [&](uint32_t leader_bar) { // elected remote arrive once the whole warp is done
             __syncwarp();
@@ -945,6 +962,66 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             uint8_t* xcur = xs + (it % NXB) * Lay::X_BYTES; // this tile's row buffer
             const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == MLP2_FIN_WARP0 + 2 && lane == 0;
             if (trf) args.trace[512 + it * 4 + 0] = clock64();
+            if constexpr (FOLDZ) {
+                // acc2 <- z of tile `zt` (fp32): this warp's 32 rows x its 32-column half of every output
+                // k-block, read from the tile's z k-blocks in X; then acc2 is handed to MMA2
+                auto zinit = [&](int zt) {
+                    mbar_wait(z_ready, zph);
+                    zph ^= 1;
+                    fence_after();
+                    const int zit = (zt - pair) / npairs;
+                    const uint8_t* xz = xs + (zit % NXB) * Lay::X_BYTES + quarter * 4096;
+#pragma unroll
+                    for (int kb = 0; kb < KBD; ++kb) {
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj) {
+                            const int j = half * 4 + jj;
+                            uint32_t zq[4], zf[8];
+                            ld_shared_v4(xz + kb * 16384 + lane * 128 + ((j ^ (lane & 7)) * 16), zq);
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) { // bf16 pair -> two fp32 (exact)
+                                zf[2 * t] = zq[t] << 16;
+                                zf[2 * t + 1] = zq[t] & 0xFFFF0000u;
+                            }
+                            tmem_st8(tmem + lane_off + kb * 64 + half * 32 + jj * 8, zf);
+                        }
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int kb = 0; kb < KBD; ++kb) mbar_arrive(&x_empty[(zit % NXB) * KB1 + kb]); // z read
+                    release(L_a2_empty); // acc2 = z: the tile's first MMA2 may accumulate onto it
+                };
+                if (tile == pair) zinit(tile);
+                mbar_wait(a2_full, e2ph);
+                e2ph ^= 1;
+                fence_after();
+                uint32_t ra[32];
+#pragma unroll 1
+                for (int kb = 0; kb < KBD; ++kb) {
+                    const int n0 = kb * 64 + half * 32;
+                    tmem_ld32_nw(tmem + lane_off + n0, ra);
+                    tmem_wait_ld32(ra);
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 bb = *reinterpret_cast<const float4*>(bias_s + n0 + i);
+                        const float2 lo = __fadd2_rn(make_float2(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1])), make_float2(bb.x, bb.y));
+                        const float2 hi = __fadd2_rn(make_float2(__uint_as_float(ra[i + 2]), __uint_as_float(ra[i + 3])), make_float2(bb.z, bb.w));
+                        __nv_bfloat162 p0 = __floats2bfloat162_rn(lo.x, lo.y), p1 = __floats2bfloat162_rn(hi.x, hi.y);
+                        pk[i / 2] = *reinterpret_cast<uint32_t*>(&p0);
+                        pk[i / 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
+                    }
+                    if (m0w + lane < ep.M) { // this row's 64 bytes of the k-block half
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(ep.out_t) + size_t(m0w + lane) * ep.ldo + n0);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    }
+                }
+                if (tile + npairs < args.tiles) zinit(tile + npairs); // drained above (waited loads): the next tile's z
+                continue;
+            }
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
             fence_after();
