@@ -208,6 +208,9 @@ __device__ __forceinline__ void tmem_wait_ld32(uint32_t (&r)[32]) {
                  : "memory");
 }
 
+#ifndef MLP2_NS_CAP
+#define MLP2_NS_CAP 16 // weight-ring slots at most (else as many as the shared memory holds)
+#endif
 template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1, int BIASB = 4 * D>
 struct Mlp2Layout {
     static constexpr int STG_WARP = STGW;
@@ -225,7 +228,7 @@ struct Mlp2Layout {
     // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
     static constexpr int STG_BYTES = KIN == D ? EW * STGW : 0;
     static constexpr int NS_RAW = (SMEM_LIMIT - FIXED - NXB * X_BYTES - STG_BYTES) / SLOT;
-    static constexpr int NS = NS_RAW > 16 ? 16 : NS_RAW;
+    static constexpr int NS = NS_RAW > MLP2_NS_CAP ? MLP2_NS_CAP : NS_RAW;
     static constexpr int STG_OFF = NXB * X_BYTES;
     static constexpr int R_OFF = NXB * X_BYTES + STG_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
