@@ -92,12 +92,23 @@ typedef struct {
 
 /* Per-bin slice of ura::RefineTrace (refine.hpp:48-54); every pointer nullable.
  * remask_rows / remask_steps are B x CIDER_MAX_THRESHOLDS (0 where a stage did not run);
- * remask_mask is B x K (1 = row re-decoded by the last remask stage that ran). */
+ * remask_mask is B x K (1 = row re-decoded by the last remask stage that ran).
+ * The reference's per-pass records: pass_first_reveals (B x (1 + CIDER_MAX_THRESHOLDS), the t = 1
+ * reveal count of every pass run, in order; n_passes[b] of them are valid) = pass_first_reveals;
+ * reveal_counts (B x max_steps, per step of the most recent pass, zero past its n_reveal_counts[b]
+ * steps) = reveal_counts; first_step_sites (B x K x L, 1 = revealed at t = 1 of the most recent
+ * pass) = first_step_sites as a mask (the reference lists the same (row, slot) pairs in row-major order). */
 typedef struct {
     int32_t* first_reveals; /* B: reveal count of the first pass's t=1 step */
     int32_t* remask_rows;
     int32_t* remask_steps;
     int32_t* remask_mask;
+    int32_t* pass_first_reveals;
+    int32_t* n_passes;
+    int max_steps;
+    int32_t* reveal_counts;
+    int32_t* n_reveal_counts;
+    uint8_t* first_step_sites;
 } cider_trace;
 
 /* ---- weights (A15) -------------------------------------------------------------------- */
@@ -130,6 +141,16 @@ int cider_denoise(cider_ctx* ctx, int B, int K, const int32_t* X, const float* S
  * final (gamma = 0) pass, as run_refinement's final_pass_logits out-param. */
 int cider_refine(cider_ctx* ctx, int B, int K, const float* S, const cider_schedule* sched,
                  const cider_remask* remask, int32_t* grid, float* final_logits, cider_trace* trace);
+
+/* Teacher-forcing probe (test / diagnostic entry point): cider_refine over B host bins
+ * (remask NONE or RANK) as ONE device chunk, recording for the n_probe bins probe_bins[] every denoiser
+ * forward's input grid and output logits and every pass's output grid, in execution order. Record r
+ * (r < *n_records <= max_records): meta[r] = {pass, t, steps, kind}; kind 0 = the forward of step t,
+ * 1 = the gamma = 0 forward, 2 = the pass output after the final argmax (no logits). probe_X:
+ * n_probe x max_records x K x L; probe_logits (nullable): n_probe x max_records x K x L x Q. */
+int cider_refine_probe(cider_ctx* ctx, int B, int K, const float* S, const cider_schedule* sched,
+                       const cider_remask* remask, int32_t* grid, int n_probe, const int32_t* probe_bins,
+                       int max_records, int32_t* meta, int32_t* probe_X, float* probe_logits, int* n_records);
 
 /* Ragged loads (the protocol's bins carry K_chi in 1..k_max, protocol.cpp:41-88):
  * B bins with loads[b] users each, S: B x L x Q; bins are bucketed by load and each bucket runs as

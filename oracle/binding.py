@@ -34,6 +34,9 @@ def _load(path: str, prefix: str) -> C.CDLL:
     getattr(h, f"{prefix}_last_error").restype = C.c_char_p
     d = getattr(h, f"{prefix}_denoise")
     d.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, P, P, P, P]
+    if prefix == "oracle":
+        h.oracle_denoise_batch.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.c_int, P, P, P,
+                                           C.c_int]
     r = getattr(h, f"{prefix}_refine")
     r.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.POINTER(ScheduleDesc),
                   C.POINTER(RemaskDesc), P, P, P, P, P, P, C.c_int]
@@ -54,6 +57,15 @@ def _load(path: str, prefix: str) -> C.CDLL:
         h.ref_save_parity_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_uint32, C.c_uint64]
         h.ref_load_parity_file.argtypes = [C.c_char_p, C.c_int, P, P, P, P, P, P, P, P]
         h.ref_bp_decode.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, P, C.c_int, C.c_double, C.c_int, P, P, P, P]
+        h.ref_weights_init.argtypes = [C.POINTER(ModelDesc), C.c_uint64, P]
+        h.ref_workload_bins.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_double, C.c_double, C.c_double,
+                                        C.c_uint64, C.c_int64, C.c_int, P, P, C.c_int]
+        h.ref_session_create.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.c_int, P,
+                                         C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), C.c_int, C.POINTER(C.c_void_p)]
+        h.ref_session_advance.argtypes = [P, C.c_int]
+        h.ref_session_status.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), P, P]
+        h.ref_session_destroy.argtypes = [P]
+        h.ref_session_destroy.restype = None
         h.ref_sic_decode.argtypes = [C.c_int, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.c_int, C.c_double, C.c_int,
                                      C.c_double, P, P, P]
     _handles[path] = h
@@ -98,6 +110,20 @@ class Checker:
         self._check(getattr(self.h, f"{self.prefix}_denoise")(C.byref(md), _p(w), C.byref(cd), K, _p(X), _p(S),
                                                               _p(lg), _p(inc)))
         return (lg, inc) if want_incoming else lg
+
+    def denoise_batch(self, model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int,
+                      X: np.ndarray, S: np.ndarray, threads: int = 0) -> np.ndarray:
+        """B independent forwards on `threads` host threads (restatement only): X B x K x L, S B x L x Q
+        -> logits B x K x L x Q (fp64), bit-identical to B denoise() calls."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        cd, _e = code_desc(edges, checks, slots)
+        X = np.ascontiguousarray(X, dtype=np.int32)
+        S = np.ascontiguousarray(S, dtype=np.float64)
+        B, K, L = X.shape
+        lg = np.empty((B, K, L, model.q), dtype=np.float64)
+        md = model.desc()
+        self._check(self.h.oracle_denoise_batch(C.byref(md), _p(w), C.byref(cd), B, K, _p(X), _p(S), _p(lg), threads))
+        return lg
 
     def refine(self, model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int, S: np.ndarray,
                K: int, sched: RevealSchedule, remask: Optional[RemaskConfig] = None, threads: int = 0,
@@ -153,6 +179,28 @@ class Reference(Checker):
         out = np.empty(n, np.float64)
         self._check(self.h.ref_random_init(q, dim, C.c_uint64(seed), _p(out)))
         return out
+
+    def weights_init(self, model: Model, seed: int) -> np.ndarray:
+        """cider.h's flat weight layout drawn with the reference's own seeding (ref_weights_init)."""
+        n = (model.q + 1) * model.dim + 2 * model.q * model.dim
+        D, H = model.dim, model.hidden
+        n += model.layers * ((H * 2 * D + H + D * H + D) * 2 + (H * D + H + D * H + D))
+        if model.heads:
+            n += model.layers * (D + D * D)
+        out = np.empty(n, np.float64)
+        md = model.desc()
+        self._check(self.h.ref_weights_init(C.byref(md), C.c_uint64(seed), _p(out)))
+        return out
+
+    def workload_bins(self, wl, edges: np.ndarray, first: int, n: int, threads: int = 0):
+        """The BASELINE evidence model over the reference's own sample_codewords (ref_workload_bins):
+        (truth n x K x L, S n x L x Q fp64 holding fp32-rounded values)."""
+        cd, _e = code_desc(edges, wl.checks, wl.slots)
+        truth = np.empty((n, wl.k, wl.slots), np.int32)
+        S = np.empty((n, wl.slots, 1 << wl.m), np.float64)
+        self._check(self.h.ref_workload_bins(wl.m, C.byref(cd), wl.k, wl.snr_db, wl.p_erase, wl.p_false,
+                                             C.c_uint64(wl.master_seed), first, n, _p(truth), _p(S), threads))
+        return truth, S
 
     def build_ldpc(self, m: int, slots: int, checks: int, col_weight: int, seed: int) -> np.ndarray:
         e = np.empty((slots * col_weight, 3), np.int32)
@@ -254,6 +302,46 @@ class Reference(Checker):
         f.restype = C.c_double
         f.argtypes = [C.c_double, C.c_int, C.c_int]
         return f(eb_db, payload_bits, slots)
+
+
+class RefSession:
+    """Decodes through the reference's own engine (ura::run_refinement + MaxProbScorer + remask_pass,
+    ref_shim's refine_one) on `threads` host threads, paused between denoiser forwards: advance(n) lets
+    every worker run n more forwards and returns when all are parked (bench.py's reference arm)."""
+
+    def __init__(self, ref: "Reference", model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int,
+                 K: int, S: np.ndarray, sched: RevealSchedule, remask: Optional[RemaskConfig], threads: int):
+        self.ref = ref
+        self._w = np.ascontiguousarray(weights, np.float64)
+        self._S = np.ascontiguousarray(S, np.float64)
+        self.cd, self._e = code_desc(edges, checks, slots)
+        self.n, self.K, self.L = self._S.shape[0], K, slots
+        md, sd, rd = model.desc(), sched.desc(), (remask or RemaskConfig()).desc()
+        h = C.c_void_p()
+        ref._check(ref.h.ref_session_create(C.byref(md), _p(self._w), C.byref(self.cd), K, self.n, _p(self._S),
+                                            C.byref(sd), C.byref(rd), threads, C.byref(h)))
+        self.h = h
+
+    def advance(self, n: int = 1):
+        self.ref._check(self.ref.h.ref_session_advance(self.h, n))
+
+    def status(self):
+        f, b = C.c_int64(), C.c_int64()
+        grids = np.empty((self.n, self.K, self.L), np.int32)
+        done = np.empty(self.n, np.int32)
+        self.ref._check(self.ref.h.ref_session_status(self.h, C.byref(f), C.byref(b), _p(grids), _p(done)))
+        return {"forwards": f.value, "bins_done": b.value, "grids": grids, "done": done.astype(bool)}
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ref.h.ref_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def derive_seed(master: int, index: int) -> int:

@@ -90,6 +90,60 @@ struct Tanner {
     }
 };
 
+// Speed without changing a single bit: the reference sums every dot product in index order, seeded
+// with its bias; dot4 runs four such chains side by side (instruction-level parallelism only, each
+// chain's operation order unchanged), and par_for spreads independent rows / sites over threads.
+inline void dot4(const double* a0, const double* a1, const double* a2, const double* a3, const double* x, int n,
+                 double* s) {
+    double s0 = s[0], s1 = s[1], s2 = s[2], s3 = s[3];
+    for (int i = 0; i < n; ++i) {
+        const double xi = x[i];
+        s0 += a0[i] * xi;
+        s1 += a1[i] * xi;
+        s2 += a2[i] * xi;
+        s3 += a3[i] * xi;
+    }
+    s[0] = s0; s[1] = s1; s[2] = s2; s[3] = s3;
+}
+inline double dot1(const double* a, const double* x, int n, double s) {
+    for (int i = 0; i < n; ++i) s += a[i] * x[i];
+    return s;
+}
+// rows r of a row-major matrix m (ld) against x, s[r] seeded by init[r] (or 0)
+void matvec(const double* m, size_t ld, int rows, const double* x, int n, const double* init, double* out) {
+    int r = 0;
+    for (; r + 4 <= rows; r += 4) {
+        double s[4] = {init ? init[r] : 0.0, init ? init[r + 1] : 0.0, init ? init[r + 2] : 0.0, init ? init[r + 3] : 0.0};
+        dot4(m + size_t(r) * ld, m + size_t(r + 1) * ld, m + size_t(r + 2) * ld, m + size_t(r + 3) * ld, x, n, s);
+        out[r] = s[0]; out[r + 1] = s[1]; out[r + 2] = s[2]; out[r + 3] = s[3];
+    }
+    for (; r < rows; ++r) out[r] = dot1(m + size_t(r) * ld, x, n, init ? init[r] : 0.0);
+}
+
+thread_local int g_intra = 1; // threads one forward may use (set per call by the C entry points)
+void par_for(int n, const std::function<void(int)>& fn) {
+    const int T = std::min(g_intra, n);
+    if (T <= 1) {
+        for (int i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::atomic<int> next{0};
+    std::exception_ptr err;
+    std::atomic<bool> bad{false};
+    auto work = [&] {
+        for (;;) {
+            int i = next.fetch_add(1);
+            if (i >= n || bad) return;
+            try { fn(i); } catch (...) { if (!bad.exchange(true)) err = std::current_exception(); return; }
+        }
+    };
+    std::vector<std::thread> ts;
+    for (int w = 1; w < T; ++w) ts.emplace_back(work);
+    work();
+    for (auto& t : ts) t.join();
+    if (err) std::rethrow_exception(err);
+}
+
 double gelu(double x) { return 0.5 * x * (1.0 + std::erf(x / std::sqrt(2.0))); } // denoiser.cpp:13
 double sigm(double x) { return 1.0 / (1.0 + std::exp(-x)); }                       // denoiser.cpp:15
 
@@ -99,16 +153,9 @@ struct Mlp {
     // y = W2 gelu(W1 x + b1) + b2, each affine row seeded with its bias (denoiser.cpp:17-34)
     void run(const double* x, double* y) const {
         std::vector<double> h(hid);
-        for (int r = 0; r < hid; ++r) {
-            double s = b1[r];
-            for (int c = 0; c < in; ++c) s += w1[size_t(r) * in + c] * x[c];
-            h[r] = gelu(s);
-        }
-        for (int r = 0; r < out; ++r) {
-            double s = b2[r];
-            for (int c = 0; c < hid; ++c) s += w2[size_t(r) * hid + c] * h[c];
-            y[r] = s;
-        }
+        matvec(w1, size_t(in), hid, x, in, b1, h.data());
+        for (int r = 0; r < hid; ++r) h[r] = gelu(h[r]);
+        matvec(w2, size_t(hid), out, h.data(), hid, b2, y);
     }
 };
 
@@ -157,11 +204,7 @@ struct Net {
 void coeff_act(const Net& n, const Field& f, const double* x, int alpha, double* out) {
     if (!alpha) throw std::domain_error("coeff_action: alpha must be nonzero");
     std::vector<double> sym(n.q), perm(n.q, 0.0);
-    for (int a = 0; a < n.q; ++a) {
-        double s = 0.0;
-        for (int i = 0; i < n.D; ++i) s += n.w(a)[i] * x[i];
-        sym[a] = s;
-    }
+    matvec(n.W, size_t(n.D), n.q, x, n.D, nullptr, sym.data());
     for (int a = 0; a < n.q; ++a) perm[f.mul(alpha, a)] = sym[a];
     std::fill(out, out + n.D, 0.0);
     for (int a = 0; a < n.q; ++a) {
@@ -170,12 +213,16 @@ void coeff_act(const Net& n, const Field& f, const double* x, int alpha, double*
     }
 }
 
-// One denoiser forward, Z is K x L x D row-major (denoiser.cpp:71-259 restated).
+// One denoiser forward, Z is K x L x D row-major (denoiser.cpp:71-259 restated). Sites, slots
+// and (row, check) pairs are independent, so they run under par_for; Module B's messages are
+// produced per (row, check) into per-edge buffers and then summed into each slot sequentially in
+// the reference's (row, check, edge) order, so the result is bit-identical at any thread count.
 void forward(const Net& n, const Field& f, const Tanner& t, int K, const int* X, const double* S,
              double* logits, double* incoming) {
     const int L = t.L, Q = n.q, D = n.D;
     const size_t KL = size_t(K) * L;
-    std::vector<double> Z(KL * D), Zt(KL * D), e(KL * D), acc(KL * D);
+    const int NE = int(t.slot.size());
+    std::vector<double> Z(KL * D), Zt(KL * D), e(KL * D), acc(KL * D), msgs(size_t(K) * NE * D);
     // embed_grid (denoiser.cpp:71-84)
     for (size_t s = 0; s < KL; ++s) {
         int tok = X[s];
@@ -183,21 +230,19 @@ void forward(const Net& n, const Field& f, const Tanner& t, int K, const int* X,
         int row = tok == -1 ? Q : tok;
         std::copy(n.E + size_t(row) * D, n.E + size_t(row + 1) * D, Z.begin() + s * D);
     }
-    std::vector<double> lbar(KL * Q), r(KL * Q), ex(K), srt(K);
-    std::vector<double> cat(2 * D), g(D), pooled(D), mapped(D), msg(D);
+    std::vector<double> lbar(KL * Q), r(KL * Q);
     for (int li = 0; li < n.N; ++li) {
         const Layer& Ly = n.layer[li];
         // intermediate logits (denoiser.cpp:86-101)
-        for (size_t s = 0; s < KL; ++s) {
-            int l = int(s % L);
-            for (int a = 0; a < Q; ++a) {
-                double acc0 = 0.0;
-                for (int i = 0; i < D; ++i) acc0 += n.w(a)[i] * Z[s * D + i];
-                lbar[s * Q + a] = acc0 + n.beta * S[size_t(l) * Q + a];
-            }
-        }
+        par_for(int(KL), [&](int si) {
+            const size_t s = size_t(si);
+            const int l = int(s % L);
+            matvec(n.W, size_t(D), Q, &Z[s * D], D, nullptr, &lbar[s * Q]);
+            for (int a = 0; a < Q; ++a) lbar[s * Q + a] = lbar[s * Q + a] + n.beta * S[size_t(l) * Q + a];
+        });
         // demixing softmax over rows, normaliser summed in descending order (denoiser.cpp:103-122)
-        for (int l = 0; l < L; ++l)
+        par_for(L, [&](int l) {
+            std::vector<double> ex(K), srt(K);
             for (int a = 0; a < Q; ++a) {
                 double mx = lbar[size_t(l) * Q + a];
                 for (int k = 1; k < K; ++k) mx = std::max(mx, lbar[(size_t(k) * L + l) * Q + a]);
@@ -208,88 +253,90 @@ void forward(const Net& n, const Field& f, const Tanner& t, int K, const int* X,
                 for (double v : srt) den += v;
                 for (int k = 0; k < K; ++k) r[(size_t(k) * L + l) * Q + a] = ex[k] / den;
             }
-        // evidence embedding (denoiser.cpp:124-139)
-        std::fill(e.begin(), e.end(), 0.0);
-        for (size_t s = 0; s < KL; ++s) {
-            int l = int(s % L);
+        });
+        // evidence embedding (denoiser.cpp:124-139) and gated fusion (denoiser.cpp:141-160), per site
+        par_for(int(KL), [&](int si) {
+            const size_t s = size_t(si);
+            const int l = int(s % L);
+            double* es = &e[s * D];
+            std::fill(es, es + D, 0.0);
             for (int a = 0; a < Q; ++a) {
                 double wgt = r[s * Q + a] * S[size_t(l) * Q + a];
                 if (wgt == 0.0) continue;
-                for (int i = 0; i < D; ++i) e[s * D + i] += wgt * n.V[size_t(a) * D + i];
+                for (int i = 0; i < D; ++i) es[i] += wgt * n.V[size_t(a) * D + i];
             }
-        }
-        // gated fusion (denoiser.cpp:141-160)
-        for (size_t s = 0; s < KL; ++s) {
+            std::vector<double> cat(2 * D), g(D);
             std::copy(&Z[s * D], &Z[s * D] + D, cat.begin());
-            std::copy(&e[s * D], &e[s * D] + D, cat.begin() + D);
+            std::copy(es, es + D, cat.begin() + D);
             Ly.gate.run(cat.data(), g.data());
             for (int i = 0; i < D; ++i) g[i] = sigm(g[i]);
-            for (int i = 0; i < D; ++i) Zt[s * D + i] = g[i] * Z[s * D + i] + (1.0 - g[i]) * e[s * D + i];
-        }
+            for (int i = 0; i < D; ++i) Zt[s * D + i] = g[i] * Z[s * D + i] + (1.0 - g[i]) * es[i];
+        });
         // parity-aware propagation (denoiser.cpp:181-228); heads>0: extrinsic pooling attention
-        std::fill(acc.begin(), acc.end(), 0.0);
         const int dh = n.heads ? D / n.heads : D;
-        for (int k = 0; k < K; ++k)
-            for (int j = 0; j < t.P; ++j) {
-                const int b0 = t.cbeg[j], d = t.cbeg[j + 1] - t.cbeg[j];
-                std::vector<double> nv(size_t(d) * D), sc(size_t(d) * std::max(1, n.heads));
+        par_for(K * t.P, [&](int kj) {
+            const int k = kj / t.P, j = kj % t.P;
+            const int b0 = t.cbeg[j], d = t.cbeg[j + 1] - t.cbeg[j];
+            std::vector<double> nv(size_t(d) * D), sc(size_t(d) * std::max(1, n.heads));
+            std::vector<double> pooled(D), mapped(D), kv(dh);
+            for (int i = 0; i < d; ++i)
+                coeff_act(n, f, &Zt[(size_t(k) * L + t.slot[b0 + i]) * D], t.coef[b0 + i], &nv[size_t(i) * D]);
+            if (n.heads) {
+                const double scale = 1.0 / std::sqrt(double(dh));
                 for (int i = 0; i < d; ++i)
-                    coeff_act(n, f, &Zt[(size_t(k) * L + t.slot[b0 + i]) * D], t.coef[b0 + i], &nv[size_t(i) * D]);
-                if (n.heads) {
-                    const double scale = 1.0 / std::sqrt(double(dh));
-                    for (int i = 0; i < d; ++i)
-                        for (int h = 0; h < n.heads; ++h) {
-                            double s = 0.0;
-                            for (int o = h * dh; o < (h + 1) * dh; ++o) {
-                                double kv = 0.0;
-                                for (int c = 0; c < D; ++c) kv += Ly.ak[size_t(o) * D + c] * nv[size_t(i) * D + c];
-                                s += Ly.aq[o] * kv;
-                            }
-                            sc[size_t(i) * n.heads + h] = s * scale;
-                        }
-                }
-                for (int i = 0; i < d; ++i) {
-                    std::fill(pooled.begin(), pooled.end(), 0.0);
-                    if (!n.heads) {
+                    for (int h = 0; h < n.heads; ++h) {
+                        matvec(Ly.ak + size_t(h) * dh * D, size_t(D), dh, &nv[size_t(i) * D], D, nullptr, kv.data());
+                        double s = 0.0;
+                        for (int o = 0; o < dh; ++o) s += Ly.aq[h * dh + o] * kv[o];
+                        sc[size_t(i) * n.heads + h] = s * scale;
+                    }
+            }
+            for (int i = 0; i < d; ++i) {
+                std::fill(pooled.begin(), pooled.end(), 0.0);
+                if (!n.heads) {
+                    for (int i2 = 0; i2 < d; ++i2) {
+                        if (i2 == i) continue;
+                        for (int o = 0; o < D; ++o) pooled[o] += nv[size_t(i2) * D + o];
+                    }
+                } else {
+                    for (int h = 0; h < n.heads; ++h) {
+                        double mx = -INFINITY, den = 0.0;
+                        for (int i2 = 0; i2 < d; ++i2)
+                            if (i2 != i) mx = std::max(mx, sc[size_t(i2) * n.heads + h]);
+                        for (int i2 = 0; i2 < d; ++i2)
+                            if (i2 != i) den += std::exp(sc[size_t(i2) * n.heads + h] - mx);
                         for (int i2 = 0; i2 < d; ++i2) {
                             if (i2 == i) continue;
-                            for (int o = 0; o < D; ++o) pooled[o] += nv[size_t(i2) * D + o];
-                        }
-                    } else {
-                        for (int h = 0; h < n.heads; ++h) {
-                            double mx = -INFINITY, den = 0.0;
-                            for (int i2 = 0; i2 < d; ++i2)
-                                if (i2 != i) mx = std::max(mx, sc[size_t(i2) * n.heads + h]);
-                            for (int i2 = 0; i2 < d; ++i2)
-                                if (i2 != i) den += std::exp(sc[size_t(i2) * n.heads + h] - mx);
-                            for (int i2 = 0; i2 < d; ++i2) {
-                                if (i2 == i) continue;
-                                double wgt = double(d - 1) * std::exp(sc[size_t(i2) * n.heads + h] - mx) / den;
-                                for (int o = h * dh; o < (h + 1) * dh; ++o) pooled[o] += wgt * nv[size_t(i2) * D + o];
-                            }
+                            double wgt = double(d - 1) * std::exp(sc[size_t(i2) * n.heads + h] - mx) / den;
+                            for (int o = h * dh; o < (h + 1) * dh; ++o) pooled[o] += wgt * nv[size_t(i2) * D + o];
                         }
                     }
-                    Ly.agg.run(pooled.data(), mapped.data());
-                    coeff_act(n, f, mapped.data(), f.inv(t.coef[b0 + i]), msg.data());
-                    double* dst = &acc[(size_t(k) * L + t.slot[b0 + i]) * D];
-                    for (int o = 0; o < D; ++o) dst[o] += msg[o];
                 }
+                Ly.agg.run(pooled.data(), mapped.data());
+                coeff_act(n, f, mapped.data(), f.inv(t.coef[b0 + i]), &msgs[(size_t(k) * NE + b0 + i) * D]);
+            }
+        });
+        std::fill(acc.begin(), acc.end(), 0.0);
+        for (int k = 0; k < K; ++k)
+            for (int ed = 0; ed < NE; ++ed) { // edges are sorted by (check, slot): the reference's order
+                const double* msg = &msgs[(size_t(k) * NE + ed) * D];
+                double* dst = &acc[(size_t(k) * L + t.slot[ed]) * D];
+                for (int o = 0; o < D; ++o) dst[o] += msg[o];
             }
         if (incoming) std::copy(acc.begin(), acc.end(), incoming + size_t(li) * KL * D);
-        for (size_t s = 0; s < KL; ++s) {
+        par_for(int(KL), [&](int si) {
+            const size_t s = size_t(si);
+            std::vector<double> cat(2 * D), g(D);
             std::copy(&Zt[s * D], &Zt[s * D] + D, cat.begin());
             std::copy(&acc[s * D], &acc[s * D] + D, cat.begin() + D);
             Ly.fuse.run(cat.data(), g.data());
             for (int i = 0; i < D; ++i) Z[s * D + i] = Zt[s * D + i] + g[i];
-        }
+        });
     }
     // final logits (denoiser.cpp:230-245)
-    for (size_t s = 0; s < KL; ++s)
-        for (int a = 0; a < Q; ++a) {
-            double v = 0.0;
-            for (int i = 0; i < D; ++i) v += n.w(a)[i] * Z[s * D + i];
-            logits[s * Q + a] = v;
-        }
+    par_for(int(KL), [&](int si) {
+        matvec(n.W, size_t(D), Q, &Z[size_t(si) * D], D, nullptr, &logits[size_t(si) * Q]);
+    });
 }
 
 // ---- the engine (refine.cpp:11-292 restated) ---------------------------------------------
@@ -502,15 +549,19 @@ int guarded(F&& fn) {
     }
 }
 
+// n independent jobs over `threads` workers (0 = all cores); when there are fewer jobs than
+// threads, each job's forwards get the spare threads (g_intra)
 void pool_for(int n, int threads, const std::function<void(int)>& fn) {
     if (threads <= 0) threads = int(std::max(1u, std::thread::hardware_concurrency()));
-    threads = std::min(threads, std::max(n, 1));
+    const int workers = std::min(threads, std::max(n, 1));
+    const int intra = std::max(1, threads / std::max(workers, 1));
     std::atomic<int> next{0};
     std::exception_ptr err;
     std::atomic<bool> bad{false};
     std::vector<std::thread> ts;
-    for (int w = 0; w < threads; ++w)
+    for (int w = 0; w < workers; ++w)
         ts.emplace_back([&] {
+            g_intra = intra;
             for (;;) {
                 int i = next.fetch_add(1);
                 if (i >= n || bad) return;
@@ -546,6 +597,20 @@ int oracle_denoise(const cider_model_desc* md, const double* weights, const cide
         Tanner t(code, f.q);
         std::vector<double> lam(size_t(K) * t.L * f.q);
         forward(n, f, t, K, X, S, logits ? logits : lam.data(), incoming);
+    });
+}
+
+// B independent forwards (X: B x K x L, S: B x L x Q, logits: B x K x L x Q) on `threads` threads
+int oracle_denoise_batch(const cider_model_desc* md, const double* weights, const cider_code_desc* code, int B,
+                         int K, const int32_t* X, const double* S, double* logits, int threads) {
+    return guarded([&] {
+        Net n(md, weights);
+        Field f(md->m, md->prim_poly);
+        Tanner t(code, f.q);
+        const size_t nx = size_t(K) * t.L, nq = nx * f.q;
+        pool_for(B, threads, [&](int b) {
+            forward(n, f, t, K, X + size_t(b) * nx, S + size_t(b) * t.L * f.q, logits + size_t(b) * nq, nullptr);
+        });
     });
 }
 

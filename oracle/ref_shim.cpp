@@ -12,7 +12,12 @@
 // module_a / module_b / final_logits per layer with shared E, W, V; heads>0 swaps Module B's
 // sum-pool Psi for the extrinsic pooling attention defined in DESIGN.md §2, built from the
 // reference's coeff_action (denoiser.cpp:162-179) and TwoLayerMap::apply_gelu (denoiser.cpp:29-34).
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
+#include <random>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -240,9 +245,10 @@ std::vector<double> rank_confidences(const std::vector<double>& conf, int k_low)
 void refine_one(const Model& model, const ura::GfContext& gf, const ura::ParityCheckMatrix& h,
                 int K, const double* S, const cider_schedule* sc, const cider_remask* rm,
                 int32_t* grid, double* final_logits, int32_t* first, int32_t* rows,
-                int32_t* steps, int32_t* mask) {
+                int32_t* steps, int32_t* mask, const ura::Denoiser* den_override = nullptr) {
     const int q = model.q, L = h.slots();
-    StackedDenoiser den(gf, model);
+    StackedDenoiser stacked(gf, model);
+    const ura::Denoiser& den = den_override ? *den_override : stacked;
     ura::EvidenceMatrix s(L, q);
     std::copy(S, S + size_t(L) * q, s.v.begin());
     ura::RevealSchedule sched;
@@ -294,9 +300,218 @@ void refine_one(const Model& model, const ura::GfContext& gf, const ura::ParityC
     if (mask) std::copy(last_mask.begin(), last_mask.end(), mask);
 }
 
+// ---- the reference arm of bench.py: decodes paused between forwards ------------------------------
+// A decode of a config-3/5 bin is 22 fp64 forwards of ~9 s each; bench.py must time bounded steps.
+// Each worker thread decodes its bins with the reference's own engine (refine_one above:
+// ura::run_refinement + MaxProbScorer + ura::remask_pass), through a Denoiser whose logits() waits for
+// a token: ref_session_advance grants every worker n forwards and returns once all of them are
+// parked again, so K bench steps time exactly the reference's decode work of those forwards.
+struct Session;
+class GatedDenoiser : public ura::Denoiser {
+public:
+    GatedDenoiser(Session& s, int w, const ura::Denoiser& inner) : s_(s), w_(w), inner_(inner) {}
+    ura::LogitGrid logits(const ura::MaskedGrid& x, const ura::EvidenceMatrix& ev, const ura::ParityCheckMatrix& h,
+                          double r) const override;
+
+private:
+    Session& s_;
+    int w_;
+    const ura::Denoiser& inner_;
+};
+
+struct Stopped : std::exception {};
+
+struct Session {
+    enum State { RUNNING, PARKED, EXITED };
+    Model model;
+    ura::GfContext gf;
+    ura::ParityCheckMatrix h;
+    int K, L, q, n_bins, threads;
+    cider_schedule sched;
+    cider_remask remask;
+    std::vector<double> S;
+    std::vector<int32_t> grids;
+    std::vector<char> done;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<int> tokens;
+    std::vector<State> state;
+    bool stop = false;
+    int64_t forwards = 0, bins_done = 0;
+    std::string error;
+    std::vector<std::thread> workers;
+
+    Session(const cider_model_desc* md, const double* w, const cider_code_desc* code, int K_, int n, const double* S_,
+            const cider_schedule* sc, const cider_remask* rm, int threads_)
+        : model(md, w), gf(make_gf(md)), h(make_h(1 << md->m, code)), K(K_), L(code->slots), q(1 << md->m), n_bins(n),
+          threads(threads_), sched(*sc), remask(rm ? *rm : cider_remask{}), S(S_, S_ + size_t(n) * code->slots * (1 << md->m)),
+          grids(size_t(n) * K_ * code->slots, -1), done(n, 0), tokens(threads_, 0), state(threads_, RUNNING) {
+        for (int t = 0; t < threads; ++t) workers.emplace_back([this, t] { run(t); });
+    }
+    ~Session() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : workers) t.join();
+    }
+    void run(int t) {
+        StackedDenoiser inner(gf, model);
+        GatedDenoiser den(*this, t, inner);
+        try {
+            for (int b = t; b < n_bins; b += threads) {
+                refine_one(model, gf, h, K, S.data() + size_t(b) * L * q, &sched, &remask, grids.data() + size_t(b) * K * L,
+                           nullptr, nullptr, nullptr, nullptr, nullptr, &den);
+                std::lock_guard<std::mutex> lk(mu);
+                done[b] = 1;
+                ++bins_done;
+            }
+        } catch (const Stopped&) {
+        } catch (const std::exception& e) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (error.empty()) error = e.what();
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        state[t] = EXITED;
+        tokens[t] = 0;
+        cv.notify_all();
+    }
+    bool all_parked() const {
+        for (int t = 0; t < threads; ++t)
+            if (!(state[t] == EXITED || (state[t] == PARKED && tokens[t] == 0))) return false;
+        return true;
+    }
+    void advance(int n) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return all_parked(); });
+        for (int t = 0; t < threads; ++t)
+            if (state[t] != EXITED) tokens[t] += n;
+        cv.notify_all();
+        cv.wait(lk, [&] { return all_parked(); });
+        if (!error.empty()) throw std::runtime_error(error);
+    }
+};
+
+ura::LogitGrid GatedDenoiser::logits(const ura::MaskedGrid& x, const ura::EvidenceMatrix& ev,
+                                     const ura::ParityCheckMatrix& h, double r) const {
+    {
+        std::unique_lock<std::mutex> lk(s_.mu);
+        s_.state[w_] = Session::PARKED;
+        s_.cv.notify_all();
+        s_.cv.wait(lk, [&] { return s_.stop || s_.tokens[w_] > 0; });
+        if (s_.stop) throw Stopped();
+        --s_.tokens[w_];
+        s_.state[w_] = Session::RUNNING;
+    }
+    ura::LogitGrid out = inner_.logits(x, ev, h, r);
+    std::lock_guard<std::mutex> lk(s_.mu);
+    ++s_.forwards;
+    return out;
+}
+
 } // namespace
 
 extern "C" {
+
+// cider_weights_init's layout and draw order with the reference's own seeding: one
+// make_rng(seed) stream of uniform(-1/sqrt(D), 1/sqrt(D)) draws in random_init's order (tables, then per
+// layer gate_a, check_agg, fuse_b), attention parameters from make_rng(derive_seed(seed, 1000 + layer)).
+// N = 1, H = D, heads = 0 is DenoiserParams::random_init (denoiser.cpp:41-69) value for value.
+int ref_weights_init(const cider_model_desc* md, uint64_t seed, double* out) {
+    return guarded([&] {
+        const size_t q = size_t(1) << md->m, D = md->dim, H = md->hidden;
+        const double bound = 1.0 / std::sqrt(double(D));
+        std::uniform_real_distribution<double> u(-bound, bound);
+        auto rng = ura::make_rng(seed);
+        size_t off = 0;
+        auto fill = [&](std::mt19937_64& g, size_t n) {
+            for (size_t i = 0; i < n; ++i) out[off++] = u(g);
+        };
+        fill(rng, (q + 1) * D);
+        fill(rng, q * D);
+        fill(rng, q * D);
+        for (int l = 0; l < md->layers; ++l)
+            for (size_t in : {2 * D, D, 2 * D}) {
+                fill(rng, H * in);
+                fill(rng, H);
+                fill(rng, D * H);
+                fill(rng, D);
+            }
+        if (md->heads > 0)
+            for (int l = 0; l < md->layers; ++l) {
+                auto ra = ura::make_rng(ura::derive_seed(seed, 1000 + uint64_t(l)));
+                fill(ra, D);
+                fill(ra, D * D);
+            }
+    });
+}
+
+// The BASELINE evidence model over the reference's own code construction: bin b's
+// stream is make_rng(derive_seed(master, 16 + b)); truth = sample_codewords(gf, derive_generator(gf, H),
+// K, rng) (ldpc.cpp:153-195); then per slot K erasure draws, one false-candidate draw (+ its symbol),
+// Q normals; S = log_softmax, rounded to fp32 (what both arms decode). Bins fan out over threads.
+int ref_workload_bins(int m, const cider_code_desc* code, int K, double snr_db, double p_erase, double p_false,
+                      uint64_t master, int64_t first, int n, int32_t* truth, double* S, int threads) {
+    return guarded([&] {
+        auto gf = ura::GfContext::with_default_poly(m);
+        auto h = make_h(gf.q(), code);
+        auto gen = ura::derive_generator(gf, h);
+        const int L = code->slots, Q = gf.q();
+        const double sigma = std::pow(10.0, -snr_db / 20.0);
+        ura::parallel_for(
+            n,
+            [&](int i) {
+                auto rng = ura::make_rng(ura::derive_seed(master, uint64_t(16 + first + i)));
+                auto g = ura::sample_codewords(gf, gen, K, rng);
+                if (truth) std::copy(g.v.begin(), g.v.end(), truth + size_t(i) * K * L);
+                std::uniform_real_distribution<double> uni(0.0, 1.0);
+                std::normal_distribution<double> nrm(0.0, 1.0);
+                std::uniform_int_distribution<int> sym(0, Q - 1);
+                std::vector<double> y(Q);
+                for (int l = 0; l < L; ++l) {
+                    std::fill(y.begin(), y.end(), 0.0);
+                    for (int k = 0; k < K; ++k) {
+                        bool erased = uni(rng) < p_erase;
+                        if (!erased) y[g.v[size_t(k) * L + l]] += 1.0;
+                    }
+                    if (uni(rng) < p_false) y[sym(rng)] += 1.0;
+                    for (int a = 0; a < Q; ++a) y[a] += sigma * nrm(rng);
+                    double mx = y[0];
+                    for (int a = 1; a < Q; ++a) mx = std::max(mx, y[a]);
+                    double se = 0.0;
+                    for (int a = 0; a < Q; ++a) se += std::exp(y[a] - mx);
+                    const double lse = mx + std::log(se);
+                    for (int a = 0; a < Q; ++a) S[(size_t(i) * L + l) * Q + a] = double(float(y[a] - lse));
+                }
+            },
+            threads);
+    });
+}
+
+int ref_session_create(const cider_model_desc* md, const double* weights, const cider_code_desc* code, int K, int n_bins,
+                       const double* S, const cider_schedule* sched, const cider_remask* remask, int threads, void** out) {
+    return guarded([&] {
+        if (threads < 1 || n_bins < 1) throw std::domain_error("ref_session: need threads >= 1 and bins >= 1");
+        *out = new Session(md, weights, code, K, n_bins, S, sched, remask, threads);
+    });
+}
+// every live worker runs n more forwards (with the decode logic between them); returns when all are parked
+int ref_session_advance(void* s, int n) {
+    return guarded([&] { static_cast<Session*>(s)->advance(n); });
+}
+int ref_session_status(void* s, int64_t* forwards, int64_t* bins_done, int32_t* grids, int32_t* done) {
+    return guarded([&] {
+        auto* ss = static_cast<Session*>(s);
+        std::lock_guard<std::mutex> lk(ss->mu);
+        *forwards = ss->forwards;
+        *bins_done = ss->bins_done;
+        if (grids) std::copy(ss->grids.begin(), ss->grids.end(), grids);
+        if (done) for (int b = 0; b < ss->n_bins; ++b) done[b] = ss->done[b];
+    });
+}
+void ref_session_destroy(void* s) { delete static_cast<Session*>(s); }
+
 
 const char* ref_last_error(void) { return g_err.c_str(); }
 

@@ -62,7 +62,10 @@ class RemaskDesc(C.Structure):
 
 class TraceDesc(C.Structure):
     _fields_ = [("first_reveals", C.POINTER(C.c_int32)), ("remask_rows", C.POINTER(C.c_int32)),
-                ("remask_steps", C.POINTER(C.c_int32)), ("remask_mask", C.POINTER(C.c_int32))]
+                ("remask_steps", C.POINTER(C.c_int32)), ("remask_mask", C.POINTER(C.c_int32)),
+                ("pass_first_reveals", C.POINTER(C.c_int32)), ("n_passes", C.POINTER(C.c_int32)),
+                ("max_steps", C.c_int), ("reveal_counts", C.POINTER(C.c_int32)),
+                ("n_reveal_counts", C.POINTER(C.c_int32)), ("first_step_sites", C.POINTER(C.c_uint8))]
 
 
 class WorkloadDesc(C.Structure):
@@ -94,6 +97,8 @@ def lib() -> C.CDLL:
         h.cider_denoise.argtypes = [P, C.c_int, C.c_int, P, P, P, P]
         h.cider_refine.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P, P,
                                    C.POINTER(TraceDesc)]
+        h.cider_refine_probe.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P,
+                                         C.c_int, P, C.c_int, P, P, P, C.POINTER(C.c_int)]
         h.cider_refine_ragged.argtypes = [P, C.c_int, P, P, C.c_int, P, P, P]
         h.cider_refine_device.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P]
         h.cider_device_count.argtypes = [C.POINTER(C.c_int)]
@@ -305,9 +310,18 @@ class Context:
         tr = None
         trd = None
         if want_trace:
+            # ura::RefineTrace (refine.hpp:48-54) per bin; reveal_counts / first_step_sites describe the
+            # most recent pass, pass_first_reveals every pass run (n_passes of them)
+            ms = max(sched.steps, 1)
             tr = {"first_reveals": np.zeros(B, np.int32), "remask_rows": np.zeros((B, MAX_THRESHOLDS), np.int32),
-                  "remask_steps": np.zeros((B, MAX_THRESHOLDS), np.int32), "remask_mask": np.zeros((B, K), np.int32)}
-            trd = TraceDesc(*(v.ctypes.data_as(C.POINTER(C.c_int32)) for v in tr.values()))
+                  "remask_steps": np.zeros((B, MAX_THRESHOLDS), np.int32), "remask_mask": np.zeros((B, K), np.int32),
+                  "pass_first_reveals": np.zeros((B, 1 + MAX_THRESHOLDS), np.int32), "n_passes": np.zeros(B, np.int32),
+                  "reveal_counts": np.zeros((B, ms), np.int32), "n_reveal_counts": np.zeros(B, np.int32),
+                  "first_step_sites": np.zeros((B, K, L), np.uint8)}
+            i32 = lambda k: tr[k].ctypes.data_as(C.POINTER(C.c_int32))  # noqa: E731
+            trd = TraceDesc(i32("first_reveals"), i32("remask_rows"), i32("remask_steps"), i32("remask_mask"),
+                            i32("pass_first_reveals"), i32("n_passes"), ms, i32("reveal_counts"), i32("n_reveal_counts"),
+                            tr["first_step_sites"].ctypes.data_as(C.POINTER(C.c_uint8)))
         _check(lib().cider_refine(self.h, B, K, _ptr(S), C.byref(sd), C.byref(rd), _ptr(grid), _ptr(fl),
                                   C.byref(trd) if trd is not None else None))
         out = [grid]
@@ -316,6 +330,28 @@ class Context:
         if want_trace:
             out.append(tr)
         return out[0] if len(out) == 1 else tuple(out)
+
+    def refine_probe(self, S: np.ndarray, K: int, sched: RevealSchedule, remask: Optional[RemaskConfig] = None,
+                     probe_bins=(0,), want_logits: bool = True, max_records: int = 0):
+        """cider_refine_probe: the decode of all B bins (one device chunk) plus, for `probe_bins`, every
+        forward's input grid / output logits and every pass's output grid in execution order.
+        Returns (grid B x K x L, meta R x 4 {pass, t, steps, kind}, X n_probe x R x K x L,
+        logits n_probe x R x K x L x Q or None)."""
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        B, L, q = S.shape
+        pb = np.ascontiguousarray(probe_bins, dtype=np.int32)
+        if not max_records:
+            max_records = 2 * (sched.steps + 2) + 4
+        grid = np.empty((B, K, L), dtype=np.int32)
+        meta = np.zeros((max_records, 4), np.int32)
+        X = np.zeros((len(pb), max_records, K, L), np.int32)
+        lg = np.zeros((len(pb), max_records, K, L, q), np.float32) if want_logits else None
+        n = C.c_int()
+        sd, rd = sched.desc(), (remask or RemaskConfig()).desc()
+        _check(lib().cider_refine_probe(self.h, B, K, _ptr(S), C.byref(sd), C.byref(rd), _ptr(grid), len(pb), _ptr(pb),
+                                        max_records, _ptr(meta), _ptr(X), _ptr(lg), C.byref(n)))
+        r = n.value
+        return grid, meta[:r], X[:, :r], (lg[:, :r] if lg is not None else None)
 
     def refine_ragged(self, S: np.ndarray, loads, sched_by_load, remask_by_load=None):
         """Bins of different loads K (1..k_max) in one call (cider_refine_ragged):

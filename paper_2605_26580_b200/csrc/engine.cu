@@ -196,6 +196,8 @@ struct Stat {
     double ms = 0.0, flops = 0.0, bytes = 0.0;
 };
 
+struct Probe;
+
 } // namespace
 } // namespace cider
 
@@ -253,6 +255,8 @@ struct cider_ctx {
     // NCCL (dlopen'ed)
     void* nccl_lib = nullptr;
     void* nccl_comm = nullptr;
+    // teacher-forcing probe of the running cider_refine_probe call (nullptr otherwise)
+    cider::Probe* probe = nullptr;
 
     ~cider_ctx();
 };
@@ -580,7 +584,7 @@ struct WS {
     int* X;
     float *Zf, *lbar, *ef, *Ztf, *accf, *keys, *logits, *kappa, *k1;
     void *Zt, *Aq, *et, *hid, *Ztt, *U, *Ae, *Nn, *pooled, *mapped, *Mq, *accq, *acct;
-    int *amax, *init_masked, *nlow, *first_count;
+    int *amax, *init_masked, *nlow;
     uint32_t* upd;
     float* S;  // staging for host evidence
     int* Xio;  // staging for host grids
@@ -636,7 +640,6 @@ WS workspace(cider_ctx& c, int nb, int K, bool want_flog) {
     }
     w.init_masked = (int*)wsbuf(c, "init_masked", size_t(nb) * 4);
     w.nlow = (int*)wsbuf(c, "nlow", size_t(nb) * 4);
-    w.first_count = (int*)wsbuf(c, "first_count", size_t(nb) * 4);
     w.upd = (uint32_t*)wsbuf(c, "upd", size_t(nb) * 4);
     w.S = (float*)wsbuf(c, "S", size_t(nb) * c.L * Q * 4);
     w.Xio = (int*)wsbuf(c, "Xio", size_t(nb) * c.L * K * 4);
@@ -1097,20 +1100,74 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
 }
 
 // ---- one pass of run_masked_loop (refine.cpp:134-195) over nb bins ------------------------------
+// Device buffers of one traced pass (RefineTrace, refine.hpp:48-54): per-step reveal counts
+// (nb x steps) and the sites revealed at t = 1 (nb x L*K, internal layout).
+struct PassTrace {
+    int* counts = nullptr;
+    uint8_t* sites = nullptr;
+};
+
+// Teacher-forcing probe (cider_refine_probe): every forward's input grid and output
+// logits of a few bins, plus each pass's output grid, copied to host buffers in execution order.
+struct Probe {
+    std::vector<int> bins; // chunk-local bin indices
+    int max_rec = 0, n_rec = 0, pass = 0;
+    int32_t *X = nullptr, *meta = nullptr;
+    float* lg = nullptr;     // host, nullable
+    float* dev_lg = nullptr; // device logits of the forward being recorded (internal layout)
+};
+
+void probe_record(cider_ctx& c, Probe& p, int K, const int* X, int t, int steps, int kind) {
+    if (p.n_rec >= p.max_rec) throw InvalidInput("cider_refine_probe: more records than max_records");
+    const int L = c.L, Q = c.Q, n = L * K, r = p.n_rec;
+    ck(cudaStreamSynchronize(c.stream), "probe sync");
+    std::vector<int> xi(n);
+    std::vector<float> li(p.lg && kind < 2 ? size_t(n) * Q : 0);
+    for (size_t i = 0; i < p.bins.size(); ++i) {
+        const int b = p.bins[i];
+        ck(cudaMemcpy(xi.data(), X + size_t(b) * n, size_t(n) * 4, cudaMemcpyDeviceToHost), "probe X");
+        int32_t* xo = p.X + (i * p.max_rec + r) * size_t(n);
+        for (int l = 0; l < L; ++l)
+            for (int k = 0; k < K; ++k) xo[size_t(k) * L + l] = xi[size_t(l) * K + k];
+        if (li.empty()) continue;
+        ck(cudaMemcpy(li.data(), p.dev_lg + size_t(b) * n * Q, size_t(n) * Q * 4, cudaMemcpyDeviceToHost), "probe logits");
+        float* lo = p.lg + (i * p.max_rec + r) * size_t(n) * Q;
+        for (int l = 0; l < L; ++l)
+            for (int k = 0; k < K; ++k)
+                std::copy(li.begin() + (size_t(l) * K + k) * Q, li.begin() + (size_t(l) * K + k + 1) * Q,
+                          lo + (size_t(k) * L + l) * Q);
+    }
+    int32_t* m = p.meta + size_t(r) * 4;
+    m[0] = p.pass; m[1] = t; m[2] = steps; m[3] = kind;
+    ++p.n_rec;
+}
+
 // X holds the start grid (internal layout); init_masked / upd describe it per bin.
 void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int steps, const cider_schedule& sc,
-                 bool count_first) {
+                 const PassTrace* pt) {
     const int n = c.L * K;
+    Probe* probe = c.probe;
+    // reveal keys: dynamic shared memory up to REVEAL_SMEM_SITES, else a per-bin global slice
+    const int cap = reveal_key_cap(n);
+    const size_t smem = cap <= REVEAL_SMEM_SITES ? size_t(cap) * 8 : 0;
+    unsigned long long* gkeys = cap > REVEAL_SMEM_SITES ? (unsigned long long*)wsbuf(c, "reveal_keys", size_t(nb) * cap * 8) : nullptr;
+    static bool attr = false;
+    if (!attr) {
+        ck(cudaFuncSetAttribute(reveal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, REVEAL_SMEM_SITES * 8), "reveal attr");
+        attr = true;
+    }
     for (int t = 1; t <= steps; ++t) {
         FwdOpts o;
         o.tau = float(infer_temperature(t, steps, sc.tau_max, sc.tau_min));
+        if (probe) o.logits_out = probe->dev_lg;
         forward(c, w, nb, K, X, S, o);
+        if (probe) probe_record(c, *probe, K, X, t, steps, 0);
         const bool first = t == 1 && sc.first_reveal;
-        if (first && count_first)
-            ck(cudaMemsetAsync(w.first_count, 0, size_t(nb) * 4, c.stream), "memset");
+        if (pt && t == 1) ck(cudaMemsetAsync(pt->sites, 0, size_t(nb) * n, c.stream), "memset");
         Launch lg(c, "reveal", 0, double(nb) * n * 12);
-        reveal_kernel<<<nb, 512, 0, c.stream>>>(X, w.kappa, w.amax, c.L, K, w.init_masked, cosine_fraction(t, steps),
-                                                first ? 1 : 0, first && count_first ? w.first_count : nullptr);
+        reveal_kernel<<<nb, 512, smem, c.stream>>>(X, w.kappa, w.amax, c.L, K, w.init_masked, cosine_fraction(t, steps),
+                                                   first ? 1 : 0, pt ? pt->counts + (t - 1) : nullptr, steps,
+                                                   pt && t == 1 ? pt->sites : nullptr, gkeys);
         check_launch("reveal");
     }
     {
@@ -1120,13 +1177,18 @@ void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int
     }
     FwdOpts o; // the gamma = 0 pass; kappa at tau = 1 feeds MaxProbScorer (refine.cpp:218-225)
     o.tau = 1.0f;
-    o.logits_out = w.flog;
+    o.logits_out = probe ? probe->dev_lg : w.flog;
     forward(c, w, nb, K, X, S, o);
+    if (probe) probe_record(c, *probe, K, X, 0, steps, 1);
     {
         Launch lg(c, "finalize", 0, double(nb) * n * 12);
         finalize_kernel<<<blocks_for(int64_t(nb) * n), 256, 0, c.stream>>>(X, w.amax, w.upd, K, int64_t(nb) * n, n);
         check_launch("finalize");
         ck(cudaMemcpyAsync(w.k1, w.kappa, size_t(nb) * n * 4, cudaMemcpyDeviceToDevice, c.stream), "k1");
+    }
+    if (probe) {
+        probe_record(c, *probe, K, X, 0, steps, 2);
+        ++probe->pass;
     }
 }
 
@@ -1153,8 +1215,39 @@ void validate_sched(const cider_schedule* sc, const cider_remask* rm, int K) {
 }
 
 struct ChunkTrace {
-    std::vector<int32_t> first, rows, steps, mask; // per bin
+    std::vector<int32_t> rows, steps, mask;      // per bin x CIDER_MAX_THRESHOLDS / K
+    std::vector<int32_t> pass_first, n_passes;   // per bin x (1 + CIDER_MAX_THRESHOLDS) / per bin
+    std::vector<int32_t> counts, n_counts;       // most recent pass: per bin x max_steps / per bin
+    std::vector<uint8_t> sites;                  // most recent pass: per bin x L*K (internal layout)
+    int max_steps = 0;
 };
+
+PassTrace pass_trace(cider_ctx& c, int m, int steps, int K) {
+    PassTrace pt;
+    pt.counts = (int*)wsbuf(c, "tr_counts", size_t(m) * steps * 4);
+    pt.sites = (uint8_t*)wsbuf(c, "tr_sites", size_t(m) * c.L * K);
+    return pt;
+}
+
+// fold one traced pass over m bins (bins[i] = chunk-local index, nullptr = identity) into the chunk trace
+void trace_pass(cider_ctx& c, ChunkTrace& tr, const PassTrace& pt, int m, int steps, int K, const int* bins) {
+    const int n = c.L * K;
+    std::vector<int32_t> cnt(size_t(m) * steps);
+    std::vector<uint8_t> st(size_t(m) * n);
+    ck(cudaMemcpyAsync(cnt.data(), pt.counts, cnt.size() * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+    ck(cudaMemcpyAsync(st.data(), pt.sites, st.size(), cudaMemcpyDeviceToHost, c.stream), "d2h");
+    ck(cudaStreamSynchronize(c.stream), "sync");
+    for (int i = 0; i < m; ++i) {
+        const int b = bins ? bins[i] : i;
+        int& np = tr.n_passes[b];
+        if (np < 1 + CIDER_MAX_THRESHOLDS) tr.pass_first[size_t(b) * (1 + CIDER_MAX_THRESHOLDS) + np] = cnt[size_t(i) * steps];
+        ++np;
+        tr.n_counts[b] = steps;
+        for (int s = 0; s < tr.max_steps; ++s)
+            tr.counts[size_t(b) * tr.max_steps + s] = s < steps ? cnt[size_t(i) * steps + s] : 0;
+        std::copy(st.begin() + size_t(i) * n, st.begin() + size_t(i + 1) * n, tr.sites.begin() + size_t(b) * n);
+    }
+}
 
 // gather / scatter of per-bin records for threshold-remask buckets
 __global__ void gather_rows_kernel(const int* __restrict__ src, int* __restrict__ dst, const int* __restrict__ idx,
@@ -1192,13 +1285,21 @@ void refine_chunk(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, co
     fill_u32_kernel<<<blocks_for(nb), 256, 0, c.stream>>>(w.upd, K >= 32 ? 0xffffffffu : ((1u << K) - 1u), nb);
     c.launches += 3;
     check_launch("init");
-    masked_pass(c, w, nb, K, S, X, sc.steps, sc, tr != nullptr);
     if (tr) {
-        tr->first.assign(nb, 0);
         tr->rows.assign(size_t(nb) * CIDER_MAX_THRESHOLDS, 0);
         tr->steps.assign(size_t(nb) * CIDER_MAX_THRESHOLDS, 0);
         tr->mask.assign(size_t(nb) * K, 0);
-        ck(cudaMemcpyAsync(tr->first.data(), w.first_count, size_t(nb) * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
+        tr->pass_first.assign(size_t(nb) * (1 + CIDER_MAX_THRESHOLDS), 0);
+        tr->n_passes.assign(nb, 0);
+        tr->counts.assign(size_t(nb) * tr->max_steps, 0);
+        tr->n_counts.assign(nb, 0);
+        tr->sites.assign(size_t(nb) * n, 0);
+    }
+    {
+        PassTrace pt;
+        if (tr) pt = pass_trace(c, nb, sc.steps, K);
+        masked_pass(c, w, nb, K, S, X, sc.steps, sc, tr ? &pt : nullptr);
+        if (tr) trace_pass(c, *tr, pt, nb, sc.steps, K, nullptr);
     }
     const int mode = rm ? rm->mode : CIDER_REMASK_NONE;
     if (mode == CIDER_REMASK_RANK) {
@@ -1212,8 +1313,11 @@ void refine_chunk(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, co
             const int T_rm = remask_steps(sc.steps, k_low, K);
             cider_schedule rs = sc;
             rs.steps = T_rm;
-            masked_pass(c, w, nb, K, S, X, T_rm, rs, false);
+            PassTrace pt;
+            if (tr) pt = pass_trace(c, nb, T_rm, K);
+            masked_pass(c, w, nb, K, S, X, T_rm, rs, tr ? &pt : nullptr);
             if (tr) {
+                trace_pass(c, *tr, pt, nb, T_rm, K, nullptr);
                 std::vector<uint32_t> upd(nb);
                 ck(cudaMemcpyAsync(upd.data(), w.upd, size_t(nb) * 4, cudaMemcpyDeviceToHost, c.stream), "d2h");
                 ck(cudaStreamSynchronize(c.stream), "sync");
@@ -1262,12 +1366,15 @@ void refine_chunk(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, co
                         tr->steps[size_t(b) * CIDER_MAX_THRESHOLDS + s] = T_rm;
                         for (int k = 0; k < K; ++k) tr->mask[size_t(b) * K + k] = (upd[b] >> k) & 1u;
                     }
-                if (int(bins.size()) == nb) {
-                    masked_pass(c, w, nb, K, S, X, T_rm, rs, false);
+                const int m = int(bins.size());
+                PassTrace pt;
+                if (tr) pt = pass_trace(c, m, T_rm, K);
+                if (m == nb) {
+                    masked_pass(c, w, nb, K, S, X, T_rm, rs, tr ? &pt : nullptr);
+                    if (tr) trace_pass(c, *tr, pt, m, T_rm, K, nullptr);
                     continue;
                 }
                 // compact sub-batch in the tail of dedicated staging buffers
-                const int m = int(bins.size());
                 int* idx = (int*)wsbuf(c, "sub_idx", size_t(m) * 4);
                 ck(cudaMemcpyAsync(idx, bins.data(), size_t(m) * 4, cudaMemcpyHostToDevice, c.stream), "h2d");
                 float* subS = (float*)wsbuf(c, "sub_S", size_t(m) * c.L * c.Q * 4);
@@ -1287,7 +1394,8 @@ void refine_chunk(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, co
                     keep_flog = (float*)wsbuf(c, "sub_flog", size_t(nb) * n * c.Q * 4);
                     ck(cudaMemcpyAsync(keep_flog, w.flog, size_t(nb) * n * c.Q * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
                 }
-                masked_pass(c, w, m, K, subS, subX, T_rm, rs, false);
+                masked_pass(c, w, m, K, subS, subX, T_rm, rs, tr ? &pt : nullptr);
+                if (tr) trace_pass(c, *tr, pt, m, T_rm, K, bins.data());
                 copy_rows(c, subX, X, idx, m, n, false);
                 copy_rows(c, w.k1, keep_k1, idx, m, n, false);
                 ck(cudaMemcpyAsync(w.k1, keep_k1, size_t(nb) * n * 4, cudaMemcpyDeviceToDevice, c.stream), "d2d");
@@ -1641,6 +1749,7 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
         if (c->bf16 && (c->Q % 64 || c->D % 64 || c->H % 64 || c->Q > 256))
             throw InvalidInput("BF16 mode needs Q, D, H multiples of 64 and Q <= 256");
         if (c->heads > ATT_MAXH) throw InvalidInput("cider: at most 32 attention heads");
+        if (c->L > 65535) throw InvalidInput("cider: at most 65535 slots"); // 16-bit slot field of the reveal keys
         for (int j = 0; j < c->P; ++j) {
             const int dj = c->tg->check_ptr[j + 1] - c->tg->check_ptr[j];
             if (dj > ATT_MAXD) throw InvalidInput("cider: check degree above 32");
@@ -1732,9 +1841,11 @@ int cider_denoise(cider_ctx* c, int B, int K, const int32_t* X, const float* S, 
 static void refine_chunk_graphed(cider_ctx& c, WS& w, int nb, int K, const float* S, const cider_schedule& sc,
                                  const cider_remask* rm) {
     char key[256];
-    std::snprintf(key, sizeof(key), "%d/%d/%p/%p/%d/%.17g/%.17g/%d/%d/%.17g/%lld", nb, K, (const void*)S, (void*)w.X, sc.steps,
-                  sc.tau_max, sc.tau_min, sc.first_reveal, rm ? rm->mode : -1, rm ? rm->rank_fraction : 0.0,
-                  (long long)alloc_generation());
+    // the key names every buffer the captured launches bake in, the final-logits one included
+    // (a graph captured without final logits never writes them)
+    std::snprintf(key, sizeof(key), "%d/%d/%p/%p/%p/%d/%.17g/%.17g/%d/%d/%.17g/%lld", nb, K, (const void*)S, (void*)w.X,
+                  (void*)w.flog, sc.steps, sc.tau_max, sc.tau_min, sc.first_reveal, rm ? rm->mode : -1,
+                  rm ? rm->rank_fraction : 0.0, (long long)alloc_generation());
     auto& g = c.graphs[key];
     if (g.exec) {
         ck(cudaGraphLaunch(g.exec, c.stream), "cudaGraphLaunch");
@@ -1780,8 +1891,9 @@ static void refine_impl(cider_ctx* c, int B, int K, const float* S, bool S_devic
             Sd = w.S;
         }
         ChunkTrace ct;
+        if (tr) ct.max_steps = std::max(0, tr->max_steps);
         static const bool no_graph = std::getenv("CIDER_NO_GRAPH") != nullptr;
-        const bool graphable = !tr && !c->profiling && !no_graph && (!rm || rm->mode != CIDER_REMASK_THRESHOLD);
+        const bool graphable = !tr && !c->probe && !c->profiling && !no_graph && (!rm || rm->mode != CIDER_REMASK_THRESHOLD);
         if (graphable && Sd != w.S) { // the graph reads S from the workspace: one key for every caller buffer
             ck(cudaMemcpyAsync(w.S, Sd, size_t(nb) * L * Q * 4, cudaMemcpyDeviceToDevice, c->stream), "d2d");
             Sd = w.S;
@@ -1803,14 +1915,28 @@ static void refine_impl(cider_ctx* c, int B, int K, const float* S, bool S_devic
         }
         if (tr || !grid_device || final_logits) ck(cudaStreamSynchronize(c->stream), "refine");
         if (tr) {
+            constexpr int NP = 1 + CIDER_MAX_THRESHOLDS;
             for (int b = 0; b < nb; ++b) {
-                if (tr->first_reveals) tr->first_reveals[b0 + b] = ct.first[b];
+                const size_t B = size_t(b0 + b);
+                if (tr->first_reveals) tr->first_reveals[B] = ct.pass_first[size_t(b) * NP];
                 for (int s = 0; s < CIDER_MAX_THRESHOLDS; ++s) {
-                    if (tr->remask_rows) tr->remask_rows[size_t(b0 + b) * CIDER_MAX_THRESHOLDS + s] = ct.rows[size_t(b) * CIDER_MAX_THRESHOLDS + s];
-                    if (tr->remask_steps) tr->remask_steps[size_t(b0 + b) * CIDER_MAX_THRESHOLDS + s] = ct.steps[size_t(b) * CIDER_MAX_THRESHOLDS + s];
+                    if (tr->remask_rows) tr->remask_rows[B * CIDER_MAX_THRESHOLDS + s] = ct.rows[size_t(b) * CIDER_MAX_THRESHOLDS + s];
+                    if (tr->remask_steps) tr->remask_steps[B * CIDER_MAX_THRESHOLDS + s] = ct.steps[size_t(b) * CIDER_MAX_THRESHOLDS + s];
                 }
                 if (tr->remask_mask)
-                    for (int k = 0; k < K; ++k) tr->remask_mask[size_t(b0 + b) * K + k] = ct.mask[size_t(b) * K + k];
+                    for (int k = 0; k < K; ++k) tr->remask_mask[B * K + k] = ct.mask[size_t(b) * K + k];
+                if (tr->pass_first_reveals)
+                    std::copy(ct.pass_first.begin() + size_t(b) * NP, ct.pass_first.begin() + size_t(b + 1) * NP,
+                              tr->pass_first_reveals + B * NP);
+                if (tr->n_passes) tr->n_passes[B] = ct.n_passes[b];
+                if (tr->reveal_counts && ct.max_steps > 0)
+                    std::copy(ct.counts.begin() + size_t(b) * ct.max_steps, ct.counts.begin() + size_t(b + 1) * ct.max_steps,
+                              tr->reveal_counts + B * ct.max_steps);
+                if (tr->n_reveal_counts) tr->n_reveal_counts[B] = ct.n_counts[b];
+                if (tr->first_step_sites)
+                    for (int l = 0; l < L; ++l)
+                        for (int k = 0; k < K; ++k)
+                            tr->first_step_sites[B * n + size_t(k) * L + l] = ct.sites[size_t(b) * n + size_t(l) * K + k];
             }
         }
     }
@@ -1823,6 +1949,42 @@ int cider_refine(cider_ctx* c, int B, int K, const float* S, const cider_schedul
         if (!c) throw InvalidInput("null context");
         std::lock_guard<std::mutex> lk(c->mu);
         refine_impl(c, B, K, S, false, sched, rm, grid, false, final_logits, tr);
+    });
+}
+
+int cider_refine_probe(cider_ctx* c, int B, int K, const float* S, const cider_schedule* sched, const cider_remask* rm,
+                       int32_t* grid, int n_probe, const int32_t* probe_bins, int max_records, int32_t* meta,
+                       int32_t* probe_X, float* probe_logits, int* n_records) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        if (rm && rm->mode == CIDER_REMASK_THRESHOLD)
+            throw InvalidInput("cider_refine_probe: threshold remasking is not supported (bins diverge into sub-batches)");
+        if (n_probe < 0 || max_records < 0 || (n_probe && (!probe_bins || !probe_X)) || !meta || !n_records)
+            throw InvalidInput("cider_refine_probe: bad probe arguments");
+        std::lock_guard<std::mutex> lk(c->mu);
+        Probe p;
+        for (int i = 0; i < n_probe; ++i) {
+            if (probe_bins[i] < 0 || probe_bins[i] >= B) throw InvalidInput("cider_refine_probe: probe bin out of range");
+            p.bins.push_back(probe_bins[i]);
+        }
+        p.max_rec = max_records;
+        p.X = probe_X;
+        p.meta = meta;
+        p.lg = probe_logits;
+        p.dev_lg = (float*)wsbuf(*c, "probe_logits", size_t(round_up(size_t(B) * c->L * K, 128)) * c->Q * 4);
+        const int keep_chunk = c->chunk_req;
+        c->chunk_req = std::max(1, B); // one device chunk: probe bins index the whole batch
+        c->probe = &p;
+        try {
+            refine_impl(c, B, K, S, false, sched, rm, grid, false, nullptr, nullptr);
+        } catch (...) {
+            c->probe = nullptr;
+            c->chunk_req = keep_chunk;
+            throw;
+        }
+        c->probe = nullptr;
+        c->chunk_req = keep_chunk;
+        *n_records = p.n_rec;
     });
 }
 

@@ -599,19 +599,31 @@ __global__ void row_stats_kernel(const float* __restrict__ logits, int64_t M, in
 // ---- reveal_step (refine.cpp:83-127), one block per bin ------------------------------------
 // first: one site per slot, the masked row with the largest kappa (strict >, lowest row wins).
 // else : reveal the (target - revealed) masked sites smallest in (kappa desc, row asc, slot asc)
-//        via a bitonic sort of 64-bit keys in shared memory.
-constexpr int REVEAL_MAX_SITES = 4096;
+//        via a bitonic sort of 64-bit keys (~bits(kappa), row, slot) — in dynamic shared memory
+//        when the padded site count fits (REVEAL_SMEM_SITES), else in a per-bin global scratch
+//        slice (gkeys + b * key_cap), so any K x L the reference accepts is handled.
+// count (nullable): count[b * count_stride] = sites revealed by this step (RefineTrace::reveal_counts,
+// refine.hpp:48-54); sites (nullable, zeroed by the caller): 1 for every site revealed by this step
+// (RefineTrace::first_step_sites when called at t = 1).
+constexpr int REVEAL_SMEM_SITES = 16384; // 128 KB of keys
+__host__ __device__ inline int reveal_key_cap(int n) {
+    int size = 1;
+    while (size < n) size <<= 1;
+    return size;
+}
 __global__ void __launch_bounds__(512)
 reveal_kernel(int* __restrict__ X, const float* __restrict__ kappa, const int* __restrict__ amax, int L,
               int K, const int* __restrict__ init_masked, double rho, int first,
-              int* __restrict__ reveal_count) {
-    __shared__ unsigned long long key[REVEAL_MAX_SITES];
+              int* __restrict__ count, int count_stride, uint8_t* __restrict__ sites,
+              unsigned long long* __restrict__ gkeys) {
+    extern __shared__ unsigned long long skey[];
     __shared__ int red[32];
     const int b = blockIdx.x;
     const int n = L * K;
     int* x = X + size_t(b) * n;
     const float* kp = kappa + size_t(b) * n;
     const int* am = amax + size_t(b) * n;
+    uint8_t* st = sites ? sites + size_t(b) * n : nullptr;
     int before = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) before += x[i] == -1;
     for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
@@ -635,20 +647,32 @@ reveal_kernel(int* __restrict__ X, const float* __restrict__ kappa, const int* _
                 if (x[i] != -1) continue;
                 if (br < 0 || kp[i] > bk) { br = k; bk = kp[i]; }
             }
-            if (br >= 0) { x[l * K + br] = am[l * K + br]; ++cnt; }
+            if (br >= 0) {
+                x[l * K + br] = am[l * K + br];
+                if (st) st[l * K + br] = 1;
+                ++cnt;
+            }
         }
-        if (reveal_count) {
+        if (count) {
             for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            if (threadIdx.x % 32 == 0) atomicAdd(reveal_count + b, cnt); // a count, not data: order-free
+            __syncthreads();
+            if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = cnt;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int s = 0;
+                for (int w = 0; w < int(blockDim.x / 32); ++w) s += red[w];
+                count[size_t(b) * count_stride] = s;
+            }
         }
         return;
     }
     const int base = n - init_masked[b];
     const int target = base + int(llround(rho * double(init_masked[b])));
-    const int need = target - (n - masked);
+    const int need = target - (n - masked); // <= masked: target <= n
+    if (count && threadIdx.x == 0) count[size_t(b) * count_stride] = need > 0 ? need : 0;
     if (need <= 0) return;
-    int size = 1;
-    while (size < n) size <<= 1;
+    const int size = reveal_key_cap(n);
+    unsigned long long* key = size <= REVEAL_SMEM_SITES ? skey : gkeys + size_t(b) * size;
     for (int i = threadIdx.x; i < size; i += blockDim.x) {
         unsigned long long kk = ~0ull;
         if (i < n && x[i] == -1) {
@@ -677,6 +701,7 @@ reveal_kernel(int* __restrict__ X, const float* __restrict__ kappa, const int* _
         if (kk == ~0ull) continue;
         int k = int((kk >> 16) & 0xffff), l = int(kk & 0xffff);
         x[l * K + k] = am[l * K + k];
+        if (st) st[l * K + k] = 1;
     }
 }
 

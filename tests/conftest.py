@@ -37,3 +37,21 @@ def rel_err(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.abs(a - b).max() / max(1e-30, np.abs(b).max()))
+
+
+_REPORT = {}
+
+
+@pytest.fixture(scope="session")
+def parity_report():
+    """Measured parity numbers (errors, decision agreement) collected by the GPU tests; written as JSON to
+    $CIDER_PARITY_REPORT at session end (the GPU runs copy it into profiles/)."""
+    return _REPORT
+
+
+def pytest_sessionfinish(session, exitstatus):
+    path = os.environ.get("CIDER_PARITY_REPORT")
+    if path and _REPORT:
+        import json
+        with open(path, "w") as f:
+            json.dump(_REPORT, f, indent=1, sort_keys=True, default=float)

@@ -4,8 +4,9 @@ inputs and weights.
 Tolerances (BASELINE.json north_star):
   FP32 mode: logits / incoming messages within 1e-3 relative (to max |value|); decoded grids,
              first-reveal counts, remask rows / steps / indices identical.
-  BF16 mode: logits / messages within 3e-2 relative (bf16 operands, fp32 accumulation, tanh-form
-             GELU in the fused MLP epilogues); SER within 0.05 of the oracle's on the same bins.
+  BF16 mode: logits / messages within 1e-2 relative (bf16 operands, fp32 accumulation, tanh-form
+             GELU in the fused MLP epilogues). Decisions at the BASELINE shapes are checked
+             teacher-forced in test_gpu_parity.py.
 """
 import numpy as np
 import pytest
@@ -15,7 +16,7 @@ from conftest import rel_err
 pytestmark = pytest.mark.gpu
 
 FP32_TOL = 1e-3
-BF16_TOL = 3e-2
+BF16_TOL = 1e-2
 
 
 def ctx_for(P, model, wl, seed=1, edges=None):
@@ -30,7 +31,7 @@ def as_run(P, model, w):
 
 # ---------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
-def test_denoise_parity_all_configs(P, oracle, name):
+def test_denoise_parity_all_configs(P, oracle, parity_report, name):
     """One forward on partially revealed grids: logits and every layer's check messages."""
     cfg = P.configs()[name]
     wl, model = cfg.workload, cfg.model
@@ -42,11 +43,13 @@ def test_denoise_parity_all_configs(P, oracle, name):
     X = X.astype(np.int32)
     lg, inc = ctx.denoise(X, S, want_incoming=True)
     tol = FP32_TOL if model.precision == P.FP32 else BF16_TOL
+    errs = []
     for b in range(nb):
         lo, io = oracle.denoise(model, as_run(P, model, w), e, wl.checks, wl.slots, X[b], S[b].astype(np.float64), True)
-        assert rel_err(lg[b], lo) < tol
-        for layer in range(model.layers):
-            assert rel_err(inc[b, layer], io[layer]) < tol
+        errs.append(rel_err(lg[b], lo))
+        errs.extend(rel_err(inc[b, layer], io[layer]) for layer in range(model.layers))
+    parity_report[f"denoise_{name}"] = {"max_rel_err": max(errs), "tol": tol}
+    assert max(errs) < tol, errs
 
 
 def test_c1_full_decode_identical_to_oracle(P, oracle):
@@ -106,37 +109,6 @@ def test_threshold_remask_buckets_with_mixed_row_counts(P, oracle):
     assert np.array_equal(grid, ro["grid"])
     assert np.array_equal(tr["remask_rows"], ro["remask_rows"])
     assert np.array_equal(tr["remask_mask"], ro["remask_mask"])
-
-
-@pytest.mark.parametrize("name", ["c2", "c4"])
-def test_bf16_config_ser_matches_oracle(P, oracle, name):
-    """BF16 configs: decoded SER on a subset agrees with the oracle's on the same bins."""
-    cfg = P.configs()[name]
-    wl = cfg.workload
-    small = P.Model(m=cfg.model.m, dim=64, hidden=128, layers=1, heads=cfg.model.heads and 2, precision=P.BF16)
-    ctx, e, w = ctx_for(P, small, wl)
-    nb = 4 if name == "c2" else 2
-    truth, S = wl.bins(e, 0, nb)
-    sched = P.RevealSchedule(steps=4)
-    grid = ctx.refine(S, wl.k, sched)
-    ro = oracle.refine(small, as_run(P, small, w), e, wl.checks, wl.slots, S.astype(np.float64), wl.k, sched)
-    assert abs(P.ser_cer(truth, grid)[0] - P.ser_cer(truth, ro["grid"])[0]) < 0.05
-
-
-def test_c3_remask_path_bf16_runs_and_matches_rows(P, oracle):
-    """Config-3 shape (K=8, Q=256, L=64) with the rank-25% remask on the tcgen05 path."""
-    cfg = P.configs()["c3"]
-    wl = cfg.workload
-    model = P.Model(m=8, dim=64, hidden=128, layers=1, heads=2, precision=P.BF16)
-    ctx, e, w = ctx_for(P, model, wl)
-    truth, S = wl.bins(e, 0, 2)
-    sched = P.RevealSchedule(steps=4)
-    grid, tr = ctx.refine(S, 8, sched, cfg.remask, want_trace=True)
-    ro = oracle.refine(model, as_run(P, model, w), e, wl.checks, wl.slots, S.astype(np.float64), 8, sched, cfg.remask)
-    assert np.all((grid >= 0) & (grid < 256))
-    assert np.all(tr["remask_rows"][:, 0] == 2) and np.all(tr["remask_steps"][:, 0] == 1)
-    assert np.all(tr["remask_mask"].sum(1) == 2)
-    assert abs(P.ser_cer(truth, grid)[0] - P.ser_cer(truth, ro["grid"])[0]) < 0.05
 
 
 # ---- invariants on the device ------------------------------------------------------------------
