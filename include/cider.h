@@ -142,6 +142,17 @@ int cider_denoise(cider_ctx* ctx, int B, int K, const int32_t* X, const float* S
 int cider_refine(cider_ctx* ctx, int B, int K, const float* S, const cider_schedule* sched,
                  const cider_remask* remask, int32_t* grid, float* final_logits, cider_trace* trace);
 
+/* One remask pass with the caller's row confidences (= ura::remask_pass, refine.hpp:97-100,
+ * refine.cpp:238-275 — any ConfidenceScorer's score_rows): for B bins, rows k with
+ * confidences[b*K + k] < threshold are masked and re-decoded for remask_steps(T, n_low, K) steps from
+ * grid_in (B x K x L, symbols in [0, Q)); the other rows of grid_out are grid_in's, bit for bit.
+ * final_logits (nullable, B x K x L x Q): the pass's gamma = 0 logits, written only for bins that had
+ * a low row (the reference leaves final_pass_logits untouched otherwise). trace (nullable): the pass's
+ * RefineTrace records (remask_rows / remask_steps stage 0, remask_mask = the low rows). */
+int cider_remask_pass(cider_ctx* ctx, int B, int K, const float* S, const cider_schedule* sched,
+                      const int32_t* grid_in, const double* confidences, double threshold, int32_t* grid_out,
+                      float* final_logits, cider_trace* trace);
+
 /* Teacher-forcing probe (test / diagnostic entry point): cider_refine over B host bins
  * (remask NONE or RANK) as ONE device chunk, recording for the n_probe bins probe_bins[] every denoiser
  * forward's input grid and output logits and every pass's output grid, in execution order. Record r
@@ -236,6 +247,9 @@ int cider_kernel_stats(cider_ctx* ctx, int idx, char* name, int name_len, int64_
 int cider_reset_stats(cider_ctx* ctx);
 
 /* ---- multi-GPU result gather (NCCL, the only collective on the path) --------------------- */
+/* decoded grids (int32, device) -> one byte per symbol (Q <= 256), async on the ctx stream: the
+ * payload of the final gather (134 MB for all 262,144 c5 bins) */
+int cider_grid_pack_u8(cider_ctx* ctx, const int32_t* grid_device, uint8_t* out_device, size_t n);
 int cider_nccl_unique_id(char out[128]);
 int cider_nccl_init(cider_ctx* ctx, const char id[128], int rank, int world);
 /* all ranks contribute n_bytes from send_device; recv_device (n_bytes*world) filled on every rank */

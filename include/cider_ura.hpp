@@ -6,8 +6,10 @@
 //   cider::GpuStructuredDenoiser : ura::Denoiser          (denoiser.hpp:109-130)
 //       drop-in for ura::StructuredDenoiser inside the reference's run_refinement /
 //       run_with_remasking / remask_pass (refine.cpp:134-292) — one forward per call.
-//   cider::GpuRefiner::run_refinement / run_with_remasking (refine.hpp:60-62, 104-107)
-//       the whole T-step loop on the device, batched over bins.
+//   cider::GpuRefiner::run_refinement / run_with_remasking / remask_pass (refine.hpp:60-62, 97-107)
+//       the whole T-step loop on the device, batched over bins; RefineTrace filled like the
+//       reference's; run_with_remasking takes any ura::ConfidenceScorer (scores on the host between
+//       the device passes, the reference's stage loop).
 //   cider::make_bin_decoder -> ura::BinDecoder            (protocol.hpp:32-40)
 //       for run_protocol_frame (protocol.cpp:73).
 //   cider::GpuBp::bp_decode / sic_decode                  (bp.hpp:72-93)
@@ -94,6 +96,17 @@ public:
         check(cider_create(&md, w.data(), &cd, device, &c));
         ctx_.reset(c);
     }
+    // config mode (BASELINE configs: N stacked blocks, MLP width H, attention heads): cider.h's flat
+    // weight layout (cider_weights_init) and model descriptor
+    Context(const cider_model_desc& md, const std::vector<float>& weights, const ura::ParityCheckMatrix& h, int device = 0)
+        : checks_(h.checks()), slots_(h.slots()), q_(1 << md.m), dim_(md.dim) {
+        if (weights.size() != cider_weights_count(&md)) throw std::domain_error("cider: weight count does not match the model");
+        edges_ = edges_of(h);
+        cider_code_desc cd{h.checks(), h.slots(), int(edges_.size() / 3), edges_.data()};
+        cider_ctx* c = nullptr;
+        check(cider_create(&md, weights.data(), &cd, device, &c));
+        ctx_.reset(c);
+    }
     cider_ctx* get() const { return ctx_.get(); }
     int q() const { return q_; }
     int slots() const { return slots_; }
@@ -144,6 +157,68 @@ public:
     ura::SymbolGrid run_refinement(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
                                    const ura::RevealSchedule& sched, int k) const {
         return run(s, h, sched, nullptr, k);
+    }
+    // = ura::run_refinement(den, s, h, sched, k, l, trace, final_pass_logits) (refine.hpp:60-62)
+    ura::SymbolGrid run_refinement(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
+                                   const ura::RevealSchedule& sched, int k, ura::RefineTrace* trace,
+                                   ura::LogitGrid* final_pass_logits) const {
+        ctx_->require_same(h);
+        const int L = ctx_->slots(), Q = ctx_->q();
+        std::vector<float> S(s.v.begin(), s.v.end());
+        std::vector<int32_t> g(size_t(k) * L);
+        std::vector<float> fl(final_pass_logits ? size_t(k) * L * Q : 0);
+        TraceBuf tb(k, L, sched.steps);
+        const cider_schedule sc = schedule(sched);
+        check(cider_refine(ctx_->get(), 1, k, S.data(), &sc, nullptr, g.data(), final_pass_logits ? fl.data() : nullptr,
+                           trace ? &tb.t : nullptr));
+        if (trace) tb.fold(*trace, k, L, false);
+        if (final_pass_logits) *final_pass_logits = logits_of(fl, k, L, Q);
+        ura::SymbolGrid out(k, L);
+        std::copy(g.begin(), g.end(), out.v.begin());
+        return out;
+    }
+    // = ura::remask_pass (refine.hpp:97-100, refine.cpp:238-275): rows with confidences[k] < threshold
+    // re-decoded on the device, the others bit-identical; final_pass_logits / trace as the reference
+    ura::SymbolGrid remask_pass(const ura::SymbolGrid& grid, const std::vector<double>& confidences, double threshold,
+                                const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
+                                const ura::RevealSchedule& sched, ura::RefineTrace* trace = nullptr,
+                                ura::LogitGrid* final_pass_logits = nullptr) const {
+        ctx_->require_same(h);
+        if (static_cast<int>(confidences.size()) != grid.rows)
+            throw std::domain_error("remask_pass: one confidence per row required");
+        const int k = grid.rows, L = ctx_->slots(), Q = ctx_->q();
+        int n_low = 0;
+        for (double c : confidences) n_low += c < threshold;
+        if (n_low == 0) return grid;
+        std::vector<float> S(s.v.begin(), s.v.end());
+        std::vector<int32_t> gin(grid.v.begin(), grid.v.end()), gout(gin.size());
+        std::vector<float> fl(final_pass_logits ? size_t(k) * L * Q : 0);
+        TraceBuf tb(k, L, sched.steps);
+        const cider_schedule sc = schedule(sched);
+        check(cider_remask_pass(ctx_->get(), 1, k, S.data(), &sc, gin.data(), confidences.data(), threshold, gout.data(),
+                                final_pass_logits ? fl.data() : nullptr, trace ? &tb.t : nullptr));
+        if (trace) tb.fold(*trace, k, L, true);
+        if (final_pass_logits) *final_pass_logits = logits_of(fl, k, L, Q);
+        ura::SymbolGrid out(k, L);
+        std::copy(gout.begin(), gout.end(), out.v.begin());
+        return out;
+    }
+    // = ura::run_with_remasking(den, scorer, s, h, sched, remask, k, l, trace) (refine.cpp:277-292) with
+    // any ConfidenceScorer: the passes run on the device, the scorer on the host between them
+    ura::SymbolGrid run_with_remasking(const ura::ConfidenceScorer& scorer, const ura::EvidenceMatrix& s,
+                                       const ura::ParityCheckMatrix& h, const ura::RevealSchedule& sched,
+                                       const ura::RemaskConfig& remask, int k, ura::RefineTrace* trace = nullptr) const {
+        ura::validate_remask_config(remask);
+        ura::LogitGrid fl;
+        ura::SymbolGrid grid = run_refinement(s, h, sched, k, trace, &fl);
+        for (double threshold : remask.thresholds) {
+            auto conf = scorer.score_rows(grid, fl);
+            bool any_low = false;
+            for (double c : conf) any_low = any_low || c < threshold;
+            if (!any_low) break;
+            grid = remask_pass(grid, conf, threshold, s, h, sched, trace, &fl);
+        }
+        return grid;
     }
     // = ura::run_with_remasking(den, MaxProbScorer, s, h, sched, remask, k, l)
     ura::SymbolGrid run_with_remasking(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h,
@@ -213,6 +288,41 @@ public:
     }
 
 private:
+    // cider_trace buffers of one bin, folded into a ura::RefineTrace like run_masked_loop / remask_pass
+    // record it (refine.cpp:160-170, 261-264): reveal_counts / first_step_sites replaced by the last
+    // pass's, pass_first_reveals / remask stages appended
+    struct TraceBuf {
+        std::vector<int32_t> first, rows, steps, mask, pass_first, n_passes, counts, n_counts;
+        std::vector<uint8_t> sites;
+        cider_trace t{};
+        TraceBuf(int k, int L, int max_steps)
+            : first(1), rows(CIDER_MAX_THRESHOLDS), steps(CIDER_MAX_THRESHOLDS), mask(k), pass_first(1 + CIDER_MAX_THRESHOLDS),
+              n_passes(1), counts(std::max(1, max_steps)), n_counts(1), sites(size_t(k) * L) {
+            t = cider_trace{first.data(), rows.data(), steps.data(), mask.data(), pass_first.data(), n_passes.data(),
+                            std::max(1, max_steps), counts.data(), n_counts.data(), sites.data()};
+        }
+        void fold(ura::RefineTrace& tr, int k, int L, bool stage) const {
+            if (n_passes[0] == 0) return;
+            for (int p = 0; p < n_passes[0] && p < 1 + CIDER_MAX_THRESHOLDS; ++p) tr.pass_first_reveals.push_back(pass_first[p]);
+            if (stage) {
+                tr.remask_rows_per_stage.push_back(rows[0]);
+                tr.remask_steps_per_stage.push_back(steps[0]);
+            }
+            tr.reveal_counts.assign(counts.begin(), counts.begin() + std::min<size_t>(counts.size(), size_t(n_counts[0])));
+            tr.first_step_sites.clear();
+            for (int r = 0; r < k; ++r)
+                for (int l = 0; l < L; ++l)
+                    if (sites[size_t(r) * L + l]) tr.first_step_sites.emplace_back(r, l);
+        }
+    };
+    static cider_schedule schedule(const ura::RevealSchedule& sched) {
+        return cider_schedule{sched.steps, sched.tau_max, sched.tau_min, sched.first_reveal ? 1 : 0};
+    }
+    static ura::LogitGrid logits_of(const std::vector<float>& fl, int k, int L, int Q) {
+        ura::LogitGrid out(k, L, Q);
+        for (size_t i = 0; i < fl.size(); ++i) out.v[i] = fl[i];
+        return out;
+    }
     ura::SymbolGrid run(const ura::EvidenceMatrix& s, const ura::ParityCheckMatrix& h, const ura::RevealSchedule& sched,
                         const cider_remask* rm, int k) const {
         return run_batch({&s}, h, sched, rm, k)[0];

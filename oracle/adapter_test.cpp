@@ -8,6 +8,10 @@
 //   (3) cider::GpuRefiner::run_refinement                    (whole loop on the B200)
 //   (4) ura::run_with_remasking vs GpuRefiner::run_with_remasking, and a BinDecoder call
 //   (5) ura::sic_decode vs cider::GpuBp::sic_decode (FFT-BP, WHT backend), and a SIC BinDecoder
+//   (6) RefineTrace (reveal_counts, first_step_sites, pass_first_reveals, remask stages) and
+//       run_with_remasking with a pluggable ConfidenceScorer (ura::OracleRowScorer) vs the reference
+//   (7) ura::run_protocol / run_protocol_frame (protocol.cpp:41-113) with a CPU decoder bank vs the
+//       request-coalescing GPU bank: identical per-bin grids and identical frame SER / CER
 // on fp32-rounded parameters and evidence (FP32 mode), and requires identical grids.
 // Exit code = number of failed checks.
 #include <cmath>
@@ -15,8 +19,13 @@
 #include <random>
 #include <thread>
 
+#include <map>
+#include <mutex>
+
 #include "cider_ura.hpp"
 #include "ura/ldpc.hpp"
+#include "ura/metrics.hpp"
+#include "ura/protocol.hpp"
 #include "ura/seeding.hpp"
 
 static void round_f32(std::vector<double>& v) {
@@ -162,6 +171,93 @@ int main() {
             const bool sic_ok = sdec(t2).v == gpu_res[0].grid.v;
             std::printf("SIC BinDecoder call: %s\n", sic_ok ? "ok" : "FAILED");
             fails += !sic_ok;
+        }
+        // (6) RefineTrace + pluggable ConfidenceScorer (refine.hpp:48-92)
+        {
+            int same = 0, same_tr = 0;
+            const int n6 = 4, k = 3;
+            for (int b = 0; b < n6; ++b) {
+                ura::EvidenceMatrix s6(16, 64);
+                auto er = ura::make_rng(ura::derive_seed(21, b));
+                std::uniform_real_distribution<double> u(-8.0, 0.0);
+                for (double& x : s6.v) x = double(float(u(er)));
+                ura::SymbolGrid truth6(k, 16);
+                auto tr6 = ura::make_rng(ura::derive_seed(22, b));
+                std::uniform_int_distribution<int> sym(0, 63);
+                for (int& v : truth6.v) v = sym(tr6);
+                ura::OracleRowScorer scorer(truth6); // every row "wrong" -> all rows re-decoded per stage
+                ura::RemaskConfig rm{{0.9, 0.5}};
+                ura::RefineTrace ta, tg;
+                auto a = ura::run_with_remasking(cpu, scorer, s6, h, sched, rm, k, 16, &ta);
+                auto g = refiner.run_with_remasking(scorer, s6, h, sched, rm, k, &tg);
+                same += a == g;
+                same_tr += ta.reveal_counts == tg.reveal_counts && ta.first_step_sites == tg.first_step_sites &&
+                           ta.pass_first_reveals == tg.pass_first_reveals && ta.remask_rows_per_stage == tg.remask_rows_per_stage &&
+                           ta.remask_steps_per_stage == tg.remask_steps_per_stage;
+            }
+            std::printf("scored remasking (OracleRowScorer) vs reference: %d/%d identical grids, %d/%d identical traces\n", same,
+                        n6, same_tr, n6);
+            fails += same != n6;
+            fails += same_tr != n6;
+        }
+        // (7) the stochastic-binning protocol: reference CPU bank vs the coalescing GPU bank
+        {
+            ura::FrameConfig base;
+            base.q = 64;
+            base.slots = 16;
+            base.n_s = 24;
+            base.eb_db = 8.0;
+            base.payload_bits = 6 * 8;
+            auto gen = ura::derive_generator(gf, h);
+            auto dicts = ura::make_dictionaries(base.q, base.n_s, base.slots, 5);
+            ura::ProtocolConfig pc;
+            pc.k_tot = 6;
+            pc.zeta = 2;
+            pc.k_max = 4;
+            std::mutex mu;
+            using Key = std::vector<double>;
+            std::map<Key, ura::SymbolGrid> cpu_out, gpu_out;
+            auto f32 = [](const ura::EvidenceMatrix& e) {
+                ura::EvidenceMatrix r = e;
+                for (double& x : r.v) x = double(float(x)); // both banks decode the fp32-rounded evidence
+                return r;
+            };
+            ura::BinDecoder cpu_dec = [&](const ura::BinTask& t) {
+                ura::RevealSchedule sc;
+                sc.steps = ura::default_steps_for_load(t.load);
+                ura::RemaskConfig rm;
+                rm.thresholds = ura::default_remask_thresholds(t.load);
+                ura::MaxProbScorer mp;
+                auto ev = f32(t.evidence);
+                auto g = ura::run_with_remasking(cpu, mp, ev, t.h, sc, rm, t.load, t.evidence.slots);
+                std::lock_guard<std::mutex> lk(mu);
+                cpu_out[ev.v] = g;
+                return g;
+            };
+            auto co = std::make_shared<cider::BinCoalescer>(ctx, pc.k_max);
+            auto gdec = cider::make_coalescing_bin_decoder(co);
+            ura::BinDecoder gpu_dec = [&](const ura::BinTask& t) {
+                auto ev = f32(t.evidence);
+                auto g = gdec(ura::BinTask{t.gf, t.h, ev, t.truth, t.load});
+                std::lock_guard<std::mutex> lk(mu);
+                gpu_out[ev.v] = g;
+                return g;
+            };
+            const int frames = 12;
+            auto ra = ura::run_protocol(pc, base, gf, h, gen, dicts, ura::DecoderBank::uniform(cpu_dec, pc.k_max), frames, 3);
+            auto rg = ura::run_protocol(pc, base, gf, h, gen, dicts, ura::DecoderBank::uniform(gpu_dec, pc.k_max), frames, 3);
+            int same = 0;
+            for (auto& [k, g] : cpu_out) {
+                auto it = gpu_out.find(k);
+                same += it != gpu_out.end() && it->second == g;
+            }
+            const bool agg = ra.ser == rg.ser && ra.cer == rg.cer && ra.overflow_rate == rg.overflow_rate;
+            std::printf("run_protocol (%d frames, %d decoded bins, %lld device batches): %d/%d identical bin grids, "
+                        "SER %.6f / %.6f, CER %.6f / %.6f: %s\n",
+                        frames, int(cpu_out.size()), (long long)co->batches(), same, int(cpu_out.size()), ra.ser, rg.ser, ra.cer,
+                        rg.cer, agg ? "ok" : "FAILED");
+            fails += same != int(cpu_out.size()) || cpu_out.size() != gpu_out.size() || cpu_out.empty();
+            fails += !agg;
         }
         // error contract: a different H must be rejected like a bad input
         auto rng2 = ura::make_rng(99);

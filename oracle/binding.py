@@ -40,6 +40,9 @@ def _load(path: str, prefix: str) -> C.CDLL:
     r = getattr(h, f"{prefix}_refine")
     r.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.POINTER(ScheduleDesc),
                   C.POINTER(RemaskDesc), P, P, P, P, P, P, C.c_int]
+    rp = getattr(h, f"{prefix}_remask_pass")
+    rp.argtypes = [C.POINTER(ModelDesc), P, C.POINTER(CodeDesc), C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), P, P,
+                   C.c_double, P, P, C.c_int]
     rv = getattr(h, f"{prefix}_reveal_step")
     rv.argtypes = [C.c_int, C.c_int, C.c_int, P, P, C.c_int, C.c_double, C.c_int, P]
     w = getattr(h, f"{prefix}_check_update_wht")
@@ -147,6 +150,23 @@ class Checker:
             _p(out["final_logits"]), _p(out["first_reveals"]), _p(out["remask_rows"]), _p(out["remask_steps"]),
             _p(out["remask_mask"]), threads))
         return out
+
+    def remask_pass(self, model: Model, weights: np.ndarray, edges: np.ndarray, checks: int, slots: int, S: np.ndarray,
+                    grid: np.ndarray, conf: np.ndarray, threshold: float, sched: RevealSchedule, threads: int = 0):
+        """remask_pass (refine.cpp:238-275) with caller confidences for B bins -> (grid, final logits or NaN)."""
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        cd, _e = code_desc(edges, checks, slots)
+        S = np.ascontiguousarray(S, dtype=np.float64)
+        g = np.ascontiguousarray(grid, dtype=np.int32)
+        cf = np.ascontiguousarray(conf, dtype=np.float64)
+        B, K, L = g.shape
+        out = np.empty_like(g)
+        fl = np.full((B, K, L, S.shape[-1]), np.nan)
+        sd = sched.desc()
+        self._check(getattr(self.h, f"{self.prefix}_remask_pass")(C.byref(model.desc()), _p(w), C.byref(cd), B, K, _p(S),
+                                                                  C.byref(sd), _p(g), _p(cf), threshold, _p(out), _p(fl),
+                                                                  threads))
+        return out, fl
 
     def reveal_step(self, X: np.ndarray, logits: np.ndarray, target: int, tau: float, first: bool):
         X = np.ascontiguousarray(X, dtype=np.int32)

@@ -641,6 +641,28 @@ int oracle_refine(const cider_model_desc* md, const double* weights, const cider
     });
 }
 
+// remask_pass with caller row confidences (refine.cpp:238-275): rows with conf < threshold re-decoded.
+int oracle_remask_pass(const cider_model_desc* md, const double* weights, const cider_code_desc* code, int B, int K,
+                       const double* S, const cider_schedule* sched, const int32_t* grid_in, const double* conf,
+                       double threshold, int32_t* grid_out, double* final_logits, int threads) {
+    return guarded([&] {
+        Net n(md, weights);
+        Field f(md->m, md->prim_poly);
+        Tanner t(code, f.q);
+        const int L = t.L, Q = f.q;
+        pool_for(B, threads, [&](int b) {
+            std::vector<int> g(grid_in + size_t(b) * K * L, grid_in + size_t(b + 1) * K * L);
+            std::vector<char> low(K, 0);
+            for (int k = 0; k < K; ++k) low[k] = conf[size_t(b) * K + k] < threshold;
+            std::vector<double> fl;
+            int rows = 0, steps = 0;
+            auto out = remask(n, f, t, K, S + size_t(b) * L * Q, *sched, g, low, fl, &rows, &steps);
+            std::copy(out.begin(), out.end(), grid_out + size_t(b) * K * L);
+            if (final_logits && rows) std::copy(fl.begin(), fl.end(), final_logits + size_t(b) * K * L * Q);
+        });
+    });
+}
+
 // Check->variable message of one GF(Q) parity check in the WHT domain (bp.cpp:128-149):
 // permute each input by its coefficient, transform, multiply, transform back, gather by the
 // target coefficient, clamp at 0, normalise (uniform if all mass vanished, bp.cpp:11-19).

@@ -644,6 +644,38 @@ int ref_refine(const cider_model_desc* md, const double* weights, const cider_co
     });
 }
 
+// ura::remask_pass (refine.cpp:238-275) on caller confidences, per bin, through the stacked denoiser.
+int ref_remask_pass(const cider_model_desc* md, const double* weights, const cider_code_desc* code, int B, int K,
+                    const double* S, const cider_schedule* sc, const int32_t* grid_in, const double* conf, double threshold,
+                    int32_t* grid_out, double* final_logits, int workers) {
+    return guarded([&] {
+        Model model(md, weights);
+        auto gf = make_gf(md);
+        auto h = make_h(gf.q(), code);
+        const int L = h.slots(), q = gf.q();
+        ura::parallel_for(
+            B,
+            [&](int b) {
+                StackedDenoiser den(gf, model);
+                ura::EvidenceMatrix s(L, q);
+                std::copy(S + size_t(b) * L * q, S + size_t(b + 1) * L * q, s.v.begin());
+                ura::SymbolGrid g(K, L);
+                std::copy(grid_in + size_t(b) * K * L, grid_in + size_t(b + 1) * K * L, g.v.begin());
+                ura::RevealSchedule sched;
+                sched.steps = sc->steps;
+                sched.tau_max = sc->tau_max;
+                sched.tau_min = sc->tau_min;
+                sched.first_reveal = sc->first_reveal != 0;
+                std::vector<double> cf(conf + size_t(b) * K, conf + size_t(b + 1) * K);
+                ura::LogitGrid fl;
+                auto out = ura::remask_pass(g, cf, threshold, den, s, h, sched, nullptr, &fl);
+                std::copy(out.v.begin(), out.v.end(), grid_out + size_t(b) * K * L);
+                if (final_logits && !fl.v.empty()) std::copy(fl.v.begin(), fl.v.end(), final_logits + size_t(b) * K * L * q);
+            },
+            workers);
+    });
+}
+
 // Reference GF(Q) FFT-BP check update (bp.cpp:128-149) — the north_star-named WHT kernel's oracle.
 int ref_check_update_wht(int m, int n_in, const double* incoming, const int32_t* coeffs,
                          int target_coeff, double* out) {

@@ -1,4 +1,5 @@
-"""Teacher-forced, margin-aware decision checker — test infrastructure.
+"""Teacher-forced, margin-aware decision checker — TEST INFRASTRUCTURE ONLY
+(used by tests/ and bench.py's parity leg as the checker, never on the measured path).
 
 The device decodes a batch through `cider_refine_probe`, which records, for a few probe bins, every
 denoiser forward's input grid X_r and output logits, and every pass's output grid (execution order).

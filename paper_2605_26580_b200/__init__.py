@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
                                    C.POINTER(TraceDesc)]
         h.cider_refine_probe.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P,
                                          C.c_int, P, C.c_int, P, P, P, C.POINTER(C.c_int)]
+        h.cider_remask_pass.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), P, P, C.c_double, P, P,
+                                        C.POINTER(TraceDesc)]
         h.cider_refine_ragged.argtypes = [P, C.c_int, P, P, C.c_int, P, P, P]
         h.cider_refine_device.argtypes = [P, C.c_int, C.c_int, P, C.POINTER(ScheduleDesc), C.POINTER(RemaskDesc), P]
         h.cider_device_count.argtypes = [C.POINTER(C.c_int)]
@@ -118,6 +120,7 @@ def lib() -> C.CDLL:
         h.cider_kernel_stats.argtypes = [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
         h.cider_reset_stats.argtypes = [P]
+        h.cider_grid_pack_u8.argtypes = [P, P, P, C.c_size_t]
         h.cider_nccl_unique_id.argtypes = [C.c_char_p]
         h.cider_nccl_init.argtypes = [P, C.c_char_p, C.c_int, C.c_int]
         h.cider_nccl_allgather.argtypes = [P, P, P, C.c_size_t]
@@ -331,6 +334,22 @@ class Context:
             out.append(tr)
         return out[0] if len(out) == 1 else tuple(out)
 
+    def remask_pass(self, S: np.ndarray, grid: np.ndarray, confidences: np.ndarray, threshold: float,
+                    sched: RevealSchedule, want_final_logits: bool = False):
+        """ura::remask_pass (refine.hpp:97-100) with caller row confidences (any ConfidenceScorer):
+        rows with confidence < threshold are re-decoded, the rest kept bit for bit. Returns grid (and
+        the pass's final logits; NaN rows for bins that had no low row)."""
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        g = np.ascontiguousarray(grid, dtype=np.int32)
+        cf = np.ascontiguousarray(confidences, dtype=np.float64)
+        B, K, L = g.shape
+        out = np.empty_like(g)
+        fl = np.full((B, K, L, self.model.q), np.nan, np.float32) if want_final_logits else None
+        sd = sched.desc()
+        _check(lib().cider_remask_pass(self.h, B, K, _ptr(S), C.byref(sd), _ptr(g), _ptr(cf), float(threshold), _ptr(out),
+                                       _ptr(fl), None))
+        return (out, fl) if want_final_logits else out
+
     def refine_probe(self, S: np.ndarray, K: int, sched: RevealSchedule, remask: Optional[RemaskConfig] = None,
                      probe_bins=(0,), want_logits: bool = True, max_records: int = 0):
         """cider_refine_probe: the decode of all B bins (one device chunk) plus, for `probe_bins`, every
@@ -420,6 +439,52 @@ def run_refinement(den: StructuredDenoiser, s: np.ndarray, sched: RevealSchedule
     if single:
         return tuple(o[0] if isinstance(o, np.ndarray) else o for o in out) if isinstance(out, tuple) else out[0]
     return out
+
+
+class MaxProbScorer:
+    """ura::MaxProbScorer (refine.cpp:218-225): mean over slots of the final-pass max softmax probability."""
+
+    def score_rows(self, grid: np.ndarray, final_logits: np.ndarray) -> np.ndarray:
+        lg = np.asarray(final_logits, np.float64)
+        kap = 1.0 / np.exp(lg - lg.max(-1, keepdims=True)).sum(-1)
+        return kap.mean(-1)
+
+
+def remask_pass(den: StructuredDenoiser, s: np.ndarray, grid: np.ndarray, confidences: np.ndarray, threshold: float,
+                sched: RevealSchedule, want_final_logits: bool = False):
+    """ura::remask_pass (refine.hpp:97-100) on the device; s: L x Q or B x L x Q."""
+    single = s.ndim == 2
+    S, g, c = (s[None], grid[None], np.asarray(confidences)[None]) if single else (s, grid, confidences)
+    out = den.ctx.remask_pass(S, g, c, threshold, sched, want_final_logits)
+    if single:
+        return tuple(o[0] for o in out) if want_final_logits else out[0]
+    return out
+
+
+def run_with_remasking_scored(den: StructuredDenoiser, scorer, s: np.ndarray, sched: RevealSchedule,
+                              thresholds, k: int):
+    """ura::run_with_remasking (refine.cpp:277-292) with any ConfidenceScorer (an object with
+    score_rows(grid, final_logits) per bin): the refinement and every remask pass on the device, the
+    row scores on the host between them, exactly the reference's stage loop. s: B x L x Q."""
+    prev = 1.0
+    for t in thresholds:  # validate_remask_config (refine.cpp:48-57)
+        if t <= 0.0 or t >= 1.0:
+            raise ValueError("remask thresholds must lie in (0,1)")
+        if t >= prev:
+            raise ValueError("remask thresholds must be strictly descending")
+        prev = t
+    grid, fl = den.ctx.refine(s, k, sched, None, want_final_logits=True)
+    live = np.ones(len(grid), bool)
+    for t in thresholds:
+        conf = np.stack([np.asarray(scorer.score_rows(grid[b], fl[b]), np.float64) for b in range(len(grid))])
+        low = (conf < t).any(1) & live
+        live &= low  # the reference stops a bin at its first all-clear stage
+        if not low.any():
+            break
+        idx = np.nonzero(low)[0]
+        g2, fl2 = den.ctx.remask_pass(s[idx], grid[idx], conf[idx], t, sched, want_final_logits=True)
+        grid[idx], fl[idx] = g2, fl2
+    return grid
 
 
 def run_with_remasking(den: StructuredDenoiser, s: np.ndarray, sched: RevealSchedule, remask: RemaskConfig, k: int,

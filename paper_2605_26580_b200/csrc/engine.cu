@@ -425,15 +425,10 @@ void gemm(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1,
     args.tiles_n = N / BN;
     args.tiles = int((M + tc::BM - 1) / tc::BM) * args.tiles_n;
     args.ep = ep;
-    static const int epw_demix = std::getenv("CIDER_EPW_DEMIX") ? std::atoi(std::getenv("CIDER_EPW_DEMIX")) : 16;
-    static const int epw_store = std::getenv("CIDER_EPW_STORE") ? std::atoi(std::getenv("CIDER_EPW_STORE")) : 4;
-    static const int epw_scores = std::getenv("CIDER_EPW_SCORES") ? std::atoi(std::getenv("CIDER_EPW_SCORES")) : 4;
-    const int epw = ep.kind == EP_DEMIX ? (epw_demix == 8 || BN == 64 ? 8 : 16) // the demix epilogue needs the > 4-warp staging
-                    : ep.kind == EP_STORE ? epw_store : ep.kind == EP_SCORES ? epw_scores : 4;
+    const int epw = ep.kind == EP_DEMIX ? (BN == 64 ? 8 : 16) : 4; // the demix epilogue needs the > 4-warp staging
     if (ep.kind == EP_DEMIX && BN != 256 && BN != 64) throw InvalidInput("fused demix epilogue needs Q = 64 or Q % 256 == 0");
     // B-resident variants: one N tile, K <= 256 (W, W^T, V^T against 128-row A tiles)
-    static const bool no_bres = std::getenv("CIDER_NO_BRES") != nullptr;
-    const bool bres = !no_bres && BN == 256 && N == 256 && K <= 256;
+    const bool bres = BN == 256 && N == 256 && K <= 256;
     // (the fused demix is epilogue-bound: it keeps 16 epilogue warps and a streamed B, measured faster
     // than 8 warps with B resident)
     if (bres && epw == 4) launch_tc<256, 4, true>(c, a0, a1, b, args);
@@ -480,8 +475,7 @@ void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, con
            "smem attr");
         attr_set = true;
     }
-    static const int cap = std::getenv("CIDER_MLP_PAIRS") ? std::atoi(std::getenv("CIDER_MLP_PAIRS")) : 0;
-    const int pairs = std::min(a.tiles, cap > 0 ? cap : c.sm_count / 2);
+    const int pairs = std::min(a.tiles, c.sm_count / 2);
     tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, out, a);
 }
 
@@ -531,9 +525,8 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     }
     ep.M = int(M);
     ep.N = D;
-    static const bool one_sm = std::getenv("CIDER_MLP_1SM") != nullptr;
     // 2-SM kernel variants: aggregator (Kin = D, plain store), gate / fusion (Kin = 2D, z (e) epilogue)
-    const bool pair = !one_sm && (D == 128 || D == 256) &&
+    const bool pair = (D == 128 || D == 256) &&
                       ((Kin == D && ep.kind == EP_STORE) || (Kin == 2 * D && (ep.kind == EP_GATE || ep.kind == EP_RESID)));
     Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
@@ -550,8 +543,6 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     a.b1 = b1;
     a.ep = ep;
     a.trace = nullptr;
-    static const int dbg = std::getenv("CIDER_MLP_DBG") ? std::atoi(std::getenv("CIDER_MLP_DBG")) : 0;
-    a.dbg = dbg;
     static const bool trace_on = std::getenv("CIDER_TRACE_MLP") != nullptr;
     long long* tbuf = nullptr;
     if (trace_on) {
@@ -740,7 +731,7 @@ void run_pool(cider_ctx& c, const LayerW& lw, const T* Nn, int nb, int K, T* poo
 // BF16, check-regular degree 6, D = 256, heads in {1, 2, 4, 8}, 6K <= 48 rows per (bin, check) block (K = 4 or 8)
 bool pool_mma_ok(const cider_ctx& c, const LayerW& lw, int K) {
     return c.bf16 && lw.aus16 && (c.D == 256 || c.D == 128) && c.max_check_deg == 6 && c.min_check_deg == 6 && 8 % c.heads == 0 &&
-           (K == 8 || (K == 4 && c.P % 2 == 0)) && !std::getenv("CIDER_NO_POOL_MMA");
+           (K == 8 || (K == 4 && c.P % 2 == 0));
 }
 const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, int ld, int box_rows);
 template <int K, int D>
@@ -768,8 +759,7 @@ void run_pool_mma(cider_ctx& c, const LayerW& lw, const void* Nn, int64_t Me, in
 
 // BF16, check-regular degree 6, D = 256, 1..16 heads dividing 32 lanes: scores from EP_SCORES
 bool pool_scored(const cider_ctx& c, const LayerW& lw) {
-    return c.bf16 && lw.aus && c.D == 256 && c.max_check_deg == 6 && c.min_check_deg == 6 && 32 % c.heads == 0 &&
-           !std::getenv("CIDER_NO_SCORE_GEMM");
+    return c.bf16 && lw.aus && c.D == 256 && c.max_check_deg == 6 && c.min_check_deg == 6 && 32 % c.heads == 0;
 }
 void run_pool_scored(cider_ctx& c, const bf16* Nn, const float* sc, int nb, int K, bf16* pooled) {
     const int64_t groups = int64_t(nb) * c.P * K;
@@ -806,47 +796,14 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     a.D = D;
     a.out_t = reinterpret_cast<bf16*>(out_t);
     a.out_f = out_f;
-    // T-resident sweep chunk: default one chunk (each CTA one contiguous group-major range). Chunks of
-    // 64-256 bins (z~ L2-resident across a slot's edges) measured slower: every extra T change drains
-    // the CTA's MMA pipeline (bench c5: normalise 83 ms whole vs 85-100 ms chunked).
-    // CIDER_GRP_CHUNK_BINS: -1 = laps (default), 0 = one contiguous group-major range per CTA, > 0 =
-    // chunked sweeps of that many bins
-    static const int mchunk_bins = std::getenv("CIDER_GRP_CHUNK_BINS") ? std::atoi(std::getenv("CIDER_GRP_CHUNK_BINS")) : -1;
-    a.mchunk = mchunk_bins < 0 ? -1 : mchunk_bins > 0 ? std::max(1, mchunk_bins / bb) : a.mtiles;
     const double rows = double(nb) * K * groups;
     // compulsory bytes: every A row once (normalise: the site rows its edges share) + the output rows
     Launch lg(c, tag, 2.0 * rows * D * D * mean_seg, (double(nb) * K * (a_rows_per_bin + out_rows_per_bin)) * D * 2.0);
     CUtensorMap ta = make_map_rows3d(A, nb, a_rows_per_bin * K, D, K, bb);
     CUtensorMap tt = make_map_ttab(c.Ttab, D, c.Q);
     const int tiles = a.groups * a.mtiles;
-    // The T-resident kernel (one T_alpha per CTA, lap schedule) measured 5% slower than the CTA-pair
-    // kernel with streamed T halves for the normalise GEMM (c5: 61.5 vs 58.4 ms per step): the pair
-    // kernel's m-tile-major order keeps a slot's z~ rows in L2 for its edges, and its deeper A / T
-    // ring hides the gather latency. CIDER_GRP_RES=1 selects the T-resident kernel.
-    static const bool use_res = std::getenv("CIDER_GRP_RES") != nullptr;
-    if (max_seg == 1 && (D == 256 || D == 128) && use_res) {
-        // single-segment groups: T-resident kernel (T loaded once per group change per CTA)
-        static bool attr_res = false;
-        if (!attr_res) {
-            ck(cudaFuncSetAttribute(tc::gemm_grp_res_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::GrpResLayout::TOTAL), "smem attr");
-            ck(cudaFuncSetAttribute(tc::gemm_grp_res_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc::GrpResLayout::TOTAL), "smem attr");
-            attr_res = true;
-        }
-        // laps: one CTA per SM, at most one per group
-        const int grid = a.mchunk < 0 ? std::min(groups, c.sm_count) : std::min(tiles, c.sm_count);
-        if (out_f || !out_t) throw InvalidInput("cider: the T-resident grouped GEMM writes one bf16 output");
-        const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb); // TMA store boxes
-        if (D == 256) tc::gemm_grp_res_kernel<256><<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, to, a);
-        else tc::gemm_grp_res_kernel<128><<<grid, tc::GRP_THREADS, tc::GrpResLayout::TOTAL, c.stream>>>(ta, tt, to, a);
-        check_launch(tag);
-        return;
-    }
     using Lay = tc::SmemLayout<256, 0>;
-    static const int grp_mode = std::getenv("CIDER_GRP_MODE") ? std::atoi(std::getenv("CIDER_GRP_MODE")) : 2;
-    static const bool no_res2 = std::getenv("CIDER_NO_GRP2_RES") != nullptr;
-    if (max_seg == 1 && !no_res2 && c.sm_count >= 2 && D == 256) {
+    if (max_seg == 1 && c.sm_count >= 2 && D == 256) {
         // single-segment groups (normalise): CTA pairs with their T halves resident, laps over the pairs
         // (c5 58.6 -> 55.7 ms, c4 45 -> 41 ms per step; at D = 128 the streamed kernel is as fast)
         static bool attr_r2 = false;
@@ -867,7 +824,7 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         check_launch(tag);
         return;
     }
-    if ((grp_mode == 2 && a.mtiles >= 2 && c.sm_count >= 2 && D == 256) || D == 128) {
+    if ((a.mtiles >= 2 && c.sm_count >= 2 && D == 256) || D == 128) {
         // CTA pairs, one cta_group::2 MMA over two m-tiles: each SM pulls half of every T k-block
         // (D = 128 always: the other grouped kernels are D = 256 only)
         static bool attr2 = false;
@@ -886,19 +843,7 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         check_launch(tag);
         return;
     }
-    if (grp_mode == 1 && a.mtiles >= 2 && c.sm_count >= 2) {
-        // cluster pairs: T_alpha multicast into both CTAs (two m-tiles of the same group)
-        static bool attr_mc = false;
-        if (!attr_mc) {
-            ck(cudaFuncSetAttribute(tc::gemm_grp_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
-            attr_mc = true;
-        }
-        const int supers = a.groups * ((a.mtiles + 1) / 2);
-        const int grid = 2 * std::min(supers, c.sm_count / 2);
-        tc::gemm_grp_mc_kernel<<<grid, tc::GRP_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
-        check_launch(tag);
-        return;
-    }
+    // a single m-tile (small batches): one CTA per (group, m-tile), T streamed
     static bool attr_set = false;
     if (!attr_set) {
         ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
@@ -912,8 +857,7 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
 // (intermediate_logits + demix_responsibilities + evidence_embed, denoiser.cpp:86-139): the 2-SM
 // fused two-layer kernel with hidden = the Q symbol columns and the demix as its hidden activation.
 bool demix_evid_ok(const cider_ctx& c, int K) {
-    static const bool off = std::getenv("CIDER_NO_DEMIX_EVID") != nullptr;
-    return !off && c.bf16 && c.D == 256 && c.Q == 256 && (K == 4 || K == 8) && !std::getenv("CIDER_MLP_1SM");
+    return c.bf16 && c.D == 256 && c.Q == 256 && (K == 4 || K == 8);
 }
 void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K, bf16* e_out) {
     const int D = c.D, Q = c.Q;
@@ -933,7 +877,6 @@ void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K,
     a.b1 = nullptr;
     a.ep = ep;
     a.trace = nullptr;
-    a.dbg = 0;
     static const bool trace_on = std::getenv("CIDER_TRACE_MLP") != nullptr;
     if (trace_on) {
         a.trace = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
@@ -973,7 +916,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             // Lambda-bar, demix and the evidence embedding in one 2-SM kernel (e is its only output)
             demix_evid(c, w.Zt, S, Ms, K, (bf16*)w.et);
         } else {
-        if (c.bf16 && 32 % K == 0 && K >= 4 && (Q % 256 == 0 || Q == 64) && !std::getenv("CIDER_NO_FUSED_DEMIX")) {
+        if (c.bf16 && 32 % K == 0 && K >= 4 && (Q % 256 == 0 || Q == 64)) {
             // intermediate logits and demixing in one kernel: Lambda-bar never leaves the chip
             e = epi(EP_DEMIX);
             e.out_t = w.Aq; e.ldo = Q; e.S = S; e.L = L; e.K = K; e.beta = float(c.md.evidence_scale);
@@ -1773,7 +1716,7 @@ int cider_create(const cider_model_desc* model, const float* weights, const cide
         // codes) would make an empty group -> generic path.
         bool every_slot_checked = true;
         for (int l = 0; l < c->L; ++l) every_slot_checked &= c->tg->slot_ptr[l + 1] > c->tg->slot_ptr[l];
-        if (c->bf16 && (c->D == 256 || c->D == 128) && every_slot_checked && !std::getenv("CIDER_NO_TPATH"))
+        if (c->bf16 && (c->D == 256 || c->D == 128) && every_slot_checked)
             build_tpath(*c);
         ck(cudaDeviceSynchronize(), "upload");
         *out = c.release();
@@ -1985,6 +1928,123 @@ int cider_refine_probe(cider_ctx* c, int B, int K, const float* S, const cider_s
         c->probe = nullptr;
         c->chunk_req = keep_chunk;
         *n_records = p.n_rec;
+    });
+}
+
+// ura::remask_pass (refine.hpp:97-100, refine.cpp:238-275) with the caller's row confidences (any
+// ConfidenceScorer): per bin, rows with conf < threshold are masked and re-decoded for
+// remask_steps(T, n_low, K) steps (updatable = those rows), the others stay bit-identical. Bins are
+// bucketed by n_low (each bucket one device batch); bins without a low row pass through untouched
+// (their final_logits rows are not written, as the reference leaves final_pass_logits alone).
+int cider_remask_pass(cider_ctx* c, int B, int K, const float* S, const cider_schedule* sched, const int32_t* grid_in,
+                      const double* confidences, double threshold, int32_t* grid_out, float* final_logits,
+                      cider_trace* tr) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        validate_sched(sched, nullptr, K);
+        if (B < 0) throw InvalidInput("remask_pass: negative B");
+        if (B && (!grid_in || !grid_out || !confidences || !S)) throw InvalidInput("remask_pass: null buffer");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const int L = c->L, Q = c->Q, n = L * K;
+        for (int64_t i = 0; i < int64_t(B) * n; ++i)
+            if (grid_in[i] < 0 || grid_in[i] >= Q) throw InvalidInput("remask_pass: grid symbol out of range");
+        std::copy(grid_in, grid_in + size_t(B) * n, grid_out);
+        std::map<int, std::vector<int>> buckets;
+        std::vector<uint32_t> low(B, 0);
+        for (int b = 0; b < B; ++b) {
+            for (int k = 0; k < K; ++k)
+                if (confidences[size_t(b) * K + k] < threshold) low[b] |= 1u << k;
+            if (low[b]) buckets[__builtin_popcount(low[b])].push_back(b);
+        }
+        constexpr int NP = 1 + CIDER_MAX_THRESHOLDS;
+        if (tr)
+            for (int b = 0; b < B; ++b) { // bins with no low row: no pass ran
+                if (tr->first_reveals) tr->first_reveals[b] = 0;
+                for (int s = 0; s < CIDER_MAX_THRESHOLDS; ++s) {
+                    if (tr->remask_rows) tr->remask_rows[size_t(b) * CIDER_MAX_THRESHOLDS + s] = 0;
+                    if (tr->remask_steps) tr->remask_steps[size_t(b) * CIDER_MAX_THRESHOLDS + s] = 0;
+                }
+                if (tr->remask_mask) for (int k = 0; k < K; ++k) tr->remask_mask[size_t(b) * K + k] = (low[b] >> k) & 1u;
+                if (tr->pass_first_reveals) std::fill(tr->pass_first_reveals + size_t(b) * NP, tr->pass_first_reveals + size_t(b + 1) * NP, 0);
+                if (tr->n_passes) tr->n_passes[b] = 0;
+                if (tr->reveal_counts && tr->max_steps > 0)
+                    std::fill(tr->reveal_counts + size_t(b) * tr->max_steps, tr->reveal_counts + size_t(b + 1) * tr->max_steps, 0);
+                if (tr->n_reveal_counts) tr->n_reveal_counts[b] = 0;
+                if (tr->first_step_sites) std::fill(tr->first_step_sites + size_t(b) * n, tr->first_step_sites + size_t(b + 1) * n, 0);
+            }
+        const int chunk = std::max(1, chunk_bins(*c, K));
+        for (auto& [nl, bins] : buckets) {
+            cider_schedule rs = *sched;
+            rs.steps = remask_steps(sched->steps, nl, K);
+            for (size_t i0 = 0; i0 < bins.size(); i0 += size_t(chunk)) {
+                const int m = int(std::min(bins.size() - i0, size_t(chunk)));
+                const int* bb = bins.data() + i0;
+                WS w = workspace(*c, m, K, final_logits != nullptr);
+                std::vector<float> Sh(size_t(m) * L * Q);
+                std::vector<int32_t> Xh(size_t(m) * n), init(m, nl * L);
+                std::vector<uint32_t> upd(m);
+                for (int i = 0; i < m; ++i) {
+                    const int b = bb[i];
+                    std::copy(S + size_t(b) * L * Q, S + size_t(b + 1) * L * Q, Sh.begin() + size_t(i) * L * Q);
+                    upd[i] = low[b];
+                    for (int k = 0; k < K; ++k) // internal layout (slot, row); low rows masked
+                        for (int l = 0; l < L; ++l)
+                            Xh[size_t(i) * n + size_t(l) * K + k] = ((low[b] >> k) & 1u) ? -1 : grid_in[size_t(b) * n + size_t(k) * L + l];
+                }
+                ck(cudaMemcpyAsync(w.S, Sh.data(), Sh.size() * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+                ck(cudaMemcpyAsync(w.X, Xh.data(), Xh.size() * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+                ck(cudaMemcpyAsync(w.init_masked, init.data(), size_t(m) * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+                ck(cudaMemcpyAsync(w.upd, upd.data(), size_t(m) * 4, cudaMemcpyHostToDevice, c->stream), "h2d");
+                ChunkTrace ct;
+                PassTrace pt;
+                if (tr) {
+                    ct.max_steps = std::max(0, tr->max_steps);
+                    ct.pass_first.assign(size_t(m) * NP, 0);
+                    ct.n_passes.assign(m, 0);
+                    ct.counts.assign(size_t(m) * ct.max_steps, 0);
+                    ct.n_counts.assign(m, 0);
+                    ct.sites.assign(size_t(m) * n, 0);
+                    pt = pass_trace(*c, m, rs.steps, K);
+                }
+                masked_pass(*c, w, m, K, w.S, w.X, rs.steps, rs, tr ? &pt : nullptr);
+                if (tr) trace_pass(*c, ct, pt, m, rs.steps, K, nullptr);
+                ck(cudaMemcpyAsync(Xh.data(), w.X, Xh.size() * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+                std::vector<float> fl;
+                if (final_logits) {
+                    fl.resize(size_t(m) * n * Q);
+                    ck(cudaMemcpyAsync(fl.data(), w.flog, fl.size() * 4, cudaMemcpyDeviceToHost, c->stream), "d2h");
+                }
+                ck(cudaStreamSynchronize(c->stream), "remask_pass");
+                for (int i = 0; i < m; ++i) {
+                    const int b = bb[i];
+                    for (int k = 0; k < K; ++k) {
+                        if (!((low[b] >> k) & 1u)) continue; // clamped rows stay bit-identical (refine.cpp:270-273)
+                        for (int l = 0; l < L; ++l) grid_out[size_t(b) * n + size_t(k) * L + l] = Xh[size_t(i) * n + size_t(l) * K + k];
+                    }
+                    if (final_logits)
+                        for (int k = 0; k < K; ++k)
+                            for (int l = 0; l < L; ++l)
+                                std::copy(fl.begin() + (size_t(i) * n + size_t(l) * K + k) * Q, fl.begin() + (size_t(i) * n + size_t(l) * K + k + 1) * Q,
+                                          final_logits + (size_t(b) * n + size_t(k) * L + l) * Q);
+                    if (!tr) continue;
+                    if (tr->first_reveals) tr->first_reveals[b] = ct.pass_first[size_t(i) * NP];
+                    if (tr->remask_rows) tr->remask_rows[size_t(b) * CIDER_MAX_THRESHOLDS] = nl;
+                    if (tr->remask_steps) tr->remask_steps[size_t(b) * CIDER_MAX_THRESHOLDS] = rs.steps;
+                    if (tr->pass_first_reveals) tr->pass_first_reveals[size_t(b) * NP] = ct.pass_first[size_t(i) * NP];
+                    if (tr->n_passes) tr->n_passes[b] = 1;
+                    if (tr->reveal_counts && ct.max_steps > 0)
+                        std::copy(ct.counts.begin() + size_t(i) * ct.max_steps, ct.counts.begin() + size_t(i + 1) * ct.max_steps,
+                                  tr->reveal_counts + size_t(b) * ct.max_steps);
+                    if (tr->n_reveal_counts) tr->n_reveal_counts[b] = ct.n_counts[i];
+                    if (tr->first_step_sites)
+                        for (int l = 0; l < L; ++l)
+                            for (int k = 0; k < K; ++k)
+                                tr->first_step_sites[size_t(b) * n + size_t(k) * L + l] = ct.sites[size_t(i) * n + size_t(l) * K + k];
+                }
+            }
+        }
+        resolve_stats(*c);
     });
 }
 
@@ -2270,6 +2330,19 @@ int cider_workload_bins_device(const cider_workload_desc* w, const int32_t* edge
         check_launch("workload_bins");
         ck(cudaDeviceSynchronize(), "workload_bins");
         di.release(); dp.release(); dr.release(); dm.release();
+    });
+}
+
+int cider_grid_pack_u8(cider_ctx* c, const int32_t* grid_device, uint8_t* out_device, size_t n) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        if (c->Q > 256) throw InvalidInput("grid_pack_u8: Q > 256");
+        if ((reinterpret_cast<uintptr_t>(grid_device) & 15) || (reinterpret_cast<uintptr_t>(out_device) & 3))
+            throw InvalidInput("grid_pack_u8: grid must be 16-byte and output 4-byte aligned");
+        if (!n) return;
+        pack_u8_kernel<<<blocks_for(int64_t((n + 3) / 4)), 256, 0, c->stream>>>(grid_device, out_device, int64_t(n));
+        ++c->launches;
+        check_launch("pack_u8");
     });
 }
 

@@ -40,7 +40,6 @@ struct GrpArgs {
     int out_rows_per_bin;             // L (site output) or E (edge output)
     const int* out_row;               // [groups]: output row block (edge or slot index)
     int D;
-    int mchunk;                       // T-resident kernel: m-tiles per sweep chunk
     bf16* out_t;                      // bf16 output [bins * out_rows_per_bin * K x D]
     float* out_f;                     // optional fp32 copy
 };
@@ -171,169 +170,6 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         }
     }
     __syncthreads();
-    if (warp == 1) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Lay::TMEM_COLS));
-    }
-}
-
-// ---- cluster-pair variant (the message GEMM, group = slot, segments = its edges) -----------------
-// The kernel is L2-bound on the T_alpha stream (per 128-row tile 3 x 128 KB of T against 3 x 64 KB of
-// gathered A). Two CTAs of a cluster take the same group for two neighbouring m-tiles: rank 0 loads
-// each T k-block ONCE with a cluster multicast into both CTAs' stage, each CTA loads its own A rows
-// and runs its own 1-SM MMAs; a stage is refilled once BOTH CTAs' MMAs have read it (every MMA commit
-// arrives on the empty barrier of both CTAs). Half the T bytes per tile leave L2.
-__device__ __forceinline__ uint32_t cl_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                     smem_u32(bar)),
-                 "h"(mask)
-                 : "memory");
-}
-__device__ __forceinline__ void cl_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GRP_THREADS, 1)
-gemm_grp_mc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT, const GrpArgs args) {
-    constexpr int BN = 256;
-    using Lay = SmemLayout<BN, 0>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // same offset in both CTAs
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = cl_rank();
-    const int cid = int(blockIdx.x) / 2, ncl = int(gridDim.x) / 2;
-    const int mpairs = (args.mtiles + 1) / 2;
-    const int supers = args.groups * mpairs;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 2); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 256); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "n"(Lay::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    fence_before();
-    cl_sync(); // both CTAs' barriers initialised before any multicast lands
-    fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    const int a_bytes = args.K * args.bb * 128;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int st = cid; st < supers; st += ncl) {
-                const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
-                const int nseg = args.seg_count[g];
-                for (int sg = 0; sg < nseg; ++sg) {
-                    const int arow = args.seg_arow[g * args.max_seg + sg];
-                    const int alpha = args.seg_alpha[g * args.max_seg + sg];
-                    for (int kk = 0; kk < args.kb_per_seg; ++kk) {
-                        mbar_wait(&empty[stage], phase ^ 1); // both CTAs' MMAs are done with this stage
-                        uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
-                        uint8_t* sb = sa + Lay::A_BYTES;
-                        mbar_expect_tx(&full[stage], a_bytes + Lay::B_BYTES);
-                        tma_load_3d(sa, &tmA, &full[stage], kk * 64, arow * args.K, mt * args.bb); // (zero rows past the bins)
-                        if (rank == 0) tma_load_3d_mc(sb, &tmT, &full[stage], kk * 64, 0, alpha, uint16_t(3));
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(BM, BN);
-            int stage = 0, acc = 0;
-            uint32_t phase = 0, acc_phase = 0;
-            for (int st = cid; st < supers; st += ncl) {
-                const int g = st % args.groups;
-                const int kblocks = args.seg_count[g] * args.kb_per_seg;
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                fence_after();
-                const uint32_t d = tmem_base + uint32_t(acc * BN);
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    fence_after();
-                    uint8_t* sa = smem + stage * Lay::STAGE_BYTES;
-                    uint8_t* sb = sa + Lay::A_BYTES;
-                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
-#pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
-                    mma_commit_mc(&empty[stage], uint16_t(3)); // both CTAs may refill (T lands in both)
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-                mma_commit(&tfull[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            }
-        }
-    } else {
-        const int quarter = warp % 4;
-        const int half = (warp - 2) / 4; // the two warps of a lane quarter split the columns
-        const int row = quarter * 32 + lane;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int st = cid; st < supers; st += ncl) {
-            const int g = st % args.groups, mt = 2 * (st / args.groups) + int(rank);
-            mbar_wait(&tfull[acc], acc_phase);
-            fence_after();
-            const int b = mt * args.bb + row / args.K, k = row % args.K;
-            const bool live = row < args.K * args.bb && b < args.bins;
-            const size_t orow = (size_t(b) * args.out_rows_per_bin + __ldg(args.out_row + g)) * args.K + k;
-            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-            const int cw = args.D / 2;
-            for (int c0 = half * cw; c0 < (half + 1) * cw; c0 += 32) {
-                float v[32];
-                tmem_ld32(tbase + c0, v);
-                if (!live) continue;
-                if (args.out_f) {
-                    float* o = args.out_f + orow * args.D + c0;
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                }
-                bf16* o = args.out_t + orow * args.D + c0;
-#pragma unroll
-                for (int i = 0; i < 32; i += 8) {
-                    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[i], v[i + 1]);
-                    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-                    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]);
-                    __nv_bfloat162 p3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-                    uint4 u;
-                    u.x = *reinterpret_cast<uint32_t*>(&p0);
-                    u.y = *reinterpret_cast<uint32_t*>(&p1);
-                    u.z = *reinterpret_cast<uint32_t*>(&p2);
-                    u.w = *reinterpret_cast<uint32_t*>(&p3);
-                    *reinterpret_cast<uint4*>(o + i) = u;
-                }
-            }
-            fence_before();
-            mbar_arrive(&tempty[acc]);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        }
-    }
-    fence_before();
-    cl_sync(); // the peer may still multicast into this CTA's stages or arrive on its barriers
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Lay::TMEM_COLS));
@@ -696,201 +532,6 @@ gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
 }
 template <int D>
 constexpr int grp2_res_smem() { return (D / 64) * (D / 2) * 64 * 2 + 8 * BM * BK * 2 + 2 * 16384 + 256 + 1024; }
-
-// ---- T-resident variant for single-segment groups (the normalise GEMM, group = edge) ------------
-// The m-tiles are swept in chunks of `mchunk` (128 bins at K = 8: 32 MB of z~, L2-resident); inside a
-// chunk every CTA takes an equal contiguous range of (group, m-tile) work, group-major, so its
-// coefficient action T_alpha (D x D bf16, 128 KB for D = 256) is loaded once per group change and
-// stays resident while only the gathered A rows stream (64 KB per 128-row tile against 2K cycles of
-// MMA). All CTAs work on the same chunk at once, so the z~ rows a slot shares among its (column
-// weight) edges come from DRAM once and from L2 for the other edges. The epilogue stages each warp's
-// 32 x 32 bf16 block in SMEM and writes whole 64-byte row segments.
-//
-// mchunk < 0 (default): "laps" — CTA c takes group c of each full lap of gridDim.x groups over ALL
-// m-tiles (groups are slot-major, so the column-weight edges of a slot run on neighbouring CTAs at
-// the same m-tile at the same time and share the gathered z~ rows through L2: DRAM reads them once
-// instead of once per edge), then the remaining groups split their m-tile range across the CTAs.
-// One T_alpha per lap per CTA.
-template <typename F>
-__device__ __forceinline__ void grp_res_sweep(const GrpArgs& args, F&& body) {
-    if (args.mchunk < 0) {
-        const int G = args.groups, C = int(gridDim.x), c = int(blockIdx.x);
-        int g0 = 0;
-        for (; G - g0 >= C; g0 += C)
-            for (int mt = 0; mt < args.mtiles; ++mt) body(g0 + c, mt);
-        const int rem = G - g0;
-        if (rem > 0) {
-            const int R = max(1, C / rem);
-            if (c < rem * R) {
-                const int part = c / rem, g = g0 + c % rem;
-                const int m0 = int(int64_t(part) * args.mtiles / R), m1 = int(int64_t(part + 1) * args.mtiles / R);
-                for (int mt = m0; mt < m1; ++mt) body(g, mt);
-            }
-        }
-        return;
-    }
-    for (int c0 = 0; c0 < args.mtiles; c0 += args.mchunk) {
-        const int mc = min(args.mchunk, args.mtiles - c0);
-        const int tot = args.groups * mc;
-        const int u0 = int(int64_t(blockIdx.x) * tot / gridDim.x), u1 = int(int64_t(blockIdx.x + 1) * tot / gridDim.x);
-        for (int u = u0; u < u1; ++u) body(u / mc, c0 + u % mc);
-    }
-}
-struct GrpResLayout {
-    static constexpr int T_OFF = 0;                 // 4 k-blocks x (256 x 64 bf16)
-    static constexpr int A_OFF = 4 * 32768;         // ring of A k-blocks, 16 KB each
-    static constexpr int NST = 4;
-    static constexpr int STG_OFF = A_OFF + NST * 16384; // 2 x 16 KB output k-block staging (SW128, TMA store)
-    static constexpr int BAR_OFF = STG_OFF + 2 * 16384;
-    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
-};
-
-template <int D>
-__global__ void __launch_bounds__(GRP_THREADS, 1)
-gemm_grp_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmT,
-                    const __grid_constant__ CUtensorMap tmO, const GrpArgs args) {
-    using Lay = GrpResLayout;
-    constexpr int BN = D;                // N = D (one tile covers the whole row)
-    constexpr int NKB = D / 64;          // k-blocks of A and of T
-    constexpr int TKB = D * 64 * 2;      // bytes of one T k-block (D rows x 64)
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u); // 1 KB aligned, stays in the shared window
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lay::BAR_OFF);
-    uint64_t* empty = full + Lay::NST;
-    uint64_t* t_full = empty + Lay::NST;
-    uint64_t* t_empty = t_full + 1;
-    uint64_t* afull = t_empty + 1;   // [2] accumulator ready
-    uint64_t* aempty = afull + 2;    // [2] accumulator drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < Lay::NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        mbar_init(t_full, 1);
-        mbar_init(t_empty, 1);
-        for (int a = 0; a < 2; ++a) { mbar_init(&afull[a], 1); mbar_init(&aempty[a], 256); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    fence_before();
-    __syncthreads();
-    fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    const int a_bytes = args.K * args.bb * 128;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0, cur = -1;
-            uint32_t phase = 0, teph = 0;
-            grp_res_sweep(args, [&](int g, int mt) {
-                const int alpha = args.seg_alpha[g * args.max_seg];
-                if (alpha != cur) { // new coefficient action: wait until the MMAs on the old one retired
-                    if (cur >= 0) { mbar_wait(t_empty, teph); teph ^= 1; }
-                    mbar_expect_tx(t_full, NKB * TKB);
-                    for (int kb = 0; kb < NKB; ++kb) tma_load_3d(smem + Lay::T_OFF + kb * TKB, &tmT, t_full, kb * 64, 0, alpha);
-                    cur = alpha;
-                }
-                const int arow = args.seg_arow[g * args.max_seg];
-                for (int kb = 0; kb < NKB; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], a_bytes);
-                    tma_load_3d(smem + Lay::A_OFF + stage * 16384, &tmA, &full[stage], kb * 64, arow * args.K, mt * args.bb);
-                    if (++stage == Lay::NST) { stage = 0; phase ^= 1; }
-                }
-            });
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(BM, BN);
-            int stage = 0, acc = 0, cur = -1;
-            uint32_t phase = 0, acc_phase = 0, tfph = 0;
-            grp_res_sweep(args, [&](int g, int) {
-                const int alpha = args.seg_alpha[g * args.max_seg];
-                if (alpha != cur) {
-                    if (cur >= 0) mma_commit(t_empty); // fires once every MMA on the old T has completed
-                    mbar_wait(t_full, tfph);
-                    tfph ^= 1;
-                    fence_after();
-                    cur = alpha;
-                }
-                mbar_wait(&aempty[acc], acc_phase ^ 1);
-                fence_after();
-                const uint32_t d = tmem_base + uint32_t(acc * BN);
-                for (int kb = 0; kb < NKB; ++kb) {
-                    mbar_wait(&full[stage], phase);
-                    fence_after();
-                    const uint64_t da = sw128_desc(smem + Lay::A_OFF + stage * 16384);
-                    const uint64_t db = sw128_desc(smem + Lay::T_OFF + kb * TKB);
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) mma_bf16(d, da + uint64_t(kk * 2), db + uint64_t(kk * 2), idesc, (kb | kk) != 0);
-                    mma_commit(&empty[stage]);
-                    if (++stage == Lay::NST) { stage = 0; phase ^= 1; }
-                }
-                mma_commit(&afull[acc]);
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            });
-        }
-    } else {
-        const int quarter = warp % 4;
-        const int half = (warp - 2) / 4; // 32-column half of every 64-column output k-block
-        const bool issuer = warp == 2 && lane == 0;
-        int acc = 0, step = 0;
-        uint32_t acc_phase = 0;
-        // Output k-block kb (128 rows x 64 columns) is staged by all 8 warps in a 16 KB SW128 block
-        // (double-buffered) and leaves as ONE TMA store of the 3-D rows box {64, K, bb} (whole
-        // 128-byte lines; was 64-byte segments per 4 lanes). Named barrier 1 (the 256 epilogue
-        // threads): staged -> store issued and the buffer of two steps ago read out.
-        grp_res_sweep(args, [&](int g, int mt) {
-            mbar_wait(&afull[acc], acc_phase);
-            fence_after();
-            const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-            const int orow_g = __ldg(args.out_row + g);
-            const int r = quarter * 32 + lane; // this thread's tile row
-#pragma unroll 1
-            for (int kb = 0; kb < args.D / 64; ++kb, ++step) {
-                float v[32];
-                tmem_ld32(tbase + kb * 64 + half * 32, v);
-                if (kb == args.D / 64 - 1) { // accumulator drained
-                    fence_before();
-                    mbar_arrive(&aempty[acc]);
-                }
-                uint8_t* stg = smem + Lay::STG_OFF + (step & 1) * 16384;
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                    uint32_t pk[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        __nv_bfloat162 p = __floats2bfloat162_rn(v[jj * 8 + 2 * q], v[jj * 8 + 2 * q + 1]);
-                        pk[q] = *reinterpret_cast<uint32_t*>(&p);
-                    }
-                    const int j = half * 4 + jj;
-                    *reinterpret_cast<uint4*>(stg + r * 128 + ((j ^ (r & 7)) * 16)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-                if (issuer) {
-                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                                     reinterpret_cast<uint64_t>(&tmO)),
-                                 "r"(smem_u32(stg)), "r"(kb * 64), "r"(orow_g * args.K), "r"(mt * args.bb)
-                                 : "memory");
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); // the other buffer is free
-                }
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-            }
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        });
-        if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == 1) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
-    }
-}
 
 } // namespace tc
 } // namespace cider

@@ -78,7 +78,6 @@ struct MlpArgs {
     int M, K0, H, tiles;
     const float* b1;
     long long* trace; // debug (CIDER_TRACE_MLP): per-chunk clock64 stamps of CTA 0, else null
-    int dbg;          // debug ablations (CIDER_MLP_DBG): 1 = skip GELU work, 2 = skip final epilogue
     Epi ep; // final epilogue (bias = b2)
 };
 

@@ -208,9 +208,7 @@ __device__ __forceinline__ void tmem_wait_ld32(uint32_t (&r)[32]) {
                  : "memory");
 }
 
-#ifndef MLP2_NS_CAP
-#define MLP2_NS_CAP 16 // weight-ring slots at most (else as many as the shared memory holds)
-#endif
+constexpr int MLP2_NS_CAP = 16; // weight-ring slots at most (else as many as the shared memory holds)
 template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1, int BIASB = 4 * D>
 struct Mlp2Layout {
     static constexpr int STG_WARP = STGW;
@@ -243,31 +241,12 @@ struct Mlp2Layout {
 // [16][33] fp32 staging block per warp; the GELU variants run 8 with 4 KB each.
 constexpr int DEMIX_STG_WARP = 16 * 33 * 4;
 // 16 epilogue warps in every variant: demix = 16 warps on every phase; GELU variants = warps 2-9 on
-// the hidden chunks and warps 10-17 on the final epilogue (which then overlaps the next tile's chunks)
-// MLP2_GELU16: the GELU variants run 16 hidden-chunk warps (4 per lane quarter, 32 columns each, the
-// demix layout) + 8 final-epilogue warps; else 8 hidden-chunk warps (64 columns each) + 8 final.
-#ifndef MLP2_GELU16
-#define MLP2_GELU16 0 // measured slower (c5: agg 356 -> 390 ms; the 72-register cap of 896 threads)
-#endif
-// MLP2_AGG_MERGED: the aggregator runs its 16 epilogue warps on both phases (32 hidden columns per
-// warp per chunk, the demix layout, then one output k-block each): half the GELU latency per chunk
-#ifndef MLP2_FIN_PREFETCH
-#define MLP2_FIN_PREFETCH 0 // measured neutral (c5: gate 205 -> 202 ms, fusion unchanged, step within noise)
-#endif
-// MLP2_FUSE_FOLDZ: the fusion's residual z enters acc2 before the tile's first MMA2 (the final
-// warps tcgen05.st it as fp32 right after draining the previous tile), the output leaves from
-// registers, so the whole row tile is free once the tile's last MMA1 has read it and the next
-// tile's rows load during the last chunks instead of after the final epilogue
-// Measured neutral (c5 fusion 197 -> 199 ms): the transition shrinks (last MMA1 -> next first MMA1
-// 12.4k -> 5.6k cycles), but the final warps' drain + per-row 16-byte global stores + z load take
-// ~9k cycles and the next tile's first MMA2 waits for them (tests/trace_mlp.py)
-#ifndef MLP2_FUSE_FOLDZ
-#define MLP2_FUSE_FOLDZ 0
-#endif
-#ifndef MLP2_AGG_MERGED
-#define MLP2_AGG_MERGED 0 // measured slower (c5: agg 356 -> 415 ms)
-#endif
-constexpr int MLP2_HW = MLP2_GELU16 ? 16 : 8;            // hidden-chunk warps of the GELU variants
+// the hidden chunks (64 columns each) and warps 10-17 on the final epilogue (which then overlaps the
+// next tile's chunks). Measured and dropped (round 1): 16 hidden-chunk warps (the 72-register cap of
+// 896 threads), the aggregator's 16 warps on both phases, the gate / fusion final epilogue with the
+// next TMEM load in flight, the fusion residual folded into acc2, register-direct gate / fusion
+// stores, an L2 prefetch of the next row tile, a polynomial exp2 for half of the demix groups.
+constexpr int MLP2_HW = 8;                                 // hidden-chunk warps of the GELU variants
 constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : MLP2_HW + 8; }
 constexpr int MLP2_FIN_WARP0 = 2 + MLP2_HW;
 constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
@@ -303,30 +282,6 @@ __device__ __forceinline__ void demix_load_sv(const MlpArgs& args, int m0, int c
             const int r0 = m0 + rh * 16 + t * KK;
             sv[p * NGL + t] = r0 < args.ep.M ? __ldg(args.ep.S + size_t(r0 / KK) * args.H + col0 + p * 16 + cl) : 0.0f;
         }
-}
-
-// 2^x for x <= 0 (the demix arguments are max-subtracted). MLP2_DEMIX_POLYEXP: every other row group
-// (a whole (bin, slot) group, so the softmax stays bitwise invariant to the order of its rows) on
-// the FMA pipe (Cody-Waite split, degree-5 minimax polynomial on [0,1), exponent by integer add; rel.
-// error < 2e-7, below the bf16 output rounding), the rest on MUFU ex2 — halves the MUFU load.
-#ifndef MLP2_DEMIX_POLYEXP
-#define MLP2_DEMIX_POLYEXP 0 // measured slower (demix_evid 62 -> 67.5 ms per c5 step: not MUFU-bound)
-#endif
-__device__ __forceinline__ float exp2_poly(float x) {
-    x = fmaxf(x, -126.0f);
-    const float fi = floorf(x);
-    const float f = x - fi; // [0, 1)
-    float p = 1.8775767e-3f;
-    p = fmaf(p, f, 8.9893397e-3f);
-    p = fmaf(p, f, 5.5826318e-2f);
-    p = fmaf(p, f, 2.4015361e-1f);
-    p = fmaf(p, f, 6.9315308e-1f);
-    p = fmaf(p, f, 9.9999994e-1f);
-    return __int_as_float(__float_as_int(p) + (int(fi) << 23));
-}
-__device__ __forceinline__ float demix_exp2(float x, int group) {
-    if (MLP2_DEMIX_POLYEXP && (group & 1)) return exp2_poly(x);
-    return ex2_approx(x);
 }
 
 template <int KK>
@@ -369,7 +324,7 @@ __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, ui
             uint32_t den = 0;
 #pragma unroll
             for (int k = 0; k < KK; ++k) {
-                const float e = demix_exp2(fmaf(xv[t * KK + k], scale2, nmx), t); // one method per (bin, slot) group
+                const float e = ex2_approx(fmaf(xv[t * KK + k], scale2, nmx));
                 xv[t * KK + k] = e;
                 den += __float_as_uint(fmaf(e, 4194304.0f, 8388608.0f)) - 0x4B000000u; // round(e 2^22)
             }
@@ -426,8 +381,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint64_t* a2_full = a1_free + 2;
     uint64_t* a2_empty = a2_full + 1;
     uint64_t* o_full = a2_empty + 1;    // [NXB][KBD] output block staged in X k-block kb (4 quarter warps)
-    uint64_t* z_ready = o_full + NXB * KBD; // FOLDZ: the tile's first MMA1 done (its z k-blocks landed), both CTAs
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(z_ready + 1);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + NXB * KBD);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
@@ -435,19 +389,12 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int NC = args.H / MLP_HC;
     constexpr int EPI_ARRIVALS = 2 * EW; // one elected lane per epilogue warp, both CTAs
-    // hidden group g: GELU = 16 columns of both 64-column warp halves (all epilogue warps); demix =
-    // the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
-    // hidden group g: one warp per quarter x 2 CTAs (32-column warps), or the 8 hidden warps x 2 CTAs
-    constexpr bool MERGED = MLP2_AGG_MERGED && !MLP2_GELU16 && EPK == EP_STORE;
-    constexpr bool W32 = EPK == EP_DEMIX || MLP2_GELU16 || MERGED; // 32-column hidden warps
-    constexpr int H_ARRIVALS = W32 ? 8 : 8 * 2;
-    // Final epilogue: the aggregator (double-buffered rows) runs it on warps 10-17 only, overlapping the
-    // next tile's chunks; gate / fusion (whose next row tile waits for it) on all 16 epilogue warps, one
-    // output k-block each, to shorten the tile transition.
-    constexpr bool FIN_ALL = MERGED; // (all 16 warps on the gate / fusion final epilogue measured no faster)
-    constexpr int FIN_STRIDE = FIN_ALL ? 4 : 2;                  // output k-blocks between one warp's
-    constexpr int FIN_WARPS = FIN_ALL ? (4 * KBD < 16 ? 4 * KBD : 16) : 8;
-    constexpr int A2_ARRIVALS = EPK == EP_DEMIX ? EPI_ARRIVALS : FIN_WARPS * 2; // warps that drain acc2
+    // hidden group g: GELU = 16 columns of both 64-column warp halves (the 8 hidden warps x 2 CTAs);
+    // demix = the 32 columns of one warp per quarter (4 quarters x 2 CTAs)
+    constexpr int H_ARRIVALS = EPK == EP_DEMIX ? 8 : 8 * 2;
+    // Final epilogue on warps 10-17 (gate / fusion / aggregator), overlapping the next tile's chunks
+    constexpr int FIN_STRIDE = 2;                                // output k-blocks between one warp's
+    constexpr int A2_ARRIVALS = EPK == EP_DEMIX ? EPI_ARRIVALS : 8 * 2; // warps that drain acc2
 
     // Gate / fusion epilogues read z (and e) from global memory (L2: the same rows were just TMA'd
     // into X), so every X k-block is free once the tile's last MMA1 has read it and the next tile's
@@ -458,40 +405,20 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     // runs over the input k-blocks starting at the second half ([e | z] order): the next tile's
     // e / acc k-blocks load during the final epilogue and the first MMA1 starts on them.
     constexpr int ROT = reads_z ? KBD : 0;
-    // MLP2_ZREG: gate / fusion results leave from registers (32-byte stores) and their z / e k-blocks are
-    // released as soon as the final epilogue has read them (no output staging in X); else staged in X
-    // and TMA-stored by the X producer
-#ifndef MLP2_XPREFETCH
-#define MLP2_XPREFETCH 0 // no measurable effect on c5 (gate 202 ms either way)
-#endif
-// Issue loops run by the whole warp (bit 0: MMA1 issuer, bit 1: MMA2 issuer; lane 0 issues) or by
-// lane 0 alone, per variant
-#ifndef MLP2_WI_AGG
-#define MLP2_WI_AGG 3
-#endif
-#ifndef MLP2_WI_GF
-#define MLP2_WI_GF 0
-#endif
-#ifndef MLP2_WI_DEMIX
-#define MLP2_WI_DEMIX 3
-#endif
-#ifndef MLP2_ZREG
-#define MLP2_ZREG 0 // measured slower (c5: gate 205 -> 227 ms, fusion 196 -> 214 ms)
-#endif
-    constexpr bool FOLDZ = MLP2_FUSE_FOLDZ && EPK == EP_RESID && NXB == 1;
-    constexpr bool XST = !(reads_z && MLP2_ZREG) && !FOLDZ; // output staged in X (demix: e in the spent Z tile)
+    // Issue loops run by the whole warp (bit 0: MMA1 issuer, bit 1: MMA2 issuer; lane 0 issues) or by
+    // lane 0 alone, per variant (whole-warp loops: aggregator +2%, gate / fusion -10%)
+    constexpr int WI = EPK == EP_DEMIX ? 3 : KIN == D ? 3 : 0;
     // gate / fusion: the 8 final warps walk the output k-blocks together (each warp one 32-column half
     // of every k-block), so k-block 0 is staged, stored and refilled first and the next tile's first
     // MMA1 is fed k-block by k-block instead of in two rounds
-    constexpr bool KB_SEQ = reads_z && XST;
+    constexpr bool KB_SEQ = reads_z;
     constexpr int O_ARRIVALS = KB_SEQ ? 8 : 4;
     if (threadIdx.x == 0) {
         // x_empty: the last MMA1 of the tile (+ the gate's 4 warps that read that e k-block); the
         // output k-blocks are refilled by the X producer itself after storing them (o_full)
         for (int kb = 0; kb < NXB * KB1; ++kb) {
             mbar_init(&x_full[kb], 1);
-            mbar_init(&x_empty[kb], 1 + (FOLDZ ? (kb % KB1 < KBD ? 8 : 0)
-                                               : ((reads_e && kb % KB1 >= KBD) || (!XST && reads_z && kb % KB1 < KBD) ? O_ARRIVALS : 0)));
+            mbar_init(&x_empty[kb], 1 + ((reads_e && kb % KB1 >= KBD) ? O_ARRIVALS : 0));
         }
         for (int s = 0; s < NS; ++s) { mbar_init(&r_full[s], 1); mbar_init(&r_empty[s], 1); }
         for (int b = 0; b < 2; ++b) {
@@ -502,7 +429,6 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         mbar_init(a2_full, 1);
         mbar_init(a2_empty, A2_ARRIVALS);
         for (int kb = 0; kb < NXB * KBD; ++kb) mbar_init(&o_full[kb], O_ARRIVALS);
-        mbar_init(z_ready, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -606,7 +532,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 for (int kb0 = 0; kb0 < KBD; kb0 += KSTEP) {
                     if (KB1 > KBD)
                         for (int kb = KBD + kb0; kb < KBD + kb0 + KSTEP; ++kb) load_kb(kb);
-                    if (XST && itx >= NXB) {
+                    if (itx >= NXB) {
                         for (int kb = kb0; kb < kb0 + KSTEP && kb < KBD; ++kb) {
                             mbar_wait(&o_full[xb * KBD + kb], oph);
                             tma_store_2d(&tmO, xsb + kb * 16384, kb * 64, prev_row0);
@@ -616,19 +542,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     }
                     for (int kb = kb0; kb < kb0 + KSTEP && kb < KBD; ++kb) load_kb(kb);
                 }
-                // single-buffered rows: pull the next tile's rows into L2 now, so that its refill at the
-                // tile transition (all CTAs at once) reads L2 instead of bursting on HBM
-                if (NXB == 1 && MLP2_XPREFETCH && tile + npairs < args.tiles) {
-                    const int nrow0 = row0 + npairs * 256;
-                    for (int kb = 0; kb < KB1; ++kb) {
-                        const int k = kb * 64;
-                        if (k < args.K0) tma_prefetch_2d(&tmX0, k, nrow0);
-                        else tma_prefetch_2d(&tmX1, k - args.K0, nrow0);
-                    }
-                }
                 if (NXB == 1) eph ^= 1;
             }
-            if constexpr (XST) { // the last NXB tiles' outputs
+            { // the last NXB tiles' outputs
                 for (int q = 0; q < NXB; ++q) {
                     const int itl = itx - NXB + q; // tile index (per CTA) whose output is still staged
                     if (itl < 0) continue;
@@ -648,7 +564,6 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // barrier wait of a single issuing thread is a pipe bubble (tools/mma_bench.cu issue2_kernel:
         // 200-cycle waits per slot cost 22% with one issuer, 11% with two). Warp 1 issues the first
         // layer (acc1 buffers), warp 10 the second (acc2); a1_free orders MMA2(n) before MMA1(n+2).
-        constexpr int WI = EPK == EP_DEMIX ? MLP2_WI_DEMIX : KIN == D ? MLP2_WI_AGG : MLP2_WI_GF;
         const bool el = lane == 0;
         if (leader && (el || ((warp == 1 ? WI & 1 : WI & 2) != 0))) {
             auto ring_slot = [&](int gpos, uint32_t& ph) { ph = uint32_t(gpos / NS) & 1u; return gpos % NS; };
@@ -688,8 +603,6 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             if (el) mma_commit_2sm(&r_empty[slot]);
                         }
                         if (el) mma_commit_2sm(&a1_full[b]);
-                        if (FOLDZ && c == 0)
-                            if (el) mma_commit_2sm(z_ready); // this tile's z k-blocks are in both CTAs
                         if (c == NC - 1)
                             for (int kb = 0; kb < KB1; ++kb) if (el) mma_commit_2sm(&x_empty[xb * KB1 + kb]);
                         if (tr && it < 4) args.trace[it * 64 + c * 8 + 7] = clock64();
@@ -719,7 +632,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                     mbar_wait(&h_full[HG * b + 2 * g + j], (hph >> b) & 1u);
                                     fence_after();
                                     if (g == 0 && j == 0 && c == 0) {
-                                        mbar_wait(a2_empty, FOLDZ ? a2ph : a2ph ^ 1); // FOLDZ: acc2 = this tile's z first
+                                        mbar_wait(a2_empty, a2ph ^ 1);
                                         a2ph ^= 1;
                                         fence_after();
                                     }
@@ -734,31 +647,6 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                                     (c | g | j) != 0);
                                     if (j == 1 && g % 2 == 1) if (el) mma_commit_2sm(&r_empty[slot]);
                                 }
-                        } else if constexpr (W32) {
-                            // group g = hidden columns [32 g, 32 g + 32) of every quarter, packed at TMEM
-                            // columns 32 g + [0, 16): k-steps 2 g, 2 g + 1 of W2 k-block g / 2
-#pragma unroll
-                            for (int g = 0; g < MLP2_GG; ++g) {
-                                mbar_wait(&h_full[HG * b + g], (hph >> b) & 1u);
-                                fence_after();
-                                if (g == 0 && c == 0) {
-                                    mbar_wait(a2_empty, FOLDZ ? a2ph : a2ph ^ 1); // FOLDZ: acc2 = this tile's z first
-                                    a2ph ^= 1;
-                                    fence_after();
-                                }
-                                uint32_t ph;
-                                const int slot = ring_slot(it * per_tile + pos_w2(c) + g / 2, ph);
-                                if (g % 2 == 0) {
-                                    mbar_wait(&r_full[slot], ph);
-                                    fence_after();
-                                }
-                                const uint64_t db = sw128_desc(ring + slot * Lay::SLOT);
-#pragma unroll
-                                for (int j = 0; j < 2; ++j)
-                                    if (el) mma_bf16_2sm_ts(tmem, a_base + 32 * g + 8 * j, db + uint64_t(((g % 2) * 2 + j) * 2), id2,
-                                                    (c | g | j) != 0);
-                                if (g % 2 == 1) if (el) mma_commit_2sm(&r_empty[slot]);
-                            }
                         } else {
                         int slots[S2];
 #pragma unroll
@@ -768,7 +656,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             if (g == 0) {
                                 if (tr && it < 4) args.trace[it * 64 + c * 8 + 1] = clock64();
                                 if (c == 0) {
-                                    mbar_wait(a2_empty, FOLDZ ? a2ph : a2ph ^ 1); // FOLDZ: acc2 = this tile's z first
+                                    mbar_wait(a2_empty, a2ph ^ 1);
                                     a2ph ^= 1;
                                     fence_after();
                                 }
@@ -782,7 +670,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                     fence_after();
                                 }
                                 const uint64_t db = sw128_desc(ring + slots[kb] * Lay::SLOT);
-                                if (el) mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, FOLDZ || (c | kb | g) != 0);
+                                if (el) mma_bf16_2sm_ts(tmem, a_base + kb * 64 + g * 8, db + uint64_t(g * 2), id2, (c | kb | g) != 0);
                                 if (g == MLP2_GG - 1) if (el) mma_commit_2sm(&r_empty[slots[kb]]);
                             }
                         }
@@ -799,12 +687,11 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // 8 epilogue warps: TMEM lane quarter = warp % 4; the two warps of a quarter own the two
         // 64-column halves of every hidden chunk, and alternate 64-column k-blocks of the output.
         const int quarter = warp % 4;
-        const bool fin = EPK != EP_DEMIX && !MERGED && warp >= MLP2_FIN_WARP0; // final-epilogue-only warp
+        const bool fin = EPK != EP_DEMIX && warp >= MLP2_FIN_WARP0; // final-epilogue-only warp
         const int half = fin ? (warp - MLP2_FIN_WARP0) / 4 : (warp - 2) / 4;
         const int row = quarter * 32 + lane;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         uint32_t e1ph = 0, e2ph = 0; // e1ph bit b: phase of a1_full[b]
-        uint32_t zph = 0;            // FOLDZ: phase of z_ready
         const Epi& ep = args.ep;
         auto release = [&](uint32_t leader_bar) { // elected remote arrive once the whole warp is done
             __syncwarp();
@@ -881,41 +768,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 if (trf) args.trace[512 + it * 4 + 2] = clock64();
                 continue;
             }
-            if (!fin && W32)
-            for (int c = 0; c < NC; ++c, ++n) {
-                // 32-column warp: fp32 columns [32 half, 32 half + 32) -> GELU -> bf16 pairs packed IN
-                // PLACE at [32 half, 32 half + 16) (16-column group g' at + 8 g'), then one release
-                const int b = n & 1;
-                const float* b1 = args.b1 + c * MLP_HC + half * 32;
-                const bool tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
-                if (tr) args.trace[it * 64 + c * 8 + 2] = clock64();
-                mbar_wait(&a1_full[b], (e1ph >> b) & 1u);
-                e1ph ^= 1u << b;
-                fence_after();
-                if (tr) args.trace[it * 64 + c * 8 + 3] = clock64();
-                const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 32;
-#pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    float4 bias4[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
-                    float v[16];
-                    tmem_ld16(base + g * 16, v);
-                    uint32_t pk[8];
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        const float4 bb = bias4[i / 4];
-                        pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
-                        pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
-                    }
-                    tmem_st8(base + g * 8, pk);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                fence_before();
-                release(L_h_full0 + (HG * b + half) * 8); // this warp's 32 columns -> MMA2 k-steps 2 half, 2 half + 1
-                if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
-            }
-            if (!fin && !W32)
+            if (!fin)
             for (int c = 0; c < NC; ++c, ++n) {
                 const int b = n & 1;
                 const float* b1 = args.b1 + c * MLP_HC + half * 64;
@@ -930,7 +783,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 const uint32_t base = tmem + lane_off + 256 + b * MLP_HC + half * 64;
 #pragma unroll
                 for (int g = 0; g < MLP2_GG; ++g) {
-                    if (!(args.dbg & 1)) {
+                    {
                         float4 bias4[4]; // this group's 16 hidden biases (L1-resident)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
@@ -951,8 +804,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 }
                 if (tr) args.trace[it * 64 + c * 8 + 4] = clock64();
             }
-            if (!fin && !FIN_ALL) continue;
-            const int fsub = FIN_ALL ? (warp - 2) / 4 : half; // first output k-block of this warp
+            if (!fin) continue;
+            const int fsub = half; // first output k-block of this warp
             if (fsub >= KBD) continue;
             // final epilogue straight from TMEM: this thread's row, output k-blocks half, half + 2, ...
             // Gate / fusion read z (and e) from the tile's own X k-blocks in SMEM (X = [z | e] / [z~ | acc]:
@@ -961,142 +814,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             // store (SW128 box = the staging layout), so the epilogue warps never wait on HBM and the
             // write burst drains while the next tile's chunks run. A z / e k-block is handed back to the
             // X producer once the store out of it has been read.
-            const int m0w = tile * 256 + int(rank) * 128 + quarter * 32;
             uint8_t* xcur = xs + (it % NXB) * Lay::X_BYTES; // this tile's row buffer
             const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == MLP2_FIN_WARP0 + 2 && lane == 0;
             if (trf) args.trace[512 + it * 4 + 0] = clock64();
-            if constexpr (FOLDZ) {
-                // acc2 <- z of tile `zt` (fp32): this warp's 32 rows x its 32-column half of every output
-                // k-block, read from the tile's z k-blocks in X; then acc2 is handed to MMA2
-                auto zinit = [&](int zt) {
-                    mbar_wait(z_ready, zph);
-                    zph ^= 1;
-                    fence_after();
-                    const int zit = (zt - pair) / npairs;
-                    const uint8_t* xz = xs + (zit % NXB) * Lay::X_BYTES + quarter * 4096;
-#pragma unroll
-                    for (int kb = 0; kb < KBD; ++kb) {
-#pragma unroll
-                        for (int jj = 0; jj < 4; ++jj) {
-                            const int j = half * 4 + jj;
-                            uint32_t zq[4], zf[8];
-                            ld_shared_v4(xz + kb * 16384 + lane * 128 + ((j ^ (lane & 7)) * 16), zq);
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) { // bf16 pair -> two fp32 (exact)
-                                zf[2 * t] = zq[t] << 16;
-                                zf[2 * t + 1] = zq[t] & 0xFFFF0000u;
-                            }
-                            tmem_st8(tmem + lane_off + kb * 64 + half * 32 + jj * 8, zf);
-                        }
-                    }
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                    fence_before();
-                    __syncwarp();
-                    if (lane == 0)
-                        for (int kb = 0; kb < KBD; ++kb) mbar_arrive(&x_empty[(zit % NXB) * KB1 + kb]); // z read
-                    release(L_a2_empty); // acc2 = z: the tile's first MMA2 may accumulate onto it
-                };
-                if (tile == pair) zinit(tile);
-                mbar_wait(a2_full, e2ph);
-                e2ph ^= 1;
-                fence_after();
-                uint32_t ra[32];
-#pragma unroll 1
-                for (int kb = 0; kb < KBD; ++kb) {
-                    const int n0 = kb * 64 + half * 32;
-                    tmem_ld32_nw(tmem + lane_off + n0, ra);
-                    tmem_wait_ld32(ra);
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        const float4 bb = *reinterpret_cast<const float4*>(bias_s + n0 + i);
-                        const float2 lo = __fadd2_rn(make_float2(__uint_as_float(ra[i]), __uint_as_float(ra[i + 1])), make_float2(bb.x, bb.y));
-                        const float2 hi = __fadd2_rn(make_float2(__uint_as_float(ra[i + 2]), __uint_as_float(ra[i + 3])), make_float2(bb.z, bb.w));
-                        __nv_bfloat162 p0 = __floats2bfloat162_rn(lo.x, lo.y), p1 = __floats2bfloat162_rn(hi.x, hi.y);
-                        pk[i / 2] = *reinterpret_cast<uint32_t*>(&p0);
-                        pk[i / 2 + 1] = *reinterpret_cast<uint32_t*>(&p1);
-                    }
-                    if (m0w + lane < ep.M) { // this row's 64 bytes of the k-block half
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(ep.out_t) + size_t(m0w + lane) * ep.ldo + n0);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                    }
-                }
-                if (tile + npairs < args.tiles) zinit(tile + npairs); // drained above (waited loads): the next tile's z
-                continue;
-            }
             mbar_wait(a2_full, e2ph);
             e2ph ^= 1;
             fence_after();
             if (trf) args.trace[512 + it * 4 + 1] = clock64();
-            if constexpr (KB_SEQ && MLP2_FIN_PREFETCH) {
-                // gate / fusion: this warp's 32 columns of every output k-block in order, the TMEM load
-                // of k-block kb + 1 in flight while k-block kb is combined with z (and e) and staged
-                auto fin_block = [&](int kb, uint32_t (&r)[32]) {
-                    const int n0 = kb * 64;
-                    uint8_t* dst = xcur + kb * 16384 + quarter * 4096;
-                    const uint8_t* esrc = xcur + (KBD + kb) * 16384 + quarter * 4096;
-                    float v[32];
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        const float4 bb = *reinterpret_cast<const float4*>(bias_s + n0 + half * 32 + i);
-                        const float2 lo = __fadd2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(bb.x, bb.y));
-                        const float2 hi = __fadd2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), make_float2(bb.z, bb.w));
-                        v[i] = lo.x; v[i + 1] = lo.y; v[i + 2] = hi.x; v[i + 3] = hi.y;
-                    }
-#pragma unroll
-                    for (int jj = 0; jj < 4; ++jj) {
-                        const int j = half * 4 + jj;
-                        const uint32_t off = uint32_t(lane * 128 + ((j ^ (lane & 7)) * 16));
-                        uint32_t zq[4], eq[4] = {0u, 0u, 0u, 0u};
-                        ld_shared_v4(dst + off, zq);
-                        if (reads_e) ld_shared_v4(esrc + off, eq);
-                        uint32_t pk[4];
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const int i = jj * 8 + 2 * t;
-                            float2 a = make_float2(v[i], v[i + 1]);
-                            const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zq[t]));
-                            if (reads_e) {
-                                const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&eq[t]));
-                                const float2 h = __fmul2_rn(a, make_float2(0.5f, 0.5f));
-                                const float2 g = __ffma2_rn(make_float2(tanh_approx(h.x), tanh_approx(h.y)), make_float2(0.5f, 0.5f),
-                                                            make_float2(0.5f, 0.5f));
-                                a = __ffma2_rn(g, __fadd2_rn(z2, make_float2(-e2.x, -e2.y)), e2);
-                            } else {
-                                a = __fadd2_rn(a, z2);
-                            }
-                            __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
-                            pk[t] = *reinterpret_cast<uint32_t*>(&p);
-                        }
-                        st_shared_v4(dst + off, pk);
-                    }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]);
-                        mbar_arrive(&o_full[(it % NXB) * KBD + kb]);
-                    }
-                };
-                uint32_t ra[32], rb[32];
-                tmem_ld32_nw(tmem + lane_off + half * 32, ra);
-                tmem_wait_ld32(ra);
-#pragma unroll
-                for (int kb = 0; kb < KBD; ++kb) {
-                    uint32_t(&cur)[32] = (kb & 1) ? rb : ra;
-                    uint32_t(&nxt)[32] = (kb & 1) ? ra : rb;
-                    if (kb + 1 < KBD) {
-                        tmem_ld32_nw(tmem + lane_off + (kb + 1) * 64 + half * 32, nxt);
-                    } else {
-                        fence_before();
-                        release(L_a2_empty); // every acc2 load of this warp has completed
-                    }
-                    fin_block(kb, cur);
-                    if (kb + 1 < KBD) tmem_wait_ld32(nxt);
-                }
-                if (trf) args.trace[512 + it * 4 + 2] = clock64();
-                continue;
-            }
 #pragma unroll 1
             for (int kb = KB_SEQ ? 0 : fsub; kb < KBD; kb += KB_SEQ ? 1 : FIN_STRIDE) {
                 const int n0 = kb * 64;
@@ -1148,26 +872,15 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                             __nv_bfloat162 p = __floats2bfloat162_rn(a.x, a.y);
                             pk[t] = *reinterpret_cast<uint32_t*>(&p);
                         }
-                        if constexpr (XST) st_shared_v4(dst + off, pk);
-                        else if (m0w + lane < ep.M) // 16 bytes of this row; the 4 chunks of a half are one 64-byte run
-                            *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(ep.out_t) + size_t(m0w + lane) * ep.ldo + n0 + s2 * 32 + jj * 8) =
-                                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        st_shared_v4(dst + off, pk);
                     }
                 }
                 if (trf) args.trace[256 + it * 16 + (kb / 2) * 5 + 3] = clock64();
-                if constexpr (XST) {
-                    fence_proxy_async_smem(); // generic-proxy writes -> visible to the X producer's TMA store
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]); // e k-block read: the next tile's may load
-                        mbar_arrive(&o_full[(it % NXB) * KBD + kb]);   // output block staged
-                    }
-                } else {
-                    __syncwarp();
-                    if (lane == 0) { // z (and e) k-block read: the next tile's may load
-                        mbar_arrive(&x_empty[(it % NXB) * KB1 + kb]);
-                        if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]);
-                    }
+                fence_proxy_async_smem(); // generic-proxy writes -> visible to the X producer's TMA store
+                __syncwarp();
+                if (lane == 0) {
+                    if (reads_e) mbar_arrive(&x_empty[(it % NXB) * KB1 + KBD + kb]); // e k-block read: the next tile's may load
+                    mbar_arrive(&o_full[(it % NXB) * KBD + kb]);   // output block staged
                 }
             }
             if (trf) args.trace[512 + it * 4 + 2] = clock64();

@@ -811,6 +811,16 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restric
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) out[i] = __float2bfloat16_rn(in[i]);
 }
+// decoded grids as one byte per symbol (Q <= 256) for the final gather
+__global__ void pack_u8_kernel(const int* __restrict__ in, uint8_t* __restrict__ out, int64_t n) {
+    int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (i + 3 < n) {
+        const int4 v = *reinterpret_cast<const int4*>(in + i);
+        *reinterpret_cast<uchar4*>(out + i) = make_uchar4(uint8_t(v.x), uint8_t(v.y), uint8_t(v.z), uint8_t(v.w));
+    } else {
+        for (; i < n; ++i) out[i] = uint8_t(in[i]);
+    }
+}
 __global__ void flush_kernel(int4* __restrict__ p, int64_t n, int v) {
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) p[i] = make_int4(v, v, v, v);

@@ -16,7 +16,7 @@ Measured numbers go to the session's parity report ($CIDER_PARITY_REPORT).
 import numpy as np
 import pytest
 
-import teacher_forced as tf
+from oracle import teacher_forced as tf
 from conftest import rel_err
 
 pytestmark = pytest.mark.gpu
@@ -171,3 +171,74 @@ def test_large_grids_reveal(P, oracle, L, K):
     ro = oracle.refine(model, P.model_weights_as_run(model, w), e, wl.checks, wl.slots, S.astype(np.float64), K, sched)
     assert np.array_equal(g, ro["grid"])
     assert np.array_equal(tr["first_reveals"], ro["first_reveals"])
+
+
+def test_nccl_world1_gather_and_pack(P):
+    """cider_nccl_unique_id / init / allgather at world 1 (the gather bench.py closes its timed region
+    with) and the uint8 packing of decoded grids."""
+    import ctypes as C
+    lib = P.lib()
+    wl = P.Workload(m=4, slots=16, checks=8, k=3, snr_db=4.0)
+    model = P.Model(m=4, dim=32, hidden=32, layers=1, precision=P.FP32)
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    uid = C.create_string_buffer(128)
+    P._check(lib.cider_nccl_unique_id(uid))
+    P._check(lib.cider_nccl_init(ctx.h, uid.raw, 0, 1))
+    g = np.random.default_rng(0).integers(0, 16, size=(5, 3, 16)).astype(np.int32)
+    dg, du, dr = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    for p, n in ((dg, g.nbytes), (du, g.size), (dr, g.size)):
+        P._check(lib.cider_device_alloc(ctx.h, n, C.byref(p)))
+    P._check(lib.cider_memcpy_h2d(ctx.h, dg, g.ctypes.data_as(C.c_void_p), g.nbytes))
+    P._check(lib.cider_grid_pack_u8(ctx.h, dg, du, g.size))
+    P._check(lib.cider_nccl_allgather(ctx.h, du, dr, g.size))
+    out = np.empty(g.size, np.uint8)
+    P._check(lib.cider_memcpy_d2h(ctx.h, out.ctypes.data_as(C.c_void_p), dr, g.size))
+    P._check(lib.cider_synchronize(ctx.h))
+    assert np.array_equal(out.reshape(g.shape).astype(np.int32), g)
+
+
+def test_bench_line_small(P):
+    """bench.py end to end on a small c2 batch: one JSON line with the gather verified, launches counted,
+    the roofline and e2e keys present."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "c2", "--steps", "2", "--warmup", "1",
+                        "--bins-per-step", "256", "--no-cpu-baseline", "--no-parity"], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["gpu_launches"] > 0 and line["value"] > 0
+    assert line["nccl_gather"]["checksums_match"] is True, line["nccl_gather"]
+    assert {"roofline", "e2e", "clocks"} <= set(line)
+
+
+def test_remask_pass_caller_confidences_and_scorer(P, oracle):
+    """cider_remask_pass (ura::remask_pass with caller confidences) vs the oracle in FP32: identical grids,
+    bins without a low row untouched; and the reference's stage loop driven by a pluggable scorer
+    (run_with_remasking_scored) with MaxProbScorer equals the built-in threshold remasking."""
+    wl = P.Workload(m=6, slots=16, checks=8, k=4, snr_db=4.0, p_erase=0.1, p_false=0.1)
+    model = P.Model(m=6, dim=64, hidden=96, layers=2, heads=2, precision=P.FP32)
+    e = wl.code()
+    w = P.weights_init(model, 3)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    wr = P.model_weights_as_run(model, w)
+    _, S = wl.bins(e, 0, 6)
+    sched = P.RevealSchedule(steps=5)
+    g0 = ctx.refine(S, wl.k, sched)
+    conf = np.random.default_rng(1).random((6, wl.k))
+    conf[2] = 0.99  # no low row
+    g, fl = ctx.remask_pass(S, g0, conf, 0.5, sched, want_final_logits=True)
+    go, flo = oracle.remask_pass(model, wr, e, wl.checks, wl.slots, S.astype(np.float64), g0, conf, 0.5, sched)
+    assert np.array_equal(g, go)
+    assert np.array_equal(g[2], g0[2]) and np.isnan(fl[2]).all()
+    has = ~np.isnan(flo[:, 0, 0, 0])
+    assert rel_err(fl[has], flo[has]) < FP32_TOL
+    den = P.StructuredDenoiser(ctx)
+    thr = (0.6, 0.3)
+    a = P.run_with_remasking_scored(den, P.MaxProbScorer(), S, sched, thr, wl.k)
+    b = ctx.refine(S, wl.k, sched, P.RemaskConfig(thresholds=thr))
+    assert np.array_equal(a, b)

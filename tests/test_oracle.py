@@ -154,3 +154,19 @@ def test_oracle_threaded_forward_bitwise(P, oracle, reference):
         lg = oracle.denoise_batch(m, w, e, wl.checks, wl.slots, X, Sb, threads=threads)
         for b in range(3):
             assert np.array_equal(lg[b], reference.denoise(m, w, e, wl.checks, wl.slots, X[b], Sb[b]))
+
+
+def test_remask_pass_with_caller_confidences_vs_reference(P, oracle, reference):
+    """remask_pass on caller confidences (any ConfidenceScorer, refine.hpp:97-100): the restatement equals
+    ura::remask_pass bit for bit, including bins with no low row (returned unchanged)."""
+    m = P.Model(m=6, dim=24, hidden=32, layers=2, heads=2)
+    wl, e, _, S = small_case(P, k=4)
+    w = P.weights_init(m, 4).astype(np.float64)
+    sched = P.RevealSchedule(steps=5)
+    g0 = oracle.refine(m, w, e, wl.checks, wl.slots, S.astype(np.float64), 4, sched)["grid"]
+    conf = np.array([[0.9, 0.1, 0.6, 0.2], [0.9, 0.8, 0.7, 0.95]])
+    a, fa = oracle.remask_pass(m, w, e, wl.checks, wl.slots, S.astype(np.float64), g0, conf, 0.5, sched)
+    b, fb = reference.remask_pass(m, w, e, wl.checks, wl.slots, S.astype(np.float64), g0, conf, 0.5, sched)
+    assert np.array_equal(a, b) and np.array_equal(fa[0], fb[0])
+    assert np.array_equal(a[1], g0[1]) and np.isnan(fa[1]).all()   # no low row: untouched
+    assert np.array_equal(a[0][[0, 2]], g0[0][[0, 2]])             # clamped rows bit-identical

@@ -3,7 +3,7 @@ trajectories: the oracle's record stream reproduces oracle.refine, checks clean 
 the checker tells a near-tie flip (explained) from a real one (unexplained)."""
 import numpy as np
 
-import teacher_forced as tf
+from oracle import teacher_forced as tf
 
 
 def _case(P):
