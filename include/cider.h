@@ -287,6 +287,30 @@ int cider_save_parity_file(const char* path, const cider_code_desc* code, int q,
                            uint64_t seed);
 int cider_load_parity_file(const char* path, int max_edges, int32_t* edges, int* n_edges, int* checks, int* slots, int* q,
                            int* col_weight, uint32_t* prim_poly, uint64_t* seed);
+/* ---- the reference's dataset format (dataset.hpp:19-99, dataset.cpp) ---------- */
+/* ura::RunConfig (dataset.hpp:19-41); rho_bg / sigma_u2 < 0 = derive the default */
+typedef struct {
+    char scale[32];
+    int q, l, p, col_weight, k, n_s;
+    double eb_db, noise_var;
+    int amp_iters;
+    double rho_bg, sigma_u2, evidence_floor;
+    uint64_t seed;
+    int frames;
+} cider_run_config;
+/* = config_to_json (canonical: keys sorted, nlohmann::json's number layout) / config_fingerprint
+ * (FNV-1a 64 of it, 16 hex digits + NUL) / file_fingerprint / format_double (shortest round trip) */
+int cider_config_to_json(const cider_run_config* cfg, char* out, int cap);
+int cider_config_fingerprint(const cider_run_config* cfg, char out[17]);
+int cider_file_fingerprint(const char* path, char out[17]);
+int cider_format_double(double x, char* out, int cap);
+/* = load_dataset (dataset.cpp:176-220) of a JSON Lines dataset: the header's config and fingerprints,
+ * *n_frames, and the first min(frames_cap, n) frames: seeds, truth (n x k x l), evidence (n x l x q,
+ * fp64) and snr_db (each nullable). Call with frames_cap = 0 to size the buffers. Malformed or
+ * inconsistent files fail with CIDER_ERUNTIME and the reference's messages. */
+int cider_dataset_load(const char* path, cider_run_config* cfg, char fingerprint[17], char h_fingerprint[17],
+                       int* n_frames, int frames_cap, uint64_t* seeds, int32_t* truth, double* evidence, double* snr_db);
+
 /* Permutation-invariant SER/CER (= ura::ser_cer, metrics.cpp:124-145) summed over n bins. */
 int cider_ser_cer(int n, int K, int L, const int32_t* truth, const int32_t* pred, double* ser_sum,
                   double* cer_sum);

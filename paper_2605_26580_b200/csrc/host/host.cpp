@@ -342,6 +342,10 @@ void systematic_tables(const Gf& gf, const Tanner& t, std::vector<int>& info, st
 
 const char* host_last_error() { return g_host_err.c_str(); }
 uint64_t host_error_tick() { return g_host_err_tick; }
+void set_host_error(const std::string& msg) {
+    g_host_err = msg;
+    g_host_err_tick = error_tick();
+}
 uint64_t error_tick() { // per-thread order of failures across the host and engine halves of the ABI
     static thread_local uint64_t t = 0;
     return ++t;

@@ -55,6 +55,7 @@ struct Tanner {
 // failure ordering for cider_last_error (the most recent message of either half of the ABI)
 uint64_t error_tick();
 uint64_t host_error_tick();
+void set_host_error(const std::string& msg); // a host-half failure for cider_last_error
 
 // systematic encoder of H (info slots, pivot slots, pivot-row coefficients [pivot][info]) for the
 // device workload generator (kernels/workload.cuh)
