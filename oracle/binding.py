@@ -364,6 +364,79 @@ class RefSession:
             pass
 
 
+class RefCli:
+    """oracle/_ref/libura_cli.so: the reference's dataset.cpp (with nlohmann/json 3.11.3) and uradec's
+    simulate / decode steps composed from the reference library (oracle/ref_cli_shim.cpp)."""
+    PATH = os.path.join(_HERE, "_ref", "libura_cli.so")
+
+    def __init__(self):
+        from paper_2605_26580_b200 import RunConfigDesc
+        self.h = C.CDLL(self.PATH)
+        h, P, RC = self.h, C.c_void_p, C.POINTER(RunConfigDesc)
+        h.refcli_last_error.restype = C.c_char_p
+        for f in ("refcli_config_to_json", "refcli_config_fingerprint"):
+            getattr(h, f).argtypes = [RC, C.c_char_p, C.c_int]
+        h.refcli_format_double.argtypes = [C.c_double, C.c_char_p, C.c_int]
+        h.refcli_json_double.argtypes = [C.c_double, C.c_char_p, C.c_int]
+        h.refcli_simulate.argtypes = [RC, C.c_char_p, C.c_char_p]
+        h.refcli_load.argtypes = [C.c_char_p, RC, C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.c_int, P, P, P, P]
+        h.refcli_decode_row.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, P, C.c_int, C.c_int,
+                                        C.c_uint64, C.c_int, C.c_char_p, C.c_int]
+
+    @staticmethod
+    def available() -> bool:
+        return os.path.exists(RefCli.PATH)
+
+    def _check(self, rc):
+        if rc == 0:
+            return
+        msg = self.h.refcli_last_error().decode()
+        raise (ValueError if rc == 3 else RuntimeError)(msg)
+
+    def _str(self, fn, *args, cap=4096):
+        buf = C.create_string_buffer(cap)
+        self._check(fn(*args, buf, cap))
+        return buf.value.decode()
+
+    def config_to_json(self, cfg):
+        return self._str(self.h.refcli_config_to_json, C.byref(cfg))
+
+    def config_fingerprint(self, cfg):
+        return self._str(self.h.refcli_config_fingerprint, C.byref(cfg))
+
+    def format_double(self, x):
+        return self._str(self.h.refcli_format_double, float(x))
+
+    def json_double(self, x):
+        return self._str(self.h.refcli_json_double, float(x))
+
+    def simulate(self, cfg, dataset_path: str, hfile: str):
+        self._check(self.h.refcli_simulate(C.byref(cfg), dataset_path.encode(), hfile.encode()))
+
+    def load(self, path: str) -> dict:
+        from paper_2605_26580_b200 import RUN_CONFIG_FIELDS, RunConfigDesc
+        cfg = RunConfigDesc()
+        fp, hfp, n = C.create_string_buffer(17), C.create_string_buffer(17), C.c_int()
+        big = 1 << 14
+        self._check(self.h.refcli_load(path.encode(), C.byref(cfg), fp, hfp, C.byref(n), 0, None, None, None, None))
+        k, L, q, m = cfg.k, cfg.l, cfg.q, n.value
+        seeds, truth = np.empty(m, np.uint64), np.empty((m, k, L), np.int32)
+        ev, snr = np.empty((m, L, q), np.float64), np.empty(m, np.float64)
+        self._check(self.h.refcli_load(path.encode(), C.byref(cfg), fp, hfp, C.byref(n), m, _p(seeds), _p(truth), _p(ev),
+                                       _p(snr)))
+        conf = {f: getattr(cfg, f) for f in RUN_CONFIG_FIELDS}
+        conf["scale"] = conf["scale"].decode()
+        del big
+        return {"config": conf, "fingerprint": fp.value.decode(), "h_fingerprint": hfp.value.decode(), "seeds": seeds,
+                "truth": truth, "evidence": ev, "snr_db": snr}
+
+    def decode_row(self, dataset: str, hfile: str, decoder: str, scorer: str = "maxprob", steps: int = 0,
+                   thresholds=(), latent_dim: int = 128, param_seed: int = 1, f32: bool = True) -> str:
+        th = np.ascontiguousarray(thresholds, np.float64)
+        return self._str(self.h.refcli_decode_row, dataset.encode(), hfile.encode(), decoder.encode(), scorer.encode(),
+                         steps, _p(th) if len(th) else None, len(th), latent_dim, C.c_uint64(param_seed), int(f32))
+
+
 def derive_seed(master: int, index: int) -> int:
     """seeding.hpp:16-22 (pure-Python restatement, used to name fixture seeds)."""
     M = (1 << 64) - 1

@@ -68,6 +68,14 @@ class TraceDesc(C.Structure):
                 ("n_reveal_counts", C.POINTER(C.c_int32)), ("first_step_sites", C.POINTER(C.c_uint8))]
 
 
+class RunConfigDesc(C.Structure):
+    """cider_run_config = ura::RunConfig (dataset.hpp:19-41)."""
+    _fields_ = [("scale", C.c_char * 32), ("q", C.c_int), ("l", C.c_int), ("p", C.c_int), ("col_weight", C.c_int),
+                ("k", C.c_int), ("n_s", C.c_int), ("eb_db", C.c_double), ("noise_var", C.c_double), ("amp_iters", C.c_int),
+                ("rho_bg", C.c_double), ("sigma_u2", C.c_double), ("evidence_floor", C.c_double), ("seed", C.c_uint64),
+                ("frames", C.c_int)]
+
+
 class WorkloadDesc(C.Structure):
     _fields_ = [("m", C.c_int), ("slots", C.c_int), ("checks", C.c_int), ("col_weight", C.c_int), ("k", C.c_int),
                 ("snr_db", C.c_double), ("p_erase", C.c_double), ("p_false", C.c_double),
@@ -124,6 +132,12 @@ def lib() -> C.CDLL:
         h.cider_nccl_unique_id.argtypes = [C.c_char_p]
         h.cider_nccl_init.argtypes = [P, C.c_char_p, C.c_int, C.c_int]
         h.cider_nccl_allgather.argtypes = [P, P, P, C.c_size_t]
+        h.cider_config_to_json.argtypes = [C.POINTER(RunConfigDesc), C.c_char_p, C.c_int]
+        h.cider_config_fingerprint.argtypes = [C.POINTER(RunConfigDesc), C.c_char_p]
+        h.cider_file_fingerprint.argtypes = [C.c_char_p, C.c_char_p]
+        h.cider_format_double.argtypes = [C.c_double, C.c_char_p, C.c_int]
+        h.cider_dataset_load.argtypes = [C.c_char_p, C.POINTER(RunConfigDesc), C.c_char_p, C.c_char_p, C.POINTER(C.c_int),
+                                         C.c_int, P, P, P, P]
         h.cider_workload_code.argtypes = [C.POINTER(WorkloadDesc), P]
         h.cider_workload_bins.argtypes = [C.POINTER(WorkloadDesc), P, C.c_int64, C.c_int, P, P, C.c_int]
         h.cider_save_parity_file.argtypes = [C.c_char_p, C.POINTER(CodeDesc), C.c_int, C.c_int, C.c_uint32, C.c_uint64]
@@ -566,6 +580,59 @@ def load_parity_file(path: str, max_edges: int = 1 << 16) -> dict:
     n = v[0].value
     return {"edges": e[:n].copy(), "checks": v[1].value, "slots": v[2].value, "q": v[3].value,
             "col_weight": v[4].value, "prim_poly": v[5].value, "seed": v[6].value}
+
+
+# ---- the reference's dataset format ----------------------------------------------
+RUN_CONFIG_FIELDS = ("scale", "q", "l", "p", "col_weight", "k", "n_s", "eb_db", "noise_var", "amp_iters", "rho_bg",
+                     "sigma_u2", "evidence_floor", "seed", "frames")
+
+
+def run_config(**kw) -> RunConfigDesc:
+    """ura::RunConfig with its defaults (dataset.hpp:19-36), overridden by `kw`."""
+    d = dict(scale="tiny", q=64, l=12, p=8, col_weight=3, k=2, n_s=24, eb_db=10.0, noise_var=1.0, amp_iters=20,
+             rho_bg=-1.0, sigma_u2=-1.0, evidence_floor=-40.0, seed=1, frames=100)
+    d.update(kw)
+    d["scale"] = d["scale"].encode()
+    return RunConfigDesc(*[d[f] for f in RUN_CONFIG_FIELDS])
+
+
+def config_to_json(cfg: RunConfigDesc) -> str:
+    buf = C.create_string_buffer(2048)
+    _check(lib().cider_config_to_json(C.byref(cfg), buf, 2048))
+    return buf.value.decode()
+
+
+def config_fingerprint(cfg: RunConfigDesc) -> str:
+    buf = C.create_string_buffer(17)
+    _check(lib().cider_config_fingerprint(C.byref(cfg), buf))
+    return buf.value.decode()
+
+
+def format_double(x: float) -> str:
+    """format_double (dataset.cpp:57-61): the shortest round-trip decimal form (std::to_chars)."""
+    buf = C.create_string_buffer(64)
+    _check(lib().cider_format_double(float(x), buf, 64))
+    return buf.value.decode()
+
+
+def load_dataset(path: str) -> dict:
+    """ura::load_dataset (dataset.cpp:176-220): {config, fingerprint, h_fingerprint, seeds, truth n x K x L,
+    evidence n x L x Q (fp64), snr_db}."""
+    cfg = RunConfigDesc()
+    fp, hfp = C.create_string_buffer(17), C.create_string_buffer(17)
+    n = C.c_int()
+    _check(lib().cider_dataset_load(path.encode(), C.byref(cfg), fp, hfp, C.byref(n), 0, None, None, None, None))
+    k, L, q = cfg.k, cfg.l, cfg.q
+    seeds = np.empty(n.value, np.uint64)
+    truth = np.empty((n.value, k, L), np.int32)
+    ev = np.empty((n.value, L, q), np.float64)
+    snr = np.empty(n.value, np.float64)
+    _check(lib().cider_dataset_load(path.encode(), C.byref(cfg), fp, hfp, C.byref(n), n.value, _ptr(seeds), _ptr(truth),
+                                    _ptr(ev), _ptr(snr)))
+    conf = {f: getattr(cfg, f) for f in RUN_CONFIG_FIELDS}
+    conf["scale"] = conf["scale"].decode()
+    return {"config": conf, "fingerprint": fp.value.decode(), "h_fingerprint": hfp.value.decode(), "seeds": seeds,
+            "truth": truth, "evidence": ev, "snr_db": snr}
 
 
 def ser_cer(truth: np.ndarray, pred: np.ndarray):

@@ -7,9 +7,9 @@
 // cudnn_frontend include tree). Two of its behaviours are part of the format and are restated here:
 //   * object keys are emitted in sorted order (json::object_t is a std::map), so the config
 //     fingerprint FNV-1a(config_to_json(cfg)) hashes {"amp_iters":..,"col_weight":..,...} in that order;
-//   * doubles are dumped as the shortest round-trip decimal digits, laid out by its
-//     format_buffer rule (fixed for decimal exponents in (-4, 15], with ".0" on integral values;
-//     else d.ddde+XX with at least two exponent digits).
+//   * doubles are dumped with Grisu2 digits (Loitsch 2010; not always the shortest form), laid out
+//     by its format_buffer rule (fixed for decimal exponents in (-4, 15], with ".0" on integral
+//     values; else d.ddde+XX with at least two exponent digits).
 // tests/test_dataset.py pins both against the reference's own write_dataset / config_fingerprint
 // (oracle/_ref, dataset.cpp compiled against that json.hpp) and round-trips reference-written files.
 #include <charconv>
@@ -227,24 +227,194 @@ struct Parser {
 };
 
 // ---- number formatting -------------------------------------------------------------------------
-// nlohmann::json's dump of a double: shortest round-trip digits, then its format_buffer layout
-// (min_exp = -4, max_exp = 15 for doubles).
+// nlohmann::json dumps a double with Grisu2 (F. Loitsch, "Printing floating-point numbers quickly and
+// accurately with integers", PLDI 2010) — usually, not always, the shortest round-trip digits — then
+// lays them out with its format_buffer rule. Both are restated here from the published algorithm:
+// boundaries m-/m+ of v, a cached power 10^-k bringing the scaled exponent into [alpha, gamma] =
+// [-60, -32], digit generation from the conservative upper bound M+ - 1 ulp until the remainder is
+// within the interval, then the closest-digit adjustment ("round / weed") toward v.
+struct DiyFp {
+    uint64_t f;
+    int e;
+};
+DiyFp diy_sub(DiyFp a, DiyFp b) { return {a.f - b.f, a.e}; }
+DiyFp diy_mul(DiyFp a, DiyFp b) { // upper 64 bits of the 128-bit product, rounded half up
+    const unsigned __int128 p = (unsigned __int128)a.f * b.f;
+    uint64_t hi = uint64_t(p >> 64);
+    hi += uint64_t(p >> 63) & 1u;
+    return {hi, a.e + b.e + 64};
+}
+DiyFp diy_normalize(DiyFp x) {
+    while ((x.f >> 63) == 0) { x.f <<= 1; --x.e; }
+    return x;
+}
+DiyFp diy_normalize_to(DiyFp x, int e) { return {x.f << (x.e - e), e}; }
+
+// 10^k = f x 2^e (f normalised, rounded to nearest) for k = -300, -292, ..., 324 (generated offline
+// with exact rational arithmetic)
+struct CachedPow {
+    uint64_t f;
+    int e, k;
+};
+const CachedPow kPow10[] = {
+    {0xAB70FE17C79AC6CAULL, -1060, -300},
+    {0xFF77B1FCBEBCDC4FULL, -1034, -292},
+    {0xBE5691EF416BD60CULL, -1007, -284},
+    {0x8DD01FAD907FFC3CULL, -980, -276},
+    {0xD3515C2831559A83ULL, -954, -268},
+    {0x9D71AC8FADA6C9B5ULL, -927, -260},
+    {0xEA9C227723EE8BCBULL, -901, -252},
+    {0xAECC49914078536DULL, -874, -244},
+    {0x823C12795DB6CE57ULL, -847, -236},
+    {0xC21094364DFB5637ULL, -821, -228},
+    {0x9096EA6F3848984FULL, -794, -220},
+    {0xD77485CB25823AC7ULL, -768, -212},
+    {0xA086CFCD97BF97F4ULL, -741, -204},
+    {0xEF340A98172AACE5ULL, -715, -196},
+    {0xB23867FB2A35B28EULL, -688, -188},
+    {0x84C8D4DFD2C63F3BULL, -661, -180},
+    {0xC5DD44271AD3CDBAULL, -635, -172},
+    {0x936B9FCEBB25C996ULL, -608, -164},
+    {0xDBAC6C247D62A584ULL, -582, -156},
+    {0xA3AB66580D5FDAF6ULL, -555, -148},
+    {0xF3E2F893DEC3F126ULL, -529, -140},
+    {0xB5B5ADA8AAFF80B8ULL, -502, -132},
+    {0x87625F056C7C4A8BULL, -475, -124},
+    {0xC9BCFF6034C13053ULL, -449, -116},
+    {0x964E858C91BA2655ULL, -422, -108},
+    {0xDFF9772470297EBDULL, -396, -100},
+    {0xA6DFBD9FB8E5B88FULL, -369, -92},
+    {0xF8A95FCF88747D94ULL, -343, -84},
+    {0xB94470938FA89BCFULL, -316, -76},
+    {0x8A08F0F8BF0F156BULL, -289, -68},
+    {0xCDB02555653131B6ULL, -263, -60},
+    {0x993FE2C6D07B7FACULL, -236, -52},
+    {0xE45C10C42A2B3B06ULL, -210, -44},
+    {0xAA242499697392D3ULL, -183, -36},
+    {0xFD87B5F28300CA0EULL, -157, -28},
+    {0xBCE5086492111AEBULL, -130, -20},
+    {0x8CBCCC096F5088CCULL, -103, -12},
+    {0xD1B71758E219652CULL, -77, -4},
+    {0x9C40000000000000ULL, -50, 4},
+    {0xE8D4A51000000000ULL, -24, 12},
+    {0xAD78EBC5AC620000ULL, 3, 20},
+    {0x813F3978F8940984ULL, 30, 28},
+    {0xC097CE7BC90715B3ULL, 56, 36},
+    {0x8F7E32CE7BEA5C70ULL, 83, 44},
+    {0xD5D238A4ABE98068ULL, 109, 52},
+    {0x9F4F2726179A2245ULL, 136, 60},
+    {0xED63A231D4C4FB27ULL, 162, 68},
+    {0xB0DE65388CC8ADA8ULL, 189, 76},
+    {0x83C7088E1AAB65DBULL, 216, 84},
+    {0xC45D1DF942711D9AULL, 242, 92},
+    {0x924D692CA61BE758ULL, 269, 100},
+    {0xDA01EE641A708DEAULL, 295, 108},
+    {0xA26DA3999AEF774AULL, 322, 116},
+    {0xF209787BB47D6B85ULL, 348, 124},
+    {0xB454E4A179DD1877ULL, 375, 132},
+    {0x865B86925B9BC5C2ULL, 402, 140},
+    {0xC83553C5C8965D3DULL, 428, 148},
+    {0x952AB45CFA97A0B3ULL, 455, 156},
+    {0xDE469FBD99A05FE3ULL, 481, 164},
+    {0xA59BC234DB398C25ULL, 508, 172},
+    {0xF6C69A72A3989F5CULL, 534, 180},
+    {0xB7DCBF5354E9BECEULL, 561, 188},
+    {0x88FCF317F22241E2ULL, 588, 196},
+    {0xCC20CE9BD35C78A5ULL, 614, 204},
+    {0x98165AF37B2153DFULL, 641, 212},
+    {0xE2A0B5DC971F303AULL, 667, 220},
+    {0xA8D9D1535CE3B396ULL, 694, 228},
+    {0xFB9B7CD9A4A7443CULL, 720, 236},
+    {0xBB764C4CA7A44410ULL, 747, 244},
+    {0x8BAB8EEFB6409C1AULL, 774, 252},
+    {0xD01FEF10A657842CULL, 800, 260},
+    {0x9B10A4E5E9913129ULL, 827, 268},
+    {0xE7109BFBA19C0C9DULL, 853, 276},
+    {0xAC2820D9623BF429ULL, 880, 284},
+    {0x80444B5E7AA7CF85ULL, 907, 292},
+    {0xBF21E44003ACDD2DULL, 933, 300},
+    {0x8E679C2F5E44FF8FULL, 960, 308},
+    {0xD433179D9C8CB841ULL, 986, 316},
+    {0x9E19DB92B4E31BA9ULL, 1013, 324}
+};
+
+void grisu2(double v, char* buf, int& len, int& dec_exp) {
+    uint64_t bits;
+    std::memcpy(&bits, &v, 8);
+    const uint64_t F = bits & ((uint64_t(1) << 52) - 1);
+    const int E = int((bits >> 52) & 0x7FF);
+    constexpr int kBias = 1075; // 1023 + 52
+    const uint64_t f = E == 0 ? F : F + (uint64_t(1) << 52);
+    const int e = E == 0 ? 1 - kBias : E - kBias;
+    const bool lower_closer = F == 0 && E > 1;
+    const DiyFp mp = diy_normalize({2 * f + 1, e - 1});
+    const DiyFp mm = diy_normalize_to(lower_closer ? DiyFp{4 * f - 1, e - 2} : DiyFp{2 * f - 1, e - 1}, mp.e);
+    const DiyFp w = diy_normalize({f, e});
+    // cached power for the exponent of m+
+    constexpr int kAlpha = -60;
+    const int fk = kAlpha - mp.e - 1;
+    const int k = (fk * 78913) / (1 << 18) + (fk > 0 ? 1 : 0);
+    const int idx = (300 + k + 7) / 8;
+    const CachedPow& c = kPow10[idx];
+    const DiyFp cm{c.f, c.e};
+    const DiyFp W = diy_mul(w, cm), Wm = diy_mul(mm, cm), Wp = diy_mul(mp, cm);
+    const DiyFp Mm{Wm.f + 1, Wm.e}, Mp{Wp.f - 1, Wp.e};
+    dec_exp = -c.k;
+    // digit generation
+    uint64_t delta = diy_sub(Mp, Mm).f;
+    uint64_t dist = diy_sub(Mp, W).f;
+    const int sh = -Mp.e;
+    const uint64_t one = uint64_t(1) << sh;
+    uint32_t p1 = uint32_t(Mp.f >> sh);
+    uint64_t p2 = Mp.f & (one - 1);
+    uint32_t pow10 = 1;
+    int n = 1;
+    while (n < 10 && p1 >= pow10 * 10ull) { pow10 *= 10; ++n; }
+    len = 0;
+    auto round_weed = [&](uint64_t rest, uint64_t ten_k) {
+        while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+            --buf[len - 1];
+            rest += ten_k;
+        }
+    };
+    while (n > 0) {
+        const uint32_t d = p1 / pow10;
+        p1 %= pow10;
+        buf[len++] = char('0' + d);
+        --n;
+        const uint64_t rest = (uint64_t(p1) << sh) + p2;
+        if (rest <= delta) {
+            dec_exp += n;
+            round_weed(rest, uint64_t(pow10) << sh);
+            return;
+        }
+        pow10 /= 10;
+    }
+    int m = 0;
+    for (;;) {
+        p2 *= 10;
+        const uint64_t d = p2 >> sh;
+        p2 &= one - 1;
+        buf[len++] = char('0' + d);
+        ++m;
+        delta *= 10;
+        dist *= 10;
+        if (p2 <= delta) break;
+    }
+    dec_exp -= m;
+    round_weed(p2, one);
+}
+
 std::string json_double(double x) {
     if (!std::isfinite(x)) return "null";
-    if (x == 0.0) return std::signbit(x) ? "-0.0" : "0.0";
-    char buf[64];
-    auto r = std::to_chars(buf, buf + sizeof(buf), x, std::chars_format::scientific); // shortest, d.ddde±XX
-    std::string sci(buf, r.ptr);
     std::string out;
-    size_t i = 0;
-    if (sci[0] == '-') { out.push_back('-'); i = 1; }
-    const size_t epos = sci.find('e');
-    std::string digits;
-    for (size_t j = i; j < epos; ++j)
-        if (sci[j] != '.') digits.push_back(sci[j]);
-    const int e10 = std::stoi(sci.substr(epos + 1)); // value = d.ddd x 10^e10
-    const int k = int(digits.size());
-    const int n = e10 + 1; // decimal point position relative to the digit string
+    if (std::signbit(x)) { out.push_back('-'); x = -x; }
+    if (x == 0.0) return out + "0.0";
+    char buf[32];
+    int k = 0, de = 0;
+    grisu2(x, buf, k, de);
+    const std::string digits(buf, size_t(k));
+    const int n = k + de; // decimal point position relative to the digit string
     constexpr int kMinExp = -4, kMaxExp = 15;
     if (k <= n && n <= kMaxExp) {
         out += digits;

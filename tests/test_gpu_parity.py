@@ -242,3 +242,36 @@ def test_remask_pass_caller_confidences_and_scorer(P, oracle):
     a = P.run_with_remasking_scored(den, P.MaxProbScorer(), S, sched, thr, wl.k)
     b = ctx.refine(S, wl.k, sched, P.RemaskConfig(thresholds=thr))
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("decoder,scorer,thr,k", [("refine-structured", "maxprob", (), 2),
+                                                  ("refine-structured", "maxprob", (0.9, 0.6), 3),
+                                                  ("refine-structured", "oracle", (0.9, 0.5), 3),
+                                                  ("sic-bp", "maxprob", (), 3)])
+def test_uradec_gpu_decode_csv_matches_reference(P, tmp_path, decoder, scorer, thr, k):
+    """`uradec-gpu decode` (csrc/tools/uradec_gpu.cpp, C ABI only) on a dataset and parity
+    file written by the reference's own code writes the reference's CSV: the same preamble, header and
+    row (every column but ms_per_sample) as uradec decode's restated steps over the reference library
+    (oracle/ref_cli_shim.cpp; FP32 inputs, the values the device's parity mode computes with)."""
+    import os
+    import subprocess
+    from oracle.binding import RefCli
+    if not RefCli.available():
+        pytest.skip("oracle/_ref/libura_cli.so not built")
+    cli = RefCli()
+    ds, hf, out = str(tmp_path / "d.jsonl"), str(tmp_path / "h.txt"), str(tmp_path / "r.csv")
+    cli.simulate(P.run_config(frames=16, k=k, eb_db=9.0, seed=5), ds, hf)
+    exe = os.path.join(os.path.dirname(P.LIB_PATH), "uradec-gpu")
+    cmd = [exe, "decode", "--dataset", ds, "--hfile", hf, "--decoder", decoder, "--scorer", scorer, "--out", out]
+    if thr:
+        cmd += ["--remask-thresholds", ",".join(str(t) for t in thr)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = open(out).read().splitlines()
+    cfg_json = cli.config_to_json(P.run_config(frames=16, k=k, eb_db=9.0, seed=5))
+    assert lines[0] == "# uradec 0.1.0" and lines[1] == "# config: " + cfg_json
+    assert lines[2].startswith("decoder,backend,scale,q,l,p,k,eb_db,snr_db,seed,samples,ser,cer,ms_per_sample")
+    ours = lines[3].split(",")
+    ref = cli.decode_row(ds, hf, decoder, scorer, 0, thr, f32=True).split(",")
+    ours[13] = ref[13] = "-"
+    assert ours == ref
