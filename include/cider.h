@@ -247,6 +247,14 @@ int cider_kernel_stats(cider_ctx* ctx, int idx, char* name, int name_len, int64_
 int cider_reset_stats(cider_ctx* ctx);
 
 /* ---- multi-GPU result gather (NCCL, the only collective on the path) --------------------- */
+/* Debug guard bands — an out-of-bounds write check for the device kernels (compute-sanitizer is not
+ * available on the GPU pool): after cider_set_debug_guard(ctx, bytes > 0) every workspace buffer is
+ * allocated with `bytes`-byte 0xA5 bands before and after it (existing workspace, graphs and tensor
+ * maps are dropped); cider_debug_check counts band bytes that were overwritten (0 = clean; the damaged
+ * buffers are named in cider_last_error). cider_debug_poke is the positive control for tests. */
+int cider_set_debug_guard(cider_ctx* ctx, size_t bytes);
+int cider_debug_check(cider_ctx* ctx, int64_t* damaged_bytes);
+int cider_debug_poke(cider_ctx* ctx, const char* buffer, int64_t offset_past_end);
 /* decoded grids (int32, device) -> one byte per symbol (Q <= 256), async on the ctx stream: the
  * payload of the final gather (134 MB for all 262,144 c5 bins) */
 int cider_grid_pack_u8(cider_ctx* ctx, const int32_t* grid_device, uint8_t* out_device, size_t n);

@@ -128,6 +128,9 @@ def lib() -> C.CDLL:
         h.cider_kernel_stats.argtypes = [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
         h.cider_reset_stats.argtypes = [P]
+        h.cider_set_debug_guard.argtypes = [P, C.c_size_t]
+        h.cider_debug_check.argtypes = [P, C.POINTER(C.c_int64)]
+        h.cider_debug_poke.argtypes = [P, C.c_char_p, C.c_int64]
         h.cider_grid_pack_u8.argtypes = [P, P, P, C.c_size_t]
         h.cider_nccl_unique_id.argtypes = [C.c_char_p]
         h.cider_nccl_init.argtypes = [P, C.c_char_p, C.c_int, C.c_int]
@@ -405,6 +408,15 @@ class Context:
             out.append(flat[o:o + k])
             o += int(k)
         return out
+
+    # debug guard bands (out-of-bounds write check, cider_set_debug_guard / cider_debug_check)
+    def set_debug_guard(self, nbytes: int):
+        _check(lib().cider_set_debug_guard(self.h, nbytes))
+
+    def debug_check(self):
+        n = C.c_int64()
+        _check(lib().cider_debug_check(self.h, C.byref(n)))
+        return n.value, lib().cider_last_error().decode()
 
     # instrumentation
     def launch_count(self) -> int:

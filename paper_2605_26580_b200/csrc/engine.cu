@@ -162,21 +162,28 @@ inline int64_t& alloc_generation() {
     return g;
 }
 struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void ensure(size_t n) {
-        if (n <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        ck(cudaMalloc(&p, n), "cudaMalloc");
+    void* p = nullptr;    // usable region
+    void* base = nullptr; // allocation (p - guard)
+    size_t bytes = 0, guard = 0;
+    // g > 0 (debug): `g`-byte guard bands of 0xA5 before and after the usable region
+    void ensure(size_t n, size_t g = 0) {
+        if (n <= bytes && g == guard) return;
+        release();
+        ck(cudaMalloc(&base, n + 2 * g), "cudaMalloc");
+        p = static_cast<char*>(base) + g;
         bytes = n;
+        guard = g;
+        if (g) {
+            ck(cudaMemset(base, 0xA5, g), "guard");
+            ck(cudaMemset(static_cast<char*>(p) + n, 0xA5, g), "guard");
+            ck(cudaDeviceSynchronize(), "guard");
+        }
         ++alloc_generation();
     }
     void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
+        if (base) cudaFree(base);
+        p = base = nullptr;
+        bytes = guard = 0;
     }
     template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
@@ -235,6 +242,7 @@ struct cider_ctx {
     int chunk_req = 0;
     int cap_bins = 0, cap_K = 0;
     std::map<std::string, DevBuf> ws;
+    size_t debug_guard = 0; // cider_set_debug_guard: guard bands around workspace buffers
     std::map<std::tuple<const void*, int64_t, int, int, int>, CUtensorMap> maps;
     // CUDA graphs of whole refinement chunks (no-remask / rank-remask passes: no host round trip),
     // keyed by shape, schedule, buffers and allocation generation; seen once eagerly, then captured
@@ -586,7 +594,7 @@ size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 void* wsbuf(cider_ctx& c, const char* name, size_t bytes) {
     DevBuf& b = c.ws[name];
-    b.ensure(round_up(std::max<size_t>(bytes, 256), 256));
+    b.ensure(round_up(std::max<size_t>(bytes, 256), 256), c.debug_guard);
     return b.p;
 }
 
@@ -1625,7 +1633,7 @@ void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
         attr = true;
     }
     if (smem > 200 * 1024 || max_deg > 32) throw InvalidInput("bp_decode: check degree x Q too large for one CTA");
-    const int cthreads = std::min(256, std::max(32, Q));
+    const int cthreads = 32 * std::max(1, std::min(max_deg, 32)); // one warp per edge row of a check
     for (int iter = 1; iter <= cfg.max_iters; ++iter) {
         ck(cudaMemsetAsync(c.nact.p, 0, 4, c.stream), "memset");
         bp::bp_check_kernel<<<unsigned(B * P), cthreads, smem, c.stream>>>(c.v2c.as<double>(), c.check_ptr.as<int>(),
@@ -2197,7 +2205,7 @@ int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const 
         const size_t smem = size_t(2) * d * Q * 8;
         if (smem > 200 * 1024) throw InvalidInput("check_update_wht: d * Q too large for one CTA");
         ck(cudaFuncSetAttribute(wht_check_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-        wht_check_update_kernel<<<n_checks, std::min(256, std::max(32, Q)), smem, st>>>(
+        wht_check_update_kernel<<<n_checks, 32 * std::max(1, std::min(d, 32)), smem, st>>>(
             din.as<double>(), dcf.as<int>(), dmul.as<uint8_t>(), d, Q, dout.as<double>());
         check_launch("wht_check_update");
         ck(cudaMemcpyAsync(c2v, dout.p, nmsg * 8, cudaMemcpyDeviceToHost, st), "d2h");
@@ -2343,6 +2351,74 @@ int cider_grid_pack_u8(cider_ctx* c, const int32_t* grid_device, uint8_t* out_de
         pack_u8_kernel<<<blocks_for(int64_t((n + 3) / 4)), 256, 0, c->stream>>>(grid_device, out_device, int64_t(n));
         ++c->launches;
         check_launch("pack_u8");
+    });
+}
+
+// ---- debug guard bands (an out-of-bounds write check in place of compute-sanitizer) ----------------
+__global__ void guard_count_kernel(const uint8_t* __restrict__ a, size_t n, unsigned long long* bad) {
+    unsigned long long c = 0;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) c += a[i] != 0xA5;
+    if (c) atomicAdd(bad, c); // a count, not data
+}
+
+int cider_set_debug_guard(cider_ctx* c, size_t bytes) {
+    return guard([&] {
+        if (!c) throw InvalidInput("null context");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        for (auto& g : c->graphs)
+            if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+        c->graphs.clear();
+        c->maps.clear();
+        for (auto& kv : c->ws) kv.second.release(); // reallocated with (or without) bands on next use
+        c->ws.clear();
+        c->debug_guard = round_up(bytes, 256);
+    });
+}
+
+int cider_debug_check(cider_ctx* c, int64_t* damaged) {
+    return guard([&] {
+        if (!c || !damaged) throw InvalidInput("null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        DevBuf cnt;
+        cnt.ensure(8);
+        int64_t total = 0;
+        std::string names;
+        for (auto& kv : c->ws) {
+            const DevBuf& b = kv.second;
+            if (!b.guard) continue;
+            unsigned long long h = 0;
+            ck(cudaMemsetAsync(cnt.p, 0, 8, c->stream), "memset");
+            guard_count_kernel<<<64, 256, 0, c->stream>>>(static_cast<const uint8_t*>(b.base), b.guard, cnt.as<unsigned long long>());
+            guard_count_kernel<<<64, 256, 0, c->stream>>>(static_cast<const uint8_t*>(b.p) + b.bytes, b.guard, cnt.as<unsigned long long>());
+            check_launch("guard_count");
+            ck(cudaMemcpyAsync(&h, cnt.p, 8, cudaMemcpyDeviceToHost, c->stream), "d2h");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            if (h) {
+                total += int64_t(h);
+                names += (names.empty() ? "" : ", ") + kv.first;
+            }
+        }
+        cnt.release();
+        *damaged = total;
+        g_err = names.empty() ? std::string("guard bands intact") : "guard bands overwritten: " + names;
+        g_err_tick = error_tick();
+    });
+}
+
+// test-only positive control: writes one byte `offset` bytes past the end of workspace buffer `name`
+int cider_debug_poke(cider_ctx* c, const char* name, int64_t offset) {
+    return guard([&] {
+        if (!c || !name) throw InvalidInput("null argument");
+        std::lock_guard<std::mutex> lk(c->mu);
+        auto it = c->ws.find(name);
+        if (it == c->ws.end() || !it->second.guard) throw InvalidInput("debug_poke: no guarded buffer of that name");
+        if (offset < 0 || size_t(offset) >= it->second.guard) throw InvalidInput("debug_poke: offset outside the guard band");
+        ck(cudaMemsetAsync(static_cast<char*>(it->second.p) + it->second.bytes + offset, 0x00, 1, c->stream), "poke");
+        ck(cudaStreamSynchronize(c->stream), "sync");
     });
 }
 

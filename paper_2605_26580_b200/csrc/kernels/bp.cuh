@@ -46,20 +46,34 @@ __device__ __forceinline__ dd dd_mul(dd a, dd b) {
     return quick_two_sum(p, e);
 }
 
-// In-place WHT of `rows` rows of length Q in SMEM (all threads of the block participate).
-__device__ __forceinline__ void wht_rows_dd(dd* y, int rows, int Q) {
-    for (int len = 1; len < Q; len <<= 1) {
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < rows * (Q / 2); idx += blockDim.x) {
-            const int r = idx / (Q / 2), p = idx % (Q / 2);
-            const int a = (p / len) * (2 * len) + (p % len);
-            dd* row = y + size_t(r) * Q;
-            const dd u = row[a], v = row[a + len];
-            row[a] = dd_add(u, v);
-            row[a + len] = dd_add(u, dd_neg(v));
+// WHT of one row held by one warp: lane l owns symbols l + 32 j (j < Q / 32; one symbol per lane
+// for Q < 32). Butterfly stages with len >= 32 pair registers of the same lane, stages with len < 32
+// pair lanes l and l ^ len through warp shuffles — no shared memory, no block barrier. Each pair
+// (u = y[a], v = y[a + len], bit len of a clear) becomes (u + v, u - v) with the same dd operations
+// the reference order implies, so the result is bit-identical to an SMEM butterfly.
+constexpr int WHT_MAXE = 8; // symbols per lane (Q <= 256)
+__device__ __forceinline__ dd shfl_dd(dd x, int m) {
+    return {__shfl_xor_sync(0xffffffffu, x.hi, m), __shfl_xor_sync(0xffffffffu, x.lo, m)};
+}
+__device__ __forceinline__ void wht_warp_dd(dd (&r)[WHT_MAXE], int Q, int lane) {
+    const int E = Q >= 32 ? Q / 32 : 1;
+    const int lw = Q >= 32 ? 32 : Q; // lane span of a row
+    for (int len = 1; len < lw; len <<= 1) {
+#pragma unroll
+        for (int j = 0; j < WHT_MAXE; ++j) {
+            if (j >= E) break;
+            const dd p = shfl_dd(r[j], len);
+            r[j] = (lane & len) ? dd_add(p, dd_neg(r[j])) : dd_add(r[j], p);
         }
     }
-    __syncthreads();
+    for (int h = 1; h < E; h <<= 1) // len = 32 h
+#pragma unroll
+        for (int j = 0; j < WHT_MAXE; ++j) {
+            if (j >= E || (j & h)) continue;
+            const dd u = r[j], v = r[j + h];
+            r[j] = dd_add(u, v);
+            r[j + h] = dd_add(u, dd_neg(v));
+        }
 }
 
 // normalize_or_uniform (bp.cpp:11-19): sequential sum in symbol order, then x *= 1/s.
@@ -104,8 +118,10 @@ __global__ void bp_init_kernel(const double* __restrict__ lambda, const int* __r
     c2v[i] = 1.0 / Q;
 }
 
-// update_check_wht (bp.cpp:222-269) for every (bin, check) of the active bins: one CTA each.
-// SMEM: y [d][Q] and spec [d][Q] in double-double, one scratch row per edge for the output.
+// update_check_wht (bp.cpp:222-269) for every (bin, check) of the active bins: one CTA each, warp i
+// on edge i's row for the transforms (registers + shuffles), all threads on the prefix / suffix
+// spectral products (thread per symbol, over the rows in SMEM).
+// SMEM: y [d][Q] and spec [d][Q] in double-double.
 __global__ void bp_check_kernel(const double* __restrict__ v2c, const int* __restrict__ check_ptr,
                                 const int* __restrict__ e_coef, const uint8_t* __restrict__ mul, int P, int E, int Q,
                                 const int* __restrict__ active, double* __restrict__ c2v) {
@@ -118,11 +134,23 @@ __global__ void bp_check_kernel(const double* __restrict__ v2c, const int* __res
     dd* y = sm_dd;                   // d x Q permuted spectra
     dd* sp = sm_dd + size_t(d) * Q;  // d x Q extrinsic spectra
     const double* in = v2c + (b * E + e0) * Q;
-    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
-        const int i = idx / Q, a = idx % Q;
-        y[size_t(i) * Q + mul[e_coef[e0 + i] * Q + a]] = dd{in[idx], 0.0}; // y[map[a]] = msg[a]
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+    const int EL = Q >= 32 ? Q / 32 : 1;
+    const bool lane_on = Q >= 32 || lane < Q;
+    for (int i = warp; i < d; i += nw) { // scatter_by (y[alpha a] = msg[a]), then the forward transform
+        const uint8_t* mrow = mul + e_coef[e0 + i] * Q;
+        for (int a = lane; a < Q; a += 32) y[size_t(i) * Q + mrow[a]] = dd{in[size_t(i) * Q + a], 0.0};
+        __syncwarp();
+        dd r[WHT_MAXE];
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) r[t] = y[size_t(i) * Q + lane + 32 * t];
+        wht_warp_dd(r, Q, lane);
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) y[size_t(i) * Q + lane + 32 * t] = r[t];
     }
-    wht_rows_dd(y, d, Q);
+    __syncthreads();
     for (int a = threadIdx.x; a < Q; a += blockDim.x) {
         // prefix left to right, suffix right to left, spec_i = pre_i * suf_{i+1} (bp.cpp:240-259)
         dd pre = {1.0, 0.0};
@@ -136,29 +164,34 @@ __global__ void bp_check_kernel(const double* __restrict__ v2c, const int* __res
             suf = dd_mul(suf, y[size_t(i) * Q + a]);
         }
     }
-    wht_rows_dd(sp, d, Q);
-    // out[a] = max(double(spec[map[a]] / Q), 0) staged in SMEM (over the dead y rows), then
-    // normalize_or_uniform per edge (sequential sums, one thread per edge) and a coalesced write
-    double* xo = reinterpret_cast<double*>(y);
-    __shared__ double inv_s[32];
-    const double scale = 1.0 / Q;
-    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
-        const int i = idx / Q, a = idx % Q;
-        const dd v = sp[size_t(i) * Q + mul[e_coef[e0 + i] * Q + a]];
-        const double x = (v.hi + v.lo) * scale; // scale is a power of two: exact
-        xo[idx] = fmax(x, 0.0);
-    }
     __syncthreads();
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        double t = 0.0;
-        for (int a = 0; a < Q; ++a) t += xo[size_t(i) * Q + a];
-        inv_s[i] = t > 0.0 ? 1.0 / t : -1.0;
-    }
-    __syncthreads();
+    // inverse transform per row, then out[a] = max(double(spec[map[a]] / Q), 0) staged over the row's
+    // dead y slot, normalize_or_uniform per edge (sequential sum by lane 0), a coalesced write
     double* out = c2v + (b * E + e0) * Q;
-    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
-        const double iv = inv_s[idx / Q];
-        out[idx] = iv < 0.0 ? 1.0 / Q : xo[idx] * iv;
+    const double scale = 1.0 / Q;
+    for (int i = warp; i < d; i += nw) {
+        dd r[WHT_MAXE];
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) r[t] = sp[size_t(i) * Q + lane + 32 * t];
+        wht_warp_dd(r, Q, lane);
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) sp[size_t(i) * Q + lane + 32 * t] = r[t];
+        __syncwarp();
+        double* xo = reinterpret_cast<double*>(y + size_t(i) * Q);
+        const uint8_t* mrow = mul + e_coef[e0 + i] * Q;
+        for (int a = lane; a < Q; a += 32) {
+            const dd v = sp[size_t(i) * Q + mrow[a]];
+            xo[a] = fmax((v.hi + v.lo) * scale, 0.0); // scale is a power of two: exact
+        }
+        __syncwarp();
+        double t = 0.0;
+        if (lane == 0)
+            for (int a = 0; a < Q; ++a) t += xo[a];
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const double iv = t > 0.0 ? 1.0 / t : -1.0;
+        for (int a = lane; a < Q; a += 32) out[size_t(i) * Q + a] = iv < 0.0 ? 1.0 / Q : xo[a] * iv;
     }
 }
 

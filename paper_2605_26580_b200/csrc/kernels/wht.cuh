@@ -5,8 +5,9 @@
 //   y_i   = WHT( scatter(v2c_i by coefficient) )          y_i[alpha_i * a] = v2c_i[a]
 //   spec_i = prod_{j<i} y_j  *  prod_{j>i} y_j            (prefix / suffix products, extrinsic)
 //   c2v_i[a] = max( WHT(spec_i)[alpha_i * a] / Q, 0 ),  normalised (uniform if all mass vanished)
-// Thread a owns spectral index a of every edge, so the prefix/suffix products are per-thread
-// register loops; the transforms are SMEM butterflies. fp64 throughout (the reference keeps the
+// Thread a owns spectral index a of every edge for the prefix/suffix products (register loops over
+// the rows in SMEM); the transforms run one row per warp in registers with warp-shuffle butterflies
+// for the strides below 32. fp64 throughout (the reference keeps the
 // spectra in long double; the GPU has no 80-bit type — parity tolerance in tests/test_gpu.py).
 #pragma once
 
@@ -16,37 +17,60 @@ namespace cider {
 
 constexpr int WHT_MAXD = 32;
 
-__device__ __forceinline__ void wht_rows_smem(double* y, int rows, int Q) {
-    for (int len = 1; len < Q; len <<= 1) {
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < rows * (Q / 2); idx += blockDim.x) {
-            const int r = idx / (Q / 2), p = idx % (Q / 2);
-            const int a = (p / len) * (2 * len) + (p % len);
-            double* row = y + size_t(r) * Q;
-            const double u = row[a], v = row[a + len];
-            row[a] = u + v;
-            row[a + len] = u - v;
+// One row per warp in registers (lane l: symbols l + 32 j), butterflies with len >= 32 inside a lane,
+// len < 32 across lanes by warp shuffles: (u, v) -> (u + v, u - v) in fp64, the same operations as an
+// SMEM butterfly, without block barriers.
+constexpr int WHT_MAXE = 8; // symbols per lane (Q <= 256)
+__device__ __forceinline__ void wht_warp(double (&r)[WHT_MAXE], int Q, int lane) {
+    const int E = Q >= 32 ? Q / 32 : 1;
+    const int lw = Q >= 32 ? 32 : Q;
+    for (int len = 1; len < lw; len <<= 1) {
+#pragma unroll
+        for (int j = 0; j < WHT_MAXE; ++j) {
+            if (j >= E) break;
+            const double p = __shfl_xor_sync(0xffffffffu, r[j], len);
+            r[j] = (lane & len) ? p - r[j] : r[j] + p;
         }
     }
-    __syncthreads();
+    for (int h = 1; h < E; h <<= 1)
+#pragma unroll
+        for (int j = 0; j < WHT_MAXE; ++j) {
+            if (j >= E || (j & h)) continue;
+            const double u = r[j], v = r[j + h];
+            r[j] = u + v;
+            r[j + h] = u - v;
+        }
 }
 
-// v2c, c2v: [n_checks][d][Q]; coef: [n_checks][d] (nonzero); mul: GF(Q) multiplication table [Q][Q]
-__global__ void __launch_bounds__(256)
+// v2c, c2v: [n_checks][d][Q]; coef: [n_checks][d] (nonzero); mul: GF(Q) multiplication table [Q][Q].
+// Warp i transforms edge i's row (scatter by coefficient, forward WHT), all threads form the
+// prefix / suffix spectral products (thread per symbol over the rows in SMEM), warp i inverse-
+// transforms, gathers by the coefficient, clamps and normalises its edge.
+__global__ void __launch_bounds__(1024)
 wht_check_update_kernel(const double* __restrict__ v2c, const int* __restrict__ coef, const uint8_t* __restrict__ mul,
                         int d, int Q, double* __restrict__ c2v) {
     extern __shared__ double sm[];
     double* y = sm;                         // d x Q spectra of the inputs
     double* s = sm + size_t(d) * Q;         // d x Q extrinsic products / outputs
-    __shared__ double red[WHT_MAXD][8];
     const int64_t ch = blockIdx.x;
     const double* in = v2c + size_t(ch) * d * Q;
     const int* cf = coef + size_t(ch) * d;
-    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
-        const int i = idx / Q, a = idx % Q;
-        y[size_t(i) * Q + mul[cf[i] * Q + a]] = in[idx]; // scatter_by: y[alpha a] = msg[a]
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+    const int EL = Q >= 32 ? Q / 32 : 1;
+    const bool lane_on = Q >= 32 || lane < Q;
+    for (int i = warp; i < d; i += nw) {
+        for (int a = lane; a < Q; a += 32) y[size_t(i) * Q + mul[cf[i] * Q + a]] = in[size_t(i) * Q + a]; // y[alpha a] = msg[a]
+        __syncwarp();
+        double r[WHT_MAXE];
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) r[t] = y[size_t(i) * Q + lane + 32 * t];
+        wht_warp(r, Q, lane);
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) y[size_t(i) * Q + lane + 32 * t] = r[t];
     }
-    wht_rows_smem(y, d, Q);
+    __syncthreads();
     for (int a = threadIdx.x; a < Q; a += blockDim.x) {
         double pre = 1.0;
         for (int i = 0; i < d; ++i) { // prefix into s, then multiply the suffix in from the back
@@ -59,28 +83,29 @@ wht_check_update_kernel(const double* __restrict__ v2c, const int* __restrict__ 
             suf *= y[size_t(i) * Q + a];
         }
     }
-    wht_rows_smem(s, d, Q);
-    // gather by the target coefficient, clamp, normalise per edge
+    __syncthreads();
     const double scale = 1.0 / Q;
-    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
-        const int i = idx / Q, a = idx % Q;
-        y[idx] = fmax(s[size_t(i) * Q + mul[cf[i] * Q + a]] * scale, 0.0);
-    }
-    __syncthreads();
-    // per-edge sums (in ascending symbol order, one warp per edge), then normalise
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-    for (int i = warp; i < d; i += nw) {
-        double acc = 0.0;
-        for (int a = lane; a < Q; a += 32) acc += y[size_t(i) * Q + a];
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) red[i][0] = acc;
-    }
-    __syncthreads();
     double* out = c2v + size_t(ch) * d * Q;
-    for (int idx = threadIdx.x; idx < d * Q; idx += blockDim.x) {
-        const int i = idx / Q;
-        const double sum = red[i][0];
-        out[idx] = sum > 0.0 ? y[idx] / sum : 1.0 / Q;
+    for (int i = warp; i < d; i += nw) {
+        double r[WHT_MAXE];
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) r[t] = s[size_t(i) * Q + lane + 32 * t];
+        wht_warp(r, Q, lane);
+#pragma unroll
+        for (int t = 0; t < WHT_MAXE; ++t)
+            if (t < EL && lane_on) s[size_t(i) * Q + lane + 32 * t] = r[t];
+        __syncwarp();
+        // gather by the target coefficient, clamp, then the edge's sum (lane-strided, xor tree)
+        double acc = 0.0;
+        for (int a = lane; a < Q; a += 32) {
+            const double v = fmax(s[size_t(i) * Q + mul[cf[i] * Q + a]] * scale, 0.0);
+            y[size_t(i) * Q + a] = v;
+            acc += v;
+        }
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        __syncwarp();
+        for (int a = lane; a < Q; a += 32) out[size_t(i) * Q + a] = acc > 0.0 ? y[size_t(i) * Q + a] / acc : 1.0 / Q;
     }
 }
 

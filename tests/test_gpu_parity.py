@@ -275,3 +275,30 @@ def test_uradec_gpu_decode_csv_matches_reference(P, tmp_path, decoder, scorer, t
     ref = cli.decode_row(ds, hf, decoder, scorer, 0, thr, f32=True).split(",")
     ours[13] = ref[13] = "-"
     assert ours == ref
+
+
+@pytest.mark.parametrize("name", ["c3", "c2", "c4"])
+def test_guard_bands_intact_after_the_kernel_set(P, name):
+    """Out-of-bounds write check for the device kernels (compute-sanitizer is closed on the GPU pool):
+    every workspace buffer gets 64 KB 0xA5 guard bands, the config's full kernel set runs (eager and
+    graph-replayed refinement with remasking, a forward with messages), and no band byte may change;
+    the positive control (a byte poked past a buffer's end) must be reported."""
+    cfg = P.configs()[name]
+    wl, model = cfg.workload, cfg.model
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    ctx.set_debug_guard(65536)
+    nb = 40 if name != "c2" else 300
+    _, S = wl.bins(e, 0, nb)
+    sched = P.RevealSchedule(steps=3)
+    for _ in range(3):  # eager, capture, replay
+        ctx.refine(S, wl.k, sched, P.RemaskConfig(rank_fraction=0.25))
+    X = np.where(np.random.default_rng(1).random((nb, wl.k, wl.slots)) < 0.5, 3, -1).astype(np.int32)
+    ctx.denoise(X, S, want_incoming=True)
+    ctx.refine(S, wl.k, sched, P.RemaskConfig(thresholds=(0.9, 0.5)), want_trace=True)
+    bad, msg = ctx.debug_check()
+    assert bad == 0, msg
+    import ctypes as C
+    P._check(P.lib().cider_debug_poke(ctx.h, b"Nn" if name != "c2" else b"X", 100))
+    bad, msg = ctx.debug_check()
+    assert bad == 1 and "overwritten" in msg, msg
