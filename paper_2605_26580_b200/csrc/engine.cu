@@ -1633,7 +1633,8 @@ void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
         attr = true;
     }
     if (smem > 200 * 1024 || max_deg > 32) throw InvalidInput("bp_decode: check degree x Q too large for one CTA");
-    const int cthreads = 32 * std::max(1, std::min(max_deg, 32)); // one warp per edge row of a check
+    const int rpw = 32 / bp::wht_lanes(Q);                           // edge rows per warp
+    const int cthreads = 32 * std::max(1, (max_deg + rpw - 1) / rpw);
     for (int iter = 1; iter <= cfg.max_iters; ++iter) {
         ck(cudaMemsetAsync(c.nact.p, 0, 4, c.stream), "memset");
         bp::bp_check_kernel<<<unsigned(B * P), cthreads, smem, c.stream>>>(c.v2c.as<double>(), c.check_ptr.as<int>(),
@@ -2205,7 +2206,8 @@ int cider_check_update_wht(int m, int n_checks, int d, const double* v2c, const 
         const size_t smem = size_t(2) * d * Q * 8;
         if (smem > 200 * 1024) throw InvalidInput("check_update_wht: d * Q too large for one CTA");
         ck(cudaFuncSetAttribute(wht_check_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
-        wht_check_update_kernel<<<n_checks, 32 * std::max(1, std::min(d, 32)), smem, st>>>(
+        const int rpw = 32 / wht_lanes(Q);
+        wht_check_update_kernel<<<n_checks, 32 * std::max(1, (d + rpw - 1) / rpw), smem, st>>>(
             din.as<double>(), dcf.as<int>(), dmul.as<uint8_t>(), d, Q, dout.as<double>());
         check_launch("wht_check_update");
         ck(cudaMemcpyAsync(c2v, dout.p, nmsg * 8, cudaMemcpyDeviceToHost, st), "d2h");

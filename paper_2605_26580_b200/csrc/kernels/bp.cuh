@@ -46,27 +46,27 @@ __device__ __forceinline__ dd dd_mul(dd a, dd b) {
     return quick_two_sum(p, e);
 }
 
-// WHT of one row held by one warp: lane l owns symbols l + 32 j (j < Q / 32; one symbol per lane
-// for Q < 32). Butterfly stages with len >= 32 pair registers of the same lane, stages with len < 32
-// pair lanes l and l ^ len through warp shuffles — no shared memory, no block barrier. Each pair
-// (u = y[a], v = y[a + len], bit len of a clear) becomes (u + v, u - v) with the same dd operations
-// the reference order implies, so the result is bit-identical to an SMEM butterfly.
+// WHT of one row held by LW lanes of a warp (LW = min(32, Q / 4): 4-8 symbols per lane; 32 / LW rows
+// per warp): lane-in-row r owns symbols r + LW j. Butterfly stages with len >= LW pair registers of
+// the same lane, stages with len < LW pair lanes through warp shuffles — no shared memory, no block
+// barrier. Each pair (u = y[a], v = y[a + len], bit len of a clear) becomes (u + v, u - v) with the same
+// dd operations as an SMEM butterfly, so the result is bit-identical to one.
 constexpr int WHT_MAXE = 8; // symbols per lane (Q <= 256)
+__host__ __device__ inline int wht_lanes(int Q) { return Q >= 128 ? 32 : (Q >= 4 ? Q / 4 : 1); }
 __device__ __forceinline__ dd shfl_dd(dd x, int m) {
     return {__shfl_xor_sync(0xffffffffu, x.hi, m), __shfl_xor_sync(0xffffffffu, x.lo, m)};
 }
-__device__ __forceinline__ void wht_warp_dd(dd (&r)[WHT_MAXE], int Q, int lane) {
-    const int E = Q >= 32 ? Q / 32 : 1;
-    const int lw = Q >= 32 ? 32 : Q; // lane span of a row
-    for (int len = 1; len < lw; len <<= 1) {
+__device__ __forceinline__ void wht_warp_dd(dd (&r)[WHT_MAXE], int Q, int LW, int lr) {
+    const int E = Q / LW;
+    for (int len = 1; len < LW; len <<= 1) {
 #pragma unroll
         for (int j = 0; j < WHT_MAXE; ++j) {
             if (j >= E) break;
             const dd p = shfl_dd(r[j], len);
-            r[j] = (lane & len) ? dd_add(p, dd_neg(r[j])) : dd_add(r[j], p);
+            r[j] = (lr & len) ? dd_add(p, dd_neg(r[j])) : dd_add(r[j], p);
         }
     }
-    for (int h = 1; h < E; h <<= 1) // len = 32 h
+    for (int h = 1; h < E; h <<= 1) // len = LW h
 #pragma unroll
         for (int j = 0; j < WHT_MAXE; ++j) {
             if (j >= E || (j & h)) continue;
@@ -134,21 +134,24 @@ __global__ void bp_check_kernel(const double* __restrict__ v2c, const int* __res
     dd* y = sm_dd;                   // d x Q permuted spectra
     dd* sp = sm_dd + size_t(d) * Q;  // d x Q extrinsic spectra
     const double* in = v2c + (b * E + e0) * Q;
+    const int LW = wht_lanes(Q), RPW = 32 / LW, EL = Q / LW;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-    const int EL = Q >= 32 ? Q / 32 : 1;
-    const bool lane_on = Q >= 32 || lane < Q;
-    for (int i = warp; i < d; i += nw) { // scatter_by (y[alpha a] = msg[a]), then the forward transform
-        const uint8_t* mrow = mul + e_coef[e0 + i] * Q;
-        for (int a = lane; a < Q; a += 32) y[size_t(i) * Q + mrow[a]] = dd{in[size_t(i) * Q + a], 0.0};
+    const int lr = lane % LW;
+    for (int i0 = warp * RPW; i0 < d; i0 += nw * RPW) { // scatter_by (y[alpha a] = msg[a]), then the forward transform
+        const int i = i0 + lane / LW;
+        const bool on = i < d;
+        if (on) {
+            const uint8_t* mrow = mul + e_coef[e0 + i] * Q;
+            for (int a = lr; a < Q; a += LW) y[size_t(i) * Q + mrow[a]] = dd{in[size_t(i) * Q + a], 0.0};
+        }
         __syncwarp();
         dd r[WHT_MAXE];
 #pragma unroll
-        for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) r[t] = y[size_t(i) * Q + lane + 32 * t];
-        wht_warp_dd(r, Q, lane);
+        for (int t = 0; t < WHT_MAXE; ++t) r[t] = (t < EL && on) ? y[size_t(i) * Q + lr + LW * t] : dd{0.0, 0.0};
+        wht_warp_dd(r, Q, LW, lr);
 #pragma unroll
         for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) y[size_t(i) * Q + lane + 32 * t] = r[t];
+            if (t < EL && on) y[size_t(i) * Q + lr + LW * t] = r[t];
     }
     __syncthreads();
     for (int a = threadIdx.x; a < Q; a += blockDim.x) {
@@ -169,29 +172,33 @@ __global__ void bp_check_kernel(const double* __restrict__ v2c, const int* __res
     // dead y slot, normalize_or_uniform per edge (sequential sum by lane 0), a coalesced write
     double* out = c2v + (b * E + e0) * Q;
     const double scale = 1.0 / Q;
-    for (int i = warp; i < d; i += nw) {
+    for (int i0 = warp * RPW; i0 < d; i0 += nw * RPW) {
+        const int i = i0 + lane / LW;
+        const bool on = i < d;
         dd r[WHT_MAXE];
 #pragma unroll
-        for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) r[t] = sp[size_t(i) * Q + lane + 32 * t];
-        wht_warp_dd(r, Q, lane);
+        for (int t = 0; t < WHT_MAXE; ++t) r[t] = (t < EL && on) ? sp[size_t(i) * Q + lr + LW * t] : dd{0.0, 0.0};
+        wht_warp_dd(r, Q, LW, lr);
 #pragma unroll
         for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) sp[size_t(i) * Q + lane + 32 * t] = r[t];
+            if (t < EL && on) sp[size_t(i) * Q + lr + LW * t] = r[t];
         __syncwarp();
-        double* xo = reinterpret_cast<double*>(y + size_t(i) * Q);
-        const uint8_t* mrow = mul + e_coef[e0 + i] * Q;
-        for (int a = lane; a < Q; a += 32) {
-            const dd v = sp[size_t(i) * Q + mrow[a]];
-            xo[a] = fmax((v.hi + v.lo) * scale, 0.0); // scale is a power of two: exact
+        double* xo = reinterpret_cast<double*>(y + size_t(on ? i : 0) * Q);
+        if (on) {
+            const uint8_t* mrow = mul + e_coef[e0 + i] * Q;
+            for (int a = lr; a < Q; a += LW) {
+                const dd v = sp[size_t(i) * Q + mrow[a]];
+                xo[a] = fmax((v.hi + v.lo) * scale, 0.0); // scale is a power of two: exact
+            }
         }
         __syncwarp();
         double t = 0.0;
-        if (lane == 0)
+        if (on && lr == 0)
             for (int a = 0; a < Q; ++a) t += xo[a];
-        t = __shfl_sync(0xffffffffu, t, 0);
+        t = __shfl_sync(0xffffffffu, t, lane - lr); // from the row's first lane
         const double iv = t > 0.0 ? 1.0 / t : -1.0;
-        for (int a = lane; a < Q; a += 32) out[size_t(i) * Q + a] = iv < 0.0 ? 1.0 / Q : xo[a] * iv;
+        if (on)
+            for (int a = lr; a < Q; a += LW) out[size_t(i) * Q + a] = iv < 0.0 ? 1.0 / Q : xo[a] * iv;
     }
 }
 

@@ -17,19 +17,19 @@ namespace cider {
 
 constexpr int WHT_MAXD = 32;
 
-// One row per warp in registers (lane l: symbols l + 32 j), butterflies with len >= 32 inside a lane,
-// len < 32 across lanes by warp shuffles: (u, v) -> (u + v, u - v) in fp64, the same operations as an
-// SMEM butterfly, without block barriers.
+// One row per LW lanes (LW = min(32, Q / 4), 4-8 symbols per lane, 32 / LW rows per warp) in
+// registers: butterflies with len >= LW inside a lane, len < LW across lanes by warp shuffles:
+// (u, v) -> (u + v, u - v) in fp64, the same operations as an SMEM butterfly, without block barriers.
 constexpr int WHT_MAXE = 8; // symbols per lane (Q <= 256)
-__device__ __forceinline__ void wht_warp(double (&r)[WHT_MAXE], int Q, int lane) {
-    const int E = Q >= 32 ? Q / 32 : 1;
-    const int lw = Q >= 32 ? 32 : Q;
-    for (int len = 1; len < lw; len <<= 1) {
+__host__ __device__ inline int wht_lanes(int Q) { return Q >= 128 ? 32 : (Q >= 4 ? Q / 4 : 1); }
+__device__ __forceinline__ void wht_warp(double (&r)[WHT_MAXE], int Q, int LW, int lr) {
+    const int E = Q / LW;
+    for (int len = 1; len < LW; len <<= 1) {
 #pragma unroll
         for (int j = 0; j < WHT_MAXE; ++j) {
             if (j >= E) break;
             const double p = __shfl_xor_sync(0xffffffffu, r[j], len);
-            r[j] = (lane & len) ? p - r[j] : r[j] + p;
+            r[j] = (lr & len) ? p - r[j] : r[j] + p;
         }
     }
     for (int h = 1; h < E; h <<= 1)
@@ -55,20 +55,22 @@ wht_check_update_kernel(const double* __restrict__ v2c, const int* __restrict__ 
     const int64_t ch = blockIdx.x;
     const double* in = v2c + size_t(ch) * d * Q;
     const int* cf = coef + size_t(ch) * d;
+    const int LW = wht_lanes(Q), RPW = 32 / LW, EL = Q / LW;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-    const int EL = Q >= 32 ? Q / 32 : 1;
-    const bool lane_on = Q >= 32 || lane < Q;
-    for (int i = warp; i < d; i += nw) {
-        for (int a = lane; a < Q; a += 32) y[size_t(i) * Q + mul[cf[i] * Q + a]] = in[size_t(i) * Q + a]; // y[alpha a] = msg[a]
+    const int lr = lane % LW;
+    for (int i0 = warp * RPW; i0 < d; i0 += nw * RPW) {
+        const int i = i0 + lane / LW;
+        const bool on = i < d;
+        if (on)
+            for (int a = lr; a < Q; a += LW) y[size_t(i) * Q + mul[cf[i] * Q + a]] = in[size_t(i) * Q + a]; // y[alpha a] = msg[a]
         __syncwarp();
         double r[WHT_MAXE];
 #pragma unroll
-        for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) r[t] = y[size_t(i) * Q + lane + 32 * t];
-        wht_warp(r, Q, lane);
+        for (int t = 0; t < WHT_MAXE; ++t) r[t] = (t < EL && on) ? y[size_t(i) * Q + lr + LW * t] : 0.0;
+        wht_warp(r, Q, LW, lr);
 #pragma unroll
         for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) y[size_t(i) * Q + lane + 32 * t] = r[t];
+            if (t < EL && on) y[size_t(i) * Q + lr + LW * t] = r[t];
     }
     __syncthreads();
     for (int a = threadIdx.x; a < Q; a += blockDim.x) {
@@ -86,26 +88,29 @@ wht_check_update_kernel(const double* __restrict__ v2c, const int* __restrict__ 
     __syncthreads();
     const double scale = 1.0 / Q;
     double* out = c2v + size_t(ch) * d * Q;
-    for (int i = warp; i < d; i += nw) {
+    for (int i0 = warp * RPW; i0 < d; i0 += nw * RPW) {
+        const int i = i0 + lane / LW;
+        const bool on = i < d;
         double r[WHT_MAXE];
 #pragma unroll
-        for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) r[t] = s[size_t(i) * Q + lane + 32 * t];
-        wht_warp(r, Q, lane);
+        for (int t = 0; t < WHT_MAXE; ++t) r[t] = (t < EL && on) ? s[size_t(i) * Q + lr + LW * t] : 0.0;
+        wht_warp(r, Q, LW, lr);
 #pragma unroll
         for (int t = 0; t < WHT_MAXE; ++t)
-            if (t < EL && lane_on) s[size_t(i) * Q + lane + 32 * t] = r[t];
+            if (t < EL && on) s[size_t(i) * Q + lr + LW * t] = r[t];
         __syncwarp();
-        // gather by the target coefficient, clamp, then the edge's sum (lane-strided, xor tree)
+        // gather by the target coefficient, clamp, then the edge's sum (lane-strided, xor tree over the row's lanes)
         double acc = 0.0;
-        for (int a = lane; a < Q; a += 32) {
-            const double v = fmax(s[size_t(i) * Q + mul[cf[i] * Q + a]] * scale, 0.0);
-            y[size_t(i) * Q + a] = v;
-            acc += v;
-        }
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (on)
+            for (int a = lr; a < Q; a += LW) {
+                const double v = fmax(s[size_t(i) * Q + mul[cf[i] * Q + a]] * scale, 0.0);
+                y[size_t(i) * Q + a] = v;
+                acc += v;
+            }
+        for (int o = LW / 2; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         __syncwarp();
-        for (int a = lane; a < Q; a += 32) out[size_t(i) * Q + a] = acc > 0.0 ? y[size_t(i) * Q + a] / acc : 1.0 / Q;
+        if (on)
+            for (int a = lr; a < Q; a += LW) out[size_t(i) * Q + a] = acc > 0.0 ? y[size_t(i) * Q + a] / acc : 1.0 / Q;
     }
 }
 

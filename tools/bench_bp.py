@@ -26,18 +26,20 @@ def main():
     ap.add_argument("--bins", type=int, default=512)
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--cpu-bins", type=int, default=16)
-    ap.add_argument("--profile", action="store_true", help="one small decode only (for ncu)")
+    ap.add_argument("--profile", action="store_true", help="one 2-iteration decode of --bins bins only (for ncu)")
     a = ap.parse_args()
     cfg = P.configs()[a.config]
     wl = cfg.workload
     e = wl.code()
-    nb = 8 if a.profile else a.bins
+    nb = a.bins
     truth, S = wl.bins(e, 0, nb)
     S = S.astype(np.float64)
     dec = P.BpDecoder(wl.m, e, wl.checks, wl.slots)
     bc = P.BpConfig(max_iters=a.iters)
-    dec.sic_decode(S[: min(nb, 8)], wl.k, bc)  # warm-up
-    if a.profile:
+    if not a.profile:
+        dec.sic_decode(S[: min(nb, 8)], wl.k, bc)  # warm-up
+    if a.profile:  # one 2-iteration decode of the whole batch: realistic launch sizes for ncu
+        dec.sic_decode(S, wl.k, P.BpConfig(max_iters=2))
         return
     t0 = time.perf_counter()
     grid, sc, si = dec.sic_decode(S, wl.k, bc)
