@@ -296,13 +296,14 @@ DevBuf& wbuf(cider_ctx& c, size_t bytes) {
 
 float bf16_round(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
 
-// Upload a host fp32 matrix, optionally transposed, in the activation type.
-void* upload_mat(cider_ctx& c, const float* src, int rows, int cols, bool transpose) {
+// Upload a host fp32 matrix, optionally transposed, in the activation type; `scale` (a power of two)
+// multiplies it first (exact in bf16).
+void* upload_mat(cider_ctx& c, const float* src, int rows, int cols, bool transpose, float scale = 1.0f) {
     const int R = transpose ? cols : rows, C = transpose ? rows : cols;
     std::vector<float> t(size_t(R) * C);
     for (int r = 0; r < rows; ++r)
         for (int q = 0; q < cols; ++q) {
-            float v = src[size_t(r) * cols + q];
+            float v = src[size_t(r) * cols + q] * scale;
             if (transpose) t[size_t(q) * rows + r] = v; else t[size_t(r) * cols + q] = v;
         }
     DevBuf& b = wbuf(c, t.size() * c.act_size);
@@ -1376,20 +1377,24 @@ void upload_model(cider_ctx& c, const float* w) {
     c.Wt = upload_mat(c, W, Q, D, true);
     c.Vt = upload_mat(c, V, Q, D, true);
     c.lw.resize(c.N);
+    // BF16 mode: every GELU on the device returns 2 GELU(x) (one multiply less per element in the
+    // MLP epilogues, mlp_tc.cuh) and the second-layer matrices are stored halved — both exact powers
+    // of two, so the products and sums are bit-identical to unscaled ones.
+    const float w2s = c.bf16 ? 0.5f : 1.0f;
     for (int l = 0; l < c.N; ++l) {
         LayerW& L = c.lw[l];
         const float* p;
         p = take(size_t(H) * 2 * D); L.g1 = upload_mat(c, p, H, 2 * D, false);
         p = take(H); L.gb1 = upload_vec(c, p, H);
-        p = take(size_t(D) * H); L.g2 = upload_mat(c, p, D, H, false);
+        p = take(size_t(D) * H); L.g2 = upload_mat(c, p, D, H, false, w2s);
         p = take(D); L.gb2 = upload_vec(c, p, D);
         p = take(size_t(H) * D); L.a1 = upload_mat(c, p, H, D, false);
         p = take(H); L.ab1 = upload_vec(c, p, H);
-        p = take(size_t(D) * H); L.a2 = upload_mat(c, p, D, H, false);
+        p = take(size_t(D) * H); L.a2 = upload_mat(c, p, D, H, false, w2s);
         p = take(D); L.ab2 = upload_vec(c, p, D);
         p = take(size_t(H) * 2 * D); L.f1 = upload_mat(c, p, H, 2 * D, false);
         p = take(H); L.fb1 = upload_vec(c, p, H);
-        p = take(size_t(D) * H); L.f2 = upload_mat(c, p, D, H, false);
+        p = take(size_t(D) * H); L.f2 = upload_mat(c, p, D, H, false, w2s);
         p = take(D); L.fb2 = upload_vec(c, p, D);
         L.ak = nullptr;
         L.aq = nullptr;

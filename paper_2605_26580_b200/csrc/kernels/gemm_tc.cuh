@@ -155,7 +155,7 @@ __device__ __forceinline__ void epi_row32(const Epi& ep, int m, int n0, float* v
     }
     if (ep.kind == EP_GELU) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = gelu_f(v[i]);
+        for (int i = 0; i < 32; ++i) v[i] = 2.0f * gelu_f(v[i]); // BF16 mode: 2 GELU, second layer stored halved
     } else if (ep.kind == EP_GATE || ep.kind == EP_RESID) {
         // z / e from the fp32 stream when present, else from the bf16 stream (BF16 mode)
         float zz[32], ee[32];

@@ -31,19 +31,19 @@ __device__ __forceinline__ float tanh_approx(float x) {
 }
 // sigmoid(x) = 0.5 tanh(x/2) + 0.5: one MUFU op (abs error ~2.5e-4, below the bf16 output rounding)
 __device__ __forceinline__ float sigmoid_fast(float x) { return fmaf(0.5f, tanh_approx(0.5f * x), 0.5f); }
-__device__ __forceinline__ float gelu_fast(float x) {
+// The device GELUs return 2 GELU(x) = x + x tanh(...): the 1/2 lives in the second-layer weights,
+// which BF16 mode stores halved (engine.cu upload_model) — exact, one multiply less per element.
+__device__ __forceinline__ float gelu_fast(float x) { // 2 GELU(x)
     const float inner = x * fmaf(0.0356774081f, x * x, 0.7978845608f);
-    const float hx = 0.5f * x;
-    return fmaf(hx, tanh_approx(inner), hx);
+    return fmaf(x, tanh_approx(inner), x);
 }
 // Two lanes at once with the sm_100 packed fp32 ops (FFMA2/FMUL2/FADD2): same arithmetic as
-// gelu_fast(x + b) per element, half the FP32 instructions.
+// gelu_fast(x + b) per element, half the FP32 instructions. Returns bf16(2 GELU(x + b)).
 __device__ __forceinline__ uint32_t gelu2_bias_bf16(float x0, float x1, float b0, float b1) {
     const float2 x = __fadd2_rn(make_float2(x0, x1), make_float2(b0, b1));
     const float2 p = __ffma2_rn(__fmul2_rn(x, x), make_float2(0.0356774081f, 0.0356774081f), make_float2(0.7978845608f, 0.7978845608f));
     const float2 in = __fmul2_rn(x, p);
-    const float2 hx = __fmul2_rn(x, make_float2(0.5f, 0.5f));
-    const float2 y = __ffma2_rn(hx, make_float2(tanh_approx(in.x), tanh_approx(in.y)), hx);
+    const float2 y = __ffma2_rn(x, make_float2(tanh_approx(in.x), tanh_approx(in.y)), x);
     __nv_bfloat162 r = __floats2bfloat162_rn(y.x, y.y);
     return *reinterpret_cast<uint32_t*>(&r);
 }
