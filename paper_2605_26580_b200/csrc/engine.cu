@@ -227,6 +227,7 @@ struct cider_ctx {
     std::vector<DevBuf> wbufs;
     float* Etab = nullptr;                 // (Q+1) x D fp32
     void *W = nullptr, *Wt = nullptr, *Vt = nullptr;
+    void *Wpad = nullptr, *Vtpad = nullptr; // BF16, Q < 128: W / V^T padded with zero symbols to 128 (demix_evid)
     std::vector<LayerW> lw;
     // Tanner tables
     int *e_slot = nullptr, *e_check = nullptr, *check_ptr = nullptr, *slot_ptr = nullptr, *slot_edge = nullptr;
@@ -866,22 +867,26 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
 // (intermediate_logits + demix_responsibilities + evidence_embed, denoiser.cpp:86-139): the 2-SM
 // fused two-layer kernel with hidden = the Q symbol columns and the demix as its hidden activation.
 bool demix_evid_ok(const cider_ctx& c, int K) {
-    return c.bf16 && c.D == 256 && c.Q == 256 && (K == 4 || K == 8);
+    return c.bf16 && (c.D == 256 || c.D == 128) && (c.Q == 256 || c.Q == 128 || c.Q == 64) && (K == 4 || K == 8);
 }
 void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K, bf16* e_out) {
     const int D = c.D, Q = c.Q;
+    const int Qp = Q < tc::MLP_HC ? tc::MLP_HC : Q; // hidden width: Q < 128 padded to one chunk (zero W / V rows)
     Epi ep = epi(EP_DEMIX);
     ep.M = int(Ms); ep.N = D; ep.out_t = e_out; ep.ldo = D; ep.S = S; ep.L = c.L; ep.K = K;
+    ep.ldz = Q; // S row stride = the valid symbol columns
     ep.beta = float(c.md.evidence_scale);
     ep.inv_tau = 1.0f / float(c.md.tau_demix); // as demix_block_kernel computes it
     Launch lg(c, "demix_evid", 2.0 * double(Ms) * Q * (D + D), double(Ms) * (2 * D * c.act_size) + double(Ms / K) * Q * 4);
     const CUtensorMap x0 = make_map_w1_3d(Zt, Ms, D, 128, D / 64); // the whole 128-row tile in one box
-    const CUtensorMap w1 = make_map_w1_3d(c.W, Q, D, tc::MLP_HC / 2);
-    const CUtensorMap& w2 = map_for(c, c.Vt, D, Q, Q, D / 2);
+    const void* W = Qp == Q ? c.W : c.Wpad;
+    const void* Vt = Qp == Q ? c.Vt : c.Vtpad;
+    const CUtensorMap w1 = make_map_w1_3d(W, Qp, D, tc::MLP_HC / 2);
+    const CUtensorMap& w2 = map_for(c, Vt, D, Qp, Qp, D / 2);
     tc::MlpArgs a;
     a.M = int(Ms);
     a.K0 = D;
-    a.H = Q;
+    a.H = Qp;
     a.tiles = int((Ms + 255) / 256);
     a.b1 = nullptr;
     a.ep = ep;
@@ -892,9 +897,10 @@ void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K,
         cudaMemsetAsync(a.trace, 0, 8 * 1024, c.stream);
     }
     const CUtensorMap om = make_map_box(e_out, Ms, D, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B); // e k-blocks staged in X
-    launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, om, a);
+    if (D == 256) launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, om, a);
+    else launch_mlp2<128, 128, EP_DEMIX>(c, x0, x0, w1, w2, om, a);
     check_launch("demix_evid");
-    if (a.trace) dump_mlp_trace(c, "demix_evid", Ms, Q, true, a.trace);
+    if (a.trace) dump_mlp_trace(c, "demix_evid", Ms, Qp, true, a.trace);
 }
 
 // ---- one denoiser forward over nb bins (denoiser.cpp:253-259) -------------------------------
@@ -1376,6 +1382,13 @@ void upload_model(cider_ctx& c, const float* w) {
     c.W = upload_mat(c, W, Q, D, false);
     c.Wt = upload_mat(c, W, Q, D, true);
     c.Vt = upload_mat(c, V, Q, D, true);
+    if (c.bf16 && Q < tc::MLP_HC) { // zero symbol rows Q..127: Lambda-bar 0, r (x) S 0 (S reads 0 there)
+        std::vector<float> wp(size_t(tc::MLP_HC) * D, 0.0f), vp(size_t(tc::MLP_HC) * D, 0.0f);
+        std::copy(W, W + size_t(Q) * D, wp.begin());
+        std::copy(V, V + size_t(Q) * D, vp.begin());
+        c.Wpad = upload_mat(c, wp.data(), tc::MLP_HC, D, false);
+        c.Vtpad = upload_mat(c, vp.data(), tc::MLP_HC, D, true);
+    }
     c.lw.resize(c.N);
     // BF16 mode: every GELU on the device returns 2 GELU(x) (one multiply less per element in the
     // MLP epilogues, mlp_tc.cuh) and the second-layer matrices are stored halved — both exact powers

@@ -280,7 +280,10 @@ __device__ __forceinline__ void demix_load_sv(const MlpArgs& args, int m0, int c
 #pragma unroll
         for (int t = 0; t < NGL; ++t) {
             const int r0 = m0 + rh * 16 + t * KK;
-            sv[p * NGL + t] = r0 < args.ep.M ? __ldg(args.ep.S + size_t(r0 / KK) * args.H + col0 + p * 16 + cl) : 0.0f;
+            // S row stride and valid symbol count = ep.ldz (Q); hidden columns past Q (Q < 128 padded to
+            // one 128-column chunk, zero rows of W and V) read S = 0, so they add nothing to e
+            const int col = col0 + p * 16 + cl;
+            sv[p * NGL + t] = r0 < args.ep.M && col < args.ep.ldz ? __ldg(args.ep.S + size_t(r0 / KK) * args.ep.ldz + col) : 0.0f;
         }
 }
 
@@ -758,12 +761,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                 __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * jj + 2 * t], v[8 * jj + 2 * t + 1]);
                                 pk[t] = *reinterpret_cast<uint32_t*>(&b2);
                             }
-                            st_shared_v4(dst + lane * 128 + ((j ^ (lane & 7)) * 16), pk);
+                            if (half < KBD) st_shared_v4(dst + lane * 128 + ((j ^ (lane & 7)) * 16), pk);
                         }
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&o_full[(it % NXB) * KBD + half]);
+                    // (D = 128: two output k-blocks; warps of halves 2, 3 only help drain acc2)
+                    if (lane == 0 && half < KBD) mbar_arrive(&o_full[(it % NXB) * KBD + half]);
                 }
                 if (trf) args.trace[512 + it * 4 + 2] = clock64();
                 continue;
