@@ -25,6 +25,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h> // header-only NVTX3: no-ops unless a tool (ncu --nvtx, nsys) is attached
+
 #include "host/host.hpp"
 #include "kernels/common.cuh"
 #include "kernels/gemm_simt.cuh"
@@ -340,6 +342,7 @@ struct Launch {
     cudaEvent_t a = nullptr, b = nullptr;
     Launch(cider_ctx& c_, const char* t, double f, double by) : c(c_), tag(t), flops(f), bytes(by) {
         ++c.launches;
+        nvtxRangePushA(t); // one NVTX range per kernel class launch (ncu --nvtx --nvtx-include, nsys)
         if (c.profiling) {
             a = take();
             cudaEventRecord(a, c.stream);
@@ -356,6 +359,7 @@ struct Launch {
         return e;
     }
     ~Launch() {
+        nvtxRangePop();
         if (c.profiling) {
             b = take();
             cudaEventRecord(b, c.stream);
@@ -910,7 +914,13 @@ struct FwdOpts {
     float* incoming = nullptr;    // internal-layout [layers][Ms x D] (nullable)
 };
 
+struct NvtxRange { // scoped NVTX range (no-op without a tool)
+    explicit NvtxRange(const char* n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, const FwdOpts& o) {
+    NvtxRange nv("cider.forward");
     const int L = c.L, E = c.E, Q = c.Q, D = c.D, H = c.H;
     const int64_t Ms = int64_t(nb) * L * K, Me = int64_t(nb) * E * K;
     {
@@ -1103,6 +1113,7 @@ void probe_record(cider_ctx& c, Probe& p, int K, const int* X, int t, int steps,
 // X holds the start grid (internal layout); init_masked / upd describe it per bin.
 void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int steps, const cider_schedule& sc,
                  const PassTrace* pt) {
+    NvtxRange nv("cider.masked_pass");
     const int n = c.L * K;
     Probe* probe = c.probe;
     // reveal keys: dynamic shared memory up to REVEAL_SMEM_SITES, else a per-bin global slice
