@@ -334,6 +334,28 @@ T* upload_raw(cider_ctx& c, const std::vector<T>& v) {
     return b.as<T>();
 }
 
+// ---- programmatic dependent launch -----------------------------------------------------------
+// The kernels of the refinement chain are launched with programmatic stream serialization: each
+// calls griddep_wait() before reading anything earlier kernels produced (kernels/common.cuh), and
+// the persistent ones (every CTA resident) call griddep_launch_dependents() right after, so the next
+// kernel's launch and prologue (barrier init, TMEM allocation, descriptor prefetch) overlap this
+// kernel's tail instead of following it. Captured into the refinement CUDA graphs as programmatic
+// edges.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 // ---- launch bookkeeping --------------------------------------------------------------------
 struct Launch {
     cider_ctx& c;
@@ -407,7 +429,7 @@ void launch_tc(cider_ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const
         attr_set = true;
     }
     int grid = std::min(args.tiles, c.sm_count);
-    tc::gemm_tc_kernel<BN, EPW, BRES><<<grid, 64 + 32 * EPW, Lay::TOTAL, c.stream>>>(a0, a1, b, args);
+    launch_pdl(tc::gemm_tc_kernel<BN, EPW, BRES>, grid, 64 + 32 * EPW, Lay::TOTAL, c.stream, a0, a1, b, args);
 }
 
 // C[M x N] = [A0 (M x K0) | A1 (M x K1)] . B[N x (K0+K1)]^T, then the epilogue.
@@ -490,7 +512,7 @@ void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, con
         attr_set = true;
     }
     const int pairs = std::min(a.tiles, c.sm_count / 2);
-    tc::mlp_tc2_kernel<KIN, D, EPK><<<2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, out, a);
+    launch_pdl(tc::mlp_tc2_kernel<KIN, D, EPK>, 2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream, x0, x1, w1, w2, out, a);
 }
 
 bool mlp_fusable(const cider_ctx& c, int Kin) {
@@ -756,7 +778,7 @@ void launch_pool_mma(cider_ctx& c, const LayerW& lw, const CUtensorMap& tm, int6
         attr = true;
     }
     const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count) * 2));
-    pool_mma_kernel<K, D><<<grid, PM_THREADS, PoolMmaLayout::TOTAL, c.stream>>>(tm, (const bf16*)lw.aus16, c.check_ptr, c.P, c.E,
+    launch_pdl(pool_mma_kernel<K, D>, grid, PM_THREADS, PoolMmaLayout::TOTAL, c.stream, tm, (const bf16*)lw.aus16, c.check_ptr, c.P, c.E,
                                                                              c.heads, blocks, (bf16*)pooled);
 }
 void run_pool_mma(cider_ctx& c, const LayerW& lw, const void* Nn, int64_t Me, int nb, int K, void* pooled) {
@@ -833,8 +855,8 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
         if (!out_t || out_f) throw InvalidInput("cider: the paired T-resident grouped GEMM writes one bf16 output");
         const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb);
-        if (D == 256) tc::gemm_grp2_res_kernel<256><<<grid, tc::GRP_THREADS, tc::grp2_res_smem<256>(), c.stream>>>(ta, tt2, to, a);
-        else tc::gemm_grp2_res_kernel<128><<<grid, tc::GRP_THREADS, tc::grp2_res_smem<128>(), c.stream>>>(ta, tt2, to, a);
+        if (D == 256) launch_pdl(tc::gemm_grp2_res_kernel<256>, grid, tc::GRP_THREADS, tc::grp2_res_smem<256>(), c.stream, ta, tt2, to, a);
+        else launch_pdl(tc::gemm_grp2_res_kernel<128>, grid, tc::GRP_THREADS, tc::grp2_res_smem<128>(), c.stream, ta, tt2, to, a);
         check_launch(tag);
         return;
     }
@@ -852,8 +874,8 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
         if (!out_t) throw InvalidInput("cider: the paired grouped GEMM writes a bf16 output");
         const CUtensorMap to = make_map_rows3d(out_t, nb, out_rows_per_bin * K, D, K, bb); // TMA store boxes
-        if (D == 256) tc::gemm_grp2_kernel<256><<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, to, a);
-        else tc::gemm_grp2_kernel<128><<<grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream>>>(ta, tt2, to, a);
+        if (D == 256) launch_pdl(tc::gemm_grp2_kernel<256>, grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream, ta, tt2, to, a);
+        else launch_pdl(tc::gemm_grp2_kernel<128>, grid, tc::GRP_THREADS, tc::GRP2_SMEM, c.stream, ta, tt2, to, a);
         check_launch(tag);
         return;
     }
@@ -863,7 +885,7 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
         attr_set = true;
     }
-    tc::gemm_grp_kernel<<<std::min(tiles, c.sm_count), tc::GRP_THREADS, Lay::TOTAL, c.stream>>>(ta, tt, a);
+    launch_pdl(tc::gemm_grp_kernel, std::min(tiles, c.sm_count), tc::GRP_THREADS, Lay::TOTAL, c.stream, ta, tt, a);
     check_launch(tag);
 }
 
@@ -926,7 +948,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
     {
         Launch lg(c, "embed", 0, double(Ms) * D * (4 + c.act_size));
         if (c.bf16 && D % 8 == 0)
-            embed_bf16x8_kernel<<<blocks_for(Ms * (D / 8)), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, (bf16*)w.Zt);
+            launch_pdl(embed_bf16x8_kernel, blocks_for(Ms * (D / 8)), 256, 0, c.stream, X, (const float*)c.Etab, Q, D, Ms, (bf16*)w.Zt);
         else if (c.bf16)
             embed_kernel<bf16><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, nullptr, (bf16*)w.Zt);
         else
@@ -1134,14 +1156,14 @@ void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int
         const bool first = t == 1 && sc.first_reveal;
         if (pt && t == 1) ck(cudaMemsetAsync(pt->sites, 0, size_t(nb) * n, c.stream), "memset");
         Launch lg(c, "reveal", 0, double(nb) * n * 12);
-        reveal_kernel<<<nb, 512, smem, c.stream>>>(X, w.kappa, w.amax, c.L, K, w.init_masked, cosine_fraction(t, steps),
-                                                   first ? 1 : 0, pt ? pt->counts + (t - 1) : nullptr, steps,
-                                                   pt && t == 1 ? pt->sites : nullptr, gkeys);
+        launch_pdl(reveal_kernel, nb, 512, smem, c.stream, X, (const float*)w.kappa, (const int*)w.amax, c.L, K,
+                   (const int*)w.init_masked, cosine_fraction(t, steps), first ? 1 : 0, pt ? pt->counts + (t - 1) : nullptr,
+                   steps, pt && t == 1 ? pt->sites : nullptr, gkeys);
         check_launch("reveal");
     }
     {
         Launch lg(c, "force_residual", 0, double(nb) * n * 12);
-        force_residual_kernel<<<blocks_for(int64_t(nb) * n), 256, 0, c.stream>>>(X, w.amax, int64_t(nb) * n);
+        launch_pdl(force_residual_kernel, blocks_for(int64_t(nb) * n), 256, 0, c.stream, X, (const int*)w.amax, int64_t(nb) * n);
         check_launch("force_residual");
     }
     FwdOpts o; // the gamma = 0 pass; kappa at tau = 1 feeds MaxProbScorer (refine.cpp:218-225)
@@ -1151,7 +1173,8 @@ void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int
     if (probe) probe_record(c, *probe, K, X, 0, steps, 1);
     {
         Launch lg(c, "finalize", 0, double(nb) * n * 12);
-        finalize_kernel<<<blocks_for(int64_t(nb) * n), 256, 0, c.stream>>>(X, w.amax, w.upd, K, int64_t(nb) * n, n);
+        launch_pdl(finalize_kernel, blocks_for(int64_t(nb) * n), 256, 0, c.stream, X, (const int*)w.amax, (const uint32_t*)w.upd, K,
+                   int64_t(nb) * n, n);
         check_launch("finalize");
         ck(cudaMemcpyAsync(w.k1, w.kappa, size_t(nb) * n * 4, cudaMemcpyDeviceToDevice, c.stream), "k1");
     }

@@ -12,6 +12,15 @@
 
 namespace cider {
 
+// Programmatic dependent launch (kernels launched with programmatic stream serialization, engine.cu
+// launch_pdl): griddep_wait() blocks until the preceding grid has completed and its writes are
+// visible — every such kernel calls it before reading anything an earlier kernel produced; a
+// persistent kernel (all CTAs resident) then lets the next grid start launching (its prologue
+// overlaps this grid's tail) with griddep_launch_dependents().
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+
 typedef __nv_bfloat16 bf16;
 
 __device__ __forceinline__ float to_f(float v) { return v; }

@@ -74,6 +74,8 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     __syncthreads();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_wait(); // (programmatic dependent launch) inputs of the previous kernel visible
+    griddep_launch_dependents();
     const int a_bytes = args.K * args.bb * 128; // the A box actually filled (<= 16 KB)
 
     if (warp == 0) {
@@ -221,6 +223,8 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     cluster_sync_all();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_wait(); // (programmatic dependent launch) inputs of the previous kernel visible
+    griddep_launch_dependents();
     const int a_bytes = args.K * args.bb * 128; // the A box actually filled (<= 16 KB)
     const uint32_t L_full0 = mapa_u32(smem_u32(&full[0]), 0);
     const uint32_t L_tempty0 = mapa_u32(smem_u32(&tempty[0]), 0);
@@ -409,6 +413,8 @@ gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     cluster_sync_all();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_wait(); // (programmatic dependent launch) inputs of the previous kernel visible
+    griddep_launch_dependents();
     const int a_bytes = args.K * args.bb * 128;
     const uint32_t L_full0 = mapa_u32(smem_u32(&full[0]), 0);
     const uint32_t L_tfull = mapa_u32(smem_u32(t_full), 0);

@@ -287,6 +287,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     __syncthreads();
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_wait(); // (programmatic dependent launch) inputs of the previous kernel visible
+    griddep_launch_dependents();
 
     if (warp == 0) {
         if (lane == 0) {

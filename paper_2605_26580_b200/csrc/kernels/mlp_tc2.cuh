@@ -445,6 +445,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     cluster_sync_all(); // barriers of both CTAs initialised before any remote signal
     fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait(); // (programmatic dependent launch) inputs of the previous kernel visible
+    griddep_launch_dependents();
     const uint32_t L_x_full0 = mapa_u32(smem_u32(&x_full[0]), 0);
     const uint32_t L_r_full0 = mapa_u32(smem_u32(&r_full[0]), 0);
     const uint32_t L_h_full0 = mapa_u32(smem_u32(&h_full[0]), 0);

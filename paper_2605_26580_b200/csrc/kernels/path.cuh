@@ -29,6 +29,7 @@ __global__ void embed_kernel(const int* __restrict__ X, const float* __restrict_
 // Vectorised BF16 variant (D % 8 == 0): 8 columns per thread, one 16-byte store.
 __global__ void embed_bf16x8_kernel(const int* __restrict__ X, const float* __restrict__ Etab, int Q, int D, int64_t M,
                                     bf16* __restrict__ Zt) {
+    griddep_wait(); // (programmatic dependent launch) the grid X of the previous step
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int cpr = D / 8; // 16-byte chunks per row
     if (i >= M * cpr) return;
@@ -616,6 +617,7 @@ reveal_kernel(int* __restrict__ X, const float* __restrict__ kappa, const int* _
               int K, const int* __restrict__ init_masked, double rho, int first,
               int* __restrict__ count, int count_stride, uint8_t* __restrict__ sites,
               unsigned long long* __restrict__ gkeys) {
+    griddep_wait(); // (programmatic dependent launch) kappa / argmax of the forward
     extern __shared__ unsigned long long skey[];
     __shared__ int red[32];
     const int b = blockIdx.x;
@@ -708,12 +710,14 @@ reveal_kernel(int* __restrict__ X, const float* __restrict__ kappa, const int* _
 // ---- end of a pass (refine.cpp:175-192) ------------------------------------------------------
 // residual masks -> the last step's argmax
 __global__ void force_residual_kernel(int* __restrict__ X, const int* __restrict__ amax, int64_t n) {
+    griddep_wait();
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n && X[i] == -1) X[i] = amax[i];
 }
 // updatable rows take the final (gamma = 0) pass's argmax; the rest stay bit-identical
 __global__ void finalize_kernel(int* __restrict__ X, const int* __restrict__ amax,
                                 const uint32_t* __restrict__ upd_mask, int K, int64_t n_bins_x_n, int n) {
+    griddep_wait();
     int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n_bins_x_n) return;
     int64_t b = i / n;

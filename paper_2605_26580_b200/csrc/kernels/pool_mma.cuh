@@ -85,6 +85,8 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    griddep_wait(); // (programmatic dependent launch) inputs of the previous kernel visible
+    griddep_launch_dependents();
 
     // this group's blocks: blockIdx.x + (2 i + grp) * gridDim.x, i = 0, 1, ...
     const int stride = 2 * int(gridDim.x);
