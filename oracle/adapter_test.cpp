@@ -259,6 +259,36 @@ int main() {
             fails += same != int(cpu_out.size()) || cpu_out.size() != gpu_out.size() || cpu_out.empty();
             fails += !agg;
         }
+        // (8) config-mode context (N = 2 layers, hidden 48, 2 attention heads) through the adapter: the
+        // reference's own loop driving GpuStructuredDenoiser equals the device loop (GpuRefiner), FP32
+        {
+            cider_model_desc md{};
+            md.m = 6;
+            md.dim = 32;
+            md.hidden = 48;
+            md.layers = 2;
+            md.heads = 2;
+            md.tau_demix = 1.0;
+            md.evidence_scale = 1.0;
+            md.precision = CIDER_FP32;
+            std::vector<float> w(cider_weights_count(&md));
+            cider::check(cider_weights_init(&md, 4, w.data()));
+            auto cctx = std::make_shared<cider::Context>(md, w, h, 0);
+            cider::GpuStructuredDenoiser cden(cctx);
+            cider::GpuRefiner cref(cctx);
+            int same = 0;
+            for (int b = 0; b < 4; ++b) {
+                ura::EvidenceMatrix s8(16, 64);
+                auto er = ura::make_rng(ura::derive_seed(31, b));
+                std::uniform_real_distribution<double> u(-8.0, 0.0);
+                for (double& x : s8.v) x = double(float(u(er)));
+                auto a = ura::run_refinement(cden, s8, h, sched, 3, 16);
+                auto d = cref.run_refinement(s8, h, sched, 3);
+                same += a == d;
+            }
+            std::printf("config-mode context (2 layers, attention): reference loop vs device loop %d/4 identical grids\n", same);
+            fails += same != 4;
+        }
         // error contract: a different H must be rejected like a bad input
         auto rng2 = ura::make_rng(99);
         auto h2 = ura::build_random_ldpc(gf, 16, 8, 3, rng2);
