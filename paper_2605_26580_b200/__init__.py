@@ -26,7 +26,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcider.so")
+# CIDER_LIB_DIR: load an A/B build of the library (csrc/Makefile OUT=...) instead of _lib
+LIB_PATH = os.path.join(os.environ.get("CIDER_LIB_DIR") or os.path.join(_HERE, "_lib"), "libcider.so")
 
 FP32, BF16 = 0, 1
 REMASK_NONE, REMASK_THRESHOLD, REMASK_RANK = 0, 1, 2

@@ -1,9 +1,9 @@
-"""Debug: achieved TFLOP/s of each fused-MLP launch class in one c5-shaped forward (CUDA events)."""
+"""Debug: achieved TFLOP/s of each fused-MLP launch class in one forward of config CFG (default c5; CUDA events)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_2605_26580_b200 as P
-cfg = P.configs()["c5"]
+cfg = P.configs()[os.environ.get("CFG", "c5")]
 wl, m = cfg.workload, cfg.model
 e = wl.code()
 nb = int(os.environ.get("BINS", "512"))
