@@ -209,7 +209,7 @@ __device__ __forceinline__ void tmem_wait_ld32(uint32_t (&r)[32]) {
 }
 
 constexpr int MLP2_NS_CAP = 16; // weight-ring slots at most (else as many as the shared memory holds)
-template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1, int BIASB = 4 * D>
+template <int KIN, int D, int STGW = 4096, int EW = 8, int NXB = 1, int BIASB = 4 * D, int B1SB = 0>
 struct Mlp2Layout {
     static constexpr int STG_WARP = STGW;
     static constexpr int XBUF = NXB; // row-tile buffers (2: the next tile's rows load during this tile)
@@ -220,7 +220,9 @@ struct Mlp2Layout {
     static constexpr int SLOT = 16384;
     static constexpr int W1_PER_SLOT = SLOT / W1_HALF;       // 2
     static constexpr int X_BYTES = KB1 * 128 * 64 * 2;
-    static constexpr int FIXED = 1024 + 512 + BIASB;  // alignment slack, barriers, output bias
+    static constexpr int B1S_BYTES = B1SB;             // hidden bias [H] fp32 in shared memory (0: read by __ldg)
+    static constexpr int B1S_OFF_FROM_BAR = 512 + BIASB;
+    static constexpr int FIXED = 1024 + 512 + BIASB + B1SB;  // alignment slack, barriers, output bias, hidden bias
     static constexpr int BIAS_OFF_FROM_BAR = 512;      // output bias [D] fp32 right after the barriers
     // output staging for coalesced stores: one 32-row x 64-column bf16 block per epilogue warp (the
     // aggregator only; gate / fusion, KIN = 2D, need the SMEM for the weight ring and store directly)
@@ -230,7 +232,7 @@ struct Mlp2Layout {
     static constexpr int STG_OFF = NXB * X_BYTES;
     static constexpr int R_OFF = NXB * X_BYTES + STG_BYTES;
     static constexpr int BAR_OFF = R_OFF + NS * SLOT;
-    static constexpr int TOTAL = BAR_OFF + 512 + BIASB + 1024;
+    static constexpr int TOTAL = BAR_OFF + 512 + BIASB + B1SB + 1024;
     static_assert(NS >= 4, "fused MLP (2-SM) does not fit in shared memory");
     static_assert((2 * NXB * KB1 + 2 * NS + 2 + 2 * 8 + 2 + 2 + NXB * (D / 64) + 1) * 8 + 4 <= 512, "barrier block");
     static_assert(D % 32 == 0 && D <= 256 && W2_HALF <= SLOT, "output width must be <= 256");
@@ -250,12 +252,19 @@ constexpr int MLP2_HW = 8;                                 // hidden-chunk warps
 constexpr int mlp2_epi_warps(int epk) { return epk == EP_DEMIX ? 16 : MLP2_HW + 8; }
 constexpr int MLP2_FIN_WARP0 = 2 + MLP2_HW;
 constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
+// D = 128: a hidden chunk is 1024 tensor-pipe cycles and its GELU >= 1024 MUFU cycles (16 tanh per clock
+// per SM), so the hidden-chunk epilogue bounds the kernel (profiles/r2/experiments/d128_mlp_epilogue.md):
+// the hidden bias is read from shared memory where a weight-ring slot can be spared (the aggregator: 10 ->
+// 9 slots, -4% kernel time; gate / fusion keep their 6 slots and the __ldg reads). Sharing one TMEM-store
+// wait / fence / arrive between two 16-column groups was measured neutral and is not used.
+constexpr int MLP2_B1_SMEM_MAXH = 1024;
+constexpr int mlp2_b1_smem_bytes(int kin, int d, int epk) { return (d == 128 && kin == 128 && epk == EP_STORE) ? 4 * MLP2_B1_SMEM_MAXH : 0; }
 // The GELU variants stage their output in the tile's own X k-blocks (no staging region); the
 // aggregator (input = output width) double-buffers its row tile.
 template <int KIN, int D, int EPK>
 using Mlp2LayoutFor = Mlp2Layout<KIN, D, EPK == EP_DEMIX ? DEMIX_STG_WARP : 0, mlp2_epi_warps(EPK),
                                  ((KIN == D && (EPK == EP_STORE || EPK == EP_DEMIX)) || KIN <= 256) ? 2 : 1,
-                                 EPK == EP_DEMIX ? 0 : 4 * D>;
+                                 EPK == EP_DEMIX ? 0 : 4 * D, mlp2_b1_smem_bytes(KIN, D, EPK)>;
 // (KIN <= 256: the D = 128 gate / fusion row tile is 64 KB, so it double-buffers as well)
 
 constexpr int MLP2_GG = 4; // GELU release groups per 64-column warp half (16 hidden columns = one MMA2 k-step)
@@ -442,6 +451,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     float* bias_s = reinterpret_cast<float*>(smem + Lay::BAR_OFF + Lay::BIAS_OFF_FROM_BAR); // final-epilogue bias
     if constexpr (EPK != EP_DEMIX)
         for (int i = threadIdx.x; i < D; i += blockDim.x) bias_s[i] = args.ep.bias ? args.ep.bias[i] : 0.0f;
+    float* b1_s = reinterpret_cast<float*>(smem + Lay::BAR_OFF + Lay::B1S_OFF_FROM_BAR); // hidden bias (if B1S_BYTES)
+    if constexpr (Lay::B1S_BYTES > 0)
+        for (int i = threadIdx.x; i < args.H && i < Lay::B1S_BYTES / 4; i += blockDim.x) b1_s[i] = args.b1[i];
     cluster_sync_all(); // barriers of both CTAs initialised before any remote signal
     fence_after();
     const uint32_t tmem = *tmem_slot;
@@ -777,7 +789,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             if (!fin)
             for (int c = 0; c < NC; ++c, ++n) {
                 const int b = n & 1;
-                const float* b1 = args.b1 + c * MLP_HC + half * 64;
+                const float* b1 = (Lay::B1S_BYTES > 0 ? b1_s : args.b1) + c * MLP_HC + half * 64;
                 const bool tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
                 if (tr) args.trace[it * 64 + c * 8 + 2] = clock64();
                 mbar_wait(&a1_full[b], (e1ph >> b) & 1u);
@@ -792,7 +804,10 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     {
                         float4 bias4[4]; // this group's 16 hidden biases (L1-resident)
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
+                        for (int q = 0; q < 4; ++q) {
+                            if constexpr (Lay::B1S_BYTES > 0) bias4[q] = *(reinterpret_cast<const float4*>(b1) + g * 4 + q); // SMEM broadcast
+                            else bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
+                        }
                         float v[16];
                         tmem_ld16(base + g * 16, v);
                         uint32_t pk[8];
