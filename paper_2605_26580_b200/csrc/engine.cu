@@ -564,7 +564,8 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     // 2-SM kernel variants: aggregator (Kin = D, plain store), gate / fusion (Kin = 2D, z (e) epilogue)
     const bool pair = (D == 128 || D == 256) &&
                       ((Kin == D && ep.kind == EP_STORE) || (Kin == 2 * D && (ep.kind == EP_GATE || ep.kind == EP_RESID))) &&
-                      (tc::mlp2_b1_smem_bytes(Kin, D, ep.kind) == 0 || H <= tc::MLP2_B1_SMEM_MAXH); // (hidden bias in SMEM)
+                      // (D = 128 variants keep the hidden bias in shared memory: H must fit, else the 1-SM kernel)
+                      (tc::mlp2_b1_smem_bytes(Kin, D, ep.kind) == 0 || H * 4 <= tc::mlp2_b1_smem_bytes(Kin, D, ep.kind));
     Launch lg(c, tag, 2.0 * double(M) * H * (Kin + D), double(M) * (Kin + D) * c.act_size);
     const CUtensorMap& x0 = map_for(c, A0, M, A1 ? K0 : Kin, A1 ? K0 : Kin, 128);
     const CUtensorMap& x1 = A1 ? map_for(c, A1, M, K1, K1, 128) : x0;

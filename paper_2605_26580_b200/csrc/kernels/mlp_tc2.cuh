@@ -254,11 +254,14 @@ constexpr int MLP2_FIN_WARP0 = 2 + MLP2_HW;
 constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
 // D = 128: a hidden chunk is 1024 tensor-pipe cycles and its GELU >= 1024 MUFU cycles (16 tanh per clock
 // per SM), so the hidden-chunk epilogue bounds the kernel (profiles/r2/experiments/d128_mlp_epilogue.md):
-// the hidden bias is read from shared memory where a weight-ring slot can be spared (the aggregator: 10 ->
-// 9 slots, -4% kernel time; gate / fusion keep their 6 slots and the __ldg reads). Sharing one TMEM-store
-// wait / fence / arrive between two 16-column groups was measured neutral and is not used.
-constexpr int MLP2_B1_SMEM_MAXH = 1024;
-constexpr int mlp2_b1_smem_bytes(int kin, int d, int epk) { return (d == 128 && kin == 128 && epk == EP_STORE) ? 4 * MLP2_B1_SMEM_MAXH : 0; }
+// the hidden bias is read from shared memory at the price of one weight-ring slot (aggregator 10 -> 9
+// slots: -6% kernel time; gate / fusion 6 -> 5: -2.4% / -1.2%); a hidden width that does not fit runs
+// on the 1-SM kernel (engine.cu mlp()). A run-time choice between the two bias sources costs the gain
+// (generic loads), so it is a compile-time property of the variant. Sharing one TMEM-store wait / fence /
+// arrive between two 16-column groups was measured neutral and is not used.
+constexpr int mlp2_b1_smem_bytes(int kin, int d, int epk) {
+    return (d == 128 && epk != EP_DEMIX) ? (kin == 128 ? 4096 : 2048) : 0; // H <= 1024 (aggregator) / 512
+}
 // The GELU variants stage their output in the tile's own X k-blocks (no staging region); the
 // aggregator (input = output width) double-buffers its row tile.
 template <int KIN, int D, int EPK>
@@ -452,7 +455,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     if constexpr (EPK != EP_DEMIX)
         for (int i = threadIdx.x; i < D; i += blockDim.x) bias_s[i] = args.ep.bias ? args.ep.bias[i] : 0.0f;
     float* b1_s = reinterpret_cast<float*>(smem + Lay::BAR_OFF + Lay::B1S_OFF_FROM_BAR); // hidden bias (if B1S_BYTES)
-    if constexpr (Lay::B1S_BYTES > 0)
+    if constexpr (Lay::B1S_BYTES > 0) // (the host launches this variant only for H <= B1S_BYTES / 4)
         for (int i = threadIdx.x; i < args.H && i < Lay::B1S_BYTES / 4; i += blockDim.x) b1_s[i] = args.b1[i];
     cluster_sync_all(); // barriers of both CTAs initialised before any remote signal
     fence_after();
@@ -805,7 +808,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         float4 bias4[4]; // this group's 16 hidden biases (L1-resident)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            if constexpr (Lay::B1S_BYTES > 0) bias4[q] = *(reinterpret_cast<const float4*>(b1) + g * 4 + q); // SMEM broadcast
+                            if constexpr (Lay::B1S_BYTES > 0) bias4[q] = *(reinterpret_cast<const float4*>(b1) + g * 4 + q); // (SMEM broadcast)
                             else bias4[q] = __ldg(reinterpret_cast<const float4*>(b1) + g * 4 + q);
                         }
                         float v[16];
