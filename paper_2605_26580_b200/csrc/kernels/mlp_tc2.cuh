@@ -257,7 +257,8 @@ constexpr int mlp2_threads(int epk) { return (mlp2_epi_warps(epk) + 4) * 32; }
 // the hidden bias is read from shared memory at the price of one weight-ring slot (aggregator 10 -> 9
 // slots: -6% kernel time; gate / fusion 6 -> 5: -2.4% / -1.2%); a hidden width that does not fit runs
 // on the 1-SM kernel (engine.cu mlp()). A run-time choice between the two bias sources costs the gain
-// (generic loads), so it is a compile-time property of the variant. Sharing one TMEM-store wait / fence /
+// (generic loads), so it is a compile-time property of the variant. At D = 256 (the GELU has 2x slack there)
+// the same trade is neutral for all three variants and is not made. Sharing one TMEM-store wait / fence /
 // arrive between two 16-column groups was measured neutral and is not used.
 constexpr int mlp2_b1_smem_bytes(int kin, int d, int epk) {
     return (d == 128 && epk != EP_DEMIX) ? (kin == 128 ? 4096 : 2048) : 0; // H <= 1024 (aggregator) / 512
