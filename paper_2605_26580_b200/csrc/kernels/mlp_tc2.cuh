@@ -300,6 +300,24 @@ __device__ __forceinline__ void demix_load_sv(const MlpArgs& args, int m0, int c
         }
 }
 
+// Symbol columns past Q (Q < 128 padded to one 128-column chunk): S = 0 there, so r (x) S = 0 — the warp
+// packs zeros for the second MMA (whose V rows are zero as well; TMEM garbage must not reach it) and skips
+// the demix arithmetic: half of the chunk at Q = 64 (c2, c4), where the kernel is bound by this epilogue.
+__device__ __forceinline__ void demix_warp_pad(uint32_t base, uint64_t* a1_full_b, uint32_t ph, uint32_t l_h_full, int lane) {
+    mbar_wait(a1_full_b, ph);
+    fence_after();
+    const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int p = 0; p < 2; ++p) tmem_st8(base + p * 8, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        mbar_arrive_cl(l_h_full);
+        mbar_arrive_cl(l_h_full + 8);
+    }
+}
+
 template <int KK>
 __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, uint32_t base, uint64_t* a1_full_b, uint32_t ph,
                                            uint32_t l_h_full, const float* svin, int lane, long long* tr) {
@@ -745,7 +763,9 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                         if (ep.K == 8) demix_load_sv<8>(args, mn, cn * MLP_HC + half * 32, lane, svn);
                         else demix_load_sv<4>(args, mn, cn * MLP_HC + half * 32, lane, svn);
                     }
-                    if (ep.K == 8)
+                    if (c * MLP_HC + half * 32 >= ep.ldz) // (warp-uniform) padded symbol columns
+                        demix_warp_pad(base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, lane);
+                    else if (ep.K == 8)
                         demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
                     else
                         demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
