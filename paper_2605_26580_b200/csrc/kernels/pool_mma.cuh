@@ -68,8 +68,13 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     constexpr int R = PM_DEG * K * CPB; // rows per block (48)
     constexpr int KBS = R * 128;     // k-block stride inside a block buffer
     constexpr int NKB = D / 64;      // 64-column k-blocks per row (4 or 2)
-    constexpr int CPL = D / 32;      // pooled columns per lane (8 or 4)
+    // pooling: every lane takes 8 columns (one 16-byte chunk) of a row, so a row is D / 8 lanes and at
+    // D = 128 a warp pools two (check, k) rows at once (the softmax work per lane is the same whatever the
+    // width: with 4 columns per lane the D = 128 kernel spent twice the instructions per byte)
+    constexpr int CPL = 8;           // pooled columns per lane
     constexpr int V = CPL / 2;       // float2 per lane per row
+    constexpr int LPR = D / CPL;     // lanes per row (32 or 16)
+    constexpr int UPW = 32 / LPR;    // (check, k) rows pooled per warp pass (1 or 2)
     constexpr int RB = D * 2;        // bytes per row of the score matrix
     static_assert(D == 256 || D == 128, "pool_mma: D = 128 or 256");
     constexpr int GB = PM_NBUF / 2;  // buffers per group
@@ -109,7 +114,8 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
     // rows of this warp's m16 tile: block rows 12 wg + q for q < 12
     const int q = lane & 15;
     const int arow = 12 * wg + (q < 2 * PM_DEG ? q : q - 4); // pad lanes repeat rows 8-11 (same address: broadcast)
-    const int h = (lane * CPL) / (D / NH); // pooling: lane = CPL-column slice of head h
+    const int lr = lane % LPR, sub = lane / LPR; // pooling: lane = columns [8 lr, 8 lr + 8) of row `sub` of the pass
+    const int h = (lr * CPL) / (D / NH);         // ... a slice of head h
     int slot = 0;
     uint32_t ph = 0; // bit s: phase of this group's full[s]
     for (int blk = first; blk < nblk; blk += stride) {
@@ -152,26 +158,20 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         {
             // (2) pooling of rows k = wg kpw + kk (not unrolled: 128-register cap at 2 CTAs / SM)
 #pragma unroll 1
-            for (int kk = 0; kk < kpw; ++kk) {
-                const int task = wg * kpw + kk, cb = task / K, k = task % K; // check cb of the block, row k
-                bf16* orow = pooled + (size_t(b * E + e0 + cb * PM_DEG) * K + k) * D + lane * CPL; // edge i at + i K D
+            for (int kk = 0; kk < kpw / UPW; ++kk) {
+                const int task = wg * kpw + kk * UPW + sub, cb = task / K, k = task % K; // check cb of the block, row k
+                bf16* orow = pooled + (size_t(b * E + e0 + cb * PM_DEG) * K + k) * D + lr * CPL; // edge i at + i K D
                 float2 f[PM_DEG][V];
                 float sc[PM_DEG];
 #pragma unroll
                 for (int i = 0; i < PM_DEG; ++i) {
                     const int r = (cb * PM_DEG + i) * K + k;
                     sc[i] = ss[r * 8 + h];
-                    if constexpr (V == 4) { // 8 columns = one 16-byte chunk of k-block lane / 8
-                        const uint4 u = *reinterpret_cast<const uint4*>(nb + (lane >> 3) * KBS + r * 128 + (((lane & 7) ^ (r & 7)) * 16));
+                    { // 8 columns = one 16-byte chunk of k-block lr / 8
+                        const uint4 u = *reinterpret_cast<const uint4*>(nb + (lr >> 3) * KBS + r * 128 + (((lr & 7) ^ (r & 7)) * 16));
                         const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
                         for (int v = 0; v < 4; ++v) f[i][v] = __bfloat1622float2(p2[v]);
-                    } else { // 4 columns = half a chunk of k-block lane / 16
-                        const uint2 u = *reinterpret_cast<const uint2*>(nb + (lane >> 4) * KBS + r * 128 +
-                                                                        ((((lane >> 1) & 7) ^ (r & 7)) * 16) + (lane & 1) * 8);
-                        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                        for (int v = 0; v < 2; ++v) f[i][v] = __bfloat1622float2(p2[v]);
                     }
                 }
                 // leave-one-out softmax: max over the edges other than i is the overall max M1 for every
@@ -201,8 +201,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                     __nv_bfloat162 po[V];
 #pragma unroll
                     for (int v = 0; v < V; ++v) po[v] = __floats2bfloat162_rn(out[v].x * fct, out[v].y * fct);
-                    if constexpr (V == 4) *reinterpret_cast<uint4*>(orow + i * K * D) = *reinterpret_cast<const uint4*>(po);
-                    else *reinterpret_cast<uint2*>(orow + i * K * D) = *reinterpret_cast<const uint2*>(po);
+                    *reinterpret_cast<uint4*>(orow + i * K * D) = *reinterpret_cast<const uint4*>(po);
                 };
                 float2 pre[PM_DEG][V]; // pre[i] = P_i (i >= 1)
                 float pd[PM_DEG];
