@@ -200,7 +200,10 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                 auto store_row = [&](int i, const float2* out, float fct) {
                     __nv_bfloat162 po[V];
 #pragma unroll
-                    for (int v = 0; v < V; ++v) po[v] = __floats2bfloat162_rn(out[v].x * fct, out[v].y * fct);
+                    for (int v = 0; v < V; ++v) {
+                        const float2 sc2 = __fmul2_rn(out[v], make_float2(fct, fct)); // (packed: same products)
+                        po[v] = __floats2bfloat162_rn(sc2.x, sc2.y);
+                    }
                     *reinterpret_cast<uint4*>(orow + i * K * D) = *reinterpret_cast<const uint4*>(po);
                 };
                 float2 pre[PM_DEG][V]; // pre[i] = P_i (i >= 1)
