@@ -186,11 +186,14 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
 #pragma unroll
                 for (int i2 = 0; i2 < PM_DEG; ++i2)
                     if (i2 != i1) m2 = fmaxf(m2, sc[i2]);
+                // exp(s - m) = 2^(s log2e - m log2e): one FFMA + one MUFU.EX2 each (flush-to-zero: a weight below
+                // 2^-126 of the largest is dropped); __expf spends ~6 instructions on the denormal range
                 float e1[PM_DEG], e2[PM_DEG];
+                const float nm1 = -m1 * 1.4426950408889634f, nm2 = -m2 * 1.4426950408889634f;
 #pragma unroll
                 for (int i2 = 0; i2 < PM_DEG; ++i2) {
-                    e1[i2] = __expf(sc[i2] - m1);
-                    e2[i2] = __expf(sc[i2] - m2);
+                    e1[i2] = ex2_approx(fmaf(sc[i2], 1.4426950408889634f, nm1));
+                    e2[i2] = ex2_approx(fmaf(sc[i2], 1.4426950408889634f, nm2));
                 }
                 // Leave-one-out sums by prefix / suffix over the edges (no term of edge i enters output i,
                 // so extrinsicity stays bitwise): for i != i1, out_i = (d-1) (P_i + S_i) / (pd_i + sd_i)
