@@ -38,16 +38,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint (ns): a waiting warp sleeps in the barrier unit instead of re-issuing
+// the try_wait loop every few dozen cycles — in the fused MLPs ~28% of the executed instructions were such
+// retries of the producer / issuer / final-epilogue warps, competing with the GELU warps for issue slots
+// (c5 +0.35% in a same-box bench A/B, profiles/r2/experiments/README.md).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     uint32_t ok = 0;
     do {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(a), "r"(parity)
+            : "r"(a), "r"(parity), "r"(1000000u)
             : "memory");
     } while (!ok);
 }

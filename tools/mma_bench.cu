@@ -89,6 +89,45 @@ __global__ void __launch_bounds__(320, 1) bench_kernel(int iters, unsigned long 
         }
         for (int s2 = 0; s2 < 4; ++s2) mbar_wait(&tb[s2], ph[s2]);
         if (blockIdx.x == 0) out[1] = nbytes;
+    } else if (warp >= 2 && (NOISE == 5 || NOISE == 6)) {
+        // the fused MLP's hidden-chunk epilogue (TMEM ld x16 -> bias + GELU -> bf16 pack -> TMEM st x8 -> fence
+        // -> arrive per 16 columns) on TMEM columns [256, 512), free-running beside the MMA stream: how many
+        // elements per clock does it sustain while the tensor pipe is busy? (NOISE 6: bias in registers)
+        const int quarter = warp % 4, half = (warp - 2) / 4;
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        uint64_t* eb = bar + 8;
+        if (threadIdx.x == 64) { for (int i = 0; i < 4; ++i) mbar_init(&eb[i], 8); }
+        const float* b1 = reinterpret_cast<const float*>(scratch); // 0x3c003c00 pattern: small finite floats
+        float4 breg[4];
+        for (int q4 = 0; q4 < 4; ++q4) breg[q4] = reinterpret_cast<const float4*>(b1)[q4];
+        unsigned long long groups = 0;
+        int c = 0;
+        while (!*stop) {
+            const uint32_t base = tmem + lane_off + 256 + (c & 1) * 128 + half * 64;
+            ++c;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                float4 bias4[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) bias4[q4] = NOISE == 6 ? breg[q4] : *(reinterpret_cast<const float4*>(b1) + ((c & 3) * 32 + half * 16 + g * 4 + q4));
+                float v[16];
+                tmem_ld16(base + g * 16, v);
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 bb = bias4[i / 4];
+                    pk[i / 2] = gelu2_bias_bf16(v[i], v[i + 1], bb.x, bb.y);
+                    pk[i / 2 + 1] = gelu2_bias_bf16(v[i + 2], v[i + 3], bb.z, bb.w);
+                }
+                tmem_st8(base + g * 8, pk);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                fence_before();
+                __syncwarp();
+                if (threadIdx.x % 32 == 0) mbar_arrive(&eb[g]);
+            }
+            groups += 4;
+        }
+        if (threadIdx.x % 32 == 0) atomicAdd(out + 1, groups * 16ull * 32ull); // elements
     } else if (warp >= 2 && NOISE && NOISE != 4) {
         const int quarter = warp % 4;
         const uint32_t ta = tmem + (uint32_t(quarter * 32) << 16) + 384;
@@ -325,12 +364,14 @@ void run(int sms, const char* label) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k, iters, d, h_map);
+    cudaMemset(d, 0, 16);
     cudaLaunchKernelEx(&cfg, k, iters, d, h_map);
     cudaError_t err = cudaDeviceSynchronize();
     unsigned long long cyc = 0, tb = 0;
     cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
     cudaMemcpy(&tb, d + 1, 8, cudaMemcpyDeviceToHost);
     if (NOISE == 4) printf("   (TMA streamed %.1f B/clk/SM alongside)\n", double(tb) / double(cyc));
+    if (NOISE == 5 || NOISE == 6) printf("   (GELU epilogue on 8 warps alongside: %.2f elements/clk/SM)\n", double(tb) / double(cyc) / (sms));
     const double macs = double(iters) * 4 * (128.0 * CG) * N * 16;
     printf("%-34s N=%3d cg=%d %s: %6.1f cyc/MMA  %5.0f MAC/clk/SM  (%.0f%% of 4096)\n", label, N, CG, TS ? "TS" : "SS",
            double(cyc) / (iters * 4.0), macs / CG / double(cyc), 100.0 * macs / CG / double(cyc) / 4096.0);
@@ -354,6 +395,10 @@ int main() {
     reinterpret_cast<EncodeFn>(p)(&h_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, mat, dims, strides, box, es,
                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    run<128, 2, false, 5, 2>(sms, "SS N=128 2-SM + GELU epilogue");
+    run<128, 2, true, 5, 2>(sms, "TS N=128 2-SM + GELU epilogue");
+    run<128, 2, false, 6, 2>(sms, "SS N=128 2-SM + GELU epi (reg bias)");
+    run<256, 2, true, 5, 2>(sms, "TS N=256 2-SM + GELU epilogue");
     run<128, 2, false, 0, 2>(sms, "SS N=128 2-SM quiet");
     run<128, 2, false, 2, 2>(sms, "SS N=128 2-SM + SMEM ld/st noise");
     run<128, 2, false, 4, 2>(sms, "SS N=128 2-SM + TMA stream");
