@@ -515,6 +515,22 @@ void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, con
     launch_pdl(tc::mlp_tc2_kernel<KIN, D, EPK>, 2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream, x0, x1, w1, w2, out, a);
 }
 
+// Per-chunk timelines of the fused MLPs: a diagnostic build (make EXTRA=-DCIDER_MLP_TRACE OUT=../_lib_trace,
+// loaded with CIDER_LIB_DIR) run with CIDER_TRACE_MLP=1; the product build carries no stamp code.
+bool mlp_trace_enabled() {
+    static const bool want = std::getenv("CIDER_TRACE_MLP") != nullptr;
+#ifdef CIDER_MLP_TRACE
+    return want;
+#else
+    static bool told = false;
+    if (want && !told) {
+        std::fprintf(stderr, "cider: CIDER_TRACE_MLP needs the diagnostic build (make EXTRA=-DCIDER_MLP_TRACE)\n");
+        told = true;
+    }
+    return false;
+#endif
+}
+
 bool mlp_fusable(const cider_ctx& c, int Kin) {
     return c.bf16 && c.H % tc::MLP_HC == 0 && (c.D == 64 || c.D == 128 || c.D == 256) && (Kin == c.D || Kin == 2 * c.D);
 }
@@ -581,7 +597,7 @@ void mlp(cider_ctx& c, const char* tag, const void* A0, int K0, const void* A1, 
     a.b1 = b1;
     a.ep = ep;
     a.trace = nullptr;
-    static const bool trace_on = std::getenv("CIDER_TRACE_MLP") != nullptr;
+    static const bool trace_on = mlp_trace_enabled();
     long long* tbuf = nullptr;
     if (trace_on) {
         tbuf = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
@@ -919,7 +935,7 @@ void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K,
     a.b1 = nullptr;
     a.ep = ep;
     a.trace = nullptr;
-    static const bool trace_on = std::getenv("CIDER_TRACE_MLP") != nullptr;
+    static const bool trace_on = mlp_trace_enabled();
     if (trace_on) {
         a.trace = (long long*)wsbuf(c, "mlp_trace", 8 * 1024);
         cudaMemsetAsync(a.trace, 0, 8 * 1024, c.stream);

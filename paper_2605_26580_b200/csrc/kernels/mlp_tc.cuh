@@ -77,14 +77,20 @@ struct MlpLayout {
 struct MlpArgs {
     int M, K0, H, tiles;
     const float* b1;
-    long long* trace; // debug (CIDER_TRACE_MLP): per-chunk clock64 stamps of CTA 0, else null
+    long long* trace; // diagnostic build (-DCIDER_MLP_TRACE) with CIDER_TRACE_MLP=1: per-chunk clock64 stamps of CTA 0
     Epi ep; // final epilogue (bias = b2)
 };
 
 template <int KIN, int D>
 __global__ void __launch_bounds__(MLP_THREADS, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
-              const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2, const MlpArgs args) {
+              const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2, const MlpArgs args_in) {
+#ifdef CIDER_MLP_TRACE
+    const MlpArgs& args = args_in;
+#else
+    MlpArgs args = args_in; // (timeline stamps compiled out)
+    args.trace = nullptr;
+#endif
     using Lay = MlpLayout<KIN, D>;
     constexpr int KB1 = Lay::KB1, KB2 = Lay::KB2, NS = Lay::NS, NHB = Lay::NHB;
     extern __shared__ uint8_t smem_raw[];

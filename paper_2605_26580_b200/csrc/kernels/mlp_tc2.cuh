@@ -392,7 +392,13 @@ template <int KIN, int D, int EPK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mlp2_threads(EPK), 1)
 mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
-               const __grid_constant__ CUtensorMap tmO, const MlpArgs args) {
+               const __grid_constant__ CUtensorMap tmO, const MlpArgs args_in) {
+#ifdef CIDER_MLP_TRACE
+    const MlpArgs& args = args_in; // diagnostic build: per-chunk clock64 stamps (tests/trace_mlp.py)
+#else
+    MlpArgs args = args_in; // the stamps and their predicates are compiled out (they cost 1-3% of the MLPs)
+    args.trace = nullptr;
+#endif
     using Lay = Mlp2LayoutFor<KIN, D, EPK>;
     constexpr int KB1 = Lay::KB1, KB2 = Lay::KB2, NS = Lay::NS;
     constexpr int EW = mlp2_epi_warps(EPK);              // epilogue warps 2 .. EW + 1

@@ -1,4 +1,9 @@
-"""Debug: per-chunk timeline of the fused MLP kernel (CIDER_TRACE_MLP=1), one c3 forward."""
+"""Debug: per-chunk timeline of the fused MLP kernels, one forward of config CFG (default c3).
+
+Needs the diagnostic build of the library:
+  make -C paper_2605_26580_b200/csrc EXTRA=-DCIDER_MLP_TRACE OUT=../_lib_trace ../_lib_trace/libcider.so
+  CIDER_LIB_DIR=$PWD/paper_2605_26580_b200/_lib_trace python tests/trace_mlp.py
+"""
 import os, sys
 os.environ["CIDER_TRACE_MLP"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
