@@ -501,18 +501,18 @@ void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, cons
     tc::mlp_tc_kernel<KIN, D><<<grid, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
 }
 
-template <int KIN, int D, int EPK>
+template <int KIN, int D, int EPK, int KK = 0>
 void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
                  const CUtensorMap& w2, const CUtensorMap& out, const tc::MlpArgs& a) {
     using Lay = tc::Mlp2LayoutFor<KIN, D, EPK>;
     static bool attr_set = false;
     if (!attr_set) {
-        ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D, EPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
+        ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D, EPK, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
         attr_set = true;
     }
     const int pairs = std::min(a.tiles, c.sm_count / 2);
-    launch_pdl(tc::mlp_tc2_kernel<KIN, D, EPK>, 2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream, x0, x1, w1, w2, out, a);
+    launch_pdl(tc::mlp_tc2_kernel<KIN, D, EPK, KK>, 2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream, x0, x1, w1, w2, out, a);
 }
 
 // Per-chunk timelines of the fused MLPs: a diagnostic build (make EXTRA=-DCIDER_MLP_TRACE OUT=../_lib_trace,
@@ -941,8 +941,13 @@ void demix_evid(cider_ctx& c, const void* Zt, const float* S, int64_t Ms, int K,
         cudaMemsetAsync(a.trace, 0, 8 * 1024, c.stream);
     }
     const CUtensorMap om = make_map_box(e_out, Ms, D, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B); // e k-blocks staged in X
-    if (D == 256) launch_mlp2<256, 256, EP_DEMIX>(c, x0, x0, w1, w2, om, a);
-    else launch_mlp2<128, 128, EP_DEMIX>(c, x0, x0, w1, w2, om, a);
+    if (D == 256) {
+        if (a.ep.K == 8) launch_mlp2<256, 256, EP_DEMIX, 8>(c, x0, x0, w1, w2, om, a);
+        else launch_mlp2<256, 256, EP_DEMIX, 4>(c, x0, x0, w1, w2, om, a);
+    } else {
+        if (a.ep.K == 8) launch_mlp2<128, 128, EP_DEMIX, 8>(c, x0, x0, w1, w2, om, a);
+        else launch_mlp2<128, 128, EP_DEMIX, 4>(c, x0, x0, w1, w2, om, a);
+    }
     check_launch("demix_evid");
     if (a.trace) dump_mlp_trace(c, "demix_evid", Ms, Qp, true, a.trace);
 }

@@ -388,7 +388,9 @@ __device__ __forceinline__ void demix_warp(const MlpArgs& args, uint8_t* stg, ui
 
 // EPK: final-epilogue kind (EP_STORE, EP_GATE or EP_RESID), a template parameter so each variant
 // carries only the registers its epilogue needs.
-template <int KIN, int D, int EPK>
+// KK (EP_DEMIX only): rows per (bin, slot) group = users per bin (4 or 8), compile-time so that one demix
+// body is instantiated per kernel.
+template <int KIN, int D, int EPK, int KK = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(mlp2_threads(EPK), 1)
 mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ CUtensorMap tmX1,
                const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
@@ -753,8 +755,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                 const int m0 = tile * 256 + int(rank) * 128 + quarter * 32;
                 const int m0n = m0 + npairs * 256; // the next tile's rows
                 if (tile == pair) { // first tile: nothing was prefetched
-                    if (ep.K == 8) demix_load_sv<8>(args, m0, half * 32, lane, svn);
-                    else demix_load_sv<4>(args, m0, half * 32, lane, svn);
+                    demix_load_sv<KK == 0 ? 8 : KK>(args, m0, half * 32, lane, svn);
                 }
                 for (int c = 0; c < NC; ++c, ++n) {
                     long long* tr = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0 ? args.trace + it * 64 + c * 8 : nullptr;
@@ -766,15 +767,12 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                     // the next chunk's S (this tile's, or the next tile's first)
                     const int cn = c + 1 < NC ? c + 1 : 0, mn = c + 1 < NC ? m0 : m0n;
                     if (c + 1 < NC || tile + npairs < args.tiles) {
-                        if (ep.K == 8) demix_load_sv<8>(args, mn, cn * MLP_HC + half * 32, lane, svn);
-                        else demix_load_sv<4>(args, mn, cn * MLP_HC + half * 32, lane, svn);
+                        demix_load_sv<KK == 0 ? 8 : KK>(args, mn, cn * MLP_HC + half * 32, lane, svn);
                     }
                     if (c * MLP_HC + half * 32 >= ep.ldz) // (warp-uniform) padded symbol columns
                         demix_warp_pad(base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, lane);
-                    else if (ep.K == 8)
-                        demix_warp<8>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
                     else
-                        demix_warp<4>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
+                        demix_warp<KK == 0 ? 8 : KK>(args, stg, base, &a1_full[b], (e1ph >> b) & 1u, L_h_full0 + (HG * b + 2 * half) * 8, svc, lane, tr);
                     e1ph ^= 1u << b;
                 }
                 const bool trf = args.trace && blockIdx.x == 0 && it < 4 && warp == 2 && lane == 0;
