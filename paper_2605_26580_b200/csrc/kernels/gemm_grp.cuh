@@ -58,6 +58,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const bool elected = elect_one_sync(); // the lane of the single-thread TMA / MMA issue loops (uniform operands)
     const int tiles = args.groups * args.mtiles;
 
     if (threadIdx.x == 0) {
@@ -79,7 +80,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const int a_bytes = args.K * args.bb * 128; // the A box actually filled (<= 16 KB)
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elected) {
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -101,7 +102,7 @@ gemm_grp_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (elected) {
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
@@ -204,6 +205,7 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const bool elected = elect_one_sync(); // the lane of the single-thread TMA / MMA issue loops (uniform operands)
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = int(blockIdx.x) / 2, npairs = int(gridDim.x) / 2;
@@ -230,7 +232,7 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const uint32_t L_tempty0 = mapa_u32(smem_u32(&tempty[0]), 0);
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elected) {
             int stage = 0;
             uint32_t phase = 0;
             for (int st = pair; st < supers; st += npairs) {
@@ -256,7 +258,7 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
+        if (leader && elected) {
             constexpr uint32_t idesc = idesc_bf16(256, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
@@ -288,7 +290,7 @@ gemm_grp2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         const int quarter = warp % 4;
         const int half = (warp - 2) / 4; // 32-column half of every 64-column output k-block
         const int row = quarter * 32 + lane;
-        const bool issuer = warp == 2 && lane == 0;
+        const bool issuer = warp == 2 && elected;
         int acc = 0, step = 0;
         uint32_t acc_phase = 0;
         for (int st = pair; st < supers; st += npairs) {
@@ -393,6 +395,7 @@ gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     uint64_t* t_empty = t_full + 1; // every MMA on the old T retired
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 1);
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const bool elected = elect_one_sync(); // the lane of the single-thread TMA / MMA issue loops (uniform operands)
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = int(blockIdx.x) / 2, npairs = int(gridDim.x) / 2;
@@ -421,7 +424,7 @@ gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
     const uint32_t L_tempty0 = mapa_u32(smem_u32(&tempty[0]), 0);
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elected) {
             int stage = 0, cur = -1;
             uint32_t phase = 0, teph = 0;
             grp_lap_sweep(pair, npairs, args.groups, mpairs, [&](int g, int mtp) {
@@ -448,7 +451,7 @@ gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
             });
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
+        if (leader && elected) {
             constexpr uint32_t idesc = idesc_bf16(256, BN);
             int stage = 0, acc = 0, cur = -1;
             uint32_t phase = 0, acc_phase = 0, tfph = 0;
@@ -483,7 +486,7 @@ gemm_grp2_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_const
         const int quarter = warp % 4;
         const int half = (warp - 2) / 4;
         const int row = quarter * 32 + lane;
-        const bool issuer = warp == 2 && lane == 0;
+        const bool issuer = warp == 2 && elected;
         int acc = 0, step = 0;
         uint32_t acc_phase = 0;
         grp_lap_sweep(pair, npairs, args.groups, mpairs, [&](int g, int mtp) {

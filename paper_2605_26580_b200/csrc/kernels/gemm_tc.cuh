@@ -62,6 +62,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
 }
+// One lane of the (converged) warp, by elect.sync: ptxas then knows that the region it guards runs in a
+// single thread and keeps the TMA / MMA operands (descriptors, coordinates, barrier addresses) in uniform
+// registers. A `lane == 0` guard compiles every tcgen05.mma into an ELECT + R2UR.BROADCAST x5 + retry-branch
+// sequence (~14 instructions per MMA against ~3).
+__device__ __forceinline__ bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -271,6 +281,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const bool elected = elect_one_sync(); // the lane of the single-thread TMA / MMA issue loops (uniform operands)
     const int kblocks = args.K / BK;
 
     if (threadIdx.x == 0) {
@@ -295,7 +306,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
     griddep_launch_dependents();
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elected) {
             int stage = 0;
             uint32_t phase = 0;
             if (BRES) { // the whole B (one N tile) once
@@ -320,7 +331,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (elected) {
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;

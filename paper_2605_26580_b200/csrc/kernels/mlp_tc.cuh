@@ -112,6 +112,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2_empty + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const bool elected = elect_one_sync(); // the lane of the single-thread TMA / MMA issue loops (uniform operands)
     const int NC = args.H / MLP_HC;
 
     if (threadIdx.x == 0) {
@@ -136,7 +137,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elected) {
             int slot = 0;
             uint32_t rph = 0, xph = 0;
             auto load_w = [&](const CUtensorMap* map, int x, int y, int bytes) {
@@ -169,7 +170,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__ 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (elected) {
             constexpr uint32_t id1 = idesc_bf16(128, MLP_HC);
             constexpr uint32_t id2 = idesc_bf16(128, Lay::N2);
             int slot = 0;

@@ -426,6 +426,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + NXB * KBD);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const bool elected = elect_one_sync(); // (all warps converged here) the lane of the single-thread issue loops
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
@@ -449,7 +450,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     constexpr int ROT = reads_z ? KBD : 0;
     // Issue loops run by the whole warp (bit 0: MMA1 issuer, bit 1: MMA2 issuer; lane 0 issues) or by
     // lane 0 alone, per variant (whole-warp loops: aggregator +2%, gate / fusion -10%)
-    constexpr int WI = EPK == EP_DEMIX ? 3 : KIN == D ? 3 : 0;
+    constexpr int WI = EPK == EP_DEMIX ? 3 : KIN == D ? 3 : 0; // (with elect.sync issue lanes the two forms measure equal)
     // gate / fusion: the 8 final warps walk the output k-blocks together (each warp one 32-column half
     // of every k-block), so k-block 0 is staged, stored and refilled first and the next tile's first
     // MMA1 is fed k-block by k-block instead of in two rounds
@@ -502,7 +503,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
     auto pos_w2 = [&](int c) { return 2 * S1 + c * S2 + min(c, NC - 2) * S1; };
 
     if (warp == 0) {
-        if (lane == 0) { // weight ring producer
+        if (elected) { // weight ring producer
             int slot = 0;
             uint32_t rph = 0;
             auto next = [&] { if (++slot == NS) { slot = 0; rph ^= 1; } };
@@ -537,7 +538,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
             }
         }
     } else if (warp == XLOAD_WARP) {
-        if (lane == 0) { // row-tile producer, one k-block at a time
+        if (elected) { // row-tile producer, one k-block at a time
             uint32_t eph = 0;
             int itx = 0;
             for (int tile = pair; tile < args.tiles; tile += npairs, ++itx) {
@@ -611,7 +612,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
         // barrier wait of a single issuing thread is a pipe bubble (tools/mma_bench.cu issue2_kernel:
         // 200-cycle waits per slot cost 22% with one issuer, 11% with two). Warp 1 issues the first
         // layer (acc1 buffers), warp 10 the second (acc2); a1_free orders MMA2(n) before MMA1(n+2).
-        const bool el = lane == 0;
+        const bool el = elected;
         if (leader && (el || ((warp == 1 ? WI & 1 : WI & 2) != 0))) {
             auto ring_slot = [&](int gpos, uint32_t& ph) { ph = uint32_t(gpos / NS) & 1u; return gpos % NS; };
             const bool tr = args.trace && blockIdx.x == 0 && el;

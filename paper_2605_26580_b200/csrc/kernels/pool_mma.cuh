@@ -107,7 +107,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
         for (int kb = 0; kb < NKB; ++kb)
             tc::tma_load_2d(smem + (grp * GB + slot) * PM_BUF + kb * KBS, &tmN, bar, kb * 64, row0);
     };
-    const bool leader = wg == 0 && lane == 0;
+    const bool leader = wg == 0 && tc::elect_one_sync(); // (all warps converged here) single-thread TMA issue
     if (leader)
         for (int s = 0; s < GB - 1; ++s)
             if (first + s * stride < nblk) issue(first + s * stride, s);
