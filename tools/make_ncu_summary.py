@@ -20,9 +20,9 @@ cfg = P.configs()["c5"]
 wl, m = cfg.workload, cfg.model
 K, L, E, D, H = wl.k, wl.slots, wl.slots * wl.col_weight, m.dim, m.hidden
 Ms, Me = bins * L * K, bins * E * K
-flops = {"<512, 256, 2>": ("mlp_gate", 2.0 * Ms * H * (2 * D + D)),
-         "<256, 256, 0>": ("mlp_agg", 2.0 * Me * H * (D + D)),
-         "<512, 256, 3>": ("mlp_fuse", 2.0 * Ms * H * (2 * D + D))}
+flops = {"<512, 256, 2,": ("mlp_gate", 2.0 * Ms * H * (2 * D + D)),
+         "<256, 256, 0,": ("mlp_agg", 2.0 * Me * H * (D + D)),
+         "<512, 256, 3,": ("mlp_fuse", 2.0 * Ms * H * (2 * D + D))}
 out = {"source": f"{os.path.basename(path)}: ncu --set full, tests/mlp_rate.py c5 {bins} bins", "kernels": {}}
 for r in rep(path):
     for tag, (name, fl) in flops.items():
