@@ -910,11 +910,14 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmX0, const __grid_constant__
                                 const float2 z2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&zq[t]));
                                 if (reads_e) {
                                     const float2 e2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&eq[t]));
-                                    // g = 0.5 tanh(a / 2) + 0.5;  out = g (z - e) + e
+                                    // g = 0.5 tanh(a / 2) + 0.5;  out = g z + (1 - g) e in the reference's form
+                                    // (denoiser.cpp:156): a saturated gate passes z or e through exactly
+                                    // (test_denoiser.cpp:141-159), which g (z - e) + e does not
                                     const float2 h = __fmul2_rn(a, make_float2(0.5f, 0.5f));
                                     const float2 g = __ffma2_rn(make_float2(tanh_approx(h.x), tanh_approx(h.y)), make_float2(0.5f, 0.5f),
                                                                 make_float2(0.5f, 0.5f));
-                                    a = __ffma2_rn(g, __fadd2_rn(z2, make_float2(-e2.x, -e2.y)), e2);
+                                    const float2 ng = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-g.x, -g.y));
+                                    a = __ffma2_rn(g, z2, __fmul2_rn(ng, e2));
                                 } else {
                                     a = __fadd2_rn(a, z2);
                                 }

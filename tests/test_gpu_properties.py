@@ -1,0 +1,204 @@
+"""The reference's own hot-path property tests (SURVEY §4 ★: test_denoiser.cpp, test_refine.cpp) run on
+the device kernels, in FP32 parity mode and through the BF16 tcgen05 kernel set at the BASELINE c3 / c5
+shapes. They need no oracle: each is an exact (bitwise or closed-form) property of the math.
+
+* gates forced open / closed give exact pass-through (test_denoiser.cpp:141-159) and, with Module B's
+  fusion zeroed, the denoiser is site-local (test_denoiser.cpp:46-68);
+* the demix responsibilities sum to one over the rows: sum_k e[k, l] = S[l] V (test_denoiser.cpp:70-139);
+* first reveal = one site per slot, the reveal target is honoured, all sites are revealed by step T
+  (test_refine.cpp:110-146, 176-202);
+* T = 1 makes two denoiser calls, the last one the gamma = 0 pass (test_refine.cpp:164-174);
+* remasking clamps the rows it does not re-decode bit for bit (test_refine.cpp:262-298).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def layer_offsets(model):
+    """Offsets into the flat weight vector (cider.h: embed | out_proj | sym_embed | per layer gate_a,
+    check_agg, fuse_b as {w1, b1, w2, b2} | per-layer attention)."""
+    Q, D, H = model.q, model.dim, model.hidden
+    off = {"embed": 0, "out_proj": (Q + 1) * D, "sym_embed": (Q + 1) * D + Q * D}
+    o = (Q + 1) * D + 2 * Q * D
+    layers = []
+    for _ in range(model.layers):
+        lay = {}
+        for name, kin in (("gate_a", 2 * D), ("check_agg", D), ("fuse_b", 2 * D)):
+            lay[name] = {"w1": o, "b1": o + H * kin, "w2": o + H * kin + H, "b2": o + H * kin + H + D * H}
+            o += H * kin + H + D * H + D
+        layers.append(lay)
+    off["layers"] = layers
+    off["end_maps"] = o
+    return off
+
+
+def forced_gate_weights(P, model, gate_bias):
+    """Every layer: gate_a's output layer = (0, gate_bias) so that g = sigmoid(gate_bias) everywhere, and
+    fuse_b's output layer = 0 so that Module B adds nothing (Z-hat = z~)."""
+    w = P.weights_init(model, 1)
+    off = layer_offsets(model)
+    assert off["end_maps"] <= w.size
+    D, H = model.dim, model.hidden
+    for lay in off["layers"]:
+        g, f = lay["gate_a"], lay["fuse_b"]
+        w[g["w2"]: g["w2"] + D * H] = 0.0
+        w[g["b2"]: g["b2"] + D] = gate_bias
+        w[f["w2"]: f["w2"] + D * H] = 0.0
+        w[f["b2"]: f["b2"] + D] = 0.0
+    return w, off
+
+
+MODELS = {
+    "fp32": dict(m=4, dim=32, hidden=64, layers=2, heads=2, k=3, slots=16, checks=8, bins=3),
+    # the bench's kernel set: Q = D = 256, 8 heads, K = 8, degree-6 checks; 40 bins = 2 gate tiles per pair-round
+    "bf16_c3": dict(m=8, dim=256, hidden=1024, layers=2, heads=8, k=8, slots=64, checks=32, bins=40),
+    "bf16_c2": dict(m=6, dim=128, hidden=512, layers=2, heads=8, k=4, slots=32, checks=16, bins=24),
+}
+
+
+def setup(P, name, gate_bias):
+    s = MODELS[name]
+    prec = P.FP32 if name == "fp32" else P.BF16
+    model = P.Model(m=s["m"], dim=s["dim"], hidden=s["hidden"], layers=s["layers"], heads=s["heads"], precision=prec)
+    wl = P.Workload(m=s["m"], slots=s["slots"], checks=s["checks"], k=s["k"], snr_db=4.0, p_erase=0.1, p_false=0.1)
+    e = wl.code()
+    w, off = forced_gate_weights(P, model, gate_bias)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    _, S = wl.bins(e, 0, s["bins"])
+    rng = np.random.default_rng(11)
+    X = rng.integers(0, model.q, size=(s["bins"], s["k"], s["slots"]))
+    X = np.where(rng.random(X.shape) < 0.4, -1, X).astype(np.int32)
+    return model, wl, ctx, w, off, S, X
+
+
+@pytest.mark.parametrize("name", ["fp32", "bf16_c3", "bf16_c2"])
+def test_gate_forced_open_is_exact_pass_through_and_site_local(P, name):
+    """g = 1: z~ = Z whatever the evidence says (test_denoiser.cpp:141-159), so with the fusion zeroed the
+    logits are E[X] W^T: independent of S bit for bit, equal to the closed form, and site-local
+    (test_denoiser.cpp:46-68: a changed token changes its own site only)."""
+    model, wl, ctx, w, off, S, X = setup(P, name, +1000.0)
+    lg = ctx.denoise(X, S)
+    S2 = np.roll(S, 1, axis=0) * 0.5 + 0.25
+    assert np.array_equal(lg, ctx.denoise(X, S2))
+    wr = P.model_weights_as_run(model, w)
+    Q, D = model.q, model.dim
+    E = wr[: (Q + 1) * D].reshape(Q + 1, D)
+    W = wr[off["out_proj"]: off["out_proj"] + Q * D].reshape(Q, D)
+    want = E[np.where(X < 0, Q, X)] @ W.T
+    err = np.abs(lg - want).max() / np.abs(want).max()
+    assert err < 1e-5, err  # operands are exact in both modes; only the fp32 accumulation differs
+    Y = X.copy()
+    b, k, l = 1, 1, 5
+    Y[b, k, l] = (max(int(Y[b, k, l]), 0) + 3) % Q
+    lg2 = ctx.denoise(Y, S)
+    same = np.ones(X.shape, bool)
+    same[b, k, l] = False
+    assert np.array_equal(lg2[same], lg[same])
+    assert not np.array_equal(lg2[b, k, l], lg[b, k, l])
+
+
+@pytest.mark.parametrize("name", ["fp32", "bf16_c3", "bf16_c2"])
+def test_gate_forced_closed_passes_the_evidence_embedding(P, name):
+    """g = 0: z~ = e (test_denoiser.cpp:141-159). e = sum_a r_a S_la v_a vanishes where the slot's evidence
+    row is zero, so those sites' logits are exactly 0 for every row and every token; and a slot's e row
+    does not depend on the tokens of other slots."""
+    model, wl, ctx, w, off, S, X = setup(P, name, -1000.0)
+    S = S.copy()
+    dead = [2, 7]
+    S[:, dead, :] = 0.0
+    lg = ctx.denoise(X, S)
+    assert np.all(lg[:, :, dead, :] == 0.0)
+    live = [l for l in range(wl.slots) if l not in dead]
+    assert np.abs(lg[:, :, live, :]).max() > 0.0
+    Y = X.copy()
+    Y[:, :, 9] = (np.maximum(Y[:, :, 9], 0) + 1) % model.q
+    lg2 = ctx.denoise(Y, S)
+    keep = [l for l in range(wl.slots) if l != 9]
+    assert np.array_equal(lg2[:, :, keep, :], lg[:, :, keep, :])
+
+
+@pytest.mark.parametrize("name", ["fp32", "bf16_c3", "bf16_c2"])
+def test_responsibilities_sum_to_one_over_the_rows(P, name):
+    """test_denoiser.cpp:70-104 (normalisation) + 106-139 (evidence embedding) through the fused kernels: with
+    the gate closed the logits are e W^T, and since sum_k r[k, l, a] = 1 the row sum of e is S[l] V whatever
+    the tokens are: sum_k logits[k, l, :] = (S[l] V) W^T."""
+    model, wl, ctx, w, off, S, X = setup(P, name, -1000.0)
+    lg = ctx.denoise(X, S).astype(np.float64)
+    wr = P.model_weights_as_run(model, w)
+    Q, D = model.q, model.dim
+    W = wr[off["out_proj"]: off["out_proj"] + Q * D].reshape(Q, D)
+    V = wr[off["sym_embed"]: off["sym_embed"] + Q * D].reshape(Q, D)
+    want = (S.astype(np.float64) @ V) @ W.T  # B x L x Q
+    got = lg.sum(axis=1)
+    err = np.abs(got - want).max() / np.abs(want).max()
+    print(name, "row-sum rel err", err)
+    assert err < (1e-4 if name == "fp32" else 1e-2), err
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_reveal_schedule_properties_at_baseline_shapes(P, name):
+    """test_refine.cpp:110-146, 176-202 on the device loop at the BASELINE shapes (bf16, 96 bins): the first
+    step reveals exactly one site per slot, the per-step counts never exceed what is masked, and step T
+    reveals everything that is left (rho(T) = 1)."""
+    cfg = P.configs()[name]
+    wl, model = cfg.workload, cfg.model
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    nb = 96
+    _, S = wl.bins(e, 0, nb)
+    sched = P.RevealSchedule(steps=cfg.steps)
+    grid, tr = ctx.refine(S, wl.k, sched, want_trace=True)
+    n = wl.k * wl.slots
+    assert np.all(tr["n_passes"] == 1) and np.all(tr["n_reveal_counts"] == cfg.steps)
+    assert np.all(tr["first_reveals"] == wl.slots)
+    sites = tr["first_step_sites"].astype(np.int64)
+    assert np.all(sites.sum(axis=1) == 1)  # one row per slot (B x K x L summed over the rows)
+    counts = tr["reveal_counts"][:, : cfg.steps].astype(np.int64)
+    assert np.all(counts >= 0) and np.all(counts[:, 0] == wl.slots)
+    cum = counts.cumsum(axis=1)
+    assert np.all(cum[:, -1] == n)
+    # cumulative cosine target: after step t at least round-down of rho(t) n sites are revealed
+    rho = 0.5 * (1.0 - np.cos(np.pi * np.arange(1, cfg.steps + 1) / cfg.steps))
+    assert np.all(cum >= np.floor(rho * n - 1e-9)[None, :] - 1)
+    assert np.all(cum[:, 1:] <= np.maximum(np.ceil(rho * n)[None, 1:] + 1, wl.slots))
+    assert np.all((grid >= 0) & (grid < model.q))
+
+
+def test_single_step_schedule_makes_two_denoiser_calls(P):
+    """test_refine.cpp:164-174: T = 1 = one masked-loop forward + the gamma = 0 pass."""
+    wl = P.Workload(m=6, slots=32, checks=16, k=4, snr_db=6.0)
+    model = P.Model(m=6, dim=128, hidden=512, layers=2, heads=8, precision=P.BF16)
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    _, S = wl.bins(e, 0, 8)
+    ctx.set_profiling(True)
+    for steps, forwards in ((1, 2), (3, 4)):
+        ctx.reset_stats()
+        ctx.refine(S, wl.k, P.RevealSchedule(steps=steps))
+        st = ctx.kernel_stats()
+        assert st["gemm_logits"]["launches"] == forwards, st["gemm_logits"]
+        assert st["mlp_agg"]["launches"] == forwards * model.layers
+
+
+@pytest.mark.parametrize("name,nb", [("c3", 300), ("c2", 1000)])
+def test_remasking_clamps_the_kept_rows_bitwise(P, name, nb):
+    """test_refine.cpp:262-298 at the BASELINE shapes (bf16, multi-tile batches): rank-25% remasking re-decodes
+    exactly K/4 rows per bin and returns every other row of the first pass unchanged."""
+    cfg = P.configs()[name]
+    wl, model = cfg.workload, cfg.model
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    _, S = wl.bins(e, 0, nb)
+    sched = P.RevealSchedule(steps=cfg.steps)
+    rm = P.RemaskConfig(rank_fraction=0.25)
+    base = ctx.refine(S, wl.k, sched)
+    grid, tr = ctx.refine(S, wl.k, sched, rm, want_trace=True)
+    mask = tr["remask_mask"].astype(bool)
+    assert np.all(mask.sum(axis=1) == max(1, wl.k // 4))
+    assert np.array_equal(grid[~mask], base[~mask])
+    assert np.all(tr["n_passes"] == 2)
+    assert np.all(tr["remask_steps"][:, 0] == max(1, cfg.steps * max(1, wl.k // 4) // wl.k))
+    # and the graph-replayed product call (no trace) returns the same grids
+    assert np.array_equal(ctx.refine(S, wl.k, sched, rm), grid)
