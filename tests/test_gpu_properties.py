@@ -202,3 +202,43 @@ def test_remasking_clamps_the_kept_rows_bitwise(P, name, nb):
     assert np.all(tr["remask_steps"][:, 0] == max(1, cfg.steps * max(1, wl.k // 4) // wl.k))
     # and the graph-replayed product call (no trace) returns the same grids
     assert np.array_equal(ctx.refine(S, wl.k, sched, rm), grid)
+
+
+def irregular_code(rng, checks, slots, q, max_deg):
+    """Edges sorted by (check, slot) with check degrees 1 .. max_deg, some slots in no check at all."""
+    rows = []
+    free = rng.choice(slots, size=max(1, slots // 5), replace=False)  # slots without checks
+    usable = np.setdiff1d(np.arange(slots), free)
+    for c in range(checks):
+        deg = int(rng.integers(1, max_deg + 1))
+        for l in sorted(rng.choice(usable, size=min(deg, usable.size), replace=False)):
+            rows.append((c, int(l), int(rng.integers(1, q))))
+    return np.array(rows, np.int32), free
+
+
+@pytest.mark.parametrize("m,dim,hidden,heads,k", [(6, 128, 256, 4, 3), (8, 256, 512, 8, 8), (6, 128, 512, 0, 4), (6, 64, 128, 2, 5)])
+def test_bf16_irregular_codes_match_the_oracle(P, oracle, m, dim, hidden, heads, k):
+    """Codes that are not check-regular (degrees 1-7, slots in no check: test_denoiser.cpp:249-267's empty
+    neighbourhoods) leave the fixed-degree fast paths: BF16 forward against the oracle, and zero messages on
+    the unconnected slots."""
+    rng = np.random.default_rng(100 + m + k)
+    slots, checks, nb = 24, 9, 5
+    model = P.Model(m=m, dim=dim, hidden=hidden, layers=2, heads=heads, precision=P.BF16)
+    edges, free = irregular_code(rng, checks, slots, model.q, 7)
+    w = P.weights_init(model, 3)
+    ctx = P.Context(model, w, edges, checks, slots)
+    S = np.log(rng.dirichlet(np.ones(model.q), size=(nb, slots))).astype(np.float32)
+    X = rng.integers(0, model.q, size=(nb, k, slots))
+    X = np.where(rng.random(X.shape) < 0.5, -1, X).astype(np.int32)
+    lg, inc = ctx.denoise(X, S, want_incoming=True)
+    wr = P.model_weights_as_run(model, w)
+    for b in (0, nb - 1):
+        lo, io = oracle.denoise(model, wr, edges, checks, slots, X[b], S[b].astype(np.float64), True)
+        el = np.abs(lg[b] - lo).max() / np.abs(lo).max()
+        ei = np.abs(inc[b] - io).max() / max(1e-30, np.abs(io).max())
+        print(f"irregular m={m} D={dim} K={k} heads={heads}: logits {el:.2e} messages {ei:.2e}")
+        assert el < 1e-2 and ei < 1e-2, (el, ei)
+    assert np.all(inc[:, :, :, free, :] == 0.0)
+    # the refinement loop on the same code: valid symbols, deterministic
+    g = ctx.refine(S, k, P.RevealSchedule(steps=4), P.RemaskConfig(rank_fraction=0.25))
+    assert np.all((g >= 0) & (g < model.q)) and np.array_equal(g, ctx.refine(S, k, P.RevealSchedule(steps=4), P.RemaskConfig(rank_fraction=0.25)))
