@@ -242,3 +242,40 @@ def test_bf16_irregular_codes_match_the_oracle(P, oracle, m, dim, hidden, heads,
     # the refinement loop on the same code: valid symbols, deterministic
     g = ctx.refine(S, k, P.RevealSchedule(steps=4), P.RemaskConfig(rank_fraction=0.25))
     assert np.all((g >= 0) & (g < model.q)) and np.array_equal(g, ctx.refine(S, k, P.RevealSchedule(steps=4), P.RemaskConfig(rank_fraction=0.25)))
+
+
+def test_concurrent_calls_on_one_context_are_safe(P):
+    """The reference calls Denoiser::logits concurrently from its parallel_for workers on one shared instance
+    (uradec.cpp:184, 294-297): 8 host threads mixing cider_denoise and cider_refine on ONE context (ctypes
+    drops the GIL) must each get what the serial call returns."""
+    import threading
+    cfg = P.configs()["c2"]
+    wl, model = cfg.workload, cfg.model
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    sched, rm = P.RevealSchedule(steps=cfg.steps), P.RemaskConfig(rank_fraction=0.25)
+    jobs = []
+    for t in range(8):
+        nb = 3 + 5 * t
+        _, S = wl.bins(e, 100 * t, nb)
+        X = np.full((nb, wl.k, wl.slots), -1, np.int32)
+        X[:, t % wl.k, ::3] = t
+        jobs.append((S, X))
+    serial = [(ctx.denoise(X, S), ctx.refine(S, wl.k, sched, rm)) for S, X in jobs]
+    out = [None] * len(jobs)
+    errs = []
+
+    def work(i):
+        try:
+            S, X = jobs[i]
+            for _ in range(3):
+                out[i] = (ctx.denoise(X, S), ctx.refine(S, wl.k, sched, rm))
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not errs, errs
+    for (lg, g), (lg2, g2) in zip(serial, out):
+        assert np.array_equal(lg, lg2) and np.array_equal(g, g2)
