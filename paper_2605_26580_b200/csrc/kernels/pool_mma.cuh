@@ -198,8 +198,7 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                 // Leave-one-out sums by prefix / suffix over the edges (no term of edge i enters output i,
                 // so extrinsicity stays bitwise): for i != i1, out_i = (d-1) (P_i + S_i) / (pd_i + sd_i)
                 // with P_i = sum_{i2 < i} e1 n, S_i = sum_{i2 > i} e1 n (pd, sd the same sums of e1); row
-                // i1 uses e2 and is computed on its own (zero weight on itself: + 0 leaves sums unchanged)
-                // and stored over the e1 value.
+                // i1 uses e2 in the same association (below) and is stored over the e1 value.
                 auto store_row = [&](int i, const float2* out, float fct) {
                     __nv_bfloat162 po[V];
 #pragma unroll
@@ -252,19 +251,45 @@ pool_mma_kernel(const __grid_constant__ CUtensorMap tmN, const bf16* __restrict_
                         }
                     }
                 }
-                { // row i1 with the runner-up max (e2), ascending over the others
-                    float2 out[V];
-                    float den = 0.0f;
+                { // row i1 with the runner-up max (e2), in the SAME prefix / suffix association as the rows above:
+                    // the edges on the other side of a partial sum enter it with weight zero (+ 0 leaves a sum
+                    // unchanged), so an output row is one fixed function of the OTHER edges' rows and scores
+                    // whether or not its own score is the largest — extrinsicity holds bit for bit by construction
+                    // (an ascending sum over the others differs from prefix + suffix in the last bit, which a
+                    // change of the row's own tokens can expose by moving the argmax: rare after the bf16
+                    // rounding, but not excluded)
+                    float2 pp[V], sp[V];
+                    float pdn, sdn;
+                    {
+                        const float w = 0 < i1 ? e2[0] : 0.0f;
 #pragma unroll
-                    for (int v = 0; v < V; ++v) out[v] = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int i2 = 0; i2 < PM_DEG; ++i2) {
-                        const float w = i2 == i1 ? 0.0f : e2[i2];
-                        den += w;
-#pragma unroll
-                        for (int v = 0; v < V; ++v) out[v] = __ffma2_rn(make_float2(w, w), f[i2][v], out[v]);
+                        for (int v = 0; v < V; ++v) pp[v] = __fmul2_rn(make_float2(w, w), f[0][v]);
+                        pdn = w;
                     }
-                    store_row(i1, out, __fdividef(float(PM_DEG - 1), den));
+#pragma unroll
+                    for (int j = 1; j < PM_DEG - 1; ++j) {
+                        const float w = j < i1 ? e2[j] : 0.0f;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) pp[v] = __ffma2_rn(make_float2(w, w), f[j][v], pp[v]);
+                        pdn = pdn + w;
+                    }
+                    {
+                        const float w = PM_DEG - 1 > i1 ? e2[PM_DEG - 1] : 0.0f;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) sp[v] = __fmul2_rn(make_float2(w, w), f[PM_DEG - 1][v]);
+                        sdn = w;
+                    }
+#pragma unroll
+                    for (int j = PM_DEG - 2; j >= 1; --j) {
+                        const float w = j > i1 ? e2[j] : 0.0f;
+#pragma unroll
+                        for (int v = 0; v < V; ++v) sp[v] = __ffma2_rn(make_float2(w, w), f[j][v], sp[v]);
+                        sdn = sdn + w;
+                    }
+                    float2 out[V];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) out[v] = __fadd2_rn(pp[v], sp[v]);
+                    store_row(i1, out, __fdividef(float(PM_DEG - 1), pdn + sdn));
                 }
             }
         }

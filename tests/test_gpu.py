@@ -427,8 +427,11 @@ def test_fused_bf16_kernels_parity_and_invariants(P, oracle, k, dim):
     p = np.roll(np.arange(k), 1)
     lgp = ctx.denoise(X[:, p], S)
     assert np.array_equal(lgp, lg[:, p])
-    for l in (0, 9):
-        Y = X.copy()
-        Y[:, :, l] = (np.maximum(Y[:, :, l], 0) + 7) % model.q
-        _, inc2 = ctx.denoise(Y, S, want_incoming=True)
-        assert np.array_equal(inc2[:, 0][:, :, l], inc[:, 0][:, :, l])
+    # every slot in turn, and a second token change: the leave-one-out softmax must be the same function of the
+    # other edges whether or not the changed slot's own score is the check's largest (pool_mma.cuh, row i1)
+    for l in range(wl.slots):
+        for add in (7, 101):
+            Y = X.copy()
+            Y[:, :, l] = (np.maximum(Y[:, :, l], 0) + add) % model.q
+            _, inc2 = ctx.denoise(Y, S, want_incoming=True)
+            assert np.array_equal(inc2[:, 0][:, :, l], inc[:, 0][:, :, l]), (l, add)
