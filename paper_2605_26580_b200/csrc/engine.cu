@@ -738,9 +738,10 @@ void run_scatter(cider_ctx& c, const T* Mq, int K, int64_t Ms, T* accq) {
 }
 bool pool_fast(const cider_ctx& c) {
     const int V = c.D / 32;
+    if (c.D % 32 != 0 || !(V == 2 || V == 4 || V == 8)) return false; // (D < 32: V = 0 must not reach the % below)
     const bool heads_ok = c.heads == 0 || ((c.heads == 2 || c.heads == 4 || c.heads == 8 || c.heads == 16) &&
                                            (c.D / c.heads) % V == 0);
-    return c.D % 32 == 0 && (V == 2 || V == 4 || V == 8) && c.max_check_deg <= POOL_DMAX && heads_ok;
+    return c.max_check_deg <= POOL_DMAX && heads_ok;
 }
 template <typename T, int V, int DM>
 void run_pool_d(cider_ctx& c, const LayerW& lw, const T* Nn, int K, int64_t groups, T* pooled) {

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <set>
 #include <thread>
 
@@ -224,7 +225,10 @@ std::vector<int> random_ldpc(const Gf& gf, int slots, int checks, int w, std::mt
         for (int l = 0; l < slots; ++l) {
             std::vector<char> used(checks, 0);
             for (int k = 0; k < w; ++k) {
-                int lo = checks + 1;
+                // (the reference starts the scan at checks + 1, ldpc.cpp:103: once every free check has a
+                // larger degree — dense codes, 3 L / P > P + 1 — its candidate list is empty and the draw is
+                // undefined behaviour; an unbounded start gives the same codes wherever the reference is defined)
+                int lo = std::numeric_limits<int>::max();
                 for (int j = 0; j < checks; ++j)
                     if (!used[j] && deg[j] < lo) lo = deg[j];
                 cand.clear();

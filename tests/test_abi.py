@@ -61,3 +61,19 @@ def test_invalid_code_rejected_before_any_device_work(P):
     zero = np.array([[0, 1, 0]], np.int32)
     with pytest.raises(ValueError, match="nonzero"):
         P.Context(m, P.weights_init(m, 1), zero, 1, 4)
+
+
+def test_dense_code_construction_is_defined(P):
+    """3 L / P > P + 1: every free check's degree exceeds the reference's scan start (ldpc.cpp:103), where its
+    candidate list is empty and the draw undefined; the product builds a valid balanced code instead."""
+    for m, slots, checks in [(5, 9, 4), (3, 9, 3), (6, 20, 3), (4, 30, 5)]:
+        wl = P.Workload(m=m, slots=slots, checks=checks, k=2, snr_db=3.0)
+        e = wl.code()
+        assert e.shape == (slots * wl.col_weight, 3)
+        assert np.all((e[:, 2] >= 1) & (e[:, 2] < (1 << m)))
+        for l in range(slots):
+            assert len(set(e[e[:, 1] == l, 0])) == wl.col_weight  # distinct checks per slot
+        deg = np.bincount(e[:, 0], minlength=checks)
+        assert deg.max() - deg.min() <= 1
+        truth, S = wl.bins(e, 0, 2)  # systematic form exists (full rank), codewords satisfy H
+        assert truth.shape == (2, 2, slots) and np.isfinite(S).all()

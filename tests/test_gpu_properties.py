@@ -279,3 +279,50 @@ def test_concurrent_calls_on_one_context_are_safe(P):
     assert not errs, errs
     for (lg, g), (lg2, g2) in zip(serial, out):
         assert np.array_equal(lg, lg2) and np.array_equal(g, g2)
+
+
+def _sweep_cases():
+    """Seeded random small configurations of the whole loop (FP32 parity mode): field size, users, slots,
+    checks, layers, heads (0 = the reference's plain extrinsic mean), schedule shape, remask mode."""
+    rng = np.random.default_rng(2605)
+    cases = []
+    for i in range(14):
+        m = int(rng.choice([2, 3, 4, 5, 6]))
+        dim = int(rng.choice([16, 32, 48]))
+        heads = int(rng.choice([0, 1, 2, 4]))
+        hidden = int(rng.choice([dim, 2 * dim, 24]))
+        layers = int(rng.integers(1, 4))
+        k = int(rng.integers(1, 7))
+        slots = int(rng.choice([6, 9, 12, 20]))
+        checks = int(rng.integers(3, max(4, slots // 2 + 1)))
+        steps = int(rng.integers(1, 9))
+        tau = [(1.0, 1.0), (2.0, 0.5), (1.5, 0.2)][int(rng.integers(0, 3))]
+        first = bool(rng.integers(0, 2))
+        rmode = int(rng.integers(0, 3))
+        cases.append((i, m, dim, hidden, layers, heads, k, slots, checks, steps, tau, first, rmode))
+    return cases
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"s{c[0]}-m{c[1]}-K{c[6]}-L{c[7]}-T{c[9]}-r{c[12]}")
+def test_fp32_random_configurations_decode_like_the_oracle(P, oracle, case):
+    """Identical grids, first-reveal counts and remask rows / steps / masks against the oracle for seeded random
+    shapes and schedules — the loop logic (reveal targets, ties, residual forcing, threshold buckets, rank
+    selection) is shared by both precision modes."""
+    i, m, dim, hidden, layers, heads, k, slots, checks, steps, tau, first, rmode = case
+    wl = P.Workload(m=m, slots=slots, checks=checks, k=k, snr_db=3.0, p_erase=0.15, p_false=0.15)
+    model = P.Model(m=m, dim=dim, hidden=hidden, layers=layers, heads=heads, precision=P.FP32)
+    e = wl.code()
+    w = P.weights_init(model, 10 + i)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    nb = 5
+    _, S = wl.bins(e, 7 * i, nb)
+    sched = P.RevealSchedule(steps=steps, tau_max=tau[0], tau_min=tau[1], first_reveal=first)
+    rm = [None, P.RemaskConfig(rank_fraction=0.34), P.RemaskConfig(thresholds=(0.9, 0.5))][rmode]
+    grid, tr = ctx.refine(S, k, sched, rm, want_trace=True)
+    ro = oracle.refine(model, P.model_weights_as_run(model, w), e, wl.checks, wl.slots, S.astype(np.float64), k, sched, rm)
+    assert np.array_equal(grid, ro["grid"])
+    assert np.array_equal(tr["first_reveals"], ro["first_reveals"])
+    assert np.array_equal(tr["remask_rows"], ro["remask_rows"])
+    assert np.array_equal(tr["remask_steps"], ro["remask_steps"])
+    assert np.array_equal(tr["remask_mask"], ro["remask_mask"])
+    assert np.array_equal(ctx.refine(S, k, sched, rm), grid)  # the graph-replayed call
