@@ -326,3 +326,52 @@ def test_fp32_random_configurations_decode_like_the_oracle(P, oracle, case):
     assert np.array_equal(tr["remask_steps"], ro["remask_steps"])
     assert np.array_equal(tr["remask_mask"], ro["remask_mask"])
     assert np.array_equal(ctx.refine(S, k, sched, rm), grid)  # the graph-replayed call
+
+
+def _bf16_sweep_cases():
+    rng = np.random.default_rng(26580)
+    cases = []
+    for i in range(12):
+        m = int(rng.choice([6, 7, 8]))
+        dim = int(rng.choice([64, 128, 256]))
+        hidden = int(rng.choice([64, 128, 256, 512]))
+        heads = int(rng.choice([0, 1, 2, 4, 8]))
+        layers = int(rng.integers(1, 4))
+        k = int(rng.integers(1, 9))
+        slots = int(rng.choice([8, 12, 16, 24, 40]))
+        checks = int(rng.integers(3, slots // 2 + 1))
+        nb = int(rng.choice([1, 3, 17, 33]))
+        cases.append((i, m, dim, hidden, layers, heads, k, slots, checks, nb))
+    return cases
+
+
+@pytest.mark.parametrize("case", _bf16_sweep_cases(), ids=lambda c: f"b{c[0]}-m{c[1]}-D{c[2]}-H{c[3]}-h{c[5]}-K{c[6]}-L{c[7]}-P{c[8]}-B{c[9]}")
+def test_bf16_random_configurations_match_the_oracle(P, oracle, case):
+    """Seeded random BF16 shapes (the dispatcher mixes the 2-SM fused kernels, the 1-SM ones and the generic
+    kernels depending on Q, D, H, K, the check degrees and the batch): forward logits and per-layer messages
+    within 1e-2 of the oracle on the first and last bin; the refinement returns valid symbols, deterministically,
+    independent of the internal chunking."""
+    i, m, dim, hidden, layers, heads, k, slots, checks, nb = case
+    wl = P.Workload(m=m, slots=slots, checks=checks, k=k, snr_db=4.0, p_erase=0.1, p_false=0.1)
+    model = P.Model(m=m, dim=dim, hidden=hidden, layers=layers, heads=heads, precision=P.BF16)
+    e = wl.code()
+    w = P.weights_init(model, 20 + i)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    _, S = wl.bins(e, 3 * i, nb)
+    rng = np.random.default_rng(i)
+    X = rng.integers(0, model.q, size=(nb, k, slots))
+    X = np.where(rng.random(X.shape) < 0.5, -1, X).astype(np.int32)
+    lg, inc = ctx.denoise(X, S, want_incoming=True)
+    wr = P.model_weights_as_run(model, w)
+    for b in sorted({0, nb - 1}):
+        lo, io = oracle.denoise(model, wr, e, wl.checks, wl.slots, X[b], S[b].astype(np.float64), True)
+        el = np.abs(lg[b] - lo).max() / np.abs(lo).max()
+        ei = np.abs(inc[b] - io).max() / max(1e-30, np.abs(io).max())
+        print(f"bf16 sweep {case}: logits {el:.2e} messages {ei:.2e}")
+        assert el < 1e-2 and ei < 1e-2, (case, el, ei)
+    sched = P.RevealSchedule(steps=3)
+    rm = P.RemaskConfig(rank_fraction=0.25)
+    g = ctx.refine(S, k, sched, rm)
+    assert np.all((g >= 0) & (g < model.q))
+    ctx.set_chunk(max(1, nb // 2))
+    assert np.array_equal(ctx.refine(S, k, sched, rm), g)
