@@ -375,3 +375,43 @@ def test_bf16_random_configurations_match_the_oracle(P, oracle, case):
     assert np.all((g >= 0) & (g < model.q))
     ctx.set_chunk(max(1, nb // 2))
     assert np.array_equal(ctx.refine(S, k, sched, rm), g)
+
+
+def _bp_sweep_cases():
+    rng = np.random.default_rng(7)
+    cases = []
+    for i in range(10):
+        m = int(rng.choice([2, 3, 4, 5, 6, 8]))
+        slots = int(rng.choice([6, 9, 12, 20, 33]))
+        checks = int(rng.integers(3, slots // 2 + 1))
+        k = int(rng.integers(1, 5))
+        nb = int(rng.choice([1, 5, 19]))
+        iters = int(rng.choice([1, 7, 25]))
+        cases.append((i, m, slots, checks, k, nb, iters))
+    return cases
+
+
+@pytest.mark.parametrize("case", _bp_sweep_cases(), ids=lambda c: f"bp{c[0]}-m{c[1]}-L{c[2]}-P{c[3]}-K{c[4]}-B{c[5]}-it{c[6]}")
+def test_bp_random_configurations_match_the_reference(P, reference, case):
+    """SURVEY §8(f) F1 on seeded random shapes (dense and sparse checks, Q = 4 .. 256): bp_decode and sic_decode
+    against the compiled reference — identical hard decisions, flags, iteration counts and SIC grids."""
+    i, m, slots, checks, k, nb, iters = case
+    wl = P.Workload(m=m, slots=slots, checks=checks, k=k, snr_db=6.0, p_erase=0.05, p_false=0.05)
+    e = wl.code()
+    _, S = wl.bins(e, 11 * i, nb)
+    S = S.astype(np.float64)
+    lam = np.exp(S - S.max(axis=-1, keepdims=True))
+    lam /= lam.sum(axis=-1, keepdims=True)
+    dec = P.BpDecoder(wl.m, e, wl.checks, wl.slots)
+    cfg = P.BpConfig(max_iters=iters)
+    hard, marg, conv, its = dec.bp_decode(lam, cfg)
+    rh, rm, rc, ri = reference.bp_decode(wl.m, e, wl.checks, wl.slots, lam, max_iters=iters)
+    assert np.array_equal(hard, rh)
+    assert np.array_equal(conv, rc.astype(bool))
+    assert np.array_equal(its, ri)
+    assert np.abs(marg - rm).max() / np.abs(rm).max() < 1e-9
+    grid, sc, si = dec.sic_decode(S, wl.k, cfg)
+    rg, rsc, rsi = reference.sic_decode(wl.m, e, wl.checks, wl.slots, S, wl.k, max_iters=iters)
+    assert np.array_equal(grid, rg)
+    assert np.array_equal(sc, rsc.astype(bool))
+    assert np.array_equal(si, rsi)
