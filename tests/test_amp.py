@@ -66,3 +66,34 @@ def test_amp_errors_like_the_reference(P):
     with pytest.raises(ValueError, match="n_s must not exceed Q"):
         P.AmpDetector(np.ones((1, 4, 8), np.complex128))
     assert det.detect(y[:0]).shape == (0, 2, 8)
+
+
+def _amp_sweep():
+    rng = np.random.default_rng(11)
+    cases = []
+    for i in range(8):
+        q = int(rng.choice([4, 16, 32, 64, 128, 256]))
+        n_s = int(rng.integers(2, q + 1))
+        slots = int(rng.choice([1, 3, 8, 20]))
+        k = int(rng.integers(1, min(q, 6) + 1))
+        B = int(rng.choice([1, 4, 9]))
+        iters = int(rng.choice([1, 5, 20]))
+        cases.append((i, q, n_s, slots, k, B, iters))
+    return cases
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", _amp_sweep(), ids=lambda c: f"amp{c[0]}-q{c[1]}-ns{c[2]}-L{c[3]}-K{c[4]}-B{c[5]}-it{c[6]}")
+def test_amp_random_configurations_match_reference(P, case):
+    """Seeded random detector shapes (Q = 4..256, n_s from 2 to Q, one slot to twenty, one to twenty iterations)."""
+    if not have_reference():
+        pytest.skip("needs oracle/_ref")
+    from oracle.binding import Reference
+    ref = Reference()
+    i, q, n_s, slots, k, B, iters = case
+    dicts, y, p_sym, _ = frames(ref, q, n_s, slots, k, B, seed=20 + i)
+    cfg = P.AmpConfig(iters=iters, rho_bg=min(0.9, k / q), sigma_u2=p_sym, evidence_floor=-40.0)
+    S = P.AmpDetector(dicts).detect(y, cfg)
+    for b in range(B):
+        R = ref.amp_detect_frame(dicts, y[b], cfg.iters, cfg.rho_bg, cfg.sigma_u2, cfg.evidence_floor)
+        assert np.abs(S[b] - R).max() < 1e-8, np.abs(S[b] - R).max()
