@@ -415,3 +415,23 @@ def test_bp_random_configurations_match_the_reference(P, reference, case):
     assert np.array_equal(grid, rg)
     assert np.array_equal(sc, rsc.astype(bool))
     assert np.array_equal(si, rsi)
+
+
+@pytest.mark.parametrize("m,d", [(1, 2), (2, 3), (3, 7), (5, 2), (5, 9), (7, 4), (8, 12), (8, 2), (4, 16)])
+def test_wht_check_update_sweep(P, oracle, m, d):
+    """SURVEY §8(a) A14 over field sizes 2..256 and check degrees 2..16 (test_bp.cpp:145-168 runs degree 3
+    only): the device's shuffle-butterfly WHT update against the oracle's restatement of check_update_wht,
+    peaked and flat messages alike."""
+    q = 1 << m
+    rng = np.random.default_rng(1000 + 17 * m + d)
+    n = 37
+    v2c = rng.random((n, d, q)) ** rng.choice([1, 3, 8], size=(n, d, 1))
+    v2c /= v2c.sum(-1, keepdims=True)
+    cf = rng.integers(1, q, size=(n, d)).astype(np.int32)
+    out = P.check_update_wht(m, v2c, cf)
+    assert out.shape == (n, d, q) and np.allclose(out.sum(-1), 1.0)
+    for c in (0, 11, n - 1):
+        for i in range(d):
+            others = [j for j in range(d) if j != i]
+            ref = oracle.check_update_wht(m, v2c[c, others], cf[c, others], int(cf[c, i]))
+            assert np.abs(out[c, i] - ref).max() < 1e-8
