@@ -1013,6 +1013,12 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
         e.out_f = w.Ztf; e.out_t = c.bf16 ? w.Ztt : nullptr; e.ldo = D;
         mlp(c, "mlp_gate", w.Zt, D, w.et, D, lw.g1, lw.gb1, lw.g2, Ms, e, w.hid);
         // Module B (denoiser.cpp:181-228)
+        if (Me == 0) {
+            // a code without edges (test_denoiser.cpp:249-267): no check sends anything, the fusion sees zero
+            // messages — none of the edge-row kernels has a grid to launch
+            ck(cudaMemsetAsync(w.acct, 0, size_t(Ms) * D * c.act_size, c.stream), "acc = 0");
+            if (w.accf && w.accf != w.acct) ck(cudaMemsetAsync(w.accf, 0, size_t(Ms) * D * 4, c.stream), "acc = 0");
+        } else {
         if (c.tpath) {
             // N[(b,e,k)] = z~[(b,slot_e,k)] . T_{alpha_e}
             grp_gemm(c, "grp_normalise", w.Ztt, L, nb, K, E, c.gn_count, c.gn_arow, c.gn_alpha, 1, c.gn_out, E, w.Nn,
@@ -1091,6 +1097,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
             e.out_f = (c.bf16 && !o.incoming) ? nullptr : w.accf; e.out_t = c.bf16 ? w.acct : nullptr; e.ldo = D;
             gemm(c, "gemm_msgback", w.accq, Q, nullptr, 0, c.Wt, Ms, D, e);
         }
+        } // Me > 0
         if (o.incoming)
             ck(cudaMemcpyAsync(o.incoming + size_t(li) * Ms * D, w.accf, size_t(Ms) * D * 4, cudaMemcpyDeviceToDevice, c.stream), "incoming");
         e = epi(EP_RESID);

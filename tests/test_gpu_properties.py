@@ -435,3 +435,53 @@ def test_wht_check_update_sweep(P, oracle, m, d):
             others = [j for j in range(d) if j != i]
             ref = oracle.check_update_wht(m, v2c[c, others], cf[c, others], int(cf[c, i]))
             assert np.abs(out[c, i] - ref).max() < 1e-8
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_degenerate_inputs_return_errors_or_empty_results(P, oracle, prec):
+    """Boundary inputs through the C ABI: no bins, no rows, too many rows, bad tokens, an edgeless code
+    (test_denoiser.cpp:249-267: Module B reduces to nothing), a single slot per check — errors come back as the
+    reference's exception types (status 3 -> ValueError), never as a crash, and the context stays usable."""
+    bf = prec == "bf16"
+    m, dim, hid = (6, 64, 128) if bf else (3, 16, 16)
+    model = P.Model(m=m, dim=dim, hidden=hid, layers=2, heads=2, precision=P.BF16 if bf else P.FP32)
+    wl = P.Workload(m=m, slots=10, checks=4, k=3, snr_db=5.0)
+    e = wl.code()
+    w = P.weights_init(model, 4)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    _, S = wl.bins(e, 0, 2)
+    q = model.q
+    sched = P.RevealSchedule(steps=3)
+    assert ctx.denoise(np.zeros((0, 3, 10), np.int32), S[:0]).shape == (0, 3, 10, q)
+    assert ctx.refine(S[:0], 3, sched).shape == (0, 3, 10)
+    for bad in (q, q + 100, -2, -(1 << 30)):
+        X = np.zeros((2, 3, 10), np.int32)
+        X[1, 2, 9] = bad
+        with pytest.raises(ValueError, match="token out of range"):
+            ctx.denoise(X, S)
+    with pytest.raises(ValueError):
+        ctx.refine(S, 0, sched)
+    with pytest.raises(ValueError):
+        ctx.refine(S, 33, sched)
+    with pytest.raises(ValueError):
+        ctx.refine(S, 3, sched, P.RemaskConfig(rank_fraction=1.5))
+    good = ctx.refine(S, 3, sched)  # still usable after the failures
+    assert np.all((good >= 0) & (good < q))
+    # an edgeless code: no messages, the forward equals the oracle's
+    none = np.zeros((0, 3), np.int32)
+    ctx0 = P.Context(model, w, none, 2, 10)
+    X = np.full((2, 3, 10), -1, np.int32)
+    X[0, 1, 4] = 1
+    lg, inc = ctx0.denoise(X, S, want_incoming=True)
+    assert np.all(inc == 0.0)
+    lo = oracle.denoise(model, P.model_weights_as_run(model, w), none, 2, 10, X[0], S[0].astype(np.float64))
+    assert np.abs(lg[0] - lo).max() / np.abs(lo).max() < (1e-2 if bf else 1e-4)
+    g0 = ctx0.refine(S, 3, sched, P.RemaskConfig(rank_fraction=0.34))
+    assert np.all((g0 >= 0) & (g0 < q))
+    # degree-1 checks only (every edge alone in its check: the extrinsic set of each edge is empty)
+    lone = np.array([[0, 2, 1], [1, 5, q - 1], [2, 7, 3]], np.int32)
+    ctx1 = P.Context(model, w, lone, 3, 10)
+    lg1, inc1 = ctx1.denoise(X, S, want_incoming=True)
+    lo1, io1 = oracle.denoise(model, P.model_weights_as_run(model, w), lone, 3, 10, X[0], S[0].astype(np.float64), True)
+    assert np.abs(lg1[0] - lo1).max() / np.abs(lo1).max() < (1e-2 if bf else 1e-4)
+    assert np.abs(inc1[0] - io1).max() <= (1e-2 if bf else 1e-4) * max(1e-30, np.abs(io1).max()) + 1e-12
