@@ -342,6 +342,9 @@ def _bf16_sweep_cases():
         checks = int(rng.integers(3, slots // 2 + 1))
         nb = int(rng.choice([1, 3, 17, 33]))
         cases.append((i, m, dim, hidden, layers, heads, k, slots, checks, nb))
+    # many users per bin (K up to the ABI's 32), a long code, a wide hidden layer, a batch of several row tiles
+    cases += [(12, 8, 256, 1024, 1, 8, 16, 12, 6, 9), (13, 8, 256, 256, 2, 8, 32, 8, 4, 5), (14, 6, 128, 512, 1, 8, 4, 200, 100, 40),
+              (15, 8, 256, 1024, 2, 8, 8, 64, 32, 70), (16, 7, 128, 256, 1, 4, 32, 16, 8, 3)]
     return cases
 
 
