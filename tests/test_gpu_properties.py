@@ -488,3 +488,59 @@ def test_degenerate_inputs_return_errors_or_empty_results(P, oracle, prec):
     lo1, io1 = oracle.denoise(model, P.model_weights_as_run(model, w), lone, 3, 10, X[0], S[0].astype(np.float64), True)
     assert np.abs(lg1[0] - lo1).max() / np.abs(lo1).max() < (1e-2 if bf else 1e-4)
     assert np.abs(inc1[0] - io1).max() <= (1e-2 if bf else 1e-4) * max(1e-30, np.abs(io1).max()) + 1e-12
+
+
+def test_graph_cache_never_replays_a_stale_capture(P):
+    """Refinement chunks are captured into CUDA graphs keyed by (bins, K, schedule, remask, buffers): a shuffled
+    sequence of calls with different batch sizes, row counts, schedules, remask modes and final-logits requests,
+    each repeated (so later calls replay), must return what a fresh context computes for that call."""
+    cfg = P.configs()["c2"]
+    wl, model = cfg.workload, cfg.model
+    e = wl.code()
+    w = P.weights_init(model, 1)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    _, S = wl.bins(e, 0, 96)
+    calls = []
+    for nb in (96, 17, 64):
+        for k in (4, 2):
+            for steps, tau in ((8, (1.0, 1.0)), (3, (2.0, 0.5))):
+                for rm in (None, P.RemaskConfig(rank_fraction=0.25), P.RemaskConfig(rank_fraction=0.5)):
+                    calls.append((nb, k, steps, tau, rm))
+    rng = np.random.default_rng(3)
+    order = list(rng.permutation(len(calls))[:14])
+    order = order + order[::-1] + order
+    want = {}
+    for n, ci in enumerate(order):
+        nb, k, steps, tau, rm = calls[ci]
+        sched = P.RevealSchedule(steps=steps, tau_max=tau[0], tau_min=tau[1])
+        fl_req = (n % 3 == 1)
+        out = ctx.refine(S[:nb], k, sched, rm, want_final_logits=fl_req)
+        grid, fl = out if fl_req else (out, None)
+        if ci not in want:
+            fresh = P.Context(model, w, e, wl.checks, wl.slots)
+            want[ci] = fresh.refine(S[:nb], k, sched, rm, want_final_logits=True)
+            fresh.close()
+        assert np.array_equal(grid, want[ci][0]), (n, calls[ci])
+        if fl_req:
+            assert np.array_equal(fl, want[ci][1]), (n, calls[ci])
+
+
+def test_bf16_ragged_loads_equal_per_load_calls(P):
+    """cider_refine_ragged at the c3 model shapes in BF16: bins of 1..8 users bucketed by load, each bucket with
+    its own schedule / remask — every bin's grid equals the uniform-K call on that bin alone."""
+    cfg = P.configs()["c3"]
+    wl, model = cfg.workload, cfg.model
+    e = wl.code()
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    rng = np.random.default_rng(8)
+    nb = 40
+    loads = rng.integers(1, 9, size=nb).astype(np.int32)
+    _, S = wl.bins(e, 0, nb)
+    scheds = [P.RevealSchedule(steps=2 + (k % 3)) for k in range(8)]
+    rms = [None, P.RemaskConfig(rank_fraction=0.5), None, P.RemaskConfig(rank_fraction=0.25), None,
+           P.RemaskConfig(thresholds=[0.02]), None, P.RemaskConfig(rank_fraction=0.25)]
+    grids = ctx.refine_ragged(S, loads, scheds, rms)
+    for b in range(nb):
+        k = int(loads[b])
+        ref = ctx.refine(S[b:b + 1], k, scheds[k - 1], rms[k - 1])
+        assert grids[b].shape == (k, wl.slots) and np.array_equal(grids[b], ref[0]), (b, k)
