@@ -300,6 +300,9 @@ def _sweep_cases():
         first = bool(rng.integers(0, 2))
         rmode = int(rng.integers(0, 3))
         cases.append((i, m, dim, hidden, layers, heads, k, slots, checks, steps, tau, first, rmode))
+    # widths that are no multiple of anything (the reference takes any dim: denoiser.cpp:41-44)
+    cases += [(14, 3, 10, 7, 1, 5, 2, 6, 3, 3, (1.0, 1.0), True, 0), (15, 2, 1, 1, 1, 0, 2, 6, 3, 2, (1.0, 1.0), True, 1),
+              (16, 4, 33, 33, 2, 3, 3, 9, 4, 4, (1.5, 0.2), False, 2), (17, 1, 3, 5, 2, 1, 2, 8, 4, 3, (1.0, 1.0), True, 1)]
     return cases
 
 
