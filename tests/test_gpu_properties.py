@@ -317,6 +317,7 @@ def test_fp32_random_configurations_decode_like_the_oracle(P, oracle, case):
     e = wl.code()
     w = P.weights_init(model, 10 + i)
     ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    ctx.set_debug_guard(65536)
     nb = 5
     _, S = wl.bins(e, 7 * i, nb)
     sched = P.RevealSchedule(steps=steps, tau_max=tau[0], tau_min=tau[1], first_reveal=first)
@@ -329,6 +330,8 @@ def test_fp32_random_configurations_decode_like_the_oracle(P, oracle, case):
     assert np.array_equal(tr["remask_steps"], ro["remask_steps"])
     assert np.array_equal(tr["remask_mask"], ro["remask_mask"])
     assert np.array_equal(ctx.refine(S, k, sched, rm), grid)  # the graph-replayed call
+    bad, msg = ctx.debug_check()
+    assert bad == 0, msg
 
 
 def _bf16_sweep_cases():
@@ -363,6 +366,7 @@ def test_bf16_random_configurations_match_the_oracle(P, oracle, case):
     e = wl.code()
     w = P.weights_init(model, 20 + i)
     ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    ctx.set_debug_guard(65536)  # 0xA5 bands around every workspace buffer: no kernel may write past its rows
     _, S = wl.bins(e, 3 * i, nb)
     rng = np.random.default_rng(i)
     X = rng.integers(0, model.q, size=(nb, k, slots))
@@ -381,6 +385,9 @@ def test_bf16_random_configurations_match_the_oracle(P, oracle, case):
     assert np.all((g >= 0) & (g < model.q))
     ctx.set_chunk(max(1, nb // 2))
     assert np.array_equal(ctx.refine(S, k, sched, rm), g)
+    ctx.refine(S, k, sched, P.RemaskConfig(thresholds=(0.9, 0.3)), want_trace=True)
+    bad, msg = ctx.debug_check()
+    assert bad == 0, msg
 
 
 def _bp_sweep_cases():
