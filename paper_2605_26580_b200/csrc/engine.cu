@@ -19,6 +19,7 @@
 #include <cstdlib>
 #include <map>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -85,6 +86,27 @@ EncodeTiledFn encode_fn() {
     });
     if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
     return fn;
+}
+
+// cudaFuncSetAttribute acts on the current device's instance of a kernel: one flag per device, so that a
+// process driving several GPUs (one cider_ctx per device) sets the attribute on each of them
+struct PerDeviceOnce {
+    std::atomic<uint64_t> done{0};
+    std::mutex mu;
+    template <class F>
+    void run(int device, F&& f) {
+        const uint64_t bit = 1ull << (unsigned(device) & 63u);
+        if (done.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> g(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return;
+        f();
+        done.fetch_or(bit, std::memory_order_release);
+    }
+};
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
 }
 
 // bf16 row-major [rows x cols] with row stride ld (elements), box = box_rows x 64, SWIZZLE_128B
@@ -422,12 +444,11 @@ const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, 
 template <int BN, int EPW = 4, bool BRES = false>
 void launch_tc(cider_ctx& c, const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b, const tc::Args& args) {
     using Lay = tc::SmemLayout<BN, EPW, BRES>;
-    static bool attr_set = false; // per process; same attribute for every device
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;
+    attr_set.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(tc::gemm_tc_kernel<BN, EPW, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
-        attr_set = true;
-    }
+    });
     int grid = std::min(args.tiles, c.sm_count);
     launch_pdl(tc::gemm_tc_kernel<BN, EPW, BRES>, grid, 64 + 32 * EPW, Lay::TOTAL, c.stream, a0, a1, b, args);
 }
@@ -491,12 +512,11 @@ template <int KIN, int D>
 void launch_mlp(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
                 const CUtensorMap& w2, const tc::MlpArgs& a) {
     using Lay = tc::MlpLayout<KIN, D>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;
+    attr_set.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(tc::mlp_tc_kernel<KIN, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
-        attr_set = true;
-    }
+    });
     const int grid = std::min(a.tiles, c.sm_count);
     tc::mlp_tc_kernel<KIN, D><<<grid, tc::MLP_THREADS, Lay::TOTAL, c.stream>>>(x0, x1, w1, w2, a);
 }
@@ -505,12 +525,11 @@ template <int KIN, int D, int EPK, int KK = 0>
 void launch_mlp2(cider_ctx& c, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& w1,
                  const CUtensorMap& w2, const CUtensorMap& out, const tc::MlpArgs& a) {
     using Lay = tc::Mlp2LayoutFor<KIN, D, EPK>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;
+    attr_set.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(tc::mlp_tc2_kernel<KIN, D, EPK, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL),
            "smem attr");
-        attr_set = true;
-    }
+    });
     const int pairs = std::min(a.tiles, c.sm_count / 2);
     launch_pdl(tc::mlp_tc2_kernel<KIN, D, EPK, KK>, 2 * pairs, tc::mlp2_threads(EPK), Lay::TOTAL, c.stream, x0, x1, w1, w2, out, a);
 }
@@ -791,11 +810,10 @@ bool pool_mma_ok(const cider_ctx& c, const LayerW& lw, int K) {
 const CUtensorMap& map_for(cider_ctx& c, const void* p, int64_t rows, int cols, int ld, int box_rows);
 template <int K, int D>
 void launch_pool_mma(cider_ctx& c, const LayerW& lw, const CUtensorMap& tm, int64_t blocks, void* pooled) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    attr.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(pool_mma_kernel<K, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, PoolMmaLayout::TOTAL), "smem attr");
-        attr = true;
-    }
+    });
     const unsigned grid = unsigned(std::min<int64_t>(blocks, int64_t(c.sm_count) * 2));
     launch_pdl(pool_mma_kernel<K, D>, grid, PM_THREADS, PoolMmaLayout::TOTAL, c.stream, tm, (const bf16*)lw.aus16, c.check_ptr, c.P, c.E,
                                                                              c.heads, blocks, (bf16*)pooled);
@@ -861,14 +879,13 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     if (max_seg == 1 && c.sm_count >= 2 && D == 256) {
         // single-segment groups (normalise): CTA pairs with their T halves resident, laps over the pairs
         // (c5 58.6 -> 55.7 ms, c4 45 -> 41 ms per step; at D = 128 the streamed kernel is as fast)
-        static bool attr_r2 = false;
-        if (!attr_r2) {
+        static PerDeviceOnce attr_r2;
+        attr_r2.run(current_device(), [&] {
             ck(cudaFuncSetAttribute(tc::gemm_grp2_res_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     tc::grp2_res_smem<256>()), "smem attr");
             ck(cudaFuncSetAttribute(tc::gemm_grp2_res_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     tc::grp2_res_smem<128>()), "smem attr");
-            attr_r2 = true;
-        }
+        });
         const int mpairs = (a.mtiles + 1) / 2;
         const int grid = 2 * std::min(groups * mpairs, c.sm_count / 2);
         const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
@@ -882,12 +899,11 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
     if ((a.mtiles >= 2 && c.sm_count >= 2 && D == 256) || D == 128) {
         // CTA pairs, one cta_group::2 MMA over two m-tiles: each SM pulls half of every T k-block
         // (D = 128 always: the other grouped kernels are D = 256 only)
-        static bool attr2 = false;
-        if (!attr2) {
+        static PerDeviceOnce attr2;
+        attr2.run(current_device(), [&] {
             ck(cudaFuncSetAttribute(tc::gemm_grp2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::GRP2_SMEM), "smem attr");
             ck(cudaFuncSetAttribute(tc::gemm_grp2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::GRP2_SMEM), "smem attr");
-            attr2 = true;
-        }
+        });
         const int supers = a.groups * ((a.mtiles + 1) / 2);
         const int grid = 2 * std::min(supers, c.sm_count / 2);
         const CUtensorMap tt2 = make_map_ttab(c.Ttab, D, c.Q, D / 2); // N-half boxes
@@ -899,11 +915,10 @@ void grp_gemm(cider_ctx& c, const char* tag, const void* A, int a_rows_per_bin, 
         return;
     }
     // a single m-tile (small batches): one CTA per (group, m-tile), T streamed
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDeviceOnce attr_set;
+    attr_set.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(tc::gemm_grp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::TOTAL), "smem attr");
-        attr_set = true;
-    }
+    });
     launch_pdl(tc::gemm_grp_kernel, std::min(tiles, c.sm_count), tc::GRP_THREADS, Lay::TOTAL, c.stream, ta, tt, a);
     check_launch(tag);
 }
@@ -1173,11 +1188,10 @@ void masked_pass(cider_ctx& c, WS& w, int nb, int K, const float* S, int* X, int
     const int cap = reveal_key_cap(n);
     const size_t smem = cap <= REVEAL_SMEM_SITES ? size_t(cap) * 8 : 0;
     unsigned long long* gkeys = cap > REVEAL_SMEM_SITES ? (unsigned long long*)wsbuf(c, "reveal_keys", size_t(nb) * cap * 8) : nullptr;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    attr.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(reveal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, REVEAL_SMEM_SITES * 8), "reveal attr");
-        attr = true;
-    }
+    });
     for (int t = 1; t <= steps; ++t) {
         FwdOpts o;
         o.tau = float(infer_temperature(t, steps, sc.tau_max, sc.tau_min));
@@ -1710,11 +1724,10 @@ void bp_run(cider_bp_ctx& c, int64_t B, const cider_bp_config& cfg) {
     int max_deg = 0;
     for (int j = 0; j < P; ++j) max_deg = std::max(max_deg, c.tg->check_ptr[j + 1] - c.tg->check_ptr[j]);
     const size_t smem = size_t(2) * max_deg * Q * sizeof(bp::dd);
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    attr.run(current_device(), [&] {
         ck(cudaFuncSetAttribute(bp::bp_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "attr");
-        attr = true;
-    }
+    });
     if (smem > 200 * 1024 || max_deg > 32) throw InvalidInput("bp_decode: check degree x Q too large for one CTA");
     const int rpw = 32 / bp::wht_lanes(Q);                           // edge rows per warp
     const int cthreads = 32 * std::max(1, (max_deg + rpw - 1) / rpw);
