@@ -302,7 +302,10 @@ def _sweep_cases():
         cases.append((i, m, dim, hidden, layers, heads, k, slots, checks, steps, tau, first, rmode))
     # widths that are no multiple of anything (the reference takes any dim: denoiser.cpp:41-44)
     cases += [(14, 3, 10, 7, 1, 5, 2, 6, 3, 3, (1.0, 1.0), True, 0), (15, 2, 1, 1, 1, 0, 2, 6, 3, 2, (1.0, 1.0), True, 1),
-              (16, 4, 33, 33, 2, 3, 3, 9, 4, 4, (1.5, 0.2), False, 2), (17, 1, 3, 5, 2, 1, 2, 8, 4, 3, (1.0, 1.0), True, 1)]
+              (16, 4, 33, 33, 2, 3, 3, 9, 4, 4, (1.5, 0.2), False, 2), (17, 1, 3, 5, 2, 1, 2, 8, 4, 3, (1.0, 1.0), True, 1),
+              # more steps than sites (most steps reveal nothing; with K = 1 the first reveal takes every site)
+              (18, 3, 16, 16, 1, 0, 1, 6, 3, 40, (1.0, 1.0), True, 1), (19, 3, 16, 16, 1, 2, 2, 6, 3, 40, (2.0, 0.5), False, 2),
+              (20, 4, 16, 16, 1, 0, 6, 6, 3, 64, (1.0, 1.0), True, 2)]
     return cases
 
 
