@@ -23,3 +23,8 @@ python tools/bench_bp.py --config c3; python tools/bench_workload.py; python too
 mkdir -p tools/_bin
 nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/_bin/mufu_bench tools/mufu_bench.cu && tools/_bin/mufu_bench
 nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/_bin/epi_bench tools/epi_bench.cu && tools/_bin/epi_bench
+# session-5 helpers: the ncu evidence of a build in one go, same-box A/B of two library builds, batch-size A/B
+bash tools/profile_round.sh                      # launch list + ncu --set full of the c5 / c2 kernel sets -> gpurun_out/
+# make -C paper_2605_26580_b200/csrc OUT=../_lib_base   (at the base commit) ; then:
+# bash tools/ab_lib.sh $PWD/paper_2605_26580_b200/_lib_base c5 c2
+bash tools/ab_bins.sh
