@@ -557,3 +557,43 @@ def test_bf16_ragged_loads_equal_per_load_calls(P):
         k = int(loads[b])
         ref = ctx.refine(S[b:b + 1], k, scheds[k - 1], rms[k - 1])
         assert grids[b].shape == (k, wl.slots) and np.array_equal(grids[b], ref[0]), (b, k)
+
+
+def _workload_sweep():
+    rng = np.random.default_rng(99)
+    cases = []
+    for i in range(10):
+        m = int(rng.choice([1, 2, 3, 5, 6, 7, 8]))
+        slots = int(rng.choice([6, 10, 17, 40]))
+        checks = int(rng.integers(3 if m > 1 else 4, slots // 2 + 1))
+        k = int(rng.integers(1, 9))
+        pe = float(rng.choice([0.0, 0.05, 0.5, 1.0]))
+        pf = float(rng.choice([0.0, 0.1, 1.0]))
+        snr = float(rng.choice([-3.0, 4.0, 20.0]))
+        first = int(rng.choice([0, 5, 100000, 262143]))
+        n = int(rng.choice([1, 7, 40]))
+        seed = int(rng.choice([0, 1, 12345678901]))
+        cases.append((i, m, slots, checks, k, pe, pf, snr, first, n, seed))
+    return cases
+
+
+@pytest.mark.parametrize("case", _workload_sweep(), ids=lambda c: f"w{c[0]}-m{c[1]}-L{c[2]}-P{c[3]}-K{c[4]}-pe{c[5]}-pf{c[6]}")
+def test_device_workload_sweep(P, case):
+    """the device evidence generator (mt19937_64 and the libstdc++ uniform / normal / integer
+    distributions restated per bin) against the host generator over field sizes 2..256, erasure and
+    false-candidate probabilities 0..1, high bin indices and master seeds: identical codewords, S equal up to the
+    last ulp of exp / log."""
+    i, m, slots, checks, k, pe, pf, snr, first, n, seed = case
+    q = 1 << m
+    if k > q ** (slots - checks):  # K distinct codewords must exist
+        k = 1
+    wl = P.Workload(m=m, slots=slots, checks=checks, k=k, snr_db=snr, p_erase=pe, p_false=pf, master_seed=seed)
+    e = wl.code()
+    model = P.Model(m=m, dim=16, hidden=16, precision=P.FP32)
+    ctx = P.Context(model, P.weights_init(model, 1), e, wl.checks, wl.slots)
+    th, Sh = wl.bins(e, first, n)
+    td, Sd = wl.bins_device(ctx, e, first, n)
+    assert np.array_equal(th, td)
+    assert np.isfinite(Sd).all()
+    assert (Sd != Sh).mean() < 1e-3
+    assert np.all(np.abs(Sd - Sh) <= np.spacing(np.abs(Sh)) * 1.0001)
