@@ -597,3 +597,33 @@ def test_device_workload_sweep(P, case):
     assert np.isfinite(Sd).all()
     assert (Sd != Sh).mean() < 1e-3
     assert np.all(np.abs(Sd - Sh) <= np.spacing(np.abs(Sh)) * 1.0001)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_remask_pass_sweep(P, oracle, seed):
+    """ura::remask_pass with caller confidences (refine.hpp:97-100) over random shapes, confidences and thresholds,
+    including thresholds no row / every row falls under and arbitrary (not decoder-produced) input grids: identical
+    grids to the oracle, untouched bins bit for bit."""
+    rng = np.random.default_rng(500 + seed)
+    m = int(rng.choice([3, 4, 6]))
+    k = int(rng.integers(1, 7))
+    slots = int(rng.choice([6, 12, 16]))
+    checks = int(rng.integers(3, slots // 2 + 1))
+    model = P.Model(m=m, dim=int(rng.choice([16, 32, 64])), hidden=32, layers=int(rng.integers(1, 3)),
+                    heads=int(rng.choice([0, 2])), precision=P.FP32)
+    wl = P.Workload(m=m, slots=slots, checks=checks, k=k, snr_db=4.0, p_erase=0.1, p_false=0.1)
+    e = wl.code()
+    w = P.weights_init(model, 30 + seed)
+    ctx = P.Context(model, w, e, wl.checks, wl.slots)
+    nb = 7
+    _, S = wl.bins(e, seed, nb)
+    sched = P.RevealSchedule(steps=int(rng.integers(1, 9)), tau_max=1.5, tau_min=0.5, first_reveal=bool(rng.integers(0, 2)))
+    g0 = rng.integers(0, model.q, size=(nb, k, slots)).astype(np.int32)
+    conf = rng.random((nb, k))
+    wr = P.model_weights_as_run(model, w)
+    for thr in (0.0, 0.35, 0.7, 1.01):
+        g = ctx.remask_pass(S, g0, conf, thr, sched)
+        go, _ = oracle.remask_pass(model, wr, e, wl.checks, wl.slots, S.astype(np.float64), g0, conf, thr, sched)
+        assert np.array_equal(g, go), (seed, thr)
+        keep = ~(conf < thr)
+        assert np.array_equal(g[keep], g0[keep])
