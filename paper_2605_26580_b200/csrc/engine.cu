@@ -250,6 +250,7 @@ struct cider_ctx {
     // weights
     std::vector<DevBuf> wbufs;
     float* Etab = nullptr;                 // (Q+1) x D fp32
+    void* Etab16 = nullptr;                // BF16 mode: the same table in bf16 (embed = one 16-byte load per store)
     void *W = nullptr, *Wt = nullptr, *Vt = nullptr;
     void *Wpad = nullptr, *Vtpad = nullptr; // BF16, Q < 128: W / V^T padded with zero symbols to 128 (demix_evid)
     std::vector<LayerW> lw;
@@ -987,7 +988,7 @@ void forward(cider_ctx& c, WS& w, int nb, int K, const int* X, const float* S, c
     {
         Launch lg(c, "embed", 0, double(Ms) * D * (4 + c.act_size));
         if (c.bf16 && D % 8 == 0)
-            launch_pdl(embed_bf16x8_kernel, blocks_for(Ms * (D / 8)), 256, 0, c.stream, X, (const float*)c.Etab, Q, D, Ms, (bf16*)w.Zt);
+            launch_pdl(embed_bf16x8_kernel, blocks_for(Ms * (D / 8)), 256, 0, c.stream, X, (const bf16*)c.Etab16, Q, D, Ms, (bf16*)w.Zt);
         else if (c.bf16)
             embed_kernel<bf16><<<blocks_for(Ms * D), 256, 0, c.stream>>>(X, c.Etab, Q, D, Ms, nullptr, (bf16*)w.Zt);
         else
@@ -1455,6 +1456,7 @@ void upload_model(cider_ctx& c, const float* w) {
     const float* W = take(size_t(Q) * D);
     const float* V = take(size_t(Q) * D);
     c.Etab = upload_vec(c, E, size_t(Q + 1) * D);
+    if (c.bf16) c.Etab16 = upload_mat(c, E, Q + 1, D, false); // (round-to-nearest-even, as the kernel's conversion)
     c.W_host.assign(W, W + size_t(Q) * D);
     if (c.bf16)
         for (float& v : c.W_host) v = bf16_round(v);

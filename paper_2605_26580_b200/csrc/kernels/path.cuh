@@ -26,8 +26,9 @@ __global__ void embed_kernel(const int* __restrict__ X, const float* __restrict_
     if (Zt) Zt[i] = from_f<T>(v);
 }
 
-// Vectorised BF16 variant (D % 8 == 0): 8 columns per thread, one 16-byte store.
-__global__ void embed_bf16x8_kernel(const int* __restrict__ X, const float* __restrict__ Etab, int Q, int D, int64_t M,
+// Vectorised BF16 variant (D % 8 == 0) on the bf16 copy of the table: 8 columns per thread, one 16-byte load and
+// one 16-byte store.
+__global__ void embed_bf16x8_kernel(const int* __restrict__ X, const bf16* __restrict__ Etab16, int Q, int D, int64_t M,
                                     bf16* __restrict__ Zt) {
     griddep_wait(); // (programmatic dependent launch) the grid X of the previous step
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -37,15 +38,7 @@ __global__ void embed_bf16x8_kernel(const int* __restrict__ X, const float* __re
     const int c = int(i - m * cpr);
     const int tok = __ldg(X + m);
     const int row = (tok < 0 || tok >= Q) ? Q : tok;
-    const float4* src = reinterpret_cast<const float4*>(Etab + size_t(row) * D + c * 8);
-    const float4 a = __ldg(src), b = __ldg(src + 1);
-    uint4 o;
-    __nv_bfloat162* po = reinterpret_cast<__nv_bfloat162*>(&o);
-    po[0] = __floats2bfloat162_rn(a.x, a.y);
-    po[1] = __floats2bfloat162_rn(a.z, a.w);
-    po[2] = __floats2bfloat162_rn(b.x, b.y);
-    po[3] = __floats2bfloat162_rn(b.z, b.w);
-    *reinterpret_cast<uint4*>(Zt + m * D + c * 8) = o;
+    *reinterpret_cast<uint4*>(Zt + m * D + c * 8) = __ldg(reinterpret_cast<const uint4*>(Etab16 + size_t(row) * D + c * 8));
 }
 
 // ---- demix_responsibilities x S (denoiser.cpp:103-122, 130) -------------------------------
